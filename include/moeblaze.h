@@ -1,0 +1,182 @@
+/*
+ * moeblaze.h — C ABI of the B200 (sm_100a) MoEBlaze hot path.
+ *
+ * The operation is one dropless top-k SwiGLU Mixture-of-Experts layer,
+ * forward and backward, computed MoEBlaze-style: no routed-token buffer and
+ * no padded per-expert buffer ever exists; experts gather token rows through
+ * compact index structures and reduce their outputs back by index.
+ * Citations "P:n" are lines of the paper text (arXiv 2601.05296, PAPER.md).
+ *
+ * Problem statement (Alg. 1):
+ *   X   [T, d]      tokens ("x in R^{L x d}", L = T)
+ *   W_g [E, d]      router, logits = X W_g^T (no bias)
+ *   w1, w2 [E, h, d]  SwiGLU gate (SiLU) and up projections, nn.Linear (out,in)
+ *                    layout: the paper's W1_e = w1[e]^T, W2_e = w2[e]^T
+ *   w3  [E, d, h]   down projection, W3_e = w3[e]^T
+ *   y_t = sum_j w[t,j] * ( SiLU(x_t W1_e) * (x_t W2_e) ) W3_e,  e = ids[t,j]
+ *
+ * Conventions common to every entry point
+ *  - All tensor pointers are DEVICE pointers to dense row-major arrays owned by
+ *    the caller.  The library never allocates device memory and keeps no
+ *    per-call state; scratch comes from the caller's `ws` (size from
+ *    moe_workspace_size).  Pointers must be 16-byte aligned.
+ *  - Calls are asynchronous and stream-ordered on `stream` (a cudaStream_t
+ *    passed as void*; NULL = legacy default stream).  No call synchronises the
+ *    host: per-expert sizes are read on the device.
+ *  - dtype MOE_BF16: X, W*, A/B checkpoints, Y and all gradients are bf16;
+ *    logits, topk_w, d_topk_w are fp32; accumulation is fp32 (tcgen05 TMEM).
+ *    dtype MOE_FP32: every tensor is fp32 and the arithmetic is true fp32
+ *    (CUDA-core FMA, no TF32).
+ *  - Argument errors are returned synchronously and nothing is launched:
+ *    MOE_ERR_INVALID_ARG (null pointer, bad shape: T < 0, d/h/E/k < 1, k > E,
+ *    E > 256, k > 16, T*k >= 2^31), MOE_ERR_UNSUPPORTED (bf16 with d or h not
+ *    a multiple of 128, or a device that is not sm_100), MOE_ERR_MISALIGNED,
+ *    MOE_ERR_WORKSPACE (ws too small).  Launch failures return MOE_ERR_CUDA.
+ *    The library never aborts the process.
+ *  - T = 0 is valid: nothing is launched except zero-fills of outputs.
+ */
+#ifndef MOEBLAZE_H_
+#define MOEBLAZE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MOE_OK = 0,
+  MOE_ERR_INVALID_ARG = 1,
+  MOE_ERR_UNSUPPORTED = 2,
+  MOE_ERR_MISALIGNED = 3,
+  MOE_ERR_WORKSPACE = 4,
+  MOE_ERR_BAD_ROUTING = 5,
+  MOE_ERR_CUDA = 6
+} moe_status;
+
+typedef enum { MOE_BF16 = 0, MOE_FP32 = 1 } moe_dtype;
+
+typedef enum { MOE_OP_ROUTE = 0, MOE_OP_DISPATCH = 1, MOE_OP_FFN_FWD = 2, MOE_OP_FFN_BWD = 3 } moe_op;
+
+typedef struct {
+  int64_t T;              /* tokens in the step (paper's L) */
+  int32_t d;              /* model dim */
+  int32_t h;              /* FFN hidden dim (d_ff) */
+  int32_t E;              /* experts, 1..256 */
+  int32_t k;              /* experts per token, 1..min(E,16) */
+  int32_t dtype;          /* moe_dtype */
+  int32_t renormalize;    /* 0: w = softmax over all E, then pick (paper default);
+                             1: w renormalised over the k picked experts (Mixtral) */
+  int32_t check_routing;  /* 1: moe_dispatch_build validates ids (range, per-token
+                             uniqueness) and records violations in the device status
+                             word at ws offset 0 (int32; 0 = ok, else MOE_ERR_BAD_ROUTING) */
+} moe_problem;
+
+/* The compact dispatch index structures of §4.1.  R = T*k.
+ *   expert_counts[E]         tokens routed to each expert (expert_lengths)
+ *   expert_offsets[E+1]      exclusive prefix sum of counts; offsets[E] = R
+ *   expert_token_indices[R]  token ids grouped by expert, ascending inside an
+ *                            expert
+ *   token_index_map[T*k]     position of (t, ids[t,j]) inside expert_token_indices
+ *                            (P:130-135); a permutation of [0, R)
+ *   row_slot[R]              inverse of token_index_map: t*k + j for row r
+ *   token_expert_indices     == topk_ids [T*k], input only
+ * Built by moe_dispatch_build (written), read by moe_ffn_fwd/bwd (read only). */
+typedef struct {
+  int32_t* expert_counts;
+  int32_t* expert_offsets;
+  int32_t* expert_token_indices;
+  int32_t* token_index_map;
+  int32_t* row_slot;
+  const int32_t* token_expert_indices;
+} moe_dispatch;
+
+/* Router backward inputs/outputs for moe_ffn_bwd (not in the paper: the
+ * derivative of P:42/P:91 through softmax; reading #14). */
+typedef struct {
+  const void* w_gate;     /* [E, d] dtype */
+  const float* logits;    /* [T, E] fp32, as written by moe_route */
+  const int32_t* topk_ids;/* [T, k] */
+  void* dw_gate;          /* [E, d] dtype, written */
+} moe_router_bwd;
+
+/* Bytes of device scratch `ws` that `op` needs for problem `p` (closed form;
+ * it has no T*k*d term: no routed-token buffer exists). */
+moe_status moe_workspace_size(const moe_problem* p, moe_op op, size_t* bytes);
+
+/* Gating.  logits = X W_g^T accumulated in fp32; ids[t,:] = the k
+ * largest logits in descending order, exact ties -> lower expert id;
+ * topk_w[t,j] = softmax(logits[t,:])[ids[t,j]] (renormalised over the k
+ * picked experts if p->renormalize).
+ *   x [T,d] dtype, w_gate [E,d] dtype -> logits [T,E] fp32, topk_ids [T,k]
+ *   int32, topk_w [T,k] fp32.  ws may be NULL (needs 0 bytes). */
+moe_status moe_route(const moe_problem* p, const void* x, const void* w_gate,
+                     float* logits, int32_t* topk_ids, float* topk_w,
+                     void* ws, size_t ws_bytes, void* stream);
+
+/* Buffer-free dispatch construction (§4.2): from topk_ids [T,k]
+ * build counts, offsets, expert_token_indices, token_index_map and row_slot
+ * in `out` (all device arrays, written).  Atomic-free and deterministic:
+ * results are bit-identical to a stable sort of (expert, token) pairs.
+ * Two launches: per-tile histogram, then scan + scatter. */
+moe_status moe_dispatch_build(const moe_problem* p, const int32_t* topk_ids, const moe_dispatch* out,
+                              void* ws, size_t ws_bytes, void* stream);
+
+/* Expert forward (§3.1, Alg. 1 FusedForward P:221-233):
+ *   for each expert e and row r in [offsets[e], offsets[e+1]), t = eti[r]:
+ *     A_r = X[t] W1_e,  B_r = X[t] W2_e   (X rows gathered through eti, never copied)
+ *     U_r = SiLU(A_r) * B_r               (transient, in ws)
+ *     y[t] += topk_w[row_slot[r]] * (U_r W3_e)     (combine fused into the down GEMM)
+ *   a_save, b_save [T*k, h] dtype: the checkpointed pre-activations A, B in
+ *   expert-sorted row order, written.  y [T,d] dtype, written. */
+moe_status moe_ffn_fwd(const moe_problem* p, const void* x, const void* w1, const void* w2,
+                       const void* w3, const float* topk_w, const moe_dispatch* disp,
+                       void* a_save, void* b_save, void* y,
+                       void* ws, size_t ws_bytes, void* stream);
+
+/* Expert backward (§3.2, Alg. 1 FusedBackward P:236-253) with the
+ * SiLU recomputed from the checkpoint:
+ *   dH_r = dy[eti[r]] W3_e^T;  d_topk_w[t,j] = <dH_r, U_r>
+ *   dw3[e] = sum_r (w_r U_r)^T dy[eti[r]]
+ *   dA_r = w_r dH_r * B_r * SiLU'(A_r);  dB_r = w_r dH_r * SiLU(A_r)
+ *   dw1[e] = sum_r dA_r^T X[eti[r]],  dw2[e] = sum_r dB_r^T X[eti[r]]
+ *   dx[t]  = sum_{r: eti[r]=t} (dA_r W1_e^T + dB_r W2_e^T)  [+ router path]
+ * a_save/b_save are read (A, B) and OVERWRITTEN with dA, dB (in place).
+ * dw1/dw2/dw3 are written (experts with no rows get zeros), not accumulated.
+ * d_topk_w [T,k] fp32 may be NULL only if router is NULL.
+ * router != NULL: also computes the router backward (renorm-aware) and adds
+ * dlogits W_g into dx; router->dw_gate is written. */
+moe_status moe_ffn_bwd(const moe_problem* p, const void* dy, const void* x, const void* w1,
+                       const void* w2, const void* w3, const float* topk_w,
+                       const moe_dispatch* disp, void* a_save, void* b_save,
+                       void* dx, void* dw1, void* dw2, void* dw3, float* d_topk_w,
+                       const moe_router_bwd* router, void* ws, size_t ws_bytes, void* stream);
+
+/* Expert-parallel helpers (the paper's "future work").
+ * moe_gather_rows: dst[i, :] = src[index[i], :] for i < n (rows of `width`
+ *   elements of `elem_bytes` in {2,4}); builds the all-to-all send buffer in
+ *   expert_token_indices order.  index entries must be in [0, n_src).
+ * moe_combine_rows: out[t, :] = sum_{j<k} rows[tim[t*k+j], :] (fixed j order,
+ *   fp32 accumulation, dtype output): the token-side combine of returned
+ *   expert rows through token_index_map ("gather its k expert
+ *   outputs"). */
+moe_status moe_gather_rows(const void* src, int64_t n_src, const int32_t* index, int64_t n,
+                           int64_t width, int32_t elem_bytes, void* dst, void* stream);
+moe_status moe_combine_rows(const moe_problem* p, const void* rows, const int32_t* token_index_map,
+                            void* out, void* stream);
+
+/* Human-readable status. */
+const char* moe_status_string(moe_status s);
+
+/* Number of CUDA kernels this library has launched since load (monotonic;
+ * used by the bench to report its own launches). */
+uint64_t moe_launch_count(void);
+
+/* Library version (major*10000 + minor*100 + patch). */
+int32_t moe_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOEBLAZE_H_ */

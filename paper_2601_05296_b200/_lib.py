@@ -1,0 +1,160 @@
+"""ctypes binding of libmoeblaze.so (the C ABI in include/moeblaze.h).
+
+Argument marshalling only: every step of the MoE layer runs in the library's
+CUDA kernels.  Torch is used for device memory (the caller-owned buffers and
+the scratch workspace) and for the current CUDA stream.  There is no CPU or
+PyTorch fallback: if the library cannot be loaded, or a call fails, this
+module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libmoeblaze.so")
+
+MOE_BF16, MOE_FP32 = 0, 1
+MOE_OP_ROUTE, MOE_OP_DISPATCH, MOE_OP_FFN_FWD, MOE_OP_FFN_BWD = 0, 1, 2, 3
+
+EXPORTS = ("moe_workspace_size", "moe_route", "moe_dispatch_build", "moe_ffn_fwd", "moe_ffn_bwd",
+           "moe_gather_rows", "moe_combine_rows", "moe_status_string", "moe_launch_count", "moe_version")
+
+
+class MoeProblem(ctypes.Structure):
+    _fields_ = [("T", ctypes.c_int64), ("d", ctypes.c_int32), ("h", ctypes.c_int32), ("E", ctypes.c_int32),
+                ("k", ctypes.c_int32), ("dtype", ctypes.c_int32), ("renormalize", ctypes.c_int32),
+                ("check_routing", ctypes.c_int32)]
+
+
+class MoeDispatch(ctypes.Structure):
+    _fields_ = [("expert_counts", ctypes.c_void_p), ("expert_offsets", ctypes.c_void_p),
+                ("expert_token_indices", ctypes.c_void_p), ("token_index_map", ctypes.c_void_p),
+                ("row_slot", ctypes.c_void_p), ("token_expert_indices", ctypes.c_void_p)]
+
+
+class MoeRouterBwd(ctypes.Structure):
+    _fields_ = [("w_gate", ctypes.c_void_p), ("logits", ctypes.c_void_p), ("topk_ids", ctypes.c_void_p),
+                ("dw_gate", ctypes.c_void_p)]
+
+
+class MoEError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def load():
+    """Load the shared library (raises if it is missing: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not found: build it with `python -m paper_2601_05296_b200.build` "
+                          "(there is no CPU/PyTorch fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, V, I32, I64, SZ = ctypes.POINTER, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+    lib.moe_workspace_size.argtypes = [P(MoeProblem), I32, P(SZ)]
+    lib.moe_route.argtypes = [P(MoeProblem), V, V, V, V, V, V, SZ, V]
+    lib.moe_dispatch_build.argtypes = [P(MoeProblem), V, P(MoeDispatch), V, SZ, V]
+    lib.moe_ffn_fwd.argtypes = [P(MoeProblem), V, V, V, V, V, P(MoeDispatch), V, V, V, V, SZ, V]
+    lib.moe_ffn_bwd.argtypes = [P(MoeProblem), V, V, V, V, V, V, P(MoeDispatch), V, V, V, V, V, V, V,
+                                P(MoeRouterBwd), V, SZ, V]
+    lib.moe_gather_rows.argtypes = [V, I64, V, I64, I64, I32, V, V]
+    lib.moe_combine_rows.argtypes = [P(MoeProblem), V, V, V, V]
+    for fn in ("moe_workspace_size", "moe_route", "moe_dispatch_build", "moe_ffn_fwd", "moe_ffn_bwd",
+               "moe_gather_rows", "moe_combine_rows"):
+        getattr(lib, fn).restype = I32
+    lib.moe_status_string.argtypes = [I32]
+    lib.moe_status_string.restype = ctypes.c_char_p
+    lib.moe_launch_count.restype = ctypes.c_uint64
+    lib.moe_version.restype = I32
+    _lib = lib
+    return lib
+
+
+def _check(status, what):
+    if status != 0:
+        msg = load().moe_status_string(status).decode()
+        raise MoEError(f"{what}: {msg} (status {status})")
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _dtype_code(dt):
+    if dt == torch.bfloat16:
+        return MOE_BF16
+    if dt == torch.float32:
+        return MOE_FP32
+    raise MoEError(f"unsupported dtype {dt} (bf16 or fp32)")
+
+
+def problem(T, d, h, E, k, dtype, renormalize=False, check_routing=False):
+    return MoeProblem(int(T), int(d), int(h), int(E), int(k), _dtype_code(dtype), int(bool(renormalize)),
+                      int(bool(check_routing)))
+
+
+def workspace_size(p, op):
+    n = ctypes.c_size_t(0)
+    _check(load().moe_workspace_size(ctypes.byref(p), op, ctypes.byref(n)), "moe_workspace_size")
+    return n.value
+
+
+def workspace(p, op, device):
+    n = workspace_size(p, op)
+    return torch.empty(max(n, 256), dtype=torch.uint8, device=device)
+
+
+def launch_count():
+    return int(load().moe_launch_count())
+
+
+# ----------------------------------------------------------------- entry points (same names as the C ABI)
+def moe_route(p, x, w_gate, logits, topk_ids, topk_w, stream=None):
+    _check(load().moe_route(ctypes.byref(p), _ptr(x), _ptr(w_gate), _ptr(logits), _ptr(topk_ids), _ptr(topk_w),
+                            None, 0, _stream(stream)), "moe_route")
+
+
+def make_dispatch(counts, offs, eti, tim, row_slot, ids):
+    return MoeDispatch(counts.data_ptr(), offs.data_ptr(), eti.data_ptr(), tim.data_ptr(), row_slot.data_ptr(),
+                       ids.data_ptr())
+
+
+def moe_dispatch_build(p, topk_ids, disp, ws, stream=None):
+    _check(load().moe_dispatch_build(ctypes.byref(p), _ptr(topk_ids), ctypes.byref(disp), _ptr(ws), ws.numel(),
+                                     _stream(stream)), "moe_dispatch_build")
+
+
+def moe_ffn_fwd(p, x, w1, w2, w3, topk_w, disp, a_save, b_save, y, ws, stream=None):
+    _check(load().moe_ffn_fwd(ctypes.byref(p), _ptr(x), _ptr(w1), _ptr(w2), _ptr(w3), _ptr(topk_w),
+                              ctypes.byref(disp), _ptr(a_save), _ptr(b_save), _ptr(y), _ptr(ws), ws.numel(),
+                              _stream(stream)), "moe_ffn_fwd")
+
+
+def moe_ffn_bwd(p, dy, x, w1, w2, w3, topk_w, disp, a_save, b_save, dx, dw1, dw2, dw3, d_topk_w, router, ws,
+                stream=None):
+    _check(load().moe_ffn_bwd(ctypes.byref(p), _ptr(dy), _ptr(x), _ptr(w1), _ptr(w2), _ptr(w3), _ptr(topk_w),
+                              ctypes.byref(disp), _ptr(a_save), _ptr(b_save), _ptr(dx), _ptr(dw1), _ptr(dw2),
+                              _ptr(dw3), _ptr(d_topk_w), ctypes.byref(router) if router is not None else None,
+                              _ptr(ws), ws.numel(), _stream(stream)), "moe_ffn_bwd")
+
+
+def moe_gather_rows(src, index, dst, stream=None):
+    n_src, width = src.shape[0], src[0].numel() if src.shape[0] else src.shape[-1]
+    _check(load().moe_gather_rows(_ptr(src), n_src, _ptr(index), index.numel(), width, src.element_size(), _ptr(dst),
+                                  _stream(stream)), "moe_gather_rows")
+
+
+def moe_combine_rows(p, rows, token_index_map, out, stream=None):
+    _check(load().moe_combine_rows(ctypes.byref(p), _ptr(rows), _ptr(token_index_map), _ptr(out), _stream(stream)),
+           "moe_combine_rows")

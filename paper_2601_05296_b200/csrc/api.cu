@@ -1,0 +1,231 @@
+// api.cu — the C ABI declared in include/moeblaze.h: validation, workspace
+// layout, and the launch sequence of every entry point.
+#include <algorithm>
+#include <atomic>
+
+#include "common.cuh"
+#include "gemm.h"
+
+namespace moeb {
+
+static std::atomic<uint64_t> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+// launchers defined in the other translation units
+moe_status launch_route(const moe_problem*, const void*, const void*, float*, int32_t*, float*, cudaStream_t);
+moe_status launch_dispatch(const moe_problem*, const int32_t*, const moe_dispatch*, int32_t*, int32_t*, cudaStream_t);
+size_t dispatch_ws_bytes(const moe_problem*);
+moe_status launch_dg_reduce(const float*, int, const int32_t*, int64_t, float*, cudaStream_t);
+int dwg_chunks(int64_t T, int d);
+moe_status launch_router_bwd(const moe_problem*, const float*, const int32_t*, const float*, const void*, float*,
+                             float*, void*, cudaStream_t);
+moe_status launch_finalize(const moe_problem*, const float*, const float*, const void*, void*, cudaStream_t);
+moe_status launch_gather_rows(const void*, const int32_t*, int64_t, int64_t, void*, cudaStream_t);
+moe_status launch_combine_rows(const moe_problem*, const void*, const int32_t*, void*, cudaStream_t);
+
+static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+
+static moe_status validate(const moe_problem* p) {
+  if (!p) return MOE_ERR_INVALID_ARG;
+  if (p->T < 0 || p->d < 1 || p->h < 1 || p->E < 1 || p->k < 1) return MOE_ERR_INVALID_ARG;
+  if (p->k > p->E || p->E > 256 || p->k > 16) return MOE_ERR_INVALID_ARG;
+  if (p->T * (int64_t)p->k >= (int64_t(1) << 31)) return MOE_ERR_INVALID_ARG;
+  if (p->dtype != MOE_BF16 && p->dtype != MOE_FP32) return MOE_ERR_INVALID_ARG;
+  if (p->dtype == MOE_BF16 && (p->d % 128 != 0 || p->h % 128 != 0)) return MOE_ERR_UNSUPPORTED;
+  if (p->dtype == MOE_FP32 && (p->d % 4 != 0)) return MOE_ERR_UNSUPPORTED;
+  return MOE_OK;
+}
+
+static bool aligned16(const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; }
+
+static size_t esize(const moe_problem* p) { return p->dtype == MOE_BF16 ? 2 : 4; }
+
+// dg partial columns per routed row: the max over the GEMM backends
+static int dg_parts(const moe_problem* p) { return (int)ceil_div(p->h, 64); }
+
+struct FwdWs { void* u; float* yacc; size_t total; };
+static FwdWs fwd_layout(const moe_problem* p, void* base) {
+  const int64_t R = p->T * p->k;
+  char* b = (char*)base;
+  size_t o = 0;
+  FwdWs w;
+  w.u = b + o; o += align256((size_t)R * p->h * esize(p));
+  w.yacc = (float*)(b + o); o += align256((size_t)p->T * p->d * 4);
+  w.total = o;
+  return w;
+}
+
+struct BwdWs { void* wu; float* dxacc; float* dgpart; float* dlogits; float* dwgpart; float* dg; size_t total; };
+static BwdWs bwd_layout(const moe_problem* p, void* base) {
+  const int64_t R = p->T * p->k;
+  char* b = (char*)base;
+  size_t o = 0;
+  BwdWs w;
+  w.wu = b + o; o += align256((size_t)R * p->h * esize(p));
+  w.dxacc = (float*)(b + o); o += align256((size_t)p->T * p->d * 4);
+  w.dgpart = (float*)(b + o); o += align256((size_t)R * dg_parts(p) * 4);
+  w.dlogits = (float*)(b + o); o += align256((size_t)p->T * p->E * 4);
+  w.dwgpart = (float*)(b + o); o += align256((size_t)dwg_chunks(p->T, p->d) * p->E * p->d * 4);
+  w.dg = (float*)(b + o); o += align256((size_t)R * 4);
+  w.total = o;
+  return w;
+}
+
+}  // namespace moeb
+
+using namespace moeb;
+
+extern "C" {
+
+const char* moe_status_string(moe_status s) {
+  switch (s) {
+    case MOE_OK: return "ok";
+    case MOE_ERR_INVALID_ARG: return "invalid argument";
+    case MOE_ERR_UNSUPPORTED: return "unsupported configuration";
+    case MOE_ERR_MISALIGNED: return "pointer not 16-byte aligned";
+    case MOE_ERR_WORKSPACE: return "workspace too small";
+    case MOE_ERR_BAD_ROUTING: return "invalid routing (expert id out of range or repeated within a token)";
+    case MOE_ERR_CUDA: return "CUDA launch error";
+  }
+  return "unknown status";
+}
+
+uint64_t moe_launch_count(void) { return g_launches.load(); }
+int32_t moe_version(void) { return 100; }
+
+moe_status moe_workspace_size(const moe_problem* p, moe_op op, size_t* bytes) {
+  moe_status s = validate(p);
+  if (s != MOE_OK) return s;
+  if (!bytes) return MOE_ERR_INVALID_ARG;
+  switch (op) {
+    case MOE_OP_ROUTE: *bytes = 0; break;
+    case MOE_OP_DISPATCH: *bytes = dispatch_ws_bytes(p); break;
+    case MOE_OP_FFN_FWD: *bytes = fwd_layout(p, nullptr).total; break;
+    case MOE_OP_FFN_BWD: *bytes = bwd_layout(p, nullptr).total; break;
+    default: return MOE_ERR_INVALID_ARG;
+  }
+  return MOE_OK;
+}
+
+moe_status moe_route(const moe_problem* p, const void* x, const void* w_gate, float* logits, int32_t* topk_ids,
+                     float* topk_w, void* ws, size_t ws_bytes, void* stream) {
+  (void)ws; (void)ws_bytes;
+  moe_status s = validate(p);
+  if (s != MOE_OK) return s;
+  if (p->T > 0 && (!x || !w_gate || !logits || !topk_ids || !topk_w)) return MOE_ERR_INVALID_ARG;
+  return launch_route(p, x, w_gate, logits, topk_ids, topk_w, (cudaStream_t)stream);
+}
+
+moe_status moe_dispatch_build(const moe_problem* p, const int32_t* topk_ids, const moe_dispatch* out, void* ws,
+                              size_t ws_bytes, void* stream) {
+  moe_status s = validate(p);
+  if (s != MOE_OK) return s;
+  if (!out || !out->expert_counts || !out->expert_offsets) return MOE_ERR_INVALID_ARG;
+  if (p->T > 0 && (!topk_ids || !out->expert_token_indices || !out->token_index_map || !ws)) return MOE_ERR_INVALID_ARG;
+  if (ws_bytes < dispatch_ws_bytes(p)) return MOE_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  int32_t* status = (int32_t*)ws;
+  if (p->check_routing) MOE_CUDA_CHECK(cudaMemsetAsync(status, 0, sizeof(int32_t), st));
+  return launch_dispatch(p, topk_ids, out, (int32_t*)((char*)ws + 256), status, st);
+}
+
+moe_status moe_ffn_fwd(const moe_problem* p, const void* x, const void* w1, const void* w2, const void* w3,
+                       const float* topk_w, const moe_dispatch* disp, void* a_save, void* b_save, void* y, void* ws,
+                       size_t ws_bytes, void* stream) {
+  moe_status s = validate(p);
+  if (s != MOE_OK) return s;
+  if (!disp || !w1 || !w2 || !w3) return MOE_ERR_INVALID_ARG;
+  if (p->T > 0 && (!x || !y || !topk_w || !a_save || !b_save || !ws || !disp->expert_offsets || !disp->expert_token_indices ||
+                   !disp->row_slot))
+    return MOE_ERR_INVALID_ARG;
+  if (!aligned16(x) || !aligned16(w1) || !aligned16(w2) || !aligned16(w3) || !aligned16(a_save) ||
+      !aligned16(b_save) || !aligned16(y))
+    return MOE_ERR_MISALIGNED;
+  FwdWs w = fwd_layout(p, ws);
+  if (ws_bytes < w.total) return MOE_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (p->T == 0) return MOE_OK;
+  MOE_CUDA_CHECK(cudaMemsetAsync(w.yacc, 0, (size_t)p->T * p->d * 4, st));
+  GemmCall c{};
+  c.x = x; c.w1 = w1; c.w2 = w2; c.w3 = w3; c.topw = topk_w;
+  c.offs = disp->expert_offsets; c.eti = disp->expert_token_indices; c.row_slot = disp->row_slot;
+  c.a_save = a_save; c.b_save = b_save; c.u = w.u; c.acc_out = w.yacc;
+  c.T = p->T; c.R = p->T * p->k; c.d = p->d; c.h = p->h; c.E = p->E; c.bf16 = p->dtype == MOE_BF16;
+  c.which = GEMM_FWD_UP;
+  if ((s = run_gemm(c, st)) != MOE_OK) return s;
+  c.which = GEMM_FWD_DOWN;
+  if ((s = run_gemm(c, st)) != MOE_OK) return s;
+  return launch_finalize(p, w.yacc, nullptr, nullptr, y, st);
+}
+
+moe_status moe_ffn_bwd(const moe_problem* p, const void* dy, const void* x, const void* w1, const void* w2,
+                       const void* w3, const float* topk_w, const moe_dispatch* disp, void* a_save, void* b_save,
+                       void* dx, void* dw1, void* dw2, void* dw3, float* d_topk_w, const moe_router_bwd* router,
+                       void* ws, size_t ws_bytes, void* stream) {
+  moe_status s = validate(p);
+  if (s != MOE_OK) return s;
+  if (!disp || !dw1 || !dw2 || !dw3 || !w1 || !w2 || !w3) return MOE_ERR_INVALID_ARG;
+  if (router && (!router->w_gate || !router->logits || !router->topk_ids || !router->dw_gate)) return MOE_ERR_INVALID_ARG;
+  if (p->T > 0 && (!dy || !x || !dx || !topk_w || !a_save || !b_save || !ws || !disp->expert_offsets ||
+                   !disp->expert_token_indices || !disp->token_index_map || !disp->row_slot))
+    return MOE_ERR_INVALID_ARG;
+  if (!aligned16(dy) || !aligned16(x) || !aligned16(a_save) || !aligned16(b_save) || !aligned16(dx) ||
+      !aligned16(dw1) || !aligned16(dw2) || !aligned16(dw3))
+    return MOE_ERR_MISALIGNED;
+  BwdWs w = bwd_layout(p, ws);
+  if (ws_bytes < w.total) return MOE_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t R = p->T * p->k;
+  GemmCall c{};
+  c.x = x; c.dy = dy; c.w1 = w1; c.w2 = w2; c.w3 = w3; c.topw = topk_w;
+  c.offs = disp->expert_offsets; c.eti = disp->expert_token_indices; c.row_slot = disp->row_slot;
+  c.a_save = a_save; c.b_save = b_save; c.u = w.wu; c.acc_out = w.dxacc; c.dg_part = w.dgpart;
+  c.dw_a = dw3; c.dw_b = nullptr;
+  c.T = p->T; c.R = R; c.d = p->d; c.h = p->h; c.E = p->E; c.bf16 = p->dtype == MOE_BF16;
+  if (p->T > 0) {
+    MOE_CUDA_CHECK(cudaMemsetAsync(w.dxacc, 0, (size_t)p->T * p->d * 4, st));
+    c.which = GEMM_BWD_DH;  // dH, SwiGLU bwd: dA/dB in place, wU, dg partials
+    if ((s = run_gemm(c, st)) != MOE_OK) return s;
+  }
+  c.which = GEMM_DW3;      // dW3 = dY^T (wU)
+  if ((s = run_gemm(c, st)) != MOE_OK) return s;
+  c.which = GEMM_DW12;     // dW1, dW2 = [dA|dB]^T X
+  c.dw_a = dw1; c.dw_b = dw2;
+  if ((s = run_gemm(c, st)) != MOE_OK) return s;
+  if (p->T == 0) {
+    if (router) {
+      MOE_CUDA_CHECK(cudaMemsetAsync(router->dw_gate, 0, (size_t)p->E * p->d * esize(p), st));
+    }
+    return MOE_OK;
+  }
+  c.which = GEMM_BWD_DX;   // dXacc += [dA|dB][W1;W2]
+  if ((s = run_gemm(c, st)) != MOE_OK) return s;
+  float* dg = d_topk_w ? d_topk_w : w.dg;
+  if ((s = launch_dg_reduce(w.dgpart, gemm_dg_parts(c), disp->token_index_map, R, dg, st)) != MOE_OK) return s;
+  const float* dl = nullptr;
+  if (router) {
+    if ((s = launch_router_bwd(p, router->logits, router->topk_ids, dg, x, w.dlogits, w.dwgpart, router->dw_gate,
+                               st)) != MOE_OK)
+      return s;
+    dl = w.dlogits;
+  }
+  return launch_finalize(p, w.dxacc, dl, router ? router->w_gate : nullptr, dx, st);
+}
+
+moe_status moe_gather_rows(const void* src, int64_t n_src, const int32_t* index, int64_t n, int64_t width,
+                           int32_t elem_bytes, void* dst, void* stream) {
+  if (n < 0 || n_src < 0 || width < 1 || (elem_bytes != 2 && elem_bytes != 4)) return MOE_ERR_INVALID_ARG;
+  if (n > 0 && (!src || !index || !dst)) return MOE_ERR_INVALID_ARG;
+  if ((width * elem_bytes) % 16 != 0 || !aligned16(src) || !aligned16(dst)) return MOE_ERR_MISALIGNED;
+  return launch_gather_rows(src, index, n, width * elem_bytes, dst, (cudaStream_t)stream);
+}
+
+moe_status moe_combine_rows(const moe_problem* p, const void* rows, const int32_t* token_index_map, void* out,
+                            void* stream) {
+  moe_status s = validate(p);
+  if (s != MOE_OK) return s;
+  if (p->T > 0 && (!rows || !token_index_map || !out)) return MOE_ERR_INVALID_ARG;
+  return launch_combine_rows(p, rows, token_index_map, out, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,54 @@
+// common.cuh — shared helpers of the MoEBlaze sm_100a kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <algorithm>
+
+#include "../../include/moeblaze.h"
+
+namespace moeb {
+
+// ----------------------------------------------------------------- launch accounting
+// Every kernel launch of the library goes through MOE_LAUNCH so the bench can
+// report how many of OUR kernels ran inside its timed region.
+void note_launch();
+
+#define MOE_LAUNCH(kernel, grid, block, smem, stream, ...)                 \
+  do {                                                                    \
+    kernel<<<(grid), (block), (smem), (cudaStream_t)(stream)>>>(__VA_ARGS__); \
+    ::moeb::note_launch();                                                \
+  } while (0)
+
+#define MOE_CUDA_CHECK(expr)                                              \
+  do {                                                                    \
+    cudaError_t _e = (expr);                                              \
+    if (_e != cudaSuccess) return MOE_ERR_CUDA;                           \
+  } while (0)
+
+// ----------------------------------------------------------------- dtype helpers
+__device__ __forceinline__ float to_f32(float v) { return v; }
+__device__ __forceinline__ float to_f32(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <typename T> __device__ __forceinline__ T from_f32(float v);
+template <> __device__ __forceinline__ float from_f32<float>(float v) { return v; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(float v) {
+  return __float2bfloat16_rn(v);
+}
+
+__device__ __forceinline__ float sigmoidf_(float a) { return 1.0f / (1.0f + __expf(-a)); }
+
+__host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Index of the expert segment containing tile `i` given per-expert tile starts
+// `start[0..E]` (start[E] = total).  Binary search, E <= 256.
+__device__ __forceinline__ int find_segment(const int* start, int E, int i) {
+  int lo = 0, hi = E;  // invariant: start[lo] <= i < start[hi]
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (start[mid] <= i) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+}  // namespace moeb

@@ -1,0 +1,236 @@
+// elementwise.cu — HBM-bound kernels around the expert GEMMs.
+//
+//  K9a dg_reduce   : d_topk_w[t,j] = sum_p partial[tim[t,j], p]  (fixed order)
+//  K9b router_bwd  : dlogits = p * (dp - <p,dp>), dp = scatter of dsel (renorm-aware)
+//  K9c dwg_partial / dwg_reduce : dW_g = dlogits^T X (split over tokens, fixed-order sum)
+//  K10 finalize    : out = dtype(acc [+ dlogits W_g])  (Y, dX)
+//  K11 gather_rows / combine_rows : expert-parallel send-buffer gather and the
+//                    token-side k-way combine through token_index_map.
+// The gate-weight gradient and router backward are the analytic derivative of
+// P:42/P:91 (not in the paper; reading #14).
+#include "common.cuh"
+
+namespace moeb {
+
+__global__ void dg_reduce_kernel(const float* __restrict__ part, int nparts, const int32_t* __restrict__ tim,
+                                 int64_t R, float* __restrict__ dg) {
+  int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= R) return;
+  const float* p = part + (int64_t)tim[f] * nparts;
+  float s = 0.f;
+  for (int i = 0; i < nparts; ++i) s += p[i];
+  dg[f] = s;
+}
+
+// one warp per token
+__global__ void router_bwd_kernel(const float* __restrict__ logits, const int32_t* __restrict__ ids,
+                                  const float* __restrict__ dg, int64_t T, int E, int k, int renorm,
+                                  float* __restrict__ dlogits) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (t >= T) return;
+  const float* l = logits + t * E;
+  float m = -INFINITY;
+  for (int e = lane; e < E; e += 32) m = fmaxf(m, l[e]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  float s = 0.f;
+  for (int e = lane; e < E; e += 32) s += expf(l[e] - m);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float inv = 1.f / s;
+  // selected probabilities and dsel (all lanes compute the same k values)
+  float psum = 0.f, dgw = 0.f;
+  for (int j = 0; j < k; ++j) psum += expf(l[ids[t * k + j]] - m) * inv;
+  if (renorm)
+    for (int j = 0; j < k; ++j) dgw += dg[t * k + j] * (expf(l[ids[t * k + j]] - m) * inv / psum);
+  // <p, dp> = sum_j p_sel_j dsel_j
+  float pdp = 0.f;
+  for (int j = 0; j < k; ++j) {
+    float ds = renorm ? (dg[t * k + j] - dgw) / psum : dg[t * k + j];
+    pdp += expf(l[ids[t * k + j]] - m) * inv * ds;
+  }
+  for (int e = lane; e < E; e += 32) {
+    float dp = 0.f;
+    for (int j = 0; j < k; ++j)
+      if (ids[t * k + j] == e) dp = renorm ? (dg[t * k + j] - dgw) / psum : dg[t * k + j];
+    float p = expf(l[e] - m) * inv;
+    dlogits[t * E + e] = p * (dp - pdp);
+  }
+}
+
+// partial[c][e][col] = sum_{t in chunk c} dlogits[t,e] X[t,col]; block: 64 cols x 4 expert groups
+constexpr int WG_COLS = 64;
+template <typename T>
+__global__ void __launch_bounds__(256) dwg_partial_kernel(const float* __restrict__ dlogits, const T* __restrict__ x,
+                                                          int64_t Tn, int d, int E, int64_t tch,
+                                                          float* __restrict__ part) {
+  extern __shared__ float dl[];  // [32][E]
+  const int col = blockIdx.x * WG_COLS + (threadIdx.x & 63);
+  const int eg = threadIdx.x >> 6;  // 0..3
+  const int64_t ta = blockIdx.y * tch, tb = min64(ta + tch, Tn);
+  float acc[64];
+#pragma unroll
+  for (int i = 0; i < 64; ++i) acc[i] = 0.f;
+  const int ne = (E - eg + 3) / 4;
+  for (int64_t t0 = ta; t0 < tb; t0 += 32) {
+    const int nt = (int)min64(32, tb - t0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < 32 * E; i += 256) {
+      int r = i / E, e = i % E;
+      dl[i] = r < nt ? dlogits[(t0 + r) * E + e] : 0.f;
+    }
+    __syncthreads();
+    if (col < d) {
+      for (int r = 0; r < nt; ++r) {
+        float xv = to_f32(x[(t0 + r) * d + col]);
+#pragma unroll
+        for (int i = 0; i < 64; ++i)
+          if (i < ne) acc[i] = fmaf(dl[r * E + eg + 4 * i], xv, acc[i]);
+      }
+    }
+  }
+  if (col < d) {
+#pragma unroll
+    for (int i = 0; i < 64; ++i)
+      if (i < ne) part[((int64_t)blockIdx.y * E + eg + 4 * i) * d + col] = acc[i];
+  }
+}
+
+template <typename T>
+__global__ void dwg_reduce_kernel(const float* __restrict__ part, int nch, int64_t n, T* __restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float s = 0.f;
+  for (int c = 0; c < nch; ++c) s += part[c * n + i];
+  out[i] = from_f32<T>(s);
+}
+
+// out[t, :] = dtype(acc[t, :] + sum_e dl[t, e] Wg[e, :]); block: 16 tokens x 256 cols
+template <typename T>
+__global__ void __launch_bounds__(256) finalize_kernel(const float* __restrict__ acc, const float* __restrict__ dl,
+                                                       const T* __restrict__ wg, int64_t Tn, int d, int E,
+                                                       T* __restrict__ out) {
+  extern __shared__ float sdl[];  // [16][E]
+  const int col = blockIdx.x * 256 + threadIdx.x;
+  const int64_t t0 = (int64_t)blockIdx.y * 16;
+  const int nt = (int)min64(16, Tn - t0);
+  float a[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) a[r] = (r < nt && col < d) ? acc[(t0 + r) * d + col] : 0.f;
+  if (dl) {
+    for (int i = threadIdx.x; i < 16 * E; i += 256) {
+      int r = i / E, e = i % E;
+      sdl[i] = r < nt ? dl[(t0 + r) * E + e] : 0.f;
+    }
+    __syncthreads();
+    if (col < d) {
+      for (int e = 0; e < E; ++e) {
+        float w = to_f32(wg[(int64_t)e * d + col]);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) a[r] = fmaf(sdl[r * E + e], w, a[r]);
+      }
+    }
+  }
+  if (col < d) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+      if (r < nt) out[(t0 + r) * d + col] = from_f32<T>(a[r]);
+  }
+}
+
+// vectorised row gather: 16-byte chunks
+__global__ void gather_rows_kernel(const uint4* __restrict__ src, const int32_t* __restrict__ index, int64_t n,
+                                   int64_t vec_per_row, uint4* __restrict__ dst) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t total = n * vec_per_row;
+  if (i >= total) return;
+  int64_t row = i / vec_per_row, c = i % vec_per_row;
+  dst[i] = src[(int64_t)index[row] * vec_per_row + c];
+}
+
+template <typename T>
+__global__ void combine_rows_kernel(const T* __restrict__ rows, const int32_t* __restrict__ tim, int64_t Tn, int d,
+                                    int k, T* __restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= Tn * d) return;
+  int64_t t = i / d;
+  int c = (int)(i % d);
+  float s = 0.f;
+  for (int j = 0; j < k; ++j) s += to_f32(rows[(int64_t)tim[t * k + j] * d + c]);
+  out[i] = from_f32<T>(s);
+}
+
+// ----------------------------------------------------------------- launchers
+moe_status launch_dg_reduce(const float* part, int nparts, const int32_t* tim, int64_t R, float* dg, cudaStream_t st) {
+  if (R == 0) return MOE_OK;
+  MOE_LAUNCH(dg_reduce_kernel, (unsigned)ceil_div(R, 256), 256, 0, st, part, nparts, tim, R, dg);
+  return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
+}
+
+int dwg_chunks(int64_t T, int d) {
+  int64_t colb = ceil_div(d, WG_COLS);
+  int64_t nch = ceil_div(2 * 148, colb);
+  nch = std::max<int64_t>(1, min64(nch, 64));
+  nch = min64(nch, std::max<int64_t>(1, ceil_div(T, 32)));
+  return (int)nch;
+}
+
+moe_status launch_router_bwd(const moe_problem* p, const float* logits, const int32_t* ids, const float* dg,
+                             const void* x, float* dlogits, float* dwg_part, void* dwg, cudaStream_t st) {
+  const int64_t T = p->T;
+  const int E = p->E, d = p->d;
+  if (T > 0) {
+    MOE_LAUNCH(router_bwd_kernel, (unsigned)ceil_div(T * 32, 256), 256, 0, st, logits, ids, dg, T, E, p->k,
+               p->renormalize, dlogits);
+  }
+  const int nch = dwg_chunks(T, d);
+  const int64_t tch = ceil_div(std::max<int64_t>(T, 1), nch);
+  dim3 grid((unsigned)ceil_div(d, WG_COLS), nch);
+  size_t sm = sizeof(float) * 32 * E;
+  const int64_t n = (int64_t)E * d;
+  if (p->dtype == MOE_BF16) {
+    MOE_LAUNCH(dwg_partial_kernel<__nv_bfloat16>, grid, 256, sm, st, dlogits, (const __nv_bfloat16*)x, T, d, E, tch, dwg_part);
+    MOE_LAUNCH(dwg_reduce_kernel<__nv_bfloat16>, (unsigned)ceil_div(n, 256), 256, 0, st, dwg_part, nch, n, (__nv_bfloat16*)dwg);
+  } else {
+    MOE_LAUNCH(dwg_partial_kernel<float>, grid, 256, sm, st, dlogits, (const float*)x, T, d, E, tch, dwg_part);
+    MOE_LAUNCH(dwg_reduce_kernel<float>, (unsigned)ceil_div(n, 256), 256, 0, st, dwg_part, nch, n, (float*)dwg);
+  }
+  return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
+}
+
+moe_status launch_finalize(const moe_problem* p, const float* acc, const float* dl, const void* wg, void* out,
+                           cudaStream_t st) {
+  if (p->T == 0) return MOE_OK;
+  dim3 grid((unsigned)ceil_div(p->d, 256), (unsigned)ceil_div(p->T, 16));
+  size_t sm = dl ? sizeof(float) * 16 * p->E : 0;
+  if (p->dtype == MOE_BF16)
+    MOE_LAUNCH(finalize_kernel<__nv_bfloat16>, grid, 256, sm, st, acc, dl, (const __nv_bfloat16*)wg, p->T, p->d, p->E,
+               (__nv_bfloat16*)out);
+  else
+    MOE_LAUNCH(finalize_kernel<float>, grid, 256, sm, st, acc, dl, (const float*)wg, p->T, p->d, p->E, (float*)out);
+  return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
+}
+
+moe_status launch_gather_rows(const void* src, const int32_t* index, int64_t n, int64_t row_bytes, void* dst,
+                              cudaStream_t st) {
+  if (n == 0) return MOE_OK;
+  const int64_t vpr = row_bytes / 16;
+  MOE_LAUNCH(gather_rows_kernel, (unsigned)ceil_div(n * vpr, 256), 256, 0, st, (const uint4*)src, index, n, vpr,
+             (uint4*)dst);
+  return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
+}
+
+moe_status launch_combine_rows(const moe_problem* p, const void* rows, const int32_t* tim, void* out, cudaStream_t st) {
+  const int64_t n = p->T * p->d;
+  if (n == 0) return MOE_OK;
+  if (p->dtype == MOE_BF16)
+    MOE_LAUNCH(combine_rows_kernel<__nv_bfloat16>, (unsigned)ceil_div(n, 256), 256, 0, st,
+               (const __nv_bfloat16*)rows, tim, p->T, p->d, p->k, (__nv_bfloat16*)out);
+  else
+    MOE_LAUNCH(combine_rows_kernel<float>, (unsigned)ceil_div(n, 256), 256, 0, st, (const float*)rows, tim, p->T,
+               p->d, p->k, (float*)out);
+  return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
+}
+
+}  // namespace moeb

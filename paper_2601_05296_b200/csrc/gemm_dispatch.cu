@@ -1,0 +1,15 @@
+// gemm_dispatch.cu — routes each expert GEMM to its kernel family.
+#include "gemm.h"
+
+namespace moeb {
+
+moe_status simt_gemm(const GemmCall& c, cudaStream_t st);
+int simt_dg_parts(int h);
+
+int gemm_dg_parts(const GemmCall& c) { return simt_dg_parts(c.h); }
+
+moe_status run_gemm(const GemmCall& c, cudaStream_t st) {
+  return simt_gemm(c, st);
+}
+
+}  // namespace moeb

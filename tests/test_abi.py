@@ -1,0 +1,87 @@
+"""C-ABI library: loads, exports every symbol include/moeblaze.h declares,
+validates arguments and sizes its workspace without a GPU (CPU test)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "moeblaze.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2601_05296_b200 import build as B
+    B.build()
+    from paper_2601_05296_b200 import _lib as L
+    return L.load()
+
+
+def declared_symbols():
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(moe_[a-z_]+)\s*\(", txt)))
+
+
+def test_header_declares_the_north_star_calls():
+    syms = declared_symbols()
+    for s in ("moe_route", "moe_dispatch_build", "moe_ffn_fwd", "moe_ffn_bwd", "moe_workspace_size"):
+        assert s in syms
+
+
+def test_every_declared_symbol_is_exported(lib):
+    for s in declared_symbols():
+        assert hasattr(lib, s), s
+    from paper_2601_05296_b200 import _lib as L
+    assert set(L.EXPORTS) == set(declared_symbols())
+
+
+def test_nm_exports_are_c_symbols():
+    import subprocess
+    so = os.path.join(ROOT, "paper_2601_05296_b200", "libmoeblaze.so")
+    out = subprocess.run(["nm", "-D", "--defined-only", so], capture_output=True, text=True).stdout
+    names = {ln.split()[-1] for ln in out.splitlines() if ln.strip()}
+    for s in declared_symbols():
+        assert s in names, s  # unmangled: extern "C"
+
+
+def _problem(L, T=1024, d=256, h=512, E=8, k=2, dtype=0, renorm=0):
+    return L.MoeProblem(T, d, h, E, k, dtype, renorm, 0)
+
+
+def test_workspace_has_no_routed_token_term(lib):
+    """By construction (SURVEY §8(c) audit 1): the fwd/bwd workspace is a closed
+    form with no T*k*d term.  Its growth in d is the same for k = 1 and k = 8
+    (only the [T, d] fp32 accumulators and router terms depend on d)."""
+    from paper_2601_05296_b200 import _lib as L
+    for (T, d, h, E) in [(1024, 256, 512, 8), (4096, 512, 256, 64), (2048, 1024, 1024, 16)]:
+        for op in (L.MOE_OP_FFN_FWD, L.MOE_OP_FFN_BWD):
+            grow = []
+            for k in (1, 8):
+                s1 = L.workspace_size(_problem(L, T, d, h, E, k), op)
+                s2 = L.workspace_size(_problem(L, T, 2 * d, h, E, k), op)
+                grow.append(s2 - s1)
+            assert abs(grow[1] - grow[0]) <= 2048, (T, d, h, E, op, grow)
+            assert grow[0] <= T * d * 4 + 64 * E * d * 4 + 4096
+
+
+def test_argument_validation(lib):
+    from paper_2601_05296_b200 import _lib as L
+    n = ctypes.c_size_t(0)
+    bad = [
+        _problem(L, k=9, E=8),          # k > E
+        _problem(L, E=300, k=2),        # E > 256
+        _problem(L, T=-1),
+        _problem(L, d=100),             # bf16 needs d % 128 == 0
+        _problem(L, h=96),
+    ]
+    codes = [lib.moe_workspace_size(ctypes.byref(p), 2, ctypes.byref(n)) for p in bad]
+    assert codes == [1, 1, 1, 2, 2]
+    ok = _problem(L, T=0)
+    assert lib.moe_workspace_size(ctypes.byref(ok), 3, ctypes.byref(n)) == 0
+    fp32 = _problem(L, d=64, h=96, dtype=1)
+    assert lib.moe_workspace_size(ctypes.byref(fp32), 2, ctypes.byref(n)) == 0
+    # null pointers are rejected synchronously, nothing is launched
+    assert lib.moe_route(ctypes.byref(_problem(L)), None, None, None, None, None, None, 0, None) == 1
+    assert lib.moe_status_string(4) == b"workspace too small"

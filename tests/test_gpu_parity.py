@@ -1,0 +1,167 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle on the same
+seeded inputs.  Index structures bit-exact; bf16 within 2e-2 and fp32 within
+1e-4 normwise max-relative error (BASELINE.json north_star, reading #18)."""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from moe_inputs import make_inputs, make_ids
+from tests._util import BF16_TOL, FP32_TOL, f64, i64, normwise
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+@pytest.fixture(scope="module")
+def M():
+    from paper_2601_05296_b200 import build as B
+    B.build()
+    import paper_2601_05296_b200 as M
+    M._lib.load()
+    return M
+
+
+# ------------------------------------------------------------------ K2 dispatch
+def _check_dispatch(M, ids_np, E):
+    ids = torch.from_numpy(ids_np.astype(np.int32)).to(DEV)
+    d = M.dispatch_build(ids, E)
+    torch.cuda.synchronize()
+    ref = O.dispatch_argsort(ids_np, E)
+    assert np.array_equal(i64(d.counts), ref["counts"])
+    assert np.array_equal(i64(d.offs), ref["offs"])
+    assert np.array_equal(i64(d.eti), ref["eti"])
+    assert np.array_equal(i64(d.tim), ref["tim"])
+    assert np.array_equal(i64(d.row_slot), ref["row_slot"])
+
+
+def test_dispatch_fig2(M):
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "fig2_dispatch.json")))
+    ids = np.array(g["ids"], dtype=np.int32)
+    _check_dispatch(M, ids, g["E"])
+    d = M.dispatch_build(torch.from_numpy(ids).to(DEV), g["E"])
+    assert d.eti.tolist() == g["expected"]["expert_token_indices"]
+    assert d.tim.tolist() == g["expected"]["token_index_map"]
+
+
+@pytest.mark.parametrize("T,E,k,kind", [
+    (1, 1, 1, "random"), (1, 8, 8, "random"), (5, 4, 2, "random"), (257, 4, 2, "random"),
+    (4097, 8, 2, "random"), (3000, 64, 6, "random"), (9000, 16, 2, "skewed"), (777, 8, 8, "random"),
+    (4100, 4, 1, "random"), (2048, 256, 16, "random"), (70001, 8, 2, "random"), (20000, 64, 8, "skewed"),
+    (1000, 16, 3, "degenerate"),
+])
+def test_dispatch_random(M, T, E, k, kind):
+    _check_dispatch(M, make_ids(T, E, k, seed=T + E, kind=kind).numpy(), E)
+
+
+def test_dispatch_large_multi_tile(M):
+    # R = 1.05M entries -> 256 tiles of 4096 entries (tile size doubling path)
+    _check_dispatch(M, make_ids(131072, 16, 8, seed=1, kind="skewed").numpy(), 16)
+
+
+def test_dispatch_check_routing(M):
+    ids = torch.tensor([[0, 1], [2, 2], [3, 0]], dtype=torch.int32, device=DEV)
+    d = M.dispatch_build(ids, 4, check_routing=True)
+    torch.cuda.synchronize()
+    assert int(d.status.item()) == 5
+    ok = M.dispatch_build(torch.tensor([[0, 1], [2, 3]], dtype=torch.int32, device=DEV), 4, check_routing=True)
+    torch.cuda.synchronize()
+    assert int(ok.status.item()) == 0
+
+
+# ------------------------------------------------------------------ K1 routing
+@pytest.mark.parametrize("T,d,E,k,dtype,renorm", [
+    (256, 64, 4, 2, "fp32", False), (1000, 256, 8, 2, "bf16", False), (777, 512, 64, 6, "bf16", True),
+    (300, 128, 256, 16, "bf16", False), (33, 128, 16, 1, "bf16", False),
+])
+def test_route(M, T, d, E, k, dtype, renorm):
+    inp = make_inputs(T, d, 128, E, k, dtype=dtype, seed=T, device=DEV, with_dy=False)
+    logits, ids, w = M.route(inp["x"], inp["w_gate"], k, renorm)
+    torch.cuda.synchronize()
+    ref = O.route(f64(inp["x"]), f64(inp["w_gate"]), k, renorm)
+    assert normwise(logits, ref["logits"]) < (FP32_TOL if dtype == "fp32" else 1e-5)
+    # ids bit-exact vs the oracle's top-k on the GPU's own fp32 logits (reading #4)
+    p, rids, rw = O.topk_from_logits(f64(logits), k, renorm)
+    assert np.array_equal(i64(ids), rids)
+    assert np.abs(f64(w) - rw).max() < 1e-5
+
+
+# ------------------------------------------------------------------ whole layer
+LAYER_CASES = [
+    # name, T, d, h, E, k, dtype, renorm, routing
+    ("tiny_fp32", 256, 64, 128, 4, 2, "fp32", False, "balanced"),
+    ("tiny_fp32_renorm", 200, 64, 96, 6, 3, "fp32", True, "skewed"),
+    ("small_bf16", 512, 256, 384, 8, 2, "bf16", False, "balanced"),
+    ("ragged_bf16", 1000, 128, 256, 16, 6, "bf16", True, "skewed"),
+    ("degenerate_bf16", 300, 128, 128, 8, 2, "bf16", False, "degenerate"),
+    ("k1_bf16", 333, 256, 256, 4, 1, "bf16", False, "balanced"),
+]
+
+
+def _run_layer(M, T, d, h, E, k, dtype, renorm, routing, seed=0):
+    inp = make_inputs(T, d, h, E, k, dtype=dtype, seed=seed, routing=routing, device=DEV)
+    x, wg, w1, w2, w3, dy = (inp[n] for n in ("x", "w_gate", "w1", "w2", "w3", "dy"))
+    logits, ids, w = M.route(x, wg, k, renorm)
+    disp = M.dispatch_build(ids, E, dtype=x.dtype)
+    y, a, b = M.ffn_fwd(x, w1, w2, w3, w, disp, renorm)
+    a0, b0 = a.clone(), b.clone()
+    g = M.ffn_bwd(dy, x, w1, w2, w3, w, disp, a, b, w_gate=wg, logits=logits, renormalize=renorm)
+    torch.cuda.synchronize()
+    out = dict(logits=logits, ids=ids, w=w, y=y, A=a0, B=b0, dA=a, dB=b, disp=disp, **g)
+    return inp, out
+
+
+@pytest.mark.parametrize("case", LAYER_CASES, ids=[c[0] for c in LAYER_CASES])
+def test_layer_fwd_bwd_parity(M, case):
+    name, T, d, h, E, k, dtype, renorm, routing = case
+    inp, out = _run_layer(M, T, d, h, E, k, dtype, renorm, routing)
+    tol = FP32_TOL if dtype == "fp32" else BF16_TOL
+    X, WG, W1, W2, W3, DY = (f64(inp[n]) for n in ("x", "w_gate", "w1", "w2", "w3", "dy"))
+    fwd = O.layer_forward(X, WG, W1, W2, W3, k, renorm, logits=f64(out["logits"]))
+    assert np.array_equal(i64(out["ids"]), fwd["ids"])
+    bwd = O.layer_backward(fwd, DY, X, WG, W1, W2, W3, renorm)
+    for key in ("offs", "eti"):
+        assert np.array_equal(i64(getattr(out["disp"], key)), fwd["disp"][key])
+    errs = {
+        "A": normwise(out["A"], fwd["A"]), "B": normwise(out["B"], fwd["B"]), "y": normwise(out["y"], fwd["y"]),
+        "dA": normwise(out["dA"], bwd["dA"]), "dB": normwise(out["dB"], bwd["dB"]),
+        "dg": normwise(out["dg"], bwd["dg"]), "dx": normwise(out["dx"], bwd["dx"]),
+        "dw1": normwise(out["dw1"], bwd["dw1"]), "dw2": normwise(out["dw2"], bwd["dw2"]),
+        "dw3": normwise(out["dw3"], bwd["dw3"]), "dw_gate": normwise(out["dw_gate"], bwd["dw_gate"]),
+    }
+    bad = {kk: v for kk, v in errs.items() if not v <= tol}
+    assert not bad, (name, errs)
+    if routing == "degenerate":
+        # experts k..E-1 got no rows: their weight grads are exact zeros
+        assert torch.count_nonzero(out["dw1"][k:]).item() == 0
+        assert torch.count_nonzero(out["dw3"][k:]).item() == 0
+
+
+def test_zero_tokens(M):
+    x = torch.empty(0, 128, dtype=torch.bfloat16, device=DEV)
+    inp = make_inputs(4, 128, 128, 4, 2, dtype="bf16", device=DEV)
+    logits, ids, w = M.route(x, inp["w_gate"], 2)
+    disp = M.dispatch_build(ids, 4)
+    y, a, b = M.ffn_fwd(x, inp["w1"], inp["w2"], inp["w3"], w, disp)
+    g = M.ffn_bwd(torch.empty_like(x), x, inp["w1"], inp["w2"], inp["w3"], w, disp, a, b, w_gate=inp["w_gate"],
+                  logits=logits)
+    torch.cuda.synchronize()
+    assert disp.offs.tolist() == [0, 0, 0, 0, 0]
+    assert y.shape == (0, 128)
+    for n in ("dw1", "dw2", "dw3", "dw_gate"):
+        assert torch.count_nonzero(g[n]).item() == 0
+
+
+def test_autograd_layer_matches_functional(M):
+    inp = make_inputs(256, 128, 256, 8, 2, dtype="bf16", seed=3, device=DEV)
+    x = inp["x"].clone().requires_grad_(True)
+    params = [inp[n].clone().requires_grad_(True) for n in ("w_gate", "w1", "w2", "w3")]
+    y = M.moe_layer(x, *params, 2)
+    y.backward(inp["dy"])
+    _, out = _run_layer(M, 256, 128, 256, 8, 2, "bf16", False, "balanced", seed=3)
+    assert torch.equal(y, out["y"])
+    assert torch.equal(x.grad, out["dx"])
+    assert torch.equal(params[1].grad, out["dw1"])
