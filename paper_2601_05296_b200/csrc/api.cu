@@ -165,7 +165,8 @@ moe_status moe_ffn_bwd(const moe_problem* p, const void* dy, const void* x, cons
   moe_status s = validate(p);
   if (s != MOE_OK) return s;
   if (!disp || !dw1 || !dw2 || !dw3 || !w1 || !w2 || !w3) return MOE_ERR_INVALID_ARG;
-  if (router && (!router->w_gate || !router->logits || !router->topk_ids || !router->dw_gate)) return MOE_ERR_INVALID_ARG;
+  if (router && (!router->w_gate || !router->dw_gate)) return MOE_ERR_INVALID_ARG;
+  if (router && p->T > 0 && (!router->logits || !router->topk_ids)) return MOE_ERR_INVALID_ARG;
   if (p->T > 0 && (!dy || !x || !dx || !topk_w || !a_save || !b_save || !ws || !disp->expert_offsets ||
                    !disp->expert_token_indices || !disp->token_index_map || !disp->row_slot))
     return MOE_ERR_INVALID_ARG;
