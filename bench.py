@@ -1,0 +1,403 @@
+#!/usr/bin/env python
+"""bench.py — MoEBlaze MoE layer forward+backward throughput on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload mixtral] [--impl ours|reference]
+
+Metric (BASELINE.json): MoE layer fwd+bwd tokens/s per B200 (1/2/4/8 GPU);
+peak activation GB.  One step = route -> dispatch build -> expert forward ->
+expert backward incl. router backward on one batch
+of synthetic, seeded inputs already resident in HBM.  N = 1 runs the
+Mixtral-like layer (BASELINE.json configs[1]); N > 1 runs the same per-GPU
+workload expert-parallel over NCCL all-to-all (weak scaling).
+
+Prints ONE JSON line on rank 0.  See DESIGN.md §Measurement for every key.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MoE layer fwd+bwd tokens/s per B200 (1/2/4/8 GPU); peak activation GB"
+UNIT = "tokens/s"
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+
+# algorithmic flops of each expert GEMM kind, in units of R*d*h
+GEMM_FLOP_FACTOR = {"FWD_UP": 4, "FWD_DOWN": 2, "BWD_DH": 2, "BWD_DX": 4, "DW3": 2, "DW12": 4}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        d["source"] = "measured"
+        return d
+    return dict(FALLBACK_PEAKS)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index=0):
+        self.rows = []
+        self.proc = None
+        self.gpu = gpu_index
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            parts = [s.strip() for s in ln.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        rows = self.rows
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        loaded = [s for s in sm if mx and s > 0.5 * max(mx)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows),
+                "power_w_max": max((float(r[3]) for r in rows if r[3].replace(".", "").isdigit()), default=None)}
+
+
+# ------------------------------------------------------------------------------------------ oracle timing
+def oracle_tokens_per_s(inp_host, cfg, budget_s=15.0, min_tokens=16, fixed_tokens=None):
+    """Time the fp64 oracle (as it stands) on a bounded token sample of the
+    workload, full weights.  Returns (tokens/s, sample tokens, seconds, threads)."""
+    import numpy as np
+    import oracle as O
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max((i.get("num_threads", 1) for i in threadpool_info()), default=os.cpu_count())
+    except Exception:
+        threads = os.cpu_count()
+    X, WG, W1, W2, W3, DY = (inp_host[n] for n in ("x", "w_gate", "w1", "w2", "w3", "dy"))
+    k = cfg.k
+
+    def run(S):
+        t0 = time.perf_counter()
+        fwd = O.layer_forward(X[:S], WG, W1, W2, W3, k)
+        O.layer_backward(fwd, DY[:S], X[:S], WG, W1, W2, W3)
+        return time.perf_counter() - t0
+
+    if fixed_tokens:
+        S = min(fixed_tokens, cfg.T)
+        t = run(S)
+        return S / t, S, t, threads
+    S = min(min_tokens, cfg.T)
+    t = run(S)
+    while t < budget_s / 4 and S < cfg.T:
+        S = min(cfg.T, max(S * 2, int(S * budget_s / max(t, 1e-3) * 0.5)))
+        t = run(S)
+    return S / t, S, t, threads
+
+
+def host_f64(inp):
+    import numpy as np
+    return {n: v.detach().to("cpu", torch.float32).numpy().astype(np.float64) for n, v in inp.items()}
+
+
+# ------------------------------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="mixtral")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--renormalize", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-memory", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=15.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    global torch
+    import torch
+    import torch.distributed as dist
+    from moe_inputs import CONFIGS
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = CONFIGS[args.workload]
+
+    if args.impl == "reference":
+        return run_reference(args, cfg, rank, world)
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2601_05296_b200 import build as B
+    if rank == 0 or world == 1:
+        B.build()
+    if world > 1:
+        dist.barrier()
+    import paper_2601_05296_b200 as M
+    from paper_2601_05296_b200 import _lib as L
+    from moe_inputs import make_inputs
+
+    inp = make_inputs(cfg.T, cfg.d, cfg.h, cfg.E, cfg.k, dtype=cfg.dtype, seed=rank, device=dev)
+    torch.cuda.synchronize()
+    k = cfg.k
+    x, wg, w1, w2, w3, dy = (inp[n] for n in ("x", "w_gate", "w1", "w2", "w3", "dy"))
+    renorm = args.renormalize
+
+    if world > 1:
+        from paper_2601_05296_b200.ep import ExpertParallelMoE
+        ep = ExpertParallelMoE(cfg.E, k, renorm, group=None)
+        # each rank keeps only its experts' weights
+        lo, hi = ep.local_experts
+        w1, w2, w3 = w1[lo:hi].contiguous(), w2[lo:hi].contiguous(), w3[lo:hi].contiguous()
+        dist.broadcast(wg, 0)
+
+        def step():
+            return ep.step(x, wg, w1, w2, w3, dy)
+    else:
+        def step():
+            logits, ids, w = M.route(x, wg, k, renorm)
+            disp = M.dispatch_build(ids, cfg.E, dtype=x.dtype)
+            y, a, b = M.ffn_fwd(x, w1, w2, w3, w, disp, renorm)
+            g = M.ffn_bwd(dy, x, w1, w2, w3, w, disp, a, b, w_gate=wg, logits=logits, renormalize=renorm)
+            return y, g
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    # ----------------------------------------------------------------- timed region (device-resident inputs)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    L.profile_reset()
+    L.profile_enable(True)
+    launches0 = L.launch_count()
+    st = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0.record(st)
+    for _ in range(args.steps):
+        step()
+    ev1.record(st)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    L.profile_enable(False)
+    launches = L.launch_count() - launches0
+    ms = ev0.elapsed_time(ev1)
+    prof = L.profile_read()
+    clk = clocks.stop()
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = world * cfg.T / (ms_step / 1e3)
+
+    # ----------------------------------------------------------------- roofline of the dominant kernel
+    peaks = load_peaks()
+    R = cfg.T * k if world == 1 else None
+    roof = None
+    gemm_total_ms = sum(v[0] for v in prof.values()) / args.steps
+    if world == 1:
+        dom = max(prof, key=lambda n: prof[n][0])
+        tot_ms, n_l = prof[dom]
+        flops = GEMM_FLOP_FACTOR[dom] * R * cfg.d * cfg.h
+        achieved = flops / (tot_ms / n_l / 1e3) / 1e12
+        peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            traffic = json.load(open(tp)).get(args.workload, {}).get(dom)
+        all_flops = 18 * R * cfg.d * cfg.h
+        roof = {"bound": "tensor", "kernel": f"tc_gemm_kernel<{dom}>", "achieved": round(achieved, 1),
+                "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                "peak_source": f"{peaks['source']} bf16 sustained (kernel timed inside the step)",
+                "frac_of_burst": round(achieved / peaks["bf16_tflops"], 4),
+                "flops_per_launch": flops, "avg_launch_ms": round(tot_ms / n_l, 4),
+                "share_of_step": round(tot_ms / args.steps / ms_step, 4),
+                "per_kernel_ms": {n: round(v[0] / max(v[1], 1), 4) for n, v in prof.items()},
+                "all_gemms": {"achieved": round(all_flops / (gemm_total_ms / 1e3) / 1e12, 1),
+                              "ms_per_step": round(gemm_total_ms, 4),
+                              "frac": round(all_flops / (gemm_total_ms / 1e3) / 1e12 / peak, 4)}}
+
+    # ----------------------------------------------------------------- e2e through the public API (autograd layer)
+    e2e = None
+    if world == 1:
+        x_h = x.detach().cpu().pin_memory()
+        dy_h = dy.detach().cpu().pin_memory()
+        y_h = torch.empty_like(x_h).pin_memory()
+        dx_h = torch.empty_like(x_h).pin_memory()
+        params = [torch.nn.Parameter(t) for t in (wg, w1, w2, w3)]
+
+        def e2e_step():
+            xd = x_h.to(dev, non_blocking=True).requires_grad_(True)
+            dyd = dy_h.to(dev, non_blocking=True)
+            for p in params:
+                p.grad = None
+            y = M.moe_layer(xd, *params, k, renorm)
+            y.backward(dyd)
+            y_h.copy_(y.detach(), non_blocking=True)
+            dx_h.copy_(xd.grad, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(st)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / args.steps
+        e2e = {"value": round(cfg.T / (ems / 1e3), 1), "unit": UNIT, "ms_per_step": round(ems, 4),
+               "h2d_bytes_per_step": 2 * x.numel() * x.element_size(),
+               "d2h_bytes_per_step": 2 * x.numel() * x.element_size(),
+               "api": "paper_2601_05296_b200.moe_layer (autograd) from pinned host X, dY; Y and dX read back"}
+
+    # ----------------------------------------------------------------- activation memory (P:289 method)
+    mem = None
+    if world == 1 and not args.no_memory:
+        mem = measure_memory(M, x, wg, w1, w2, w3, dy, k, renorm)
+
+    # ----------------------------------------------------------------- CPU oracle baseline (rank 0, N = 1)
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            host = host_f64({n: inp[n] for n in ("x", "w_gate", "w1", "w2", "w3", "dy")})
+            tps, S, secs, threads = oracle_tokens_per_s(host, cfg, budget_s=args.cpu_budget_s)
+            cpu = {"value": round(tps, 3), "unit": UNIT, "cores": threads, "kind": "oracle",
+                   "sample": f"{S} of {cfg.T} tokens of the {cfg.name} layer, full weights, fwd+bwd incl. router, "
+                             f"fp64 NumPy, {secs:.1f} s", "host_cpus": os.cpu_count()}
+            del host
+        except Exception as exc:  # report, never fake
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "error": repr(exc)[:300]}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded, moe_inputs)",
+            "config": {"workload": cfg.name, "T_per_gpu": cfg.T, "d": cfg.d, "h": cfg.h, "E": cfg.E, "k": cfg.k,
+                       "renormalize": renorm,
+                       "parallelism": "single-GPU" if world == 1 else f"ep{world}",
+                       "l2": "no flush: inputs larger than L2 (weights %.2f GB + X %.0f MB vs 126 MB L2)" % (
+                           3 * w1.numel() * 2 * (world if world > 1 else 1) / 1e9, x.numel() * 2 / 1e6)},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "gpu_launches_per_step": launches / args.steps, "clocks": clk,
+            "peak_activation_gb": mem["ours"]["peak_gb"] if mem else None, "memory": mem,
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def measure_memory(M, x, wg, w1, w2, w3, dy, k, renorm):
+    """Saved-activation bytes via autograd saved-tensor hooks, deduped by
+    storage and excluding parameters, plus the peak allocation delta over one
+    fwd+bwd — for our layer and for the materialise-everything baseline."""
+    import torch
+    from materialized_baseline import materialized_moe
+
+    def one(fn):
+        params = [torch.nn.Parameter(t.detach().clone()) for t in (wg, w1, w2, w3)]
+        pids = {p.untyped_storage().data_ptr() for p in params}
+        xd = x.detach().clone().requires_grad_(True)
+        seen = {}
+
+        def pack(t):
+            s = t.untyped_storage()
+            if s.data_ptr() not in pids:
+                seen[s.data_ptr()] = s.nbytes()
+            return t
+
+        torch.cuda.synchronize()
+        base = torch.cuda.memory_allocated()
+        torch.cuda.reset_peak_memory_stats()
+        with torch.autograd.graph.saved_tensors_hooks(pack, lambda t: t):
+            y = fn(xd, *params)
+        y.backward(dy)
+        torch.cuda.synchronize()
+        peak = torch.cuda.max_memory_allocated() - base
+        return {"saved_gb": round(sum(seen.values()) / 1e9, 4), "peak_gb": round(peak / 1e9, 4)}
+
+    out = {"method": "torch.autograd.graph.saved_tensors_hooks, unique storages excl. parameters (P:289); "
+                     "peak = max_memory_allocated delta over fwd+bwd"}
+    out["ours"] = one(lambda xx, a, b, c, d_: M.moe_layer(xx, a, b, c, d_, k, renorm))
+    try:
+        out["materialized_baseline"] = one(lambda xx, a, b, c, d_: materialized_moe(xx, a, b, c, d_, k, renorm))
+        out["saved_ratio"] = round(out["materialized_baseline"]["saved_gb"] / out["ours"]["saved_gb"], 3)
+    except Exception as exc:
+        out["materialized_baseline"] = {"error": repr(exc)[:300]}
+    return out
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the fp64 CPU oracle (this tier's reference arm), rank 0 only."""
+    if rank != 0:
+        return
+    import torch
+    from moe_inputs import make_inputs
+    inp = make_inputs(cfg.T, cfg.d, cfg.h, cfg.E, cfg.k, dtype=cfg.dtype, seed=0, device="cpu")
+    host = host_f64(inp)
+    # per-step sample sized so the whole W + K run stays within ~3 minutes
+    budget = 150.0 / (args.steps + args.warmup)
+    _, S, t, threads = oracle_tokens_per_s(host, cfg, budget_s=budget)
+    for _ in range(args.warmup):
+        oracle_tokens_per_s(host, cfg, fixed_tokens=S)
+    times = []
+    for _ in range(args.steps):
+        times.append(oracle_tokens_per_s(host, cfg, fixed_tokens=S)[2])
+    tot = sum(times)
+    value = S * args.steps / tot
+    out = {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * tot / args.steps, 2),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded, moe_inputs)",
+           "config": {"workload": cfg.name, "T_per_gpu": cfg.T, "d": cfg.d, "h": cfg.h, "E": cfg.E, "k": cfg.k},
+           "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": threads, "kind": "oracle",
+                            "sample": f"{S} of {cfg.T} tokens per step, full weights, fwd+bwd incl. router, "
+                                      "fp64 NumPy oracle"},
+           "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

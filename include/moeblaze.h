@@ -166,6 +166,17 @@ moe_status moe_gather_rows(const void* src, int64_t n_src, const int32_t* index,
 moe_status moe_combine_rows(const moe_problem* p, const void* rows, const int32_t* token_index_map,
                             void* out, void* stream);
 
+/* Bench instrumentation.  While enabled, every expert-GEMM launch is
+ * bracketed by two CUDA events recorded on the launch stream.
+ * moe_profile_read returns, for one GEMM kind (0 FWD_UP: A,B = X W1, X W2 +
+ * SwiGLU; 1 FWD_DOWN: U W3 + combine; 2 BWD_DH: dY W3^T + SwiGLU bwd;
+ * 3 BWD_DX: [dA|dB][W1;W2]; 4 DW3; 5 DW12), the summed event time in ms and
+ * the number of launches since the last reset (it waits for those events).
+ * Not thread-safe; off by default. */
+moe_status moe_profile_enable(int32_t on);
+moe_status moe_profile_reset(void);
+moe_status moe_profile_read(int32_t kind, double* total_ms, int64_t* launches);
+
 /* Human-readable status. */
 const char* moe_status_string(moe_status s);
 

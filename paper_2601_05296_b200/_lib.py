@@ -20,7 +20,9 @@ MOE_BF16, MOE_FP32 = 0, 1
 MOE_OP_ROUTE, MOE_OP_DISPATCH, MOE_OP_FFN_FWD, MOE_OP_FFN_BWD = 0, 1, 2, 3
 
 EXPORTS = ("moe_workspace_size", "moe_route", "moe_dispatch_build", "moe_ffn_fwd", "moe_ffn_bwd",
-           "moe_gather_rows", "moe_combine_rows", "moe_status_string", "moe_launch_count", "moe_version")
+           "moe_gather_rows", "moe_combine_rows", "moe_status_string", "moe_launch_count", "moe_version",
+           "moe_profile_enable", "moe_profile_reset", "moe_profile_read")
+GEMM_KINDS = ("FWD_UP", "FWD_DOWN", "BWD_DH", "BWD_DX", "DW3", "DW12")
 
 
 class MoeProblem(ctypes.Structure):
@@ -72,6 +74,10 @@ def load():
     lib.moe_status_string.restype = ctypes.c_char_p
     lib.moe_launch_count.restype = ctypes.c_uint64
     lib.moe_version.restype = I32
+    lib.moe_profile_enable.argtypes = [I32]
+    lib.moe_profile_read.argtypes = [I32, P(ctypes.c_double), P(I64)]
+    for fn in ("moe_profile_enable", "moe_profile_reset", "moe_profile_read"):
+        getattr(lib, fn).restype = I32
     _lib = lib
     return lib
 
@@ -158,3 +164,21 @@ def moe_gather_rows(src, index, dst, stream=None):
 def moe_combine_rows(p, rows, token_index_map, out, stream=None):
     _check(load().moe_combine_rows(ctypes.byref(p), _ptr(rows), _ptr(token_index_map), _ptr(out), _stream(stream)),
            "moe_combine_rows")
+
+
+def profile_enable(on=True):
+    _check(load().moe_profile_enable(int(bool(on))), "moe_profile_enable")
+
+
+def profile_reset():
+    _check(load().moe_profile_reset(), "moe_profile_reset")
+
+
+def profile_read():
+    """{kind name: (total_ms, launches)} for the six expert-GEMM kinds."""
+    out = {}
+    for i, name in enumerate(GEMM_KINDS):
+        ms, n = ctypes.c_double(0), ctypes.c_int64(0)
+        _check(load().moe_profile_read(i, ctypes.byref(ms), ctypes.byref(n)), "moe_profile_read")
+        out[name] = (ms.value, n.value)
+    return out

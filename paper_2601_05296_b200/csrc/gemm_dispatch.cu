@@ -1,4 +1,7 @@
-// gemm_dispatch.cu — routes each expert GEMM to its kernel family.
+// gemm_dispatch.cu — routes each expert GEMM to its kernel family, and the
+// optional per-launch CUDA-event instrumentation used by bench.py.
+#include <vector>
+
 #include "gemm.h"
 
 namespace moeb {
@@ -10,8 +13,65 @@ int tc_dg_parts(int h);
 
 int gemm_dg_parts(const GemmCall& c) { return c.bf16 ? tc_dg_parts(c.h) : simt_dg_parts(c.h); }
 
+namespace {
+struct ProfRec { int kind; cudaEvent_t a, b; };
+bool g_prof = false;
+std::vector<ProfRec> g_recs;
+std::vector<cudaEvent_t> g_pool;
+cudaEvent_t take_event() {
+  if (!g_pool.empty()) { cudaEvent_t e = g_pool.back(); g_pool.pop_back(); return e; }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+}  // namespace
+
 moe_status run_gemm(const GemmCall& c, cudaStream_t st) {
-  return c.bf16 ? tc_gemm(c, st) : simt_gemm(c, st);
+  if (!g_prof) return c.bf16 ? tc_gemm(c, st) : simt_gemm(c, st);
+  ProfRec r{c.which, take_event(), take_event()};
+  cudaEventRecord(r.a, st);
+  moe_status s = c.bf16 ? tc_gemm(c, st) : simt_gemm(c, st);
+  cudaEventRecord(r.b, st);
+  g_recs.push_back(r);
+  return s;
 }
 
 }  // namespace moeb
+
+using namespace moeb;
+
+extern "C" {
+
+moe_status moe_profile_enable(int32_t on) {
+  g_prof = on != 0;
+  return MOE_OK;
+}
+
+moe_status moe_profile_reset(void) {
+  for (auto& r : g_recs) {
+    cudaEventSynchronize(r.b);
+    g_pool.push_back(r.a);
+    g_pool.push_back(r.b);
+  }
+  g_recs.clear();
+  return MOE_OK;
+}
+
+moe_status moe_profile_read(int32_t kind, double* total_ms, int64_t* launches) {
+  if (!total_ms || !launches) return MOE_ERR_INVALID_ARG;
+  double t = 0;
+  int64_t n = 0;
+  for (auto& r : g_recs) {
+    if (r.kind != kind) continue;
+    float ms = 0.f;
+    if (cudaEventSynchronize(r.b) != cudaSuccess) return MOE_ERR_CUDA;
+    if (cudaEventElapsedTime(&ms, r.a, r.b) != cudaSuccess) return MOE_ERR_CUDA;
+    t += ms;
+    ++n;
+  }
+  *total_ms = t;
+  *launches = n;
+  return MOE_OK;
+}
+
+}  // extern "C"

@@ -26,6 +26,7 @@
 // zeros: this zero-pads the K tail of the weight-gradient GEMMs in shared
 // memory only (no padded buffer exists in HBM).
 #include <cudaTypedefs.h>
+#include <cstdlib>
 
 #include "gemm.h"
 #include "ptx.cuh"
@@ -39,10 +40,13 @@ constexpr int TSTAGES = 4;
 constexpr int TA_BYTES = TBM * TBK * 2;   // 16 KB
 constexpr int TB_BYTES = TBN * TBK * 2;   // 32 KB
 constexpr int TSTAGE_BYTES = TA_BYTES + TB_BYTES;
-constexpr int TC_THREADS = 256;
+constexpr int TC_THREADS = 384;   // 12 warps: 0 TMA, 1 MMA, 2 TMEM, 4-7 epilogue, 8-11 cp.async gathers
+constexpr int GATHER_THREADS = 128;
 constexpr int TC_SMEM = TSTAGES * TSTAGE_BYTES + 1024 /*align*/ + 1024 /*barriers*/ + 2 * 260 * 4;
 
 struct TcParams {
+  const __nv_bfloat16* x;   // gathered operand sources for the cp.async path
+  const __nv_bfloat16* dy;
   const int32_t* offs;
   const int32_t* eti;
   const int32_t* row_slot;
@@ -65,6 +69,13 @@ struct KindTraits {
   static constexpr bool a_mn = wgrad;                                     // A operand MN-major?
   static constexpr bool b_mn = (KIND == TC_BWD_DH || KIND == TC_BWD_DX || wgrad);
   static constexpr int NT = (KIND == TC_FWD_UP) ? 128 : 256;             // output columns per tile
+  static constexpr bool gather_a = (KIND == TC_FWD_UP || KIND == TC_BWD_DH || KIND == TC_DW3);
+  static constexpr bool gather_b = (KIND == TC_DW12);
+  // bytes per stage delivered by TMA tile loads (the rest comes from row gathers)
+  __host__ __device__ static constexpr uint32_t tile_bytes(bool cpa) {
+    return cpa ? ((gather_a ? 0u : (uint32_t)TA_BYTES) + (gather_b ? 0u : (uint32_t)TB_BYTES))
+               : (uint32_t)TSTAGE_BYTES;
+  }
   static constexpr uint32_t IDESC = ptx::umma_idesc_bf16(TBM, TBN, a_mn ? 1 : 0, b_mn ? 1 : 0);
 };
 
@@ -129,7 +140,7 @@ __device__ __forceinline__ void load_bf16x32(const __nv_bfloat16* src, float* v)
   }
 }
 
-template <int KIND>
+template <int KIND, bool CPA>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
                const __grid_constant__ CUtensorMap mB0, const __grid_constant__ CUtensorMap mB1, const TcParams P) {
@@ -156,7 +167,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < TSTAGES; ++s) {
-      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&full[s], 1 + ((CPA && (K::gather_a || K::gather_b)) ? GATHER_THREADS : 0));
       ptx::mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
@@ -189,7 +200,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
     TileInfo t;
     for (int tile = blockIdx.x; decode_tile<KIND>(tile, P, s_offs, s_tstart, t); tile += gridDim.x) {
       int gi0 = 0, gi1 = 0, gi2 = 0, gi3 = 0;
-      if constexpr (KIND == TC_FWD_UP || KIND == TC_BWD_DH) {
+      if constexpr (!CPA && (KIND == TC_FWD_UP || KIND == TC_BWD_DH)) {
         const int r = t.m0 + 4 * lane;
         gi0 = r + 0 < t.seg1 ? P.eti[r + 0] : oob;
         gi1 = r + 1 < t.seg1 ? P.eti[r + 1] : oob;
@@ -201,18 +212,18 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
         uint8_t* sA = smem + stage * TSTAGE_BYTES;
         uint8_t* sB = sA + TA_BYTES;
         uint64_t* bar = &full[stage];
-        if (lane == 0) ptx::mbar_arrive_expect_tx(bar, TSTAGE_BYTES);
+        if (lane == 0) ptx::mbar_arrive_expect_tx(bar, K::tile_bytes(CPA));
         __syncwarp();
         const int k0 = kb * TBK;
         if constexpr (KIND == TC_FWD_UP) {
-          ptx::tma_gather4(sA + 512 * lane, &mA0, bar, k0, gi0, gi1, gi2, gi3);
+          if (!CPA) ptx::tma_gather4(sA + 512 * lane, &mA0, bar, k0, gi0, gi1, gi2, gi3);
           if (lane == 0) ptx::tma_load_2d(sB, &mB0, bar, k0, t.e * P.h + t.n0);
           if (lane == 1) ptx::tma_load_2d(sB + TB_BYTES / 2, &mB1, bar, k0, t.e * P.h + t.n0);
         } else if constexpr (KIND == TC_FWD_DOWN) {
           if (lane == 0) ptx::tma_load_2d(sA, &mA0, bar, k0, t.m0);
           if (lane == 1) ptx::tma_load_2d(sB, &mB0, bar, k0, t.e * P.d + t.n0);
         } else if constexpr (KIND == TC_BWD_DH) {
-          ptx::tma_gather4(sA + 512 * lane, &mA0, bar, k0, gi0, gi1, gi2, gi3);
+          if (!CPA) ptx::tma_gather4(sA + 512 * lane, &mA0, bar, k0, gi0, gi1, gi2, gi3);
           if (lane < 4) ptx::tma_load_2d(sB + lane * 8192, &mB0, bar, t.n0 + 64 * lane, t.e * P.d + k0);
         } else if constexpr (KIND == TC_BWD_DX) {
           const bool second = k0 >= P.h;
@@ -222,25 +233,29 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
             ptx::tma_load_2d(sB + (lane - 4) * 8192, second ? &mB1 : &mB0, bar, t.n0 + 64 * (lane - 4),
                              t.e * P.h + kk);
         } else if constexpr (KIND == TC_DW3) {
-          const int g = lane & 15, p = lane >> 4;
-          const int r = t.seg0 + k0 + 4 * g;
-          const int i0 = r + 0 < t.seg1 ? P.eti[r + 0] : oob;
-          const int i1 = r + 1 < t.seg1 ? P.eti[r + 1] : oob;
-          const int i2 = r + 2 < t.seg1 ? P.eti[r + 2] : oob;
-          const int i3 = r + 3 < t.seg1 ? P.eti[r + 3] : oob;
-          ptx::tma_gather4(sA + p * 8192 + g * 512, &mA0, bar, t.m0 + 64 * p, i0, i1, i2, i3);
+          if (!CPA) {
+            const int g = lane & 15, p = lane >> 4;
+            const int r = t.seg0 + k0 + 4 * g;
+            const int i0 = r + 0 < t.seg1 ? P.eti[r + 0] : oob;
+            const int i1 = r + 1 < t.seg1 ? P.eti[r + 1] : oob;
+            const int i2 = r + 2 < t.seg1 ? P.eti[r + 2] : oob;
+            const int i3 = r + 3 < t.seg1 ? P.eti[r + 3] : oob;
+            ptx::tma_gather4(sA + p * 8192 + g * 512, &mA0, bar, t.m0 + 64 * p, i0, i1, i2, i3);
+          }
           if (lane < 4) ptx::tma_load_2d(sB + lane * 8192, &mB0, bar, t.n0 + 64 * lane, t.seg0 + k0);
         } else {  // TC_DW12
-          const int g = lane & 15, ph = lane >> 4;
-          const int r = t.seg0 + k0 + 4 * g;
-          const int i0 = r + 0 < t.seg1 ? P.eti[r + 0] : oob;
-          const int i1 = r + 1 < t.seg1 ? P.eti[r + 1] : oob;
-          const int i2 = r + 2 < t.seg1 ? P.eti[r + 2] : oob;
-          const int i3 = r + 3 < t.seg1 ? P.eti[r + 3] : oob;
+          if (!CPA) {
+            const int g = lane & 15, ph = lane >> 4;
+            const int r = t.seg0 + k0 + 4 * g;
+            const int i0 = r + 0 < t.seg1 ? P.eti[r + 0] : oob;
+            const int i1 = r + 1 < t.seg1 ? P.eti[r + 1] : oob;
+            const int i2 = r + 2 < t.seg1 ? P.eti[r + 2] : oob;
+            const int i3 = r + 3 < t.seg1 ? P.eti[r + 3] : oob;
 #pragma unroll
-          for (int pp = 0; pp < 2; ++pp) {
-            const int p = 2 * ph + pp;
-            ptx::tma_gather4(sB + p * 8192 + g * 512, &mB0, bar, t.n0 + 64 * p, i0, i1, i2, i3);
+            for (int pp = 0; pp < 2; ++pp) {
+              const int p = 2 * ph + pp;
+              ptx::tma_gather4(sB + p * 8192 + g * 512, &mB0, bar, t.n0 + 64 * p, i0, i1, i2, i3);
+            }
           }
           const bool second = t.m0 >= P.h;
           if (lane >= 2 && lane < 4)
@@ -248,6 +263,64 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
                              (second ? t.m0 - P.h : t.m0) + 64 * (lane - 2), t.seg0 + k0);
         }
         if (++stage == TSTAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp >= 8) {
+    // ======================= cp.async row gathers (CPA) =======================
+    // 128 threads copy the gathered operand 16 B at a time straight into the
+    // 128B-swizzled UMMA layout (chunk c of smem row q lands at q*128 +
+    // ((c ^ (q & 7)) << 4)); rows outside the expert segment are zero-filled.
+    if constexpr (CPA && (K::gather_a || K::gather_b)) {
+      const int gt = threadIdx.x - 256;
+      int stage = 0;
+      uint32_t phase = 0;
+      TileInfo t;
+      const __nv_bfloat16* src_base = (KIND == TC_FWD_UP || KIND == TC_DW12) ? P.x : P.dy;
+      for (int tile = blockIdx.x; decode_tile<KIND>(tile, P, s_offs, s_tstart, t); tile += gridDim.x) {
+        int row_tok = -1;
+        if constexpr (KIND == TC_FWD_UP || KIND == TC_BWD_DH) {
+          const int r = t.m0 + gt;
+          row_tok = r < t.seg1 ? P.eti[r] : -1;
+        }
+        for (int kb = 0; kb < t.nk; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          const uint32_t sbase = ptx::smem_u32(smem + stage * TSTAGE_BYTES);
+          const int k0 = kb * TBK;
+          if constexpr (KIND == TC_FWD_UP || KIND == TC_BWD_DH) {
+            // K-major A: thread gt owns smem row gt (128 B = 8 chunks of the token row)
+            const __nv_bfloat16* src = src_base + (int64_t)(row_tok < 0 ? 0 : row_tok) * P.d + k0;
+            const uint32_t nb = row_tok < 0 ? 0u : 16u;
+            const uint32_t drow = sbase + gt * 128;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) ptx::cp_async16(drow + ((c ^ (gt & 7)) << 4), src + c * 8, nb);
+          } else {
+            // MN-major: smem row q = K index (gathered token), panels of 64 columns
+            const int q = gt & 63, half = gt >> 6;
+            const int r = t.seg0 + k0 + q;
+            const int tok = r < t.seg1 ? P.eti[r] : -1;
+            const __nv_bfloat16* src = src_base + (int64_t)(tok < 0 ? 0 : tok) * P.d;
+            if constexpr (KIND == TC_DW3) {
+              const int col = t.m0 + 64 * half;
+              const uint32_t nb = tok < 0 ? 0u : 16u;
+              const uint32_t drow = sbase + half * 8192 + q * 128;
+#pragma unroll
+              for (int c = 0; c < 8; ++c) ptx::cp_async16(drow + ((c ^ (q & 7)) << 4), src + col + c * 8, nb);
+            } else {
+#pragma unroll
+              for (int pp = 0; pp < 2; ++pp) {
+                const int p = 2 * half + pp;
+                const int col = t.n0 + 64 * p;
+                const uint32_t nb = (tok < 0 || col >= P.d) ? 0u : 16u;
+                const __nv_bfloat16* sp = nb ? src + col : src;
+                const uint32_t drow = sbase + TA_BYTES + p * 8192 + q * 128;
+#pragma unroll
+                for (int c = 0; c < 8; ++c) ptx::cp_async16(drow + ((c ^ (q & 7)) << 4), sp + (nb ? c * 8 : 0), nb);
+              }
+            }
+          }
+          ptx::cp_async_mbar_arrive(&full[stage]);
+          if (++stage == TSTAGES) { stage = 0; phase ^= 1; }
+        }
       }
     }
   } else if (warp == 1) {
@@ -263,6 +336,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
       const uint32_t d_tmem = tmem_base + as * TBN;
       for (int kb = 0; kb < t.nk; ++kb) {
         ptx::mbar_wait(&full[stage], phase);
+        if (CPA) ptx::fence_proxy_async();  // cp.async (generic proxy) writes -> tcgen05 operand reads
         ptx::tc_fence_after();
         if (lane == 0) {
           const uint32_t sA = ptx::smem_u32(smem + stage * TSTAGE_BYTES);
@@ -287,7 +361,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
       __syncwarp();
       if (++as == 2) { as = 0; aphase ^= 1; }
     }
-  } else if (warp >= 4) {
+  } else if (warp >= 4 && warp < 8) {
     // ============================ epilogue ============================
     const int wq = warp & 3;
     const int row = wq * 32 + lane;
@@ -460,20 +534,38 @@ static int num_sms() {
   return n;
 }
 
-template <int KIND>
-static moe_status launch_tc(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0,
-                            const CUtensorMap& b1, const TcParams& P, int64_t tiles_upper, cudaStream_t st) {
+// Row-gather engine: cp.async producer warps (default) or TMA tile::gather4
+// (MOEBLAZE_GATHER=tma; kept for the measured comparison in DESIGN.md).
+static bool use_cpasync() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MOEBLAZE_GATHER");
+    v = (e && e[0] == 't') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <int KIND, bool CPA>
+static moe_status launch_tc_impl(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0,
+                                 const CUtensorMap& b1, const TcParams& P, int grid, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(tc_gemm_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM) !=
+    if (cudaFuncSetAttribute(tc_gemm_kernel<KIND, CPA>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM) !=
         cudaSuccess)
       return MOE_ERR_CUDA;
     attr = true;
   }
+  MOE_LAUNCH((tc_gemm_kernel<KIND, CPA>), grid, TC_THREADS, TC_SMEM, st, a0, a1, b0, b1, P);
+  return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
+}
+
+template <int KIND>
+static moe_status launch_tc(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0,
+                            const CUtensorMap& b1, const TcParams& P, int64_t tiles_upper, cudaStream_t st) {
   if (tiles_upper <= 0) return MOE_OK;
   const int grid = (int)std::min<int64_t>(tiles_upper, num_sms());
-  MOE_LAUNCH(tc_gemm_kernel<KIND>, grid, TC_THREADS, TC_SMEM, st, a0, a1, b0, b1, P);
-  return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
+  if (use_cpasync()) return launch_tc_impl<KIND, true>(a0, a1, b0, b1, P, grid, st);
+  return launch_tc_impl<KIND, false>(a0, a1, b0, b1, P, grid, st);
 }
 
 int tc_dg_parts(int h) { return (int)ceil_div(h, TBN); }
@@ -483,6 +575,7 @@ moe_status tc_gemm(const GemmCall& c, cudaStream_t st) {
   const int64_t T = c.T, R = c.R;
   const int d = c.d, h = c.h, E = c.E;
   TcParams P{};
+  P.x = (const bf*)c.x; P.dy = (const bf*)c.dy;
   P.offs = c.offs; P.eti = c.eti; P.row_slot = c.row_slot; P.topw = c.topw;
   P.a_save = (bf*)c.a_save; P.b_save = (bf*)c.b_save; P.u = (bf*)c.u;
   P.acc_out = c.acc_out; P.dg_part = c.dg_part;
