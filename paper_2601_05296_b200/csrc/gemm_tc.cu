@@ -271,55 +271,64 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
     // 128B-swizzled UMMA layout (chunk c of smem row q lands at q*128 +
     // ((c ^ (q & 7)) << 4)); rows outside the expert segment are zero-filled.
     if constexpr (CPA && (K::gather_a || K::gather_b)) {
+      // Lane mapping: consecutive lanes copy consecutive 16-byte chunks of the
+      // same gathered row, so one warp instruction covers whole 128-byte lines.
       const int gt = threadIdx.x - 256;
       int stage = 0;
       uint32_t phase = 0;
       TileInfo t;
       const __nv_bfloat16* src_base = (KIND == TC_FWD_UP || KIND == TC_DW12) ? P.x : P.dy;
       for (int tile = blockIdx.x; decode_tile<KIND>(tile, P, s_offs, s_tstart, t); tile += gridDim.x) {
-        int row_tok = -1;
         if constexpr (KIND == TC_FWD_UP || KIND == TC_BWD_DH) {
-          const int r = t.m0 + gt;
-          row_tok = r < t.seg1 ? P.eti[r] : -1;
-        }
-        for (int kb = 0; kb < t.nk; ++kb) {
-          ptx::mbar_wait(&empty[stage], phase ^ 1);
-          const uint32_t sbase = ptx::smem_u32(smem + stage * TSTAGE_BYTES);
-          const int k0 = kb * TBK;
-          if constexpr (KIND == TC_FWD_UP || KIND == TC_BWD_DH) {
-            // K-major A: thread gt owns smem row gt (128 B = 8 chunks of the token row)
-            const __nv_bfloat16* src = src_base + (int64_t)(row_tok < 0 ? 0 : row_tok) * P.d + k0;
-            const uint32_t nb = row_tok < 0 ? 0u : 16u;
-            const uint32_t drow = sbase + gt * 128;
+          // K-major A, 128 rows x 8 chunks: thread -> chunk c = gt&7, rows q = (gt>>3) + 16 i
+          const int c = gt & 7, rb = gt >> 3;
+          const __nv_bfloat16* src[8];
+          uint32_t nb[8];
 #pragma unroll
-            for (int c = 0; c < 8; ++c) ptx::cp_async16(drow + ((c ^ (gt & 7)) << 4), src + c * 8, nb);
-          } else {
-            // MN-major: smem row q = K index (gathered token), panels of 64 columns
-            const int q = gt & 63, half = gt >> 6;
-            const int r = t.seg0 + k0 + q;
+          for (int i = 0; i < 8; ++i) {
+            const int r = t.m0 + rb + 16 * i;
             const int tok = r < t.seg1 ? P.eti[r] : -1;
-            const __nv_bfloat16* src = src_base + (int64_t)(tok < 0 ? 0 : tok) * P.d;
-            if constexpr (KIND == TC_DW3) {
-              const int col = t.m0 + 64 * half;
-              const uint32_t nb = tok < 0 ? 0u : 16u;
-              const uint32_t drow = sbase + half * 8192 + q * 128;
-#pragma unroll
-              for (int c = 0; c < 8; ++c) ptx::cp_async16(drow + ((c ^ (q & 7)) << 4), src + col + c * 8, nb);
-            } else {
-#pragma unroll
-              for (int pp = 0; pp < 2; ++pp) {
-                const int p = 2 * half + pp;
-                const int col = t.n0 + 64 * p;
-                const uint32_t nb = (tok < 0 || col >= P.d) ? 0u : 16u;
-                const __nv_bfloat16* sp = nb ? src + col : src;
-                const uint32_t drow = sbase + TA_BYTES + p * 8192 + q * 128;
-#pragma unroll
-                for (int c = 0; c < 8; ++c) ptx::cp_async16(drow + ((c ^ (q & 7)) << 4), sp + (nb ? c * 8 : 0), nb);
-              }
-            }
+            src[i] = src_base + (int64_t)(tok < 0 ? 0 : tok) * P.d + c * 8;
+            nb[i] = tok < 0 ? 0u : 16u;
           }
-          ptx::cp_async_mbar_arrive(&full[stage]);
-          if (++stage == TSTAGES) { stage = 0; phase ^= 1; }
+          for (int kb = 0; kb < t.nk; ++kb) {
+            ptx::mbar_wait(&empty[stage], phase ^ 1);
+            const uint32_t sbase = ptx::smem_u32(smem + stage * TSTAGE_BYTES);
+            const int k0 = kb * TBK;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int q = rb + 16 * i;
+              ptx::cp_async16(sbase + q * 128 + ((c ^ (q & 7)) << 4), src[i] + k0, nb[i]);
+            }
+            ptx::cp_async_mbar_arrive(&full[stage]);
+            if (++stage == TSTAGES) { stage = 0; phase ^= 1; }
+          }
+        } else {
+          // MN-major: smem row q = K index (a gathered token row); DW3 copies 2
+          // panels (256 B) of dY per row, DW12 4 panels (512 B) of X per row.
+          constexpr int CPR = (KIND == TC_DW3) ? 16 : 32;       // 16-byte chunks per row
+          constexpr int RPI = GATHER_THREADS / CPR;             // rows per pass
+          constexpr int NPASS = 64 / RPI;
+          const int cidx = gt % CPR, rb = gt / CPR;
+          const int p = cidx >> 3, cc = cidx & 7;
+          const int col = ((KIND == TC_DW3) ? t.m0 : t.n0) + 64 * p + cc * 8;
+          const bool col_ok = col < P.d;
+          const uint32_t dst_off = ((KIND == TC_DW3) ? 0u : (uint32_t)TA_BYTES) + p * 8192;
+          for (int kb = 0; kb < t.nk; ++kb) {
+            ptx::mbar_wait(&empty[stage], phase ^ 1);
+            const uint32_t sbase = ptx::smem_u32(smem + stage * TSTAGE_BYTES) + dst_off;
+            const int k0 = t.seg0 + kb * TBK;
+#pragma unroll
+            for (int i = 0; i < NPASS; ++i) {
+              const int q = rb + RPI * i;
+              const int r = k0 + q;
+              const int tok = (r < t.seg1 && col_ok) ? P.eti[r] : -1;
+              const __nv_bfloat16* sp = src_base + (int64_t)(tok < 0 ? 0 : tok) * P.d + (col_ok ? col : 0);
+              ptx::cp_async16(sbase + q * 128 + ((cc ^ (q & 7)) << 4), sp, tok < 0 ? 0u : 16u);
+            }
+            ptx::cp_async_mbar_arrive(&full[stage]);
+            if (++stage == TSTAGES) { stage = 0; phase ^= 1; }
+          }
         }
       }
     }
