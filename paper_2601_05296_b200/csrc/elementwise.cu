@@ -59,41 +59,52 @@ __global__ void router_bwd_kernel(const float* __restrict__ logits, const int32_
   }
 }
 
-// partial[c][e][col] = sum_{t in chunk c} dlogits[t,e] X[t,col]; block: 64 cols x 4 expert groups
-constexpr int WG_COLS = 64;
-template <typename T>
+// partial[c][e][col] = sum_{t in chunk c} dlogits[t,e] X[t,col].
+// Block: 256 columns (one per thread) x ET experts (registers) x one token chunk;
+// X is read exactly once over the grid (coalesced rows), dlogits tiles are
+// staged in shared memory and read as float4 broadcasts.
+constexpr int WG_COLS = 256;
+constexpr int WG_TT = 32;  // tokens per shared-memory tile
+template <typename T, int ET>
 __global__ void __launch_bounds__(256) dwg_partial_kernel(const float* __restrict__ dlogits, const T* __restrict__ x,
                                                           int64_t Tn, int d, int E, int64_t tch,
                                                           float* __restrict__ part) {
-  extern __shared__ float dl[];  // [32][E]
-  const int col = blockIdx.x * WG_COLS + (threadIdx.x & 63);
-  const int eg = threadIdx.x >> 6;  // 0..3
-  const int64_t ta = blockIdx.y * tch, tb = min64(ta + tch, Tn);
-  float acc[64];
+  __shared__ __align__(16) float dl[WG_TT][ET];
+  const int col = blockIdx.x * WG_COLS + threadIdx.x;
+  const int e0 = blockIdx.y * ET;
+  const int64_t ta = blockIdx.z * tch, tb = min64(ta + tch, Tn);
+  float acc[ET];
 #pragma unroll
-  for (int i = 0; i < 64; ++i) acc[i] = 0.f;
-  const int ne = (E - eg + 3) / 4;
-  for (int64_t t0 = ta; t0 < tb; t0 += 32) {
-    const int nt = (int)min64(32, tb - t0);
+  for (int i = 0; i < ET; ++i) acc[i] = 0.f;
+  for (int64_t t0 = ta; t0 < tb; t0 += WG_TT) {
+    const int nt = (int)min64(WG_TT, tb - t0);
     __syncthreads();
-    for (int i = threadIdx.x; i < 32 * E; i += 256) {
-      int r = i / E, e = i % E;
-      dl[i] = r < nt ? dlogits[(t0 + r) * E + e] : 0.f;
+    for (int i = threadIdx.x; i < WG_TT * ET; i += 256) {
+      const int r = i / ET, e = i % ET;
+      dl[r][e] = (r < nt && e0 + e < E) ? dlogits[(t0 + r) * E + e0 + e] : 0.f;
     }
     __syncthreads();
     if (col < d) {
-      for (int r = 0; r < nt; ++r) {
-        float xv = to_f32(x[(t0 + r) * d + col]);
+      float xv[WG_TT];
 #pragma unroll
-        for (int i = 0; i < 64; ++i)
-          if (i < ne) acc[i] = fmaf(dl[r * E + eg + 4 * i], xv, acc[i]);
+      for (int r = 0; r < WG_TT; ++r) xv[r] = r < nt ? to_f32(x[(t0 + r) * d + col]) : 0.f;
+#pragma unroll 4
+      for (int r = 0; r < WG_TT; ++r) {
+#pragma unroll
+        for (int e = 0; e < ET; e += 4) {
+          const float4 w = *reinterpret_cast<const float4*>(&dl[r][e]);
+          acc[e] = fmaf(w.x, xv[r], acc[e]);
+          acc[e + 1] = fmaf(w.y, xv[r], acc[e + 1]);
+          acc[e + 2] = fmaf(w.z, xv[r], acc[e + 2]);
+          acc[e + 3] = fmaf(w.w, xv[r], acc[e + 3]);
+        }
       }
     }
   }
   if (col < d) {
 #pragma unroll
-    for (int i = 0; i < 64; ++i)
-      if (i < ne) part[((int64_t)blockIdx.y * E + eg + 4 * i) * d + col] = acc[i];
+    for (int e = 0; e < ET; ++e)
+      if (e0 + e < E) part[((int64_t)blockIdx.z * E + e0 + e) * d + col] = acc[e];
   }
 }
 
@@ -168,12 +179,24 @@ moe_status launch_dg_reduce(const float* part, int nparts, const int32_t* tim, i
   return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
 }
 
+static int dwg_et(int E) { return E <= 8 ? 8 : (E <= 16 ? 16 : 32); }
+
 int dwg_chunks(int64_t T, int d) {
-  int64_t colb = ceil_div(d, WG_COLS);
-  int64_t nch = ceil_div(2 * 148, colb);
-  nch = std::max<int64_t>(1, min64(nch, 64));
-  nch = min64(nch, std::max<int64_t>(1, ceil_div(T, 32)));
-  return (int)nch;
+  // token chunks so that (column blocks x chunks) >= ~3 waves of 148 SMs, >= 128 tokens per chunk
+  const int64_t colb = ceil_div(d, WG_COLS);
+  int64_t nch = ceil_div(3 * 148, colb);
+  nch = std::min<int64_t>(nch, std::max<int64_t>(1, T / 128));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(nch, 256));
+}
+
+template <typename T>
+static void launch_dwg_partial(const float* dl, const T* x, int64_t Tn, int d, int E, int nch, int64_t tch, float* part,
+                               cudaStream_t st) {
+  const int et = dwg_et(E);
+  dim3 grid((unsigned)ceil_div(d, WG_COLS), (unsigned)ceil_div(E, et), nch);
+  if (et == 8) MOE_LAUNCH((dwg_partial_kernel<T, 8>), grid, 256, 0, st, dl, x, Tn, d, E, tch, part);
+  else if (et == 16) MOE_LAUNCH((dwg_partial_kernel<T, 16>), grid, 256, 0, st, dl, x, Tn, d, E, tch, part);
+  else MOE_LAUNCH((dwg_partial_kernel<T, 32>), grid, 256, 0, st, dl, x, Tn, d, E, tch, part);
 }
 
 moe_status launch_router_bwd(const moe_problem* p, const float* logits, const int32_t* ids, const float* dg,
@@ -186,14 +209,12 @@ moe_status launch_router_bwd(const moe_problem* p, const float* logits, const in
   }
   const int nch = dwg_chunks(T, d);
   const int64_t tch = ceil_div(std::max<int64_t>(T, 1), nch);
-  dim3 grid((unsigned)ceil_div(d, WG_COLS), nch);
-  size_t sm = sizeof(float) * 32 * E;
   const int64_t n = (int64_t)E * d;
   if (p->dtype == MOE_BF16) {
-    MOE_LAUNCH(dwg_partial_kernel<__nv_bfloat16>, grid, 256, sm, st, dlogits, (const __nv_bfloat16*)x, T, d, E, tch, dwg_part);
+    launch_dwg_partial<__nv_bfloat16>(dlogits, (const __nv_bfloat16*)x, T, d, E, nch, tch, dwg_part, st);
     MOE_LAUNCH(dwg_reduce_kernel<__nv_bfloat16>, (unsigned)ceil_div(n, 256), 256, 0, st, dwg_part, nch, n, (__nv_bfloat16*)dwg);
   } else {
-    MOE_LAUNCH(dwg_partial_kernel<float>, grid, 256, sm, st, dlogits, (const float*)x, T, d, E, tch, dwg_part);
+    launch_dwg_partial<float>(dlogits, (const float*)x, T, d, E, nch, tch, dwg_part, st);
     MOE_LAUNCH(dwg_reduce_kernel<float>, (unsigned)ceil_div(n, 256), 256, 0, st, dwg_part, nch, n, (float*)dwg);
   }
   return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;

@@ -33,7 +33,7 @@
 
 namespace moeb {
 
-enum TcKind { TC_FWD_UP = 0, TC_FWD_DOWN = 1, TC_BWD_DH = 2, TC_BWD_DX = 3, TC_DW3 = 4, TC_DW12 = 5 };
+enum TcKind { TC_FWD_UP = 0, TC_FWD_DOWN = 1, TC_BWD_DH = 2, TC_BWD_DX = 3, TC_DW3 = 4, TC_DW12 = 5, TC_ROUTE = 6 };
 
 constexpr int TBM = 128, TBN = 256, TBK = 64;
 constexpr int TSTAGES = 4;
@@ -61,6 +61,12 @@ struct TcParams {
   int T, d, h, E;
   int n_tiles, m_tiles;
   int dg_parts;
+  // TC_ROUTE (K1): logits = X Wg^T on tensor cores, softmax + top-k in the epilogue
+  float* logits;
+  int32_t* ids;
+  float* route_w;
+  int k, renorm, route_n;
+  uint32_t route_idesc;
 };
 
 template <int KIND>
@@ -87,7 +93,16 @@ template <int KIND>
 __device__ __forceinline__ bool decode_tile(int tile, const TcParams& P, const int* s_offs, const int* s_tstart,
                                             TileInfo& t) {
   using K = KindTraits<KIND>;
-  if constexpr (K::wgrad) {
+  if constexpr (KIND == TC_ROUTE) {
+    if (tile * TBM >= P.T) return false;
+    t.e = 0;
+    t.seg0 = 0;
+    t.seg1 = P.T;
+    t.m0 = tile * TBM;
+    t.n0 = 0;
+    t.n_tile = 0;
+    t.nk = P.d / TBK;
+  } else if constexpr (K::wgrad) {
     const int per_e = P.m_tiles * P.n_tiles;
     if (tile >= P.E * per_e) return false;
     t.e = tile / per_e;
@@ -158,7 +173,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int E = P.E;
 
-  for (int i = threadIdx.x; i <= E; i += TC_THREADS) s_offs[i] = P.offs[i];
+  if constexpr (KIND != TC_ROUTE)
+    for (int i = threadIdx.x; i <= E; i += TC_THREADS) s_offs[i] = P.offs[i];
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch(&mA0);
     ptx::tma_prefetch(&mA1);
@@ -179,7 +195,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
   }
   if (warp == 2) ptx::tmem_alloc(tmem_holder, 512);
   __syncthreads();
-  if (!K::wgrad && threadIdx.x == 0) {
+  if (!K::wgrad && KIND != TC_ROUTE && threadIdx.x == 0) {
     int s = 0;
     for (int e = 0; e < E; ++e) {
       s_tstart[e] = s;
@@ -212,10 +228,15 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
         uint8_t* sA = smem + stage * TSTAGE_BYTES;
         uint8_t* sB = sA + TA_BYTES;
         uint64_t* bar = &full[stage];
-        if (lane == 0) ptx::mbar_arrive_expect_tx(bar, K::tile_bytes(CPA));
+        if (lane == 0)
+          ptx::mbar_arrive_expect_tx(bar, KIND == TC_ROUTE ? (uint32_t)(TA_BYTES + P.route_n * 128)
+                                                           : K::tile_bytes(CPA));
         __syncwarp();
         const int k0 = kb * TBK;
-        if constexpr (KIND == TC_FWD_UP) {
+        if constexpr (KIND == TC_ROUTE) {
+          if (lane == 0) ptx::tma_load_2d(sA, &mA0, bar, k0, t.m0);
+          if (lane == 1) ptx::tma_load_2d(sB, &mB0, bar, k0, 0);
+        } else if constexpr (KIND == TC_FWD_UP) {
           if (!CPA) ptx::tma_gather4(sA + 512 * lane, &mA0, bar, k0, gi0, gi1, gi2, gi3);
           if (lane == 0) ptx::tma_load_2d(sB, &mB0, bar, k0, t.e * P.h + t.n0);
           if (lane == 1) ptx::tma_load_2d(sB + TB_BYTES / 2, &mB1, bar, k0, t.e * P.h + t.n0);
@@ -356,7 +377,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
                                         : ptx::umma_desc_sw128(sA + ks * 32, 16, 1024);
             const uint64_t bd = K::b_mn ? ptx::umma_desc_sw128(sB + ks * 2048, 8192, 1024)
                                         : ptx::umma_desc_sw128(sB + ks * 32, 16, 1024);
-            ptx::umma_bf16(d_tmem, ad, bd, K::IDESC, (kb | ks) != 0);
+            ptx::umma_bf16(d_tmem, ad, bd, KIND == TC_ROUTE ? P.route_idesc : K::IDESC, (kb | ks) != 0);
           }
           ptx::umma_commit(&empty[stage]);
         }
@@ -382,7 +403,70 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
       ptx::tc_fence_after();
       const uint32_t tb = tmem_base + ((uint32_t)(wq * 32) << 16) + as * TBN;
       uint32_t v[32];
-      if constexpr (KIND == TC_FWD_UP) {
+      if constexpr (KIND == TC_ROUTE) {
+        // one token row per thread: logits out, softmax, top-k (desc, ties -> lower id)
+        const int r = t.m0 + row;
+        const bool valid = r < P.T;
+        const int E = P.E;
+        float mx = -INFINITY;
+#pragma unroll 1
+        for (int c = 0; c < P.route_n; c += 32) {
+          ptx::tmem_ld32(tb + c, v);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            if (c + i < E) {
+              const float f = __uint_as_float(v[i]);
+              mx = fmaxf(mx, f);
+              if (valid) P.logits[(int64_t)r * E + c + i] = f;
+            }
+          }
+        }
+        float sum = 0.f;
+#pragma unroll 1
+        for (int c = 0; c < P.route_n; c += 32) {
+          ptx::tmem_ld32(tb + c, v);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (c + i < E) sum += expf(__uint_as_float(v[i]) - mx);
+        }
+        uint32_t taken[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        float wsum = 0.f;
+        int sel_e[16];
+        float sel_p[16];
+#pragma unroll 1
+        for (int j = 0; j < P.k; ++j) {
+          float bv = -INFINITY;
+          int be = 0x7fffffff;
+#pragma unroll 1
+          for (int c = 0; c < P.route_n; c += 32) {
+            ptx::tmem_ld32(tb + c, v);
+            ptx::tmem_wait_ld();
+            const uint32_t tk = taken[c >> 5];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const float f = __uint_as_float(v[i]);
+              if (c + i < E && !((tk >> i) & 1u) && (f > bv || (f == bv && c + i < be))) {
+                bv = f;
+                be = c + i;
+              }
+            }
+          }
+          taken[be >> 5] |= 1u << (be & 31);
+          const float pr = expf(bv - mx) / sum;
+          sel_e[j] = be;
+          sel_p[j] = pr;
+          wsum += pr;
+        }
+        if (valid) {
+#pragma unroll 1
+          for (int j = 0; j < P.k; ++j) {
+            P.ids[(int64_t)r * P.k + j] = sel_e[j];
+            P.route_w[(int64_t)r * P.k + j] = P.renorm ? sel_p[j] / wsum : sel_p[j];
+          }
+        }
+      } else if constexpr (KIND == TC_FWD_UP) {
         const int r = t.m0 + row;
         const bool valid = r < t.seg1;
         uint32_t bv[32];
@@ -578,6 +662,23 @@ static moe_status launch_tc(const CUtensorMap& a0, const CUtensorMap& a1, const 
 }
 
 int tc_dg_parts(int h) { return (int)ceil_div(h, TBN); }
+
+// K1 on tensor cores (bf16): logits = X Wg^T with M = 128 tokens, N = E padded
+// to a multiple of 16 (rows past E are TMA zero-fill), K = d.
+moe_status tc_route(const moe_problem* p, const void* x, const void* wg, float* logits, int32_t* ids, float* topw,
+                    cudaStream_t st) {
+  if (p->T == 0) return MOE_OK;
+  TcParams P{};
+  P.T = (int)p->T; P.d = p->d; P.h = p->h; P.E = p->E;
+  P.logits = logits; P.ids = ids; P.route_w = topw; P.k = p->k; P.renorm = p->renormalize;
+  P.route_n = std::max(16, (int)ceil_div(p->E, 16) * 16);
+  P.route_idesc = ptx::umma_idesc_bf16(TBM, P.route_n, 0, 0);
+  CUtensorMap a0, b0;
+  if (!make_map(&a0, x, p->T, p->d, 64, 128) || !make_map(&b0, wg, p->E, p->d, 64, P.route_n)) return MOE_ERR_CUDA;
+  const int64_t tiles = ceil_div(p->T, TBM);
+  const int grid = (int)std::min<int64_t>(tiles, num_sms());
+  return launch_tc_impl<TC_ROUTE, false>(a0, a0, b0, b0, P, grid, st);
+}
 
 moe_status tc_gemm(const GemmCall& c, cudaStream_t st) {
   typedef __nv_bfloat16 bf;

@@ -118,20 +118,19 @@ size_t route_smem_bytes(int E) {
   return sizeof(float) * (RT_TOK * (RT_DC + 1) + (size_t)E * (RT_DC + 1) + RT_TOK * (E + 1));
 }
 
+moe_status tc_route(const moe_problem* p, const void* x, const void* wg, float* logits, int32_t* ids, float* topw,
+                    cudaStream_t st);
+
+// bf16: tensor-core router (gemm_tc.cu, TC_ROUTE); fp32 storage mode: the CUDA-core kernel above.
 moe_status launch_route(const moe_problem* p, const void* x, const void* wg, float* logits, int32_t* ids,
                         float* topw, cudaStream_t st) {
   if (p->T == 0) return MOE_OK;
+  if (p->dtype == MOE_BF16) return tc_route(p, x, wg, logits, ids, topw, st);
   dim3 grid((unsigned)ceil_div(p->T, RT_TOK));
   size_t smem = route_smem_bytes(p->E);
-  if (p->dtype == MOE_BF16) {
-    MOE_CUDA_CHECK(cudaFuncSetAttribute(route_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    MOE_LAUNCH(route_kernel<__nv_bfloat16>, grid, RT_THREADS, smem, st, (const __nv_bfloat16*)x,
-               (const __nv_bfloat16*)wg, p->T, p->d, p->E, p->k, p->renormalize, logits, ids, topw);
-  } else {
-    MOE_CUDA_CHECK(cudaFuncSetAttribute(route_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    MOE_LAUNCH(route_kernel<float>, grid, RT_THREADS, smem, st, (const float*)x, (const float*)wg, p->T, p->d,
-               p->E, p->k, p->renormalize, logits, ids, topw);
-  }
+  MOE_CUDA_CHECK(cudaFuncSetAttribute(route_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  MOE_LAUNCH(route_kernel<float>, grid, RT_THREADS, smem, st, (const float*)x, (const float*)wg, p->T, p->d,
+             p->E, p->k, p->renormalize, logits, ids, topw);
   MOE_CUDA_CHECK(cudaGetLastError());
   return MOE_OK;
 }
