@@ -93,7 +93,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------ oracle timing
-def oracle_tokens_per_s(inp_host, cfg, budget_s=15.0, min_tokens=16, fixed_tokens=None):
+def oracle_tokens_per_s(inp_host, cfg, budget_s=15.0, min_tokens=64, fixed_tokens=None):
     """Time the fp64 oracle (as it stands) on a bounded token sample of the
     workload, full weights.  Returns (tokens/s, sample tokens, seconds, threads)."""
     import numpy as np
@@ -116,11 +116,19 @@ def oracle_tokens_per_s(inp_host, cfg, budget_s=15.0, min_tokens=16, fixed_token
         S = min(fixed_tokens, cfg.T)
         t = run(S)
         return S / t, S, t, threads
-    S = min(min_tokens, cfg.T)
+    # The oracle's cost is (weight-sized fixed work) + (per-token work): time two
+    # small samples, fit both terms, then time one sample sized to the budget.
+    s1, s2 = min(min_tokens, cfg.T), min(4 * min_tokens, cfg.T)
+    t1 = run(s1)
+    if s2 == s1 or t1 > budget_s:
+        return s1 / t1, s1, t1, threads
+    t2 = run(s2)
+    per_tok = max((t2 - t1) / (s2 - s1), 1e-6)
+    fixed = max(t1 - per_tok * s1, 0.0)
+    S = int(min(cfg.T, max(s2, (budget_s - fixed) / per_tok)))
+    if S <= s2:
+        return s2 / t2, s2, t2, threads
     t = run(S)
-    while t < budget_s / 4 and S < cfg.T:
-        S = min(cfg.T, max(S * 2, int(S * budget_s / max(t, 1e-3) * 0.5)))
-        t = run(S)
     return S / t, S, t, threads
 
 
