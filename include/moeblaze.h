@@ -57,7 +57,8 @@ typedef enum {
 
 typedef enum { MOE_BF16 = 0, MOE_FP32 = 1 } moe_dtype;
 
-typedef enum { MOE_OP_ROUTE = 0, MOE_OP_DISPATCH = 1, MOE_OP_FFN_FWD = 2, MOE_OP_FFN_BWD = 3 } moe_op;
+typedef enum { MOE_OP_ROUTE = 0, MOE_OP_DISPATCH = 1, MOE_OP_FFN_FWD = 2, MOE_OP_FFN_BWD = 3,
+               MOE_OP_ROUTER_BWD = 4 } moe_op;
 
 typedef struct {
   int64_t T;              /* tokens in the step (paper's L) */
@@ -153,14 +154,30 @@ moe_status moe_ffn_bwd(const moe_problem* p, const void* dy, const void* x, cons
                        void* dx, void* dw1, void* dw2, void* dw3, float* d_topk_w,
                        const moe_router_bwd* router, void* ws, size_t ws_bytes, void* stream);
 
+/* Router backward on its own (used by the expert-parallel path, where the
+ * gate-weight gradient d_topk_w arrives from the expert owners):
+ *   dlogits = softmax-Jacobian of the (renormalised) gate weights applied to
+ *   d_topk_w [T,k] fp32; router->dw_gate = dlogits^T X (written);
+ *   dx = dx_partial + dlogits W_g  (dx_partial, dx: [T,d] dtype; may alias). */
+moe_status moe_router_backward(const moe_problem* p, const float* d_topk_w, const void* x,
+                               const moe_router_bwd* router, const void* dx_partial, void* dx,
+                               void* ws, size_t ws_bytes, void* stream);
+
 /* Expert-parallel helpers (the paper's "future work").
+ * moe_ep_row_meta: for every routed row r (expert-sorted order) row_w[r] =
+ *   topk_w[row_slot[r]] and row_local_expert[r] = ids[row_slot[r]] mod
+ *   experts_per_rank: the per-row payload that travels with the row to the
+ *   rank owning its expert (ranks own contiguous expert ranges).
  * moe_gather_rows: dst[i, :] = src[index[i], :] for i < n (rows of `width`
- *   elements of `elem_bytes` in {2,4}); builds the all-to-all send buffer in
- *   expert_token_indices order.  index entries must be in [0, n_src).
+ *   elements of `elem_bytes` in {2,4}; row bytes a multiple of 4); builds the
+ *   all-to-all send buffer in expert_token_indices order.  index entries must
+ *   be in [0, n_src).
  * moe_combine_rows: out[t, :] = sum_{j<k} rows[tim[t*k+j], :] (fixed j order,
  *   fp32 accumulation, dtype output): the token-side combine of returned
  *   expert rows through token_index_map ("gather its k expert
  *   outputs"). */
+moe_status moe_ep_row_meta(const moe_problem* p, const moe_dispatch* disp, const float* topk_w,
+                           int32_t experts_per_rank, float* row_w, int32_t* row_local_expert, void* stream);
 moe_status moe_gather_rows(const void* src, int64_t n_src, const int32_t* index, int64_t n,
                            int64_t width, int32_t elem_bytes, void* dst, void* stream);
 moe_status moe_combine_rows(const moe_problem* p, const void* rows, const int32_t* token_index_map,

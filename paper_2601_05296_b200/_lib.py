@@ -17,11 +17,11 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libmoeblaze.so")
 
 MOE_BF16, MOE_FP32 = 0, 1
-MOE_OP_ROUTE, MOE_OP_DISPATCH, MOE_OP_FFN_FWD, MOE_OP_FFN_BWD = 0, 1, 2, 3
+MOE_OP_ROUTE, MOE_OP_DISPATCH, MOE_OP_FFN_FWD, MOE_OP_FFN_BWD, MOE_OP_ROUTER_BWD = 0, 1, 2, 3, 4
 
 EXPORTS = ("moe_workspace_size", "moe_route", "moe_dispatch_build", "moe_ffn_fwd", "moe_ffn_bwd",
            "moe_gather_rows", "moe_combine_rows", "moe_status_string", "moe_launch_count", "moe_version",
-           "moe_profile_enable", "moe_profile_reset", "moe_profile_read")
+           "moe_profile_enable", "moe_profile_reset", "moe_profile_read", "moe_router_backward", "moe_ep_row_meta")
 GEMM_KINDS = ("FWD_UP", "FWD_DOWN", "BWD_DH", "BWD_DX", "DW3", "DW12")
 
 
@@ -67,8 +67,10 @@ def load():
                                 P(MoeRouterBwd), V, SZ, V]
     lib.moe_gather_rows.argtypes = [V, I64, V, I64, I64, I32, V, V]
     lib.moe_combine_rows.argtypes = [P(MoeProblem), V, V, V, V]
+    lib.moe_router_backward.argtypes = [P(MoeProblem), V, V, P(MoeRouterBwd), V, V, V, SZ, V]
+    lib.moe_ep_row_meta.argtypes = [P(MoeProblem), P(MoeDispatch), V, I32, V, V, V]
     for fn in ("moe_workspace_size", "moe_route", "moe_dispatch_build", "moe_ffn_fwd", "moe_ffn_bwd",
-               "moe_gather_rows", "moe_combine_rows"):
+               "moe_gather_rows", "moe_combine_rows", "moe_router_backward", "moe_ep_row_meta"):
         getattr(lib, fn).restype = I32
     lib.moe_status_string.argtypes = [I32]
     lib.moe_status_string.restype = ctypes.c_char_p
@@ -76,7 +78,7 @@ def load():
     lib.moe_version.restype = I32
     lib.moe_profile_enable.argtypes = [I32]
     lib.moe_profile_read.argtypes = [I32, P(ctypes.c_double), P(I64)]
-    for fn in ("moe_profile_enable", "moe_profile_reset", "moe_profile_read"):
+    for fn in ("moe_profile_enable", "moe_profile_reset", "moe_profile_read", "moe_router_backward", "moe_ep_row_meta"):
         getattr(lib, fn).restype = I32
     _lib = lib
     return lib
@@ -155,8 +157,22 @@ def moe_ffn_bwd(p, dy, x, w1, w2, w3, topk_w, disp, a_save, b_save, dx, dw1, dw2
                               _ptr(ws), ws.numel(), _stream(stream)), "moe_ffn_bwd")
 
 
+def moe_router_backward(p, d_topk_w, x, router, dx_partial, dx, ws, stream=None):
+    _check(load().moe_router_backward(ctypes.byref(p), _ptr(d_topk_w), _ptr(x), ctypes.byref(router),
+                                      _ptr(dx_partial), _ptr(dx), _ptr(ws), ws.numel(), _stream(stream)),
+           "moe_router_backward")
+
+
+def moe_ep_row_meta(p, disp, topk_w, experts_per_rank, row_w, row_local_expert, stream=None):
+    _check(load().moe_ep_row_meta(ctypes.byref(p), ctypes.byref(disp), _ptr(topk_w), int(experts_per_rank),
+                                  _ptr(row_w), _ptr(row_local_expert), _stream(stream)), "moe_ep_row_meta")
+
+
 def moe_gather_rows(src, index, dst, stream=None):
-    n_src, width = src.shape[0], src[0].numel() if src.shape[0] else src.shape[-1]
+    n_src = src.shape[0]
+    width = 1
+    for s_ in src.shape[1:]:
+        width *= s_
     _check(load().moe_gather_rows(_ptr(src), n_src, _ptr(index), index.numel(), width, src.element_size(), _ptr(dst),
                                   _stream(stream)), "moe_gather_rows")
 

@@ -19,7 +19,8 @@ moe_status launch_dg_reduce(const float*, int, const int32_t*, int64_t, float*, 
 int dwg_chunks(int64_t T, int d);
 moe_status launch_router_bwd(const moe_problem*, const float*, const int32_t*, const float*, const void*, float*,
                              float*, void*, cudaStream_t);
-moe_status launch_finalize(const moe_problem*, const float*, const float*, const void*, void*, cudaStream_t);
+moe_status launch_finalize(const moe_problem*, const void*, const float*, const void*, void*, cudaStream_t, bool);
+moe_status launch_ep_row_meta(const int32_t*, const int32_t*, const float*, int64_t, int, float*, int32_t*, cudaStream_t);
 moe_status launch_gather_rows(const void*, const int32_t*, int64_t, int64_t, void*, cudaStream_t);
 moe_status launch_combine_rows(const moe_problem*, const void*, const int32_t*, void*, cudaStream_t);
 
@@ -51,6 +52,17 @@ static FwdWs fwd_layout(const moe_problem* p, void* base) {
   FwdWs w;
   w.u = b + o; o += align256((size_t)R * p->h * esize(p));
   w.yacc = (float*)(b + o); o += align256((size_t)p->T * p->d * 4);
+  w.total = o;
+  return w;
+}
+
+struct RouterWs { float* dlogits; float* dwgpart; size_t total; };
+static RouterWs router_layout(const moe_problem* p, void* base) {
+  char* b = (char*)base;
+  size_t o = 0;
+  RouterWs w;
+  w.dlogits = (float*)(b + o); o += align256((size_t)p->T * p->E * 4);
+  w.dwgpart = (float*)(b + o); o += align256((size_t)dwg_chunks(p->T, p->d) * p->E * p->d * 4);
   w.total = o;
   return w;
 }
@@ -102,6 +114,7 @@ moe_status moe_workspace_size(const moe_problem* p, moe_op op, size_t* bytes) {
     case MOE_OP_DISPATCH: *bytes = dispatch_ws_bytes(p); break;
     case MOE_OP_FFN_FWD: *bytes = fwd_layout(p, nullptr).total; break;
     case MOE_OP_FFN_BWD: *bytes = bwd_layout(p, nullptr).total; break;
+    case MOE_OP_ROUTER_BWD: *bytes = router_layout(p, nullptr).total; break;
     default: return MOE_ERR_INVALID_ARG;
   }
   return MOE_OK;
@@ -155,7 +168,7 @@ moe_status moe_ffn_fwd(const moe_problem* p, const void* x, const void* w1, cons
   if ((s = run_gemm(c, st)) != MOE_OK) return s;
   c.which = GEMM_FWD_DOWN;
   if ((s = run_gemm(c, st)) != MOE_OK) return s;
-  return launch_finalize(p, w.yacc, nullptr, nullptr, y, st);
+  return launch_finalize(p, w.yacc, nullptr, nullptr, y, st, false);
 }
 
 moe_status moe_ffn_bwd(const moe_problem* p, const void* dy, const void* x, const void* w1, const void* w2,
@@ -210,14 +223,47 @@ moe_status moe_ffn_bwd(const moe_problem* p, const void* dy, const void* x, cons
       return s;
     dl = w.dlogits;
   }
-  return launch_finalize(p, w.dxacc, dl, router ? router->w_gate : nullptr, dx, st);
+  return launch_finalize(p, w.dxacc, dl, router ? router->w_gate : nullptr, dx, st, false);
+}
+
+moe_status moe_router_backward(const moe_problem* p, const float* d_topk_w, const void* x, const moe_router_bwd* router,
+                               const void* dx_partial, void* dx, void* ws, size_t ws_bytes, void* stream) {
+  moe_status s = validate(p);
+  if (s != MOE_OK) return s;
+  if (!router || !router->w_gate || !router->dw_gate) return MOE_ERR_INVALID_ARG;
+  if (p->T > 0 && (!d_topk_w || !x || !router->logits || !router->topk_ids || !dx_partial || !dx || !ws))
+    return MOE_ERR_INVALID_ARG;
+  RouterWs w = router_layout(p, ws);
+  if (ws_bytes < w.total) return MOE_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (p->T == 0) {
+    MOE_CUDA_CHECK(cudaMemsetAsync(router->dw_gate, 0, (size_t)p->E * p->d * esize(p), st));
+    return MOE_OK;
+  }
+  if ((s = launch_router_bwd(p, router->logits, router->topk_ids, d_topk_w, x, w.dlogits, w.dwgpart, router->dw_gate,
+                             st)) != MOE_OK)
+    return s;
+  return launch_finalize(p, dx_partial, w.dlogits, router->w_gate, dx, st, true);
+}
+
+moe_status moe_ep_row_meta(const moe_problem* p, const moe_dispatch* disp, const float* topk_w, int32_t experts_per_rank,
+                           float* row_w, int32_t* row_local_expert, void* stream) {
+  moe_status s = validate(p);
+  if (s != MOE_OK) return s;
+  if (!disp || experts_per_rank < 1) return MOE_ERR_INVALID_ARG;
+  const int64_t R = p->T * p->k;
+  if (R > 0 && (!disp->row_slot || !disp->token_expert_indices || !topk_w || !row_w || !row_local_expert))
+    return MOE_ERR_INVALID_ARG;
+  return launch_ep_row_meta(disp->row_slot, disp->token_expert_indices, topk_w, R, experts_per_rank, row_w,
+                            row_local_expert, (cudaStream_t)stream);
 }
 
 moe_status moe_gather_rows(const void* src, int64_t n_src, const int32_t* index, int64_t n, int64_t width,
                            int32_t elem_bytes, void* dst, void* stream) {
   if (n < 0 || n_src < 0 || width < 1 || (elem_bytes != 2 && elem_bytes != 4)) return MOE_ERR_INVALID_ARG;
   if (n > 0 && (!src || !index || !dst)) return MOE_ERR_INVALID_ARG;
-  if ((width * elem_bytes) % 16 != 0 || !aligned16(src) || !aligned16(dst)) return MOE_ERR_MISALIGNED;
+  if ((width * elem_bytes) % 4 != 0) return MOE_ERR_MISALIGNED;
+  if ((width * elem_bytes) % 16 == 0 && (!aligned16(src) || !aligned16(dst))) return MOE_ERR_MISALIGNED;
   return launch_gather_rows(src, index, n, width * elem_bytes, dst, (cudaStream_t)stream);
 }
 

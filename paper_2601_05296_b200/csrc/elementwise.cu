@@ -118,8 +118,8 @@ __global__ void dwg_reduce_kernel(const float* __restrict__ part, int nch, int64
 }
 
 // out[t, :] = dtype(acc[t, :] + sum_e dl[t, e] Wg[e, :]); block: 16 tokens x 256 cols
-template <typename T>
-__global__ void __launch_bounds__(256) finalize_kernel(const float* __restrict__ acc, const float* __restrict__ dl,
+template <typename T, typename A>
+__global__ void __launch_bounds__(256) finalize_kernel(const A* __restrict__ acc, const float* __restrict__ dl,
                                                        const T* __restrict__ wg, int64_t Tn, int d, int E,
                                                        T* __restrict__ out) {
   extern __shared__ float sdl[];  // [16][E]
@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(const float* __restrict__
   const int nt = (int)min64(16, Tn - t0);
   float a[16];
 #pragma unroll
-  for (int r = 0; r < 16; ++r) a[r] = (r < nt && col < d) ? acc[(t0 + r) * d + col] : 0.f;
+  for (int r = 0; r < 16; ++r) a[r] = (r < nt && col < d) ? to_f32(acc[(t0 + r) * d + col]) : 0.f;
   if (dl) {
     for (int i = threadIdx.x; i < 16 * E; i += 256) {
       int r = i / E, e = i % E;
@@ -148,6 +148,26 @@ __global__ void __launch_bounds__(256) finalize_kernel(const float* __restrict__
     for (int r = 0; r < 16; ++r)
       if (r < nt) out[(t0 + r) * d + col] = from_f32<T>(a[r]);
   }
+}
+
+// per-row EP payload: gate weight and local expert id of every routed row
+__global__ void ep_row_meta_kernel(const int32_t* __restrict__ row_slot, const int32_t* __restrict__ ids,
+                                   const float* __restrict__ topw, int64_t R, int epr, float* __restrict__ row_w,
+                                   int32_t* __restrict__ row_e) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= R) return;
+  const int s = row_slot[r];
+  row_w[r] = topw[s];
+  row_e[r] = ids[s] % epr;
+}
+
+// 4-byte row gather for rows that are not a multiple of 16 bytes
+__global__ void gather_rows4_kernel(const uint32_t* __restrict__ src, const int32_t* __restrict__ index, int64_t n,
+                                    int64_t w_per_row, uint32_t* __restrict__ dst) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * w_per_row) return;
+  int64_t row = i / w_per_row, c = i % w_per_row;
+  dst[i] = src[(int64_t)index[row] * w_per_row + c];
 }
 
 // vectorised row gather: 16-byte chunks
@@ -220,22 +240,42 @@ moe_status launch_router_bwd(const moe_problem* p, const float* logits, const in
   return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
 }
 
-moe_status launch_finalize(const moe_problem* p, const float* acc, const float* dl, const void* wg, void* out,
-                           cudaStream_t st) {
+// acc_is_dtype: the accumulator is a [T,d] tensor of the run dtype (EP path) instead of fp32
+moe_status launch_finalize(const moe_problem* p, const void* acc, const float* dl, const void* wg, void* out,
+                           cudaStream_t st, bool acc_is_dtype) {
   if (p->T == 0) return MOE_OK;
   dim3 grid((unsigned)ceil_div(p->d, 256), (unsigned)ceil_div(p->T, 16));
   size_t sm = dl ? sizeof(float) * 16 * p->E : 0;
-  if (p->dtype == MOE_BF16)
-    MOE_LAUNCH(finalize_kernel<__nv_bfloat16>, grid, 256, sm, st, acc, dl, (const __nv_bfloat16*)wg, p->T, p->d, p->E,
-               (__nv_bfloat16*)out);
-  else
-    MOE_LAUNCH(finalize_kernel<float>, grid, 256, sm, st, acc, dl, (const float*)wg, p->T, p->d, p->E, (float*)out);
+  typedef __nv_bfloat16 bf;
+  if (p->dtype == MOE_BF16) {
+    if (acc_is_dtype)
+      MOE_LAUNCH((finalize_kernel<bf, bf>), grid, 256, sm, st, (const bf*)acc, dl, (const bf*)wg, p->T, p->d, p->E, (bf*)out);
+    else
+      MOE_LAUNCH((finalize_kernel<bf, float>), grid, 256, sm, st, (const float*)acc, dl, (const bf*)wg, p->T, p->d, p->E,
+                 (bf*)out);
+  } else {
+    MOE_LAUNCH((finalize_kernel<float, float>), grid, 256, sm, st, (const float*)acc, dl, (const float*)wg, p->T, p->d,
+               p->E, (float*)out);
+  }
+  return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
+}
+
+moe_status launch_ep_row_meta(const int32_t* row_slot, const int32_t* ids, const float* topw, int64_t R, int epr,
+                              float* row_w, int32_t* row_e, cudaStream_t st) {
+  if (R == 0) return MOE_OK;
+  MOE_LAUNCH(ep_row_meta_kernel, (unsigned)ceil_div(R, 256), 256, 0, st, row_slot, ids, topw, R, epr, row_w, row_e);
   return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
 }
 
 moe_status launch_gather_rows(const void* src, const int32_t* index, int64_t n, int64_t row_bytes, void* dst,
                               cudaStream_t st) {
   if (n == 0) return MOE_OK;
+  if (row_bytes % 16 != 0) {
+    const int64_t wpr = row_bytes / 4;
+    MOE_LAUNCH(gather_rows4_kernel, (unsigned)ceil_div(n * wpr, 256), 256, 0, st, (const uint32_t*)src, index, n,
+               wpr, (uint32_t*)dst);
+    return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
+  }
   const int64_t vpr = row_bytes / 16;
   MOE_LAUNCH(gather_rows_kernel, (unsigned)ceil_div(n * vpr, 256), 256, 0, st, (const uint4*)src, index, n, vpr,
              (uint4*)dst);

@@ -1,0 +1,132 @@
+"""Expert-parallel bookkeeping on CPU: world size 2 (and 4) over gloo.
+
+The EP orchestrator (paper_2601_05296_b200/ep.py) is run with oracle-backed
+compute ops (fp64, test-only) and gloo all-to-all, so what is tested is the
+host logic: split sizes, send order, per-row payload, the receiver's local
+index build, the return exchange and the token-side combine through
+token_index_map, and the dW_g all-reduce.  Every rank's outputs must equal the
+single-process oracle over the concatenated tokens (fp64, 1e-10)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle as O
+from moe_inputs import make_inputs
+
+
+class OracleOps:
+    """Test-only compute for the EP orchestrator: the fp64 oracle on CPU."""
+
+    class D:
+        def __init__(self, d, ids):
+            self.counts = torch.from_numpy(d["counts"].astype(np.int32))
+            self.offs = torch.from_numpy(d["offs"].astype(np.int32))
+            self.eti = torch.from_numpy(d["eti"].astype(np.int64))
+            self.tim = torch.from_numpy(d["tim"].astype(np.int64))
+            self.row_slot = torch.from_numpy(d["row_slot"].astype(np.int64))
+            self.ids = ids
+            self.raw = d
+
+    def route(self, x, wg, k, renorm):
+        r = O.route(x.numpy(), wg.numpy(), k, renorm)
+        return torch.from_numpy(r["logits"]), torch.from_numpy(r["ids"]), torch.from_numpy(r["w"])
+
+    def dispatch(self, ids, E, dtype):
+        return OracleOps.D(O.dispatch_argsort(ids.numpy(), E), ids)
+
+    def row_meta(self, disp, w, epr, dtype):
+        rs = disp.row_slot
+        return w.reshape(-1)[rs].clone(), (disp.ids.reshape(-1)[rs] % epr).to(torch.int32)
+
+    def gather_rows(self, src, index):
+        return src[index.reshape(-1).long()].clone()
+
+    def ffn_fwd(self, x, w1, w2, w3, w, disp):
+        f = O.ffn_forward(x.numpy(), w1.numpy(), w2.numpy(), w3.numpy(), disp.ids.numpy(), w.numpy(), disp.raw)
+        return torch.from_numpy(f["y"]), torch.from_numpy(f["A"]), torch.from_numpy(f["B"])
+
+    def ffn_bwd(self, dy, x, w1, w2, w3, w, disp, a, b):
+        g = O.ffn_backward(dy.numpy(), x.numpy(), w1.numpy(), w2.numpy(), w3.numpy(), disp.ids.numpy(), w.numpy(),
+                           disp.raw, a.numpy(), b.numpy())
+        return {n: torch.from_numpy(np.ascontiguousarray(g[n])) for n in ("dx", "dw1", "dw2", "dw3", "dg")}
+
+    def combine(self, rows, tim, T, d, k):
+        return rows[tim.reshape(T, k).long()].sum(1)
+
+    def router_backward(self, dg, x, wg, logits, ids, dx_partial, renorm):
+        rb = O.router_backward(dg.numpy(), x.numpy(), wg.numpy(), logits.numpy(), ids.numpy(), renorm)
+        return dx_partial + torch.from_numpy(rb["dx"]), torch.from_numpy(rb["dw_gate"])
+
+
+def gloo_a2a(send, send_split, recv_split, group=None):
+    out = torch.empty((sum(recv_split),) + tuple(send.shape[1:]), dtype=send.dtype)
+    dist.all_to_all_single(out, send.contiguous(), recv_split, send_split, group=group)
+    return out
+
+
+CFG = dict(T=40, d=16, h=24, E=8, k=2)
+
+
+def _inputs(rank, P, renorm, routing):
+    c = CFG
+    W = make_inputs(c["T"], c["d"], c["h"], c["E"], c["k"], dtype="fp32", seed=100, routing=routing)
+    X = [make_inputs(c["T"], c["d"], c["h"], c["E"], c["k"], dtype="fp32", seed=r, routing=routing) for r in range(P)]
+    f = lambda t: t.double()  # noqa: E731
+    return {n: f(W[n]) for n in ("w_gate", "w1", "w2", "w3")}, [(f(X[r]["x"]), f(X[r]["dy"])) for r in range(P)]
+
+
+def _worker(rank, P, port, renorm, routing, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=P)
+    from paper_2601_05296_b200.ep import ExpertParallelMoE
+    W, XS = _inputs(rank, P, renorm, routing)
+    ep = ExpertParallelMoE(CFG["E"], CFG["k"], renorm, ops=OracleOps(), a2a=gloo_a2a)
+    lo, hi = ep.local_experts
+    x, dy = XS[rank]
+    y, g = ep.step(x, W["w_gate"], W["w1"][lo:hi], W["w2"][lo:hi], W["w3"][lo:hi], dy)
+    q.put((rank, y.numpy(), {n: v.numpy() for n, v in g.items()}, (lo, hi)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("P,renorm,routing", [(2, False, "balanced"), (2, True, "skewed"), (4, False, "balanced")])
+def test_ep_matches_single_process_oracle(P, renorm, routing):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, P, port, renorm, routing, q)) for r in range(P)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(P)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    res.sort(key=lambda t: t[0])
+    W, XS = _inputs(0, P, renorm, routing)
+    Xall = torch.cat([x for x, _ in XS]).numpy()
+    DYall = torch.cat([dy for _, dy in XS]).numpy()
+    Wn = {n: v.numpy() for n, v in W.items()}
+    fwd = O.layer_forward(Xall, Wn["w_gate"], Wn["w1"], Wn["w2"], Wn["w3"], CFG["k"], renorm)
+    bwd = O.layer_backward(fwd, DYall, Xall, Wn["w_gate"], Wn["w1"], Wn["w2"], Wn["w3"], renorm)
+    T = CFG["T"]
+    for rank, y, g, (lo, hi) in res:
+        sl = slice(rank * T, (rank + 1) * T)
+        np.testing.assert_allclose(y, fwd["y"][sl], rtol=1e-10, atol=1e-12)
+        np.testing.assert_allclose(g["dx"], bwd["dx"][sl], rtol=1e-10, atol=1e-12)
+        np.testing.assert_allclose(g["dg"], bwd["dg"][sl], rtol=1e-10, atol=1e-12)
+        np.testing.assert_allclose(g["dw_gate"], bwd["dw_gate"], rtol=1e-10, atol=1e-12)
+        for n in ("dw1", "dw2", "dw3"):
+            np.testing.assert_allclose(g[n], bwd[n][lo:hi], rtol=1e-10, atol=1e-12)

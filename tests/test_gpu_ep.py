@@ -1,0 +1,102 @@
+"""Expert-parallel layer with the real CUDA kernels (C ABI) on one B200.
+
+NCCL cannot place two ranks on one GPU, so the 2-rank case runs two processes
+on cuda:0 with gloo and a host-staged all-to-all; every compute step is the
+library's (CudaOps).  Compared with the single-GPU path on the concatenated
+tokens (ids exact; floats within 1e-2: return rows travel in bf16, SURVEY
+§8(e)) and with the fp64 oracle (2e-2)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle as O
+from moe_inputs import make_inputs
+from tests._util import BF16_TOL, f64, normwise
+
+pytestmark = pytest.mark.gpu
+
+CFG = dict(T=384, d=256, h=256, E=8, k=2)
+
+
+def staged_a2a(send, send_split, recv_split, group=None):
+    out = torch.empty((sum(recv_split),) + tuple(send.shape[1:]), dtype=send.dtype)
+    dist.all_to_all_single(out, send.detach().cpu().contiguous(), recv_split, send_split, group=group)
+    return out.to(send.device)
+
+
+def _inputs(P):
+    c = CFG
+    W = make_inputs(c["T"], c["d"], c["h"], c["E"], c["k"], dtype="bf16", seed=100)
+    XS = [make_inputs(c["T"], c["d"], c["h"], c["E"], c["k"], dtype="bf16", seed=r) for r in range(P)]
+    return W, [(X["x"], X["dy"]) for X in XS]
+
+
+def _worker(rank, P, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=P)
+    from paper_2601_05296_b200.ep import ExpertParallelMoE
+    W, XS = _inputs(P)
+    dev = torch.device("cuda", 0)
+    ep = ExpertParallelMoE(CFG["E"], CFG["k"], False, a2a=staged_a2a)
+    lo, hi = ep.local_experts
+    x, dy = (t.to(dev) for t in XS[rank])
+    wl = [W[n][lo:hi].contiguous().to(dev) for n in ("w1", "w2", "w3")]
+    y, g = ep.step(x, W["w_gate"].to(dev), *wl, dy)
+    torch.cuda.synchronize()
+    q.put((rank, y.cpu(), {n: v.cpu() for n, v in g.items()}, (lo, hi)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("P", [1, 2])
+def test_ep_cuda_matches_single_gpu(P):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, P, port, q)) for r in range(P)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(P)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    import paper_2601_05296_b200 as M
+    W, XS = _inputs(P)
+    dev = torch.device("cuda", 0)
+    x = torch.cat([a for a, _ in XS]).to(dev)
+    dy = torch.cat([b for _, b in XS]).to(dev)
+    wg, w1, w2, w3 = (W[n].to(dev) for n in ("w_gate", "w1", "w2", "w3"))
+    k = CFG["k"]
+    logits, ids, w = M.route(x, wg, k)
+    disp = M.dispatch_build(ids, CFG["E"])
+    y, a, b = M.ffn_fwd(x, w1, w2, w3, w, disp)
+    g1 = M.ffn_bwd(dy, x, w1, w2, w3, w, disp, a, b, w_gate=wg, logits=logits)
+    torch.cuda.synchronize()
+    fwd = O.layer_forward(f64(x), f64(wg), f64(w1), f64(w2), f64(w3), k, logits=f64(logits))
+    bwd = O.layer_backward(fwd, f64(dy), f64(x), f64(wg), f64(w1), f64(w2), f64(w3))
+    T = CFG["T"]
+    for rank, ye, ge, (lo, hi) in res:
+        sl = slice(rank * T, (rank + 1) * T)
+        assert normwise(ye, f64(y[sl])) < 1e-2
+        assert normwise(ge["dx"], f64(g1["dx"][sl])) < 1e-2
+        assert normwise(ge["dg"], f64(g1["dg"][sl])) < 1e-2
+        assert normwise(ge["dw_gate"], f64(g1["dw_gate"])) < 1e-2
+        for n in ("dw1", "dw2", "dw3"):
+            assert normwise(ge[n], f64(g1[n][lo:hi])) < 1e-2, n
+            assert normwise(ge[n], bwd[n][lo:hi]) < BF16_TOL, n
+        assert normwise(ye, fwd["y"][sl]) < BF16_TOL
+        assert normwise(ge["dx"], bwd["dx"][sl]) < BF16_TOL
