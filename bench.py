@@ -149,6 +149,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-memory", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
+    ap.add_argument("--ep", action="store_true", help="use the expert-parallel path even at N = 1")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -167,12 +168,17 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    use_ep = world > 1 or args.ep
+    if use_ep:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=dev)
     from paper_2601_05296_b200 import build as B
     if rank == 0 or world == 1:
         B.build()
-    if world > 1:
+    if use_ep:
         dist.barrier()
     import paper_2601_05296_b200 as M
     from paper_2601_05296_b200 import _lib as L
@@ -184,13 +190,15 @@ def main():
     x, wg, w1, w2, w3, dy = (inp[n] for n in ("x", "w_gate", "w1", "w2", "w3", "dy"))
     renorm = args.renormalize
 
-    if world > 1:
+    ep = None
+    if use_ep:
         from paper_2601_05296_b200.ep import ExpertParallelMoE
         ep = ExpertParallelMoE(cfg.E, k, renorm, group=None)
-        # each rank keeps only its experts' weights
+        # each rank keeps only its experts' weights; the router is replicated
         lo, hi = ep.local_experts
         w1, w2, w3 = w1[lo:hi].contiguous(), w2[lo:hi].contiguous(), w3[lo:hi].contiguous()
         dist.broadcast(wg, 0)
+        torch.cuda.empty_cache()
 
         def step():
             return ep.step(x, wg, w1, w2, w3, dy)
@@ -205,7 +213,7 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    if world > 1:
+    if use_ep:
         dist.barrier()
 
     # ----------------------------------------------------------------- timed region (device-resident inputs)
@@ -217,7 +225,7 @@ def main():
     launches0 = L.launch_count()
     st = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
+    if use_ep:
         dist.barrier()
     torch.cuda.synchronize()
     ev0.record(st)
@@ -225,14 +233,14 @@ def main():
         step()
     ev1.record(st)
     torch.cuda.synchronize()
-    if world > 1:
+    if use_ep:
         dist.barrier()
     L.profile_enable(False)
     launches = L.launch_count() - launches0
     ms = ev0.elapsed_time(ev1)
     prof = L.profile_read()
     clk = clocks.stop()
-    if world > 1:
+    if use_ep:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -241,10 +249,10 @@ def main():
 
     # ----------------------------------------------------------------- roofline of the dominant kernel
     peaks = load_peaks()
-    R = cfg.T * k if world == 1 else None
+    R = cfg.T * k if ep is None else ep.last_rows_received
     roof = None
     gemm_total_ms = sum(v[0] for v in prof.values()) / args.steps
-    if world == 1:
+    if True:
         dom = max(prof, key=lambda n: prof[n][0])
         tot_ms, n_l = prof[dom]
         flops = GEMM_FLOP_FACTOR[dom] * R * cfg.d * cfg.h
@@ -268,7 +276,7 @@ def main():
 
     # ----------------------------------------------------------------- e2e through the public API (autograd layer)
     e2e = None
-    if world == 1:
+    if True:
         x_h = x.detach().cpu().pin_memory()
         dy_h = dy.detach().cpu().pin_memory()
         y_h = torch.empty_like(x_h).pin_memory()
@@ -276,14 +284,20 @@ def main():
         params = [torch.nn.Parameter(t) for t in (wg, w1, w2, w3)]
 
         def e2e_step():
-            xd = x_h.to(dev, non_blocking=True).requires_grad_(True)
+            xd = x_h.to(dev, non_blocking=True)
             dyd = dy_h.to(dev, non_blocking=True)
-            for p in params:
-                p.grad = None
-            y = M.moe_layer(xd, *params, k, renorm)
-            y.backward(dyd)
+            if ep is not None:
+                y, g = ep.step(xd, wg, w1, w2, w3, dyd)
+                dxd = g["dx"]
+            else:
+                xd.requires_grad_(True)
+                for p in params:
+                    p.grad = None
+                y = M.moe_layer(xd, *params, k, renorm)
+                y.backward(dyd)
+                dxd = xd.grad
             y_h.copy_(y.detach(), non_blocking=True)
-            dx_h.copy_(xd.grad, non_blocking=True)
+            dx_h.copy_(dxd, non_blocking=True)
 
         for _ in range(2):
             e2e_step()
@@ -295,14 +309,19 @@ def main():
         e1.record(st)
         torch.cuda.synchronize()
         ems = e0.elapsed_time(e1) / args.steps
-        e2e = {"value": round(cfg.T / (ems / 1e3), 1), "unit": UNIT, "ms_per_step": round(ems, 4),
+        if use_ep:
+            t = torch.tensor([ems], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": round(world * cfg.T / (ems / 1e3), 1), "unit": UNIT, "ms_per_step": round(ems, 4),
                "h2d_bytes_per_step": 2 * x.numel() * x.element_size(),
                "d2h_bytes_per_step": 2 * x.numel() * x.element_size(),
-               "api": "paper_2601_05296_b200.moe_layer (autograd) from pinned host X, dY; Y and dX read back"}
+               "api": ("paper_2601_05296_b200.ep.ExpertParallelMoE.step" if ep is not None else
+                       "paper_2601_05296_b200.moe_layer (autograd)") + " from pinned host X, dY; Y and dX read back"}
 
     # ----------------------------------------------------------------- activation memory (P:289 method)
     mem = None
-    if world == 1 and not args.no_memory:
+    if ep is None and not args.no_memory:
         mem = measure_memory(M, x, wg, w1, w2, w3, dy, k, renorm)
 
     # ----------------------------------------------------------------- CPU oracle baseline (rank 0, N = 1)
@@ -325,7 +344,7 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded, moe_inputs)",
             "config": {"workload": cfg.name, "T_per_gpu": cfg.T, "d": cfg.d, "h": cfg.h, "E": cfg.E, "k": cfg.k,
                        "renormalize": renorm,
-                       "parallelism": "single-GPU" if world == 1 else f"ep{world}",
+                       "parallelism": f"ep{world}" if ep is not None else "single-GPU",
                        "l2": "no flush: inputs larger than L2 (weights %.2f GB + X %.0f MB vs 126 MB L2)" % (
                            3 * w1.numel() * 2 * (world if world > 1 else 1) / 1e9, x.numel() * 2 / 1e6)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
@@ -333,7 +352,7 @@ def main():
             "peak_activation_gb": mem["ours"]["peak_gb"] if mem else None, "memory": mem,
         }
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if use_ep:
         dist.destroy_process_group()
 
 

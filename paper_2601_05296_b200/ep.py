@@ -103,6 +103,7 @@ class ExpertParallelMoE:
         self.local_experts = (self.rank * self.El, (self.rank + 1) * self.El)
         self.ops = ops or CudaOps()
         self._a2a = a2a or nccl_a2a
+        self.last_rows_received = 0
 
     def a2a(self, send, send_split, recv_split):
         return self._a2a(send, send_split, recv_split, self.group)
@@ -119,6 +120,7 @@ class ExpertParallelMoE:
         send_split = [offs_h[(q + 1) * El] - offs_h[q * El] for q in range(P)]
         rc = recv_counts.cpu().view(P, El)
         recv_split = rc.sum(1).tolist()
+        self.last_rows_received = int(sum(recv_split))
         # C2: routed rows (exactly T*k rows in expert order; a comm buffer, not an activation)
         xs = ops.gather_rows(x, disp.eti)
         x_recv = self.a2a(xs, send_split, recv_split)
