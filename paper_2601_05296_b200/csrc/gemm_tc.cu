@@ -1,20 +1,27 @@
-// gemm_tc.cu — the six expert GEMMs of the MoE layer on sm_100a tensor cores.
+// gemm_tc.cu — the expert GEMMs (and the router) of the MoE layer on sm_100a
+// tensor cores.
 //
 // One persistent, warp-specialised kernel template (tcgen05.mma kind::f16,
-// bf16 operands, fp32 accumulators in TMEM, operands staged by TMA):
-//   warp 0      TMA producer: tile loads + row-GATHER loads (tile::gather4)
-//               straight from the unpermuted X / dY through
-//               expert_token_indices — no routed-token buffer
-//   warp 1      MMA issuer (one thread): 4 x tcgen05.mma (M128 N256 K16) per
-//               64-wide K block, tcgen05.commit frees the smem stage
+// bf16 operands, fp32 accumulators in TMEM):
+//   warp 0      TMA producer: tile loads of the non-gathered operand
+//   warp 1      MMA issuer (one thread): 4 x tcgen05.mma (K16) per 64-wide K
+//               block; tcgen05.commit frees the smem stage / publishes the
+//               accumulator
 //   warp 2      TMEM allocator (512 columns = 2 accumulator stages x 256)
-//   warps 4-7   epilogue: tcgen05.ld one row per thread, fused epilogue
-// Tile = 128 rows x 256 columns; smem ring of 4 stages x (16 KB A + 32 KB B),
-// 128B-swizzled, K-major or MN-major UMMA descriptors as the operand's
-// global layout dictates (no transposes are ever materialised).
+//   warp 3      (CTA pair) relays cp.async-gather completion to the leader
+//   warps 4-7   epilogue: tcgen05.ld, one accumulator row per thread
+//   warps 8-11  row gathers: 16-byte cp.async straight from the unpermuted X /
+//               dY through expert_token_indices into the 128B-swizzled UMMA
+//               layout — no routed-token buffer exists
 //
-// Kinds ("rows" = the routed rows of one expert segment, read from device
-// expert_token_offsets: no host sync):
+// CG = 2 (default for the expert GEMMs): a CTA pair (cluster of 2) computes a
+// 256 x 256 tile with tcgen05.mma.cta_group::2 — each CTA stages 128 rows of A
+// and 128 columns of B (32 KB per stage, 6 stages), holds its 128 rows of the
+// accumulator in its own TMEM; the leader CTA issues the MMAs and commits
+// multicast to both CTAs' barriers.  CG = 1: one CTA, 128 x 256 tile, 4 stages
+// of 48 KB (used by the router and kept for the measured comparison).
+//
+// Kinds ("rows" = routed rows of one expert segment, from device offsets):
 //   FWD_UP   M=rows N=2x128 K=d  A=gather X (K-major)     B=[W1;W2] stacked   epi: A,B saved, U=SiLU(A)B   Alg.1 l.9
 //   FWD_DOWN M=rows N=256   K=h  A=U rows (K-major)       B=W3 (K-major)      epi: red.add w*O -> Yacc      Alg.1 l.10
 //   BWD_DH   M=rows N=256   K=d  A=gather dY (K-major)    B=W3 (MN-major)     epi: SwiGLU bwd, dA/dB in place,
@@ -22,10 +29,12 @@
 //   BWD_DX   M=rows N=256   K=2h A=dA|dB rows (K-major)   B=W1|W2 (MN-major)  epi: red.add -> dXacc        Alg.1 l.30
 //   DW3      M=d    N=256   K=rows A=gather dY (MN-major) B=wU rows (MN)      epi: store dW3_e             Alg.1 l.18
 //   DW12     M=2h   N=256   K=rows A=dA|dB rows (MN)      B=gather X (MN)     epi: store dW1_e, dW2_e      Alg.1 l.29
-// Rows past a segment end gather the out-of-bounds row T, which TMA fills with
-// zeros: this zero-pads the K tail of the weight-gradient GEMMs in shared
-// memory only (no padded buffer exists in HBM).
+//   ROUTE    M=128 tokens N=E(16-padded) K=d: logits, softmax, top-k epilogue
+// Rows past a segment end are zero-filled in shared memory (cp.async src-size
+// 0, or TMA out-of-bounds fill), which zero-pads the K tail of the weight-
+// gradient GEMMs on chip only (no padded buffer exists in HBM).
 #include <cudaTypedefs.h>
+
 #include <cstdlib>
 
 #include "gemm.h"
@@ -35,17 +44,22 @@ namespace moeb {
 
 enum TcKind { TC_FWD_UP = 0, TC_FWD_DOWN = 1, TC_BWD_DH = 2, TC_BWD_DX = 3, TC_DW3 = 4, TC_DW12 = 5, TC_ROUTE = 6 };
 
-constexpr int TBM = 128, TBN = 256, TBK = 64;
-constexpr int TSTAGES = 4;
-constexpr int TA_BYTES = TBM * TBK * 2;   // 16 KB
-constexpr int TB_BYTES = TBN * TBK * 2;   // 32 KB
-constexpr int TSTAGE_BYTES = TA_BYTES + TB_BYTES;
-constexpr int TC_THREADS = 384;   // 12 warps: 0 TMA, 1 MMA, 2 TMEM, 4-7 epilogue, 8-11 cp.async gathers
+constexpr int TBN = 256, TBK = 64;         // MMA N per tile, K block
+constexpr int TA_BYTES = 128 * TBK * 2;    // 16 KB: 128 rows of A per CTA
+constexpr int TC_THREADS = 384;            // 12 warps
 constexpr int GATHER_THREADS = 128;
-constexpr int TC_SMEM = TSTAGES * TSTAGE_BYTES + 1024 /*align*/ + 1024 /*barriers*/ + 2 * 260 * 4;
+
+template <int CG>
+struct CgCfg {
+  static constexpr int TM = 128 * CG;                   // tile rows per CTA group
+  static constexpr int B_BYTES = (TBN / CG) * TBK * 2;  // B per CTA per stage
+  static constexpr int STAGE = TA_BYTES + B_BYTES;
+  static constexpr int STAGES = CG == 1 ? 4 : 6;
+  static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 1024 /*barriers*/ + 2 * 260 * 4;
+};
 
 struct TcParams {
-  const __nv_bfloat16* x;   // gathered operand sources for the cp.async path
+  const __nv_bfloat16* x;   // gathered operand sources
   const __nv_bfloat16* dy;
   const int32_t* offs;
   const int32_t* eti;
@@ -59,7 +73,7 @@ struct TcParams {
   __nv_bfloat16* out0;
   __nv_bfloat16* out1;
   int T, d, h, E;
-  int n_tiles, m_tiles;
+  int n_tiles, m_tiles, m_tiles2;  // m_tiles at tile height 128 / 256 (weight-gradient kinds)
   int dg_parts;
   // TC_ROUTE (K1): logits = X Wg^T on tensor cores, softmax + top-k in the epilogue
   float* logits;
@@ -72,33 +86,36 @@ struct TcParams {
 template <int KIND>
 struct KindTraits {
   static constexpr bool wgrad = (KIND == TC_DW3 || KIND == TC_DW12);
-  static constexpr bool a_mn = wgrad;                                     // A operand MN-major?
+  static constexpr bool a_mn = wgrad;  // A operand MN-major?
   static constexpr bool b_mn = (KIND == TC_BWD_DH || KIND == TC_BWD_DX || wgrad);
-  static constexpr int NT = (KIND == TC_FWD_UP) ? 128 : 256;             // output columns per tile
+  static constexpr int NT = (KIND == TC_FWD_UP) ? 128 : 256;  // output columns per tile
   static constexpr bool gather_a = (KIND == TC_FWD_UP || KIND == TC_BWD_DH || KIND == TC_DW3);
   static constexpr bool gather_b = (KIND == TC_DW12);
-  // bytes per stage delivered by TMA tile loads (the rest comes from row gathers)
-  __host__ __device__ static constexpr uint32_t tile_bytes(bool cpa) {
-    return cpa ? ((gather_a ? 0u : (uint32_t)TA_BYTES) + (gather_b ? 0u : (uint32_t)TB_BYTES))
-               : (uint32_t)TSTAGE_BYTES;
-  }
-  static constexpr uint32_t IDESC = ptx::umma_idesc_bf16(TBM, TBN, a_mn ? 1 : 0, b_mn ? 1 : 0);
+  static constexpr bool gathered = gather_a || gather_b;
 };
+
+// bytes per CTA per stage delivered by TMA (the rest comes from cp.async gathers)
+template <int KIND, bool CPA, int CG>
+__host__ __device__ constexpr uint32_t tma_bytes_per_cta() {
+  return ((CPA && KindTraits<KIND>::gather_a) ? 0u : (uint32_t)TA_BYTES) +
+         ((CPA && KindTraits<KIND>::gather_b) ? 0u : (uint32_t)CgCfg<CG>::B_BYTES);
+}
 
 struct TileInfo {
   int e, m0, n0, n_tile, seg0, seg1, nk;
 };
 
-template <int KIND>
+template <int KIND, int CG>
 __device__ __forceinline__ bool decode_tile(int tile, const TcParams& P, const int* s_offs, const int* s_tstart,
                                             TileInfo& t) {
   using K = KindTraits<KIND>;
+  constexpr int TM = CgCfg<CG>::TM;
   if constexpr (KIND == TC_ROUTE) {
-    if (tile * TBM >= P.T) return false;
+    if (tile * TM >= P.T) return false;
     t.e = 0;
     t.seg0 = 0;
     t.seg1 = P.T;
-    t.m0 = tile * TBM;
+    t.m0 = tile * TM;
     t.n0 = 0;
     t.n_tile = 0;
     t.nk = P.d / TBK;
@@ -109,7 +126,7 @@ __device__ __forceinline__ bool decode_tile(int tile, const TcParams& P, const i
     const int rem = tile - t.e * per_e;
     const int mt = rem / P.n_tiles;
     t.n_tile = rem - mt * P.n_tiles;
-    t.m0 = mt * TBM;
+    t.m0 = mt * TM;
     t.n0 = t.n_tile * TBN;
     t.seg0 = s_offs[t.e];
     t.seg1 = s_offs[t.e + 1];
@@ -119,10 +136,10 @@ __device__ __forceinline__ bool decode_tile(int tile, const TcParams& P, const i
     t.e = find_segment(s_tstart, P.E, tile);
     t.seg0 = s_offs[t.e];
     t.seg1 = s_offs[t.e + 1];
-    const int mt_e = (t.seg1 - t.seg0 + TBM - 1) / TBM;
+    const int mt_e = (t.seg1 - t.seg0 + TM - 1) / TM;
     const int local = tile - s_tstart[t.e];
     t.n_tile = local / mt_e;
-    t.m0 = t.seg0 + (local - t.n_tile * mt_e) * TBM;
+    t.m0 = t.seg0 + (local - t.n_tile * mt_e) * TM;
     t.n0 = t.n_tile * K::NT;
     const int Kdim = (KIND == TC_FWD_UP || KIND == TC_BWD_DH) ? P.d : (KIND == TC_FWD_DOWN ? P.h : 2 * P.h);
     t.nk = Kdim / TBK;
@@ -155,23 +172,37 @@ __device__ __forceinline__ void load_bf16x32(const __nv_bfloat16* src, float* v)
   }
 }
 
-template <int KIND, bool CPA>
+template <int KIND, bool CPA, int CG>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
                const __grid_constant__ CUtensorMap mB0, const __grid_constant__ CUtensorMap mB1, const TcParams P) {
   using K = KindTraits<KIND>;
+  using C = CgCfg<CG>;
+  static_assert(CG == 1 || CPA, "the CTA-pair path uses the cp.async gather engine");
+  constexpr int STAGES = C::STAGES;
+  constexpr int NB = TBN / CG;     // B columns (rows of the B tile) held by this CTA
+  constexpr int NPANEL = NB / 64;  // 64-column MN-major panels of B in this CTA
+  constexpr uint32_t IDESC = ptx::umma_idesc_bf16(128 * CG, TBN, K::a_mn ? 1 : 0, K::b_mn ? 1 : 0);
+
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + TSTAGES * TSTAGE_BYTES);
-  uint64_t* empty = full + TSTAGES;
-  uint64_t* tfull = empty + TSTAGES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE);
+  uint64_t* empty = full + STAGES;
+  uint64_t* gfull = empty + STAGES;
+  uint64_t* tfull = gfull + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
-  int* s_offs = reinterpret_cast<int*>(smem + TSTAGES * TSTAGE_BYTES + 1024);
+  int* s_offs = reinterpret_cast<int*>(smem + STAGES * C::STAGE + 1024);
   int* s_tstart = s_offs + 260;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int E = P.E;
+  const uint32_t crank = (CG == 2) ? ptx::cluster_ctarank() : 0u;
+  const bool leader = crank == 0;
+  const int rowoff = 128 * (int)crank;  // this CTA's rows within the tile (A / accumulator)
+  const int coloff = NB * (int)crank;   // this CTA's columns of B within the tile
+  const int cluster_id = (CG == 2) ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int n_clusters = (CG == 2) ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
   if constexpr (KIND != TC_ROUTE)
     for (int i = threadIdx.x; i <= E; i += TC_THREADS) s_offs[i] = P.offs[i];
@@ -182,39 +213,47 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
     ptx::tma_prefetch(&mB1);
   }
   if (warp == 1 && lane == 0) {
-    for (int s = 0; s < TSTAGES; ++s) {
-      ptx::mbar_init(&full[s], 1 + ((CPA && (K::gather_a || K::gather_b)) ? GATHER_THREADS : 0));
+    const uint32_t full_count =
+        CG == 1 ? 1 + ((CPA && K::gathered) ? GATHER_THREADS : 0)
+                : 1 + ((CPA && K::gathered) ? 2 : 0);
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full[s], full_count);
       ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&gfull[s], GATHER_THREADS);
     }
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&tfull[s], 1);
-      ptx::mbar_init(&tempty[s], 4);
+      ptx::mbar_init(&tempty[s], 4 * CG);
     }
     ptx::fence_mbar_init();
     ptx::fence_proxy_async();
   }
-  if (warp == 2) ptx::tmem_alloc(tmem_holder, 512);
+  if (warp == 2) {
+    if constexpr (CG == 2) ptx::tmem_alloc_cg2(tmem_holder, 512);
+    else ptx::tmem_alloc(tmem_holder, 512);
+  }
   __syncthreads();
   if (!K::wgrad && KIND != TC_ROUTE && threadIdx.x == 0) {
     int s = 0;
     for (int e = 0; e < E; ++e) {
       s_tstart[e] = s;
-      s += ((s_offs[e + 1] - s_offs[e] + TBM - 1) / TBM) * P.n_tiles;
+      s += ((s_offs[e + 1] - s_offs[e] + C::TM - 1) / C::TM) * P.n_tiles;
     }
     s_tstart[E] = s;
   }
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) ptx::cluster_sync();  // peer barriers initialised + TMEM allocated
+  else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
-  const int oob = P.T;  // gather row index past the end: TMA zero-fills it
 
   if (warp == 0) {
     // ============================ TMA producer ============================
+    const int oob = P.T;  // TMA gather4 row past the end: zero-filled (CG = 1, !CPA only)
     int stage = 0;
     uint32_t phase = 0;
     TileInfo t;
-    for (int tile = blockIdx.x; decode_tile<KIND>(tile, P, s_offs, s_tstart, t); tile += gridDim.x) {
+    for (int tile = cluster_id; decode_tile<KIND, CG>(tile, P, s_offs, s_tstart, t); tile += n_clusters) {
       int gi0 = 0, gi1 = 0, gi2 = 0, gi3 = 0;
       if constexpr (!CPA && (KIND == TC_FWD_UP || KIND == TC_BWD_DH)) {
         const int r = t.m0 + 4 * lane;
@@ -225,34 +264,49 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
       }
       for (int kb = 0; kb < t.nk; ++kb) {
         ptx::mbar_wait(&empty[stage], phase ^ 1);
-        uint8_t* sA = smem + stage * TSTAGE_BYTES;
+        uint8_t* sA = smem + stage * C::STAGE;
         uint8_t* sB = sA + TA_BYTES;
         uint64_t* bar = &full[stage];
-        if (lane == 0)
-          ptx::mbar_arrive_expect_tx(bar, KIND == TC_ROUTE ? (uint32_t)(TA_BYTES + P.route_n * 128)
-                                                           : K::tile_bytes(CPA));
+        const uint32_t bar_c = (CG == 2) ? ptx::mapa(ptx::smem_u32(bar), 0) : 0u;
+        if (lane == 0) {
+          if constexpr (KIND == TC_ROUTE) {
+            ptx::mbar_arrive_expect_tx(bar, (uint32_t)(TA_BYTES + P.route_n * 128));
+          } else if constexpr (CG == 1) {
+            ptx::mbar_arrive_expect_tx(bar, tma_bytes_per_cta<KIND, CPA, CG>());
+          } else {
+            if (leader) ptx::mbar_arrive_expect_tx(bar, 2 * tma_bytes_per_cta<KIND, CPA, CG>());
+          }
+        }
         __syncwarp();
+        auto load = [&](void* dst, const CUtensorMap* m, int c0, int c1) {
+          if constexpr (CG == 2) ptx::tma_load_2d_cg2(dst, m, bar_c, c0, c1);
+          else ptx::tma_load_2d(dst, m, bar, c0, c1);
+        };
         const int k0 = kb * TBK;
         if constexpr (KIND == TC_ROUTE) {
-          if (lane == 0) ptx::tma_load_2d(sA, &mA0, bar, k0, t.m0);
-          if (lane == 1) ptx::tma_load_2d(sB, &mB0, bar, k0, 0);
+          if (lane == 0) load(sA, &mA0, k0, t.m0);
+          if (lane == 1) load(sB, &mB0, k0, 0);
         } else if constexpr (KIND == TC_FWD_UP) {
           if (!CPA) ptx::tma_gather4(sA + 512 * lane, &mA0, bar, k0, gi0, gi1, gi2, gi3);
-          if (lane == 0) ptx::tma_load_2d(sB, &mB0, bar, k0, t.e * P.h + t.n0);
-          if (lane == 1) ptx::tma_load_2d(sB + TB_BYTES / 2, &mB1, bar, k0, t.e * P.h + t.n0);
+          if constexpr (CG == 1) {
+            if (lane == 0) load(sB, &mB0, k0, t.e * P.h + t.n0);
+            if (lane == 1) load(sB + C::B_BYTES / 2, &mB1, k0, t.e * P.h + t.n0);
+          } else {
+            // the pair's B = [W1 tile ; W2 tile]: CTA 0 holds the W1 rows, CTA 1 the W2 rows
+            if (lane == 0) load(sB, crank ? &mB1 : &mB0, k0, t.e * P.h + t.n0);
+          }
         } else if constexpr (KIND == TC_FWD_DOWN) {
-          if (lane == 0) ptx::tma_load_2d(sA, &mA0, bar, k0, t.m0);
-          if (lane == 1) ptx::tma_load_2d(sB, &mB0, bar, k0, t.e * P.d + t.n0);
+          if (lane == 0) load(sA, &mA0, k0, t.m0 + rowoff);
+          if (lane == 1) load(sB, &mB0, k0, t.e * P.d + t.n0 + coloff);
         } else if constexpr (KIND == TC_BWD_DH) {
           if (!CPA) ptx::tma_gather4(sA + 512 * lane, &mA0, bar, k0, gi0, gi1, gi2, gi3);
-          if (lane < 4) ptx::tma_load_2d(sB + lane * 8192, &mB0, bar, t.n0 + 64 * lane, t.e * P.d + k0);
+          if (lane < NPANEL) load(sB + lane * 8192, &mB0, t.n0 + coloff + 64 * lane, t.e * P.d + k0);
         } else if constexpr (KIND == TC_BWD_DX) {
           const bool second = k0 >= P.h;
           const int kk = second ? k0 - P.h : k0;
-          if (lane == 0) ptx::tma_load_2d(sA, second ? &mA1 : &mA0, bar, kk, t.m0);
-          if (lane >= 4 && lane < 8)
-            ptx::tma_load_2d(sB + (lane - 4) * 8192, second ? &mB1 : &mB0, bar, t.n0 + 64 * (lane - 4),
-                             t.e * P.h + kk);
+          if (lane == 0) load(sA, second ? &mA1 : &mA0, kk, t.m0 + rowoff);
+          if (lane >= 4 && lane < 4 + NPANEL)
+            load(sB + (lane - 4) * 8192, second ? &mB1 : &mB0, t.n0 + coloff + 64 * (lane - 4), t.e * P.h + kk);
         } else if constexpr (KIND == TC_DW3) {
           if (!CPA) {
             const int g = lane & 15, p = lane >> 4;
@@ -263,7 +317,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
             const int i3 = r + 3 < t.seg1 ? P.eti[r + 3] : oob;
             ptx::tma_gather4(sA + p * 8192 + g * 512, &mA0, bar, t.m0 + 64 * p, i0, i1, i2, i3);
           }
-          if (lane < 4) ptx::tma_load_2d(sB + lane * 8192, &mB0, bar, t.n0 + 64 * lane, t.seg0 + k0);
+          if (lane < NPANEL) load(sB + lane * 8192, &mB0, t.n0 + coloff + 64 * lane, t.seg0 + k0);
         } else {  // TC_DW12
           if (!CPA) {
             const int g = lane & 15, ph = lane >> 4;
@@ -278,127 +332,175 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
               ptx::tma_gather4(sB + p * 8192 + g * 512, &mB0, bar, t.n0 + 64 * p, i0, i1, i2, i3);
             }
           }
-          const bool second = t.m0 >= P.h;
+          const int m = t.m0 + rowoff;
+          const bool second = m >= P.h;
           if (lane >= 2 && lane < 4)
-            ptx::tma_load_2d(sA + (lane - 2) * 8192, second ? &mA1 : &mA0, bar,
-                             (second ? t.m0 - P.h : t.m0) + 64 * (lane - 2), t.seg0 + k0);
+            load(sA + (lane - 2) * 8192, second ? &mA1 : &mA0, (second ? m - P.h : m) + 64 * (lane - 2), t.seg0 + k0);
         }
-        if (++stage == TSTAGES) { stage = 0; phase ^= 1; }
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp >= 8) {
-    // ======================= cp.async row gathers (CPA) =======================
-    // 128 threads copy the gathered operand 16 B at a time straight into the
-    // 128B-swizzled UMMA layout (chunk c of smem row q lands at q*128 +
-    // ((c ^ (q & 7)) << 4)); rows outside the expert segment are zero-filled.
-    if constexpr (CPA && (K::gather_a || K::gather_b)) {
-      // Lane mapping: consecutive lanes copy consecutive 16-byte chunks of the
-      // same gathered row, so one warp instruction covers whole 128-byte lines.
+    // ======================= cp.async row gathers =======================
+    // Consecutive lanes copy consecutive 16-byte chunks of the same gathered
+    // row (one warp instruction = whole 128-byte lines) into the swizzled
+    // layout: chunk c of smem row q lands at q*128 + ((c ^ (q & 7)) << 4).
+    if constexpr (CPA && K::gathered) {
       const int gt = threadIdx.x - 256;
       int stage = 0;
       uint32_t phase = 0;
       TileInfo t;
       const __nv_bfloat16* src_base = (KIND == TC_FWD_UP || KIND == TC_DW12) ? P.x : P.dy;
-      for (int tile = blockIdx.x; decode_tile<KIND>(tile, P, s_offs, s_tstart, t); tile += gridDim.x) {
+      uint64_t* const done_bar = CG == 2 ? gfull : full;
+      for (int tile = cluster_id; decode_tile<KIND, CG>(tile, P, s_offs, s_tstart, t); tile += n_clusters) {
         if constexpr (KIND == TC_FWD_UP || KIND == TC_BWD_DH) {
-          // K-major A, 128 rows x 8 chunks: thread -> chunk c = gt&7, rows q = (gt>>3) + 16 i
+          // K-major A, this CTA's 128 rows x 8 chunks: chunk c = gt&7, rows (gt>>3) + 16 i
           const int c = gt & 7, rb = gt >> 3;
           const __nv_bfloat16* src[8];
           uint32_t nb[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            const int r = t.m0 + rb + 16 * i;
+            const int r = t.m0 + rowoff + rb + 16 * i;
             const int tok = r < t.seg1 ? P.eti[r] : -1;
             src[i] = src_base + (int64_t)(tok < 0 ? 0 : tok) * P.d + c * 8;
             nb[i] = tok < 0 ? 0u : 16u;
           }
           for (int kb = 0; kb < t.nk; ++kb) {
             ptx::mbar_wait(&empty[stage], phase ^ 1);
-            const uint32_t sbase = ptx::smem_u32(smem + stage * TSTAGE_BYTES);
+            const uint32_t sbase = ptx::smem_u32(smem + stage * C::STAGE);
             const int k0 = kb * TBK;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               const int q = rb + 16 * i;
               ptx::cp_async16(sbase + q * 128 + ((c ^ (q & 7)) << 4), src[i] + k0, nb[i]);
             }
-            ptx::cp_async_mbar_arrive(&full[stage]);
-            if (++stage == TSTAGES) { stage = 0; phase ^= 1; }
+            ptx::cp_async_mbar_arrive(&done_bar[stage]);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
         } else {
-          // MN-major: smem row q = K index (a gathered token row); DW3 copies 2
-          // panels (256 B) of dY per row, DW12 4 panels (512 B) of X per row.
-          constexpr int CPR = (KIND == TC_DW3) ? 16 : 32;       // 16-byte chunks per row
-          constexpr int RPI = GATHER_THREADS / CPR;             // rows per pass
+          // MN-major: smem row q = K index (a gathered token row); this CTA copies
+          // DW3: 2 panels (its 128 M columns of dY); DW12: 4 (CG 1) / 2 (CG 2)
+          // panels of its N columns of X.
+          constexpr int NP = (KIND == TC_DW3) ? 2 : NPANEL;
+          constexpr int CPR = NP * 8;                // 16-byte chunks per row
+          constexpr int RPI = GATHER_THREADS / CPR;  // rows per pass
           constexpr int NPASS = 64 / RPI;
           const int cidx = gt % CPR, rb = gt / CPR;
           const int p = cidx >> 3, cc = cidx & 7;
-          const int col = ((KIND == TC_DW3) ? t.m0 : t.n0) + 64 * p + cc * 8;
+          const int col = ((KIND == TC_DW3) ? t.m0 + rowoff : t.n0 + coloff) + 64 * p + cc * 8;
           const bool col_ok = col < P.d;
           const uint32_t dst_off = ((KIND == TC_DW3) ? 0u : (uint32_t)TA_BYTES) + p * 8192;
+          int tok_next[NPASS];
+#pragma unroll
+          for (int i = 0; i < NPASS; ++i) {
+            const int r = t.seg0 + rb + RPI * i;
+            tok_next[i] = (r < t.seg1 && col_ok) ? P.eti[r] : -1;
+          }
           for (int kb = 0; kb < t.nk; ++kb) {
+            int tok[NPASS];
+#pragma unroll
+            for (int i = 0; i < NPASS; ++i) tok[i] = tok_next[i];
+            if (kb + 1 < t.nk) {  // prefetch the next k-block's row indices
+#pragma unroll
+              for (int i = 0; i < NPASS; ++i) {
+                const int r = t.seg0 + (kb + 1) * TBK + rb + RPI * i;
+                tok_next[i] = (r < t.seg1 && col_ok) ? P.eti[r] : -1;
+              }
+            }
             ptx::mbar_wait(&empty[stage], phase ^ 1);
-            const uint32_t sbase = ptx::smem_u32(smem + stage * TSTAGE_BYTES) + dst_off;
-            const int k0 = t.seg0 + kb * TBK;
+            const uint32_t sbase = ptx::smem_u32(smem + stage * C::STAGE) + dst_off;
 #pragma unroll
             for (int i = 0; i < NPASS; ++i) {
               const int q = rb + RPI * i;
-              const int r = k0 + q;
-              const int tok = (r < t.seg1 && col_ok) ? P.eti[r] : -1;
-              const __nv_bfloat16* sp = src_base + (int64_t)(tok < 0 ? 0 : tok) * P.d + (col_ok ? col : 0);
-              ptx::cp_async16(sbase + q * 128 + ((cc ^ (q & 7)) << 4), sp, tok < 0 ? 0u : 16u);
+              const __nv_bfloat16* sp = src_base + (int64_t)(tok[i] < 0 ? 0 : tok[i]) * P.d + (col_ok ? col : 0);
+              ptx::cp_async16(sbase + q * 128 + ((cc ^ (q & 7)) << 4), sp, tok[i] < 0 ? 0u : 16u);
             }
-            ptx::cp_async_mbar_arrive(&full[stage]);
-            if (++stage == TSTAGES) { stage = 0; phase ^= 1; }
+            ptx::cp_async_mbar_arrive(&done_bar[stage]);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
+        }
+      }
+    }
+  } else if (warp == 3) {
+    // ============ CTA pair: relay this CTA's gather completion to the leader ============
+    // The whole warp runs the loop (it stays converged for the final .aligned
+    // cluster barrier); lane 0 relays.  The local barrier completes only once
+    // this CTA's cp.async writes have landed, so the relay is a relaxed
+    // arrive after a generic->async proxy fence: a release.cluster arrive
+    // would add a GPU-scope membar per k-block (measured 2x slower).
+    if constexpr (CG == 2 && K::gathered) {
+      int stage = 0;
+      uint32_t phase = 0;
+      TileInfo t;
+      for (int tile = cluster_id; decode_tile<KIND, CG>(tile, P, s_offs, s_tstart, t); tile += n_clusters) {
+        for (int kb = 0; kb < t.nk; ++kb) {
+          ptx::mbar_wait(&gfull[stage], phase);
+          if (lane == 0) {
+            ptx::fence_proxy_async();
+            ptx::mbar_arrive_cluster_relaxed(ptx::mapa(ptx::smem_u32(&full[stage]), 0));
+          }
+          __syncwarp();
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
     // ============================ MMA issuer ============================
-    int stage = 0;
-    uint32_t phase = 0;
-    int as = 0;
-    uint32_t aphase = 0;
-    TileInfo t;
-    for (int tile = blockIdx.x; decode_tile<KIND>(tile, P, s_offs, s_tstart, t); tile += gridDim.x) {
-      ptx::mbar_wait(&tempty[as], aphase ^ 1);
-      ptx::tc_fence_after();
-      const uint32_t d_tmem = tmem_base + as * TBN;
-      for (int kb = 0; kb < t.nk; ++kb) {
-        ptx::mbar_wait(&full[stage], phase);
-        if (CPA) ptx::fence_proxy_async();  // cp.async (generic proxy) writes -> tcgen05 operand reads
+    if (CG == 1 || leader) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int as = 0;
+      uint32_t aphase = 0;
+      TileInfo t;
+      const uint32_t idesc = (KIND == TC_ROUTE) ? P.route_idesc : IDESC;
+      for (int tile = cluster_id; decode_tile<KIND, CG>(tile, P, s_offs, s_tstart, t); tile += n_clusters) {
+        if constexpr (CG == 2) ptx::mbar_wait_cluster(&tempty[as], aphase ^ 1);
+        else ptx::mbar_wait(&tempty[as], aphase ^ 1);
         ptx::tc_fence_after();
-        if (lane == 0) {
-          const uint32_t sA = ptx::smem_u32(smem + stage * TSTAGE_BYTES);
-          const uint32_t sB = sA + TA_BYTES;
+        const uint32_t d_tmem = tmem_base + as * TBN;
+        for (int kb = 0; kb < t.nk; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          if (CPA && K::gathered) ptx::fence_proxy_async();  // cp.async (generic proxy) -> tcgen05 reads
+          ptx::tc_fence_after();
+          if (lane == 0) {
+            const uint32_t sA = ptx::smem_u32(smem + stage * C::STAGE);
+            const uint32_t sB = sA + TA_BYTES;
 #pragma unroll
-          for (int ks = 0; ks < TBK / 16; ++ks) {
-            const uint64_t ad = K::a_mn ? ptx::umma_desc_sw128(sA + ks * 2048, 8192, 1024)
-                                        : ptx::umma_desc_sw128(sA + ks * 32, 16, 1024);
-            const uint64_t bd = K::b_mn ? ptx::umma_desc_sw128(sB + ks * 2048, 8192, 1024)
-                                        : ptx::umma_desc_sw128(sB + ks * 32, 16, 1024);
-            ptx::umma_bf16(d_tmem, ad, bd, KIND == TC_ROUTE ? P.route_idesc : K::IDESC, (kb | ks) != 0);
+            for (int ks = 0; ks < TBK / 16; ++ks) {
+              const uint64_t ad = K::a_mn ? ptx::umma_desc_sw128(sA + ks * 2048, 8192, 1024)
+                                          : ptx::umma_desc_sw128(sA + ks * 32, 16, 1024);
+              const uint64_t bd = K::b_mn ? ptx::umma_desc_sw128(sB + ks * 2048, 8192, 1024)
+                                          : ptx::umma_desc_sw128(sB + ks * 32, 16, 1024);
+              if constexpr (CG == 2) ptx::umma_bf16_cg2(d_tmem, ad, bd, idesc, (kb | ks) != 0);
+              else ptx::umma_bf16(d_tmem, ad, bd, idesc, (kb | ks) != 0);
+            }
+            if constexpr (CG == 2) ptx::umma_commit_cg2(&empty[stage], 0x3);
+            else ptx::umma_commit(&empty[stage]);
           }
-          ptx::umma_commit(&empty[stage]);
+          __syncwarp();
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (lane == 0) {
+          if (t.nk > 0) {
+            if constexpr (CG == 2) ptx::umma_commit_cg2(&tfull[as], 0x3);
+            else ptx::umma_commit(&tfull[as]);
+          } else {
+            ptx::mbar_arrive(&tfull[as]);
+            if constexpr (CG == 2) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tfull[as]), 1));
+          }
         }
         __syncwarp();
-        if (++stage == TSTAGES) { stage = 0; phase ^= 1; }
+        if (++as == 2) { as = 0; aphase ^= 1; }
       }
-      if (lane == 0) {
-        if (t.nk > 0) ptx::umma_commit(&tfull[as]);
-        else ptx::mbar_arrive(&tfull[as]);
-      }
-      __syncwarp();
-      if (++as == 2) { as = 0; aphase ^= 1; }
     }
   } else if (warp >= 4 && warp < 8) {
     // ============================ epilogue ============================
     const int wq = warp & 3;
-    const int row = wq * 32 + lane;
+    const int row = rowoff + wq * 32 + lane;  // row of the tile owned by this thread
     int as = 0;
     uint32_t aphase = 0;
     TileInfo t;
-    for (int tile = blockIdx.x; decode_tile<KIND>(tile, P, s_offs, s_tstart, t); tile += gridDim.x) {
+    for (int tile = cluster_id; decode_tile<KIND, CG>(tile, P, s_offs, s_tstart, t); tile += n_clusters) {
       ptx::mbar_wait(&tfull[as], aphase);
       ptx::tc_fence_after();
       const uint32_t tb = tmem_base + ((uint32_t)(wq * 32) << 16) + as * TBN;
@@ -407,7 +509,6 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
         // one token row per thread: logits out, softmax, top-k (desc, ties -> lower id)
         const int r = t.m0 + row;
         const bool valid = r < P.T;
-        const int E = P.E;
         float mx = -INFINITY;
 #pragma unroll 1
         for (int c = 0; c < P.route_n; c += 32) {
@@ -549,6 +650,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
         if (valid) P.dg_part[(int64_t)r * P.dg_parts + t.n_tile] = rowsum;
       } else {  // DW3 / DW12: store the weight-gradient tile
         const int m = t.m0 + row;
+        const int M = (KIND == TC_DW3) ? P.d : 2 * P.h;
         __nv_bfloat16* dst;
         int N;
         if constexpr (KIND == TC_DW3) {
@@ -572,19 +674,25 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
 #pragma unroll
             for (int i = 0; i < 32; ++i) f[i] = 0.f;
           }
-          store_bf16x32(dst + t.n0 + c, f);
+          if (m < M) store_bf16x32(dst + t.n0 + c, f);
         }
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&tempty[as]);
+      if (lane == 0) {
+        if constexpr (CG == 2) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty[as]), 0));
+        else ptx::mbar_arrive(&tempty[as]);
+      }
       if (++as == 2) { as = 0; aphase ^= 1; }
     }
   }
-  __syncthreads();
+  ptx::tc_fence_before();
+  if constexpr (CG == 2) ptx::cluster_sync();
+  else __syncthreads();
   if (warp == 2) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem_base, 512);
+    if constexpr (CG == 2) ptx::tmem_dealloc_cg2(tmem_base, 512);
+    else ptx::tmem_dealloc(tmem_base, 512);
   }
 }
 
@@ -627,38 +735,62 @@ static int num_sms() {
   return n;
 }
 
-// Row-gather engine: cp.async producer warps (default) or TMA tile::gather4
-// (MOEBLAZE_GATHER=tma; kept for the measured comparison in DESIGN.md).
-static bool use_cpasync() {
+// Engine selection (MOEBLAZE_GEMM): "pair" (default) = CTA pair + cp.async
+// gathers; "cta" = one CTA per tile + cp.async gathers; "tma" = one CTA per
+// tile + TMA tile::gather4.  The alternatives are kept for the measured
+// comparison in DESIGN.md / profiles.
+enum Engine { ENG_PAIR = 0, ENG_CTA = 1, ENG_TMA = 2 };
+static Engine engine() {
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("MOEBLAZE_GATHER");
-    v = (e && e[0] == 't') ? 0 : 1;
+    const char* e = getenv("MOEBLAZE_GEMM");
+    v = ENG_PAIR;
+    if (e && e[0] == 'c') v = ENG_CTA;
+    if (e && e[0] == 't') v = ENG_TMA;
   }
-  return v == 1;
+  return (Engine)v;
 }
 
-template <int KIND, bool CPA>
+template <int KIND, bool CPA, int CG>
 static moe_status launch_tc_impl(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0,
-                                 const CUtensorMap& b1, const TcParams& P, int grid, cudaStream_t st) {
+                                 const CUtensorMap& b1, const TcParams& P, int64_t tiles, cudaStream_t st) {
   static bool attr = false;
+  auto kern = tc_gemm_kernel<KIND, CPA, CG>;
   if (!attr) {
-    if (cudaFuncSetAttribute(tc_gemm_kernel<KIND, CPA>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM) !=
-        cudaSuccess)
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CgCfg<CG>::SMEM) != cudaSuccess)
       return MOE_ERR_CUDA;
     attr = true;
   }
-  MOE_LAUNCH((tc_gemm_kernel<KIND, CPA>), grid, TC_THREADS, TC_SMEM, st, a0, a1, b0, b1, P);
+  if (tiles <= 0) return MOE_OK;
+  const int groups = (int)std::min<int64_t>(tiles, num_sms() / CG);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(groups * CG);
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = CgCfg<CG>::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = CG;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, kern, a0, a1, b0, b1, P) != cudaSuccess) return MOE_ERR_CUDA;
+  note_launch();
   return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
 }
 
-template <int KIND>
+// tiles_for(TM): number of tiles (an upper bound for row kinds) at tile height TM
+template <int KIND, typename F>
 static moe_status launch_tc(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0,
-                            const CUtensorMap& b1, const TcParams& P, int64_t tiles_upper, cudaStream_t st) {
-  if (tiles_upper <= 0) return MOE_OK;
-  const int grid = (int)std::min<int64_t>(tiles_upper, num_sms());
-  if (use_cpasync()) return launch_tc_impl<KIND, true>(a0, a1, b0, b1, P, grid, st);
-  return launch_tc_impl<KIND, false>(a0, a1, b0, b1, P, grid, st);
+                            const CUtensorMap& b1, TcParams P, F tiles_for, cudaStream_t st) {
+  switch (engine()) {
+    case ENG_PAIR:
+      P.m_tiles = P.m_tiles2;
+      return launch_tc_impl<KIND, true, 2>(a0, a1, b0, b1, P, tiles_for(256), st);
+    case ENG_CTA: return launch_tc_impl<KIND, true, 1>(a0, a1, b0, b1, P, tiles_for(128), st);
+    default: return launch_tc_impl<KIND, false, 1>(a0, a1, b0, b1, P, tiles_for(128), st);
+  }
 }
 
 int tc_dg_parts(int h) { return (int)ceil_div(h, TBN); }
@@ -672,18 +804,17 @@ moe_status tc_route(const moe_problem* p, const void* x, const void* wg, float* 
   P.T = (int)p->T; P.d = p->d; P.h = p->h; P.E = p->E;
   P.logits = logits; P.ids = ids; P.route_w = topw; P.k = p->k; P.renorm = p->renormalize;
   P.route_n = std::max(16, (int)ceil_div(p->E, 16) * 16);
-  P.route_idesc = ptx::umma_idesc_bf16(TBM, P.route_n, 0, 0);
+  P.route_idesc = ptx::umma_idesc_bf16(128, P.route_n, 0, 0);
   CUtensorMap a0, b0;
   if (!make_map(&a0, x, p->T, p->d, 64, 128) || !make_map(&b0, wg, p->E, p->d, 64, P.route_n)) return MOE_ERR_CUDA;
-  const int64_t tiles = ceil_div(p->T, TBM);
-  const int grid = (int)std::min<int64_t>(tiles, num_sms());
-  return launch_tc_impl<TC_ROUTE, false>(a0, a0, b0, b0, P, grid, st);
+  return launch_tc_impl<TC_ROUTE, false, 1>(a0, a0, b0, b0, P, ceil_div(p->T, 128), st);
 }
 
 moe_status tc_gemm(const GemmCall& c, cudaStream_t st) {
   typedef __nv_bfloat16 bf;
   const int64_t T = c.T, R = c.R;
   const int d = c.d, h = c.h, E = c.E;
+  const uint32_t bw = engine() == ENG_PAIR ? 128 : 256;  // K-major W3 box rows held per CTA
   TcParams P{};
   P.x = (const bf*)c.x; P.dy = (const bf*)c.dy;
   P.offs = c.offs; P.eti = c.eti; P.row_slot = c.row_slot; P.topw = c.topw;
@@ -694,7 +825,8 @@ moe_status tc_gemm(const GemmCall& c, cudaStream_t st) {
   P.dg_parts = tc_dg_parts(h);
   CUtensorMap a0, a1, b0, b1;
   bool ok = true;
-  const int64_t mt_upper = ceil_div(R, TBM) + E;
+  // upper bound on row tiles of height TM over all expert segments
+  auto rows_tiles = [&](int64_t n_tiles) { return [=](int TM) { return (ceil_div(R, TM) + E) * n_tiles; }; };
   switch (c.which) {
     case GEMM_FWD_UP: {
       if (R == 0) return MOE_OK;
@@ -703,15 +835,15 @@ moe_status tc_gemm(const GemmCall& c, cudaStream_t st) {
       ok &= make_map(&b1, c.w2, (uint64_t)E * h, d, 64, 128);
       if (!ok) return MOE_ERR_CUDA;
       P.n_tiles = h / 128;
-      return launch_tc<TC_FWD_UP>(a0, a0, b0, b1, P, mt_upper * P.n_tiles, st);
+      return launch_tc<TC_FWD_UP>(a0, a0, b0, b1, P, rows_tiles(P.n_tiles), st);
     }
     case GEMM_FWD_DOWN: {
       if (R == 0) return MOE_OK;
       ok &= make_map(&a0, c.u, R, h, 64, 128);
-      ok &= make_map(&b0, c.w3, (uint64_t)E * d, h, 64, 256);
+      ok &= make_map(&b0, c.w3, (uint64_t)E * d, h, 64, bw);
       if (!ok) return MOE_ERR_CUDA;
       P.n_tiles = (int)ceil_div(d, TBN);
-      return launch_tc<TC_FWD_DOWN>(a0, a0, b0, b0, P, mt_upper * P.n_tiles, st);
+      return launch_tc<TC_FWD_DOWN>(a0, a0, b0, b0, P, rows_tiles(P.n_tiles), st);
     }
     case GEMM_BWD_DH: {
       if (R == 0) return MOE_OK;
@@ -719,7 +851,7 @@ moe_status tc_gemm(const GemmCall& c, cudaStream_t st) {
       ok &= make_map(&b0, c.w3, (uint64_t)E * d, h, 64, 64);
       if (!ok) return MOE_ERR_CUDA;
       P.n_tiles = (int)ceil_div(h, TBN);
-      return launch_tc<TC_BWD_DH>(a0, a0, b0, b0, P, mt_upper * P.n_tiles, st);
+      return launch_tc<TC_BWD_DH>(a0, a0, b0, b0, P, rows_tiles(P.n_tiles), st);
     }
     case GEMM_BWD_DX: {
       if (R == 0) return MOE_OK;
@@ -729,7 +861,7 @@ moe_status tc_gemm(const GemmCall& c, cudaStream_t st) {
       ok &= make_map(&b1, c.w2, (uint64_t)E * h, d, 64, 64);
       if (!ok) return MOE_ERR_CUDA;
       P.n_tiles = (int)ceil_div(d, TBN);
-      return launch_tc<TC_BWD_DX>(a0, a1, b0, b1, P, mt_upper * P.n_tiles, st);
+      return launch_tc<TC_BWD_DX>(a0, a1, b0, b1, P, rows_tiles(P.n_tiles), st);
     }
     case GEMM_DW3: {
       if (R == 0) {  // no rows at all: every expert's gradient is exactly zero
@@ -739,9 +871,11 @@ moe_status tc_gemm(const GemmCall& c, cudaStream_t st) {
       ok &= make_map(&a0, c.dy, T, d, 64, 1);
       ok &= make_map(&b0, c.u, R, h, 64, 64);
       if (!ok) return MOE_ERR_CUDA;
-      P.m_tiles = d / TBM;
       P.n_tiles = (int)ceil_div(h, TBN);
-      return launch_tc<TC_DW3>(a0, a0, b0, b0, P, (int64_t)E * P.m_tiles * P.n_tiles, st);
+      P.m_tiles = (int)ceil_div(d, 128);
+      P.m_tiles2 = (int)ceil_div(d, 256);
+      const int64_t nt = P.n_tiles;
+      return launch_tc<TC_DW3>(a0, a0, b0, b0, P, [=](int TM) { return (int64_t)E * ceil_div(d, TM) * nt; }, st);
     }
     case GEMM_DW12: {
       if (R == 0) {
@@ -753,9 +887,12 @@ moe_status tc_gemm(const GemmCall& c, cudaStream_t st) {
       ok &= make_map(&a1, c.b_save, R, h, 64, 64);
       ok &= make_map(&b0, c.x, T, d, 64, 1);
       if (!ok) return MOE_ERR_CUDA;
-      P.m_tiles = 2 * h / TBM;
       P.n_tiles = (int)ceil_div(d, TBN);
-      return launch_tc<TC_DW12>(a0, a1, b0, b0, P, (int64_t)E * P.m_tiles * P.n_tiles, st);
+      P.m_tiles = (int)ceil_div(2 * h, 128);
+      P.m_tiles2 = (int)ceil_div(2 * h, 256);
+      const int64_t nt = P.n_tiles;
+      return launch_tc<TC_DW12>(a0, a1, b0, b0, P, [=](int TM) { return (int64_t)E * ceil_div(2 * h, TM) * nt; },
+                                st);
     }
   }
   return MOE_ERR_INVALID_ARG;

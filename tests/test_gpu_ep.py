@@ -49,7 +49,9 @@ def _worker(rank, P, port, q):
     wl = [W[n][lo:hi].contiguous().to(dev) for n in ("w1", "w2", "w3")]
     y, g = ep.step(x, W["w_gate"].to(dev), *wl, dy)
     torch.cuda.synchronize()
-    q.put((rank, y.cpu(), {n: v.cpu() for n, v in g.items()}, (lo, hi)))
+    # numpy (pickled by value): torch tensors would be shared by fd and can
+    # vanish when this worker exits before the parent reads the queue
+    q.put((rank, y.float().cpu().numpy(), {n: v.float().cpu().numpy() for n, v in g.items()}, (lo, hi)))
     dist.barrier()
     dist.destroy_process_group()
 
