@@ -60,51 +60,128 @@ __global__ void router_bwd_kernel(const float* __restrict__ logits, const int32_
 }
 
 // partial[c][e][col] = sum_{t in chunk c} dlogits[t,e] X[t,col].
-// Block: 256 columns (one per thread) x ET experts (registers) x one token chunk;
-// X is read exactly once over the grid (coalesced rows), dlogits tiles are
-// staged in shared memory and read as float4 broadcasts.
-constexpr int WG_COLS = 256;
+// Block: 128 columns x ET experts x one token chunk; thread = 4 columns x
+// ET/8 experts in registers; 32-token tiles of X and dlogits staged in shared
+// memory (fp32) and read as float4: X is read exactly once over the grid.
+constexpr int WG_COLS = 128;
 constexpr int WG_TT = 32;  // tokens per shared-memory tile
 template <typename T, int ET>
 __global__ void __launch_bounds__(256) dwg_partial_kernel(const float* __restrict__ dlogits, const T* __restrict__ x,
                                                           int64_t Tn, int d, int E, int64_t tch,
                                                           float* __restrict__ part) {
-  __shared__ __align__(16) float dl[WG_TT][ET];
-  const int col = blockIdx.x * WG_COLS + threadIdx.x;
+  constexpr int EPT = ET / 8;  // experts per thread
+  __shared__ __align__(16) float xs[WG_TT][WG_COLS];
+  __shared__ __align__(16) float ds[WG_TT][ET];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int c0 = blockIdx.x * WG_COLS;
   const int e0 = blockIdx.y * ET;
   const int64_t ta = blockIdx.z * tch, tb = min64(ta + tch, Tn);
-  float acc[ET];
+  float acc[EPT][4];
 #pragma unroll
-  for (int i = 0; i < ET; ++i) acc[i] = 0.f;
+  for (int i = 0; i < EPT; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
   for (int64_t t0 = ta; t0 < tb; t0 += WG_TT) {
     const int nt = (int)min64(WG_TT, tb - t0);
     __syncthreads();
+    for (int i = threadIdx.x; i < WG_TT * WG_COLS; i += 256) {
+      const int r = i / WG_COLS, c = i % WG_COLS;
+      xs[r][c] = (r < nt && c0 + c < d) ? to_f32(x[(t0 + r) * d + c0 + c]) : 0.f;
+    }
     for (int i = threadIdx.x; i < WG_TT * ET; i += 256) {
       const int r = i / ET, e = i % ET;
-      dl[r][e] = (r < nt && e0 + e < E) ? dlogits[(t0 + r) * E + e0 + e] : 0.f;
+      ds[r][e] = (r < nt && e0 + e < E) ? dlogits[(t0 + r) * E + e0 + e] : 0.f;
     }
     __syncthreads();
-    if (col < d) {
-      float xv[WG_TT];
-#pragma unroll
-      for (int r = 0; r < WG_TT; ++r) xv[r] = r < nt ? to_f32(x[(t0 + r) * d + col]) : 0.f;
 #pragma unroll 4
-      for (int r = 0; r < WG_TT; ++r) {
+    for (int r = 0; r < WG_TT; ++r) {
+      const float4 xv = *reinterpret_cast<const float4*>(&xs[r][4 * tx]);
+      float dv[EPT];
+      if constexpr (EPT % 4 == 0) {
 #pragma unroll
-        for (int e = 0; e < ET; e += 4) {
-          const float4 w = *reinterpret_cast<const float4*>(&dl[r][e]);
-          acc[e] = fmaf(w.x, xv[r], acc[e]);
-          acc[e + 1] = fmaf(w.y, xv[r], acc[e + 1]);
-          acc[e + 2] = fmaf(w.z, xv[r], acc[e + 2]);
-          acc[e + 3] = fmaf(w.w, xv[r], acc[e + 3]);
+        for (int q = 0; q < EPT; q += 4) {
+          const float4 t4 = *reinterpret_cast<const float4*>(&ds[r][ty * EPT + q]);
+          dv[q] = t4.x; dv[q + 1] = t4.y; dv[q + 2] = t4.z; dv[q + 3] = t4.w;
         }
+      } else {
+#pragma unroll
+        for (int q = 0; q < EPT; ++q) dv[q] = ds[r][ty * EPT + q];
+      }
+#pragma unroll
+      for (int q = 0; q < EPT; ++q) {
+        acc[q][0] = fmaf(dv[q], xv.x, acc[q][0]);
+        acc[q][1] = fmaf(dv[q], xv.y, acc[q][1]);
+        acc[q][2] = fmaf(dv[q], xv.z, acc[q][2]);
+        acc[q][3] = fmaf(dv[q], xv.w, acc[q][3]);
       }
     }
   }
-  if (col < d) {
 #pragma unroll
-    for (int e = 0; e < ET; ++e)
-      if (e0 + e < E) part[((int64_t)blockIdx.z * E + e0 + e) * d + col] = acc[e];
+  for (int q = 0; q < EPT; ++q) {
+    const int e = e0 + ty * EPT + q;
+    if (e >= E) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int col = c0 + 4 * tx + j;
+      if (col < d) part[((int64_t)blockIdx.z * E + e) * d + col] = acc[q][j];
+    }
+  }
+}
+
+// dx[t, :] = dtype(acc[t, :] + sum_e dl[t, e] Wg[e, :]) — the router's share of
+// the token gradient, fused with the fp32 -> dtype finalisation.  Block: 64
+// tokens x 128 columns; thread = 8 tokens x 4 columns; experts in chunks of 32
+// (W_g chunk and dl^T chunk staged in shared memory as fp32).
+template <typename T, typename A>
+__global__ void __launch_bounds__(256) router_dx_kernel(const A* __restrict__ acc, const float* __restrict__ dl,
+                                                        const T* __restrict__ wg, int64_t Tn, int d, int E,
+                                                        T* __restrict__ out) {
+  __shared__ __align__(16) float ws_[32][128];
+  __shared__ __align__(16) float dsT[32][64];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t t0 = (int64_t)blockIdx.y * 64;
+  const int c0 = blockIdx.x * 128;
+  const int col = c0 + 4 * tx;
+  float a[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t t = t0 + ty * 8 + i;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) a[i][j] = (t < Tn && col + j < d) ? to_f32(acc[t * d + col + j]) : 0.f;
+  }
+  for (int e0 = 0; e0 < E; e0 += 32) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < 32 * 128; i += 256) {
+      const int e = i / 128, c = i % 128;
+      ws_[e][c] = (e0 + e < E && c0 + c < d) ? to_f32(wg[(int64_t)(e0 + e) * d + c0 + c]) : 0.f;
+    }
+    for (int i = threadIdx.x; i < 32 * 64; i += 256) {
+      const int r = i / 32, e = i % 32;
+      dsT[e][r] = (t0 + r < Tn && e0 + e < E) ? dl[(t0 + r) * E + e0 + e] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int e = 0; e < 32; ++e) {
+      const float4 w = *reinterpret_cast<const float4*>(&ws_[e][4 * tx]);
+      const float4 p0 = *reinterpret_cast<const float4*>(&dsT[e][ty * 8]);
+      const float4 p1 = *reinterpret_cast<const float4*>(&dsT[e][ty * 8 + 4]);
+      const float pv[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        a[i][0] = fmaf(pv[i], w.x, a[i][0]);
+        a[i][1] = fmaf(pv[i], w.y, a[i][1]);
+        a[i][2] = fmaf(pv[i], w.z, a[i][2]);
+        a[i][3] = fmaf(pv[i], w.w, a[i][3]);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t t = t0 + ty * 8 + i;
+    if (t >= Tn) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (col + j < d) out[t * d + col + j] = from_f32<T>(a[i][j]);
   }
 }
 
@@ -199,7 +276,7 @@ moe_status launch_dg_reduce(const float* part, int nparts, const int32_t* tim, i
   return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
 }
 
-static int dwg_et(int E) { return E <= 8 ? 8 : (E <= 16 ? 16 : 32); }
+static int dwg_et(int E) { return E <= 8 ? 8 : (E <= 16 ? 16 : (E <= 32 ? 32 : 64)); }
 
 int dwg_chunks(int64_t T, int d) {
   // token chunks so that (column blocks x chunks) >= ~3 waves of 148 SMs, >= 128 tokens per chunk
@@ -216,7 +293,8 @@ static void launch_dwg_partial(const float* dl, const T* x, int64_t Tn, int d, i
   dim3 grid((unsigned)ceil_div(d, WG_COLS), (unsigned)ceil_div(E, et), nch);
   if (et == 8) MOE_LAUNCH((dwg_partial_kernel<T, 8>), grid, 256, 0, st, dl, x, Tn, d, E, tch, part);
   else if (et == 16) MOE_LAUNCH((dwg_partial_kernel<T, 16>), grid, 256, 0, st, dl, x, Tn, d, E, tch, part);
-  else MOE_LAUNCH((dwg_partial_kernel<T, 32>), grid, 256, 0, st, dl, x, Tn, d, E, tch, part);
+  else if (et == 32) MOE_LAUNCH((dwg_partial_kernel<T, 32>), grid, 256, 0, st, dl, x, Tn, d, E, tch, part);
+  else MOE_LAUNCH((dwg_partial_kernel<T, 64>), grid, 256, 0, st, dl, x, Tn, d, E, tch, part);
 }
 
 moe_status launch_router_bwd(const moe_problem* p, const float* logits, const int32_t* ids, const float* dg,
@@ -244,9 +322,23 @@ moe_status launch_router_bwd(const moe_problem* p, const float* logits, const in
 moe_status launch_finalize(const moe_problem* p, const void* acc, const float* dl, const void* wg, void* out,
                            cudaStream_t st, bool acc_is_dtype) {
   if (p->T == 0) return MOE_OK;
-  dim3 grid((unsigned)ceil_div(p->d, 256), (unsigned)ceil_div(p->T, 16));
-  size_t sm = dl ? sizeof(float) * 16 * p->E : 0;
   typedef __nv_bfloat16 bf;
+  if (dl) {
+    dim3 g2((unsigned)ceil_div(p->d, 128), (unsigned)ceil_div(p->T, 64));
+    if (p->dtype == MOE_BF16) {
+      if (acc_is_dtype)
+        MOE_LAUNCH((router_dx_kernel<bf, bf>), g2, 256, 0, st, (const bf*)acc, dl, (const bf*)wg, p->T, p->d, p->E, (bf*)out);
+      else
+        MOE_LAUNCH((router_dx_kernel<bf, float>), g2, 256, 0, st, (const float*)acc, dl, (const bf*)wg, p->T, p->d, p->E,
+                   (bf*)out);
+    } else {
+      MOE_LAUNCH((router_dx_kernel<float, float>), g2, 256, 0, st, (const float*)acc, dl, (const float*)wg, p->T, p->d,
+                 p->E, (float*)out);
+    }
+    return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
+  }
+  dim3 grid((unsigned)ceil_div(p->d, 256), (unsigned)ceil_div(p->T, 16));
+  size_t sm = 0;
   if (p->dtype == MOE_BF16) {
     if (acc_is_dtype)
       MOE_LAUNCH((finalize_kernel<bf, bf>), grid, 256, sm, st, (const bf*)acc, dl, (const bf*)wg, p->T, p->d, p->E, (bf*)out);
