@@ -148,7 +148,7 @@ def main():
     ap.add_argument("--renormalize", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-memory", action="store_true")
-    ap.add_argument("--cpu-budget-s", type=float, default=15.0)
+    ap.add_argument("--cpu-budget-s", type=float, default=10.0)
     ap.add_argument("--ep", action="store_true", help="use the expert-parallel path even at N = 1")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

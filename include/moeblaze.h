@@ -30,7 +30,7 @@
  *  - Argument errors are returned synchronously and nothing is launched:
  *    MOE_ERR_INVALID_ARG (null pointer, bad shape: T < 0, d/h/E/k < 1, k > E,
  *    E > 256, k > 16, T*k >= 2^31), MOE_ERR_UNSUPPORTED (bf16 with d or h not
- *    a multiple of 128, or a device that is not sm_100), MOE_ERR_MISALIGNED,
+ *    a multiple of 128, fp32 with d not a multiple of 8), MOE_ERR_MISALIGNED,
  *    MOE_ERR_WORKSPACE (ws too small).  Launch failures return MOE_ERR_CUDA.
  *    The library never aborts the process.
  *  - T = 0 is valid: nothing is launched except zero-fills of outputs.

@@ -16,7 +16,7 @@ moe_status launch_route(const moe_problem*, const void*, const void*, float*, in
 moe_status launch_dispatch(const moe_problem*, const int32_t*, const moe_dispatch*, int32_t*, int32_t*, cudaStream_t);
 size_t dispatch_ws_bytes(const moe_problem*);
 moe_status launch_dg_reduce(const float*, int, const int32_t*, int64_t, float*, cudaStream_t);
-int dwg_chunks(int64_t T, int d);
+int dwg_chunks(int64_t T, int d, int E);
 moe_status launch_router_bwd(const moe_problem*, const float*, const int32_t*, const float*, const void*, float*,
                              float*, void*, cudaStream_t);
 moe_status launch_finalize(const moe_problem*, const void*, const float*, const void*, void*, cudaStream_t, bool);
@@ -33,7 +33,7 @@ static moe_status validate(const moe_problem* p) {
   if (p->T * (int64_t)p->k >= (int64_t(1) << 31)) return MOE_ERR_INVALID_ARG;
   if (p->dtype != MOE_BF16 && p->dtype != MOE_FP32) return MOE_ERR_INVALID_ARG;
   if (p->dtype == MOE_BF16 && (p->d % 128 != 0 || p->h % 128 != 0)) return MOE_ERR_UNSUPPORTED;
-  if (p->dtype == MOE_FP32 && (p->d % 4 != 0)) return MOE_ERR_UNSUPPORTED;
+  if (p->dtype == MOE_FP32 && (p->d % 8 != 0)) return MOE_ERR_UNSUPPORTED;
   return MOE_OK;
 }
 
@@ -62,7 +62,7 @@ static RouterWs router_layout(const moe_problem* p, void* base) {
   size_t o = 0;
   RouterWs w;
   w.dlogits = (float*)(b + o); o += align256((size_t)p->T * p->E * 4);
-  w.dwgpart = (float*)(b + o); o += align256((size_t)dwg_chunks(p->T, p->d) * p->E * p->d * 4);
+  w.dwgpart = (float*)(b + o); o += align256((size_t)dwg_chunks(p->T, p->d, p->E) * p->E * p->d * 4);
   w.total = o;
   return w;
 }
@@ -77,7 +77,7 @@ static BwdWs bwd_layout(const moe_problem* p, void* base) {
   w.dxacc = (float*)(b + o); o += align256((size_t)p->T * p->d * 4);
   w.dgpart = (float*)(b + o); o += align256((size_t)R * dg_parts(p) * 4);
   w.dlogits = (float*)(b + o); o += align256((size_t)p->T * p->E * 4);
-  w.dwgpart = (float*)(b + o); o += align256((size_t)dwg_chunks(p->T, p->d) * p->E * p->d * 4);
+  w.dwgpart = (float*)(b + o); o += align256((size_t)dwg_chunks(p->T, p->d, p->E) * p->E * p->d * 4);
   w.dg = (float*)(b + o); o += align256((size_t)R * 4);
   w.total = o;
   return w;

@@ -59,129 +59,174 @@ __global__ void router_bwd_kernel(const float* __restrict__ logits, const int32_
   }
 }
 
+// 8 consecutive elements of a row as fp32 (16-byte load for bf16, 2 x 16 for fp32)
+__device__ __forceinline__ void load8(const __nv_bfloat16* p, float* v) {
+  const uint4 q = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(h[i]);
+    v[2 * i] = f.x;
+    v[2 * i + 1] = f.y;
+  }
+}
+__device__ __forceinline__ void load8(const float* p, float* v) {
+  const float4 a = *reinterpret_cast<const float4*>(p);
+  const float4 b = *reinterpret_cast<const float4*>(p + 4);
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void store8(__nv_bfloat16* p, const float* v) {
+  uint4 q;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&q);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+  *reinterpret_cast<uint4*>(p) = q;
+}
+__device__ __forceinline__ void store8(float* p, const float* v) {
+  *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  *reinterpret_cast<float4*>(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
+}
+
 // partial[c][e][col] = sum_{t in chunk c} dlogits[t,e] X[t,col].
-// Block: 128 columns x ET experts x one token chunk; thread = 4 columns x
-// ET/8 experts in registers; 32-token tiles of X and dlogits staged in shared
-// memory (fp32) and read as float4: X is read exactly once over the grid.
-constexpr int WG_COLS = 128;
-constexpr int WG_TT = 32;  // tokens per shared-memory tile
-template <typename T, int ET>
+// Thread tile: 8 consecutive columns x 8 experts (64 fp32 accumulators).
+// Block = 256 threads = CGR column groups x EGR expert groups (EGR =
+// ceil(E/8) <= 8).  X streams through a double-buffered 16 KB shared-memory
+// tile filled with 16-byte cp.async (TT = 4*EGR tokens per tile) so enough
+// bytes are in flight to run at HBM speed; the chunk's dlogits rows are
+// staged alongside.  X is read exactly once.  Requires d % 8 == 0.
+__device__ __forceinline__ void cpa16(void* dst, const void* src, bool ok) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(ok ? 16u : 0u) : "memory");
+}
+template <typename T, int EGR>
 __global__ void __launch_bounds__(256) dwg_partial_kernel(const float* __restrict__ dlogits, const T* __restrict__ x,
                                                           int64_t Tn, int d, int E, int64_t tch,
                                                           float* __restrict__ part) {
-  constexpr int EPT = ET / 8;  // experts per thread
-  __shared__ __align__(16) float xs[WG_TT][WG_COLS];
-  __shared__ __align__(16) float ds[WG_TT][ET];
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int c0 = blockIdx.x * WG_COLS;
-  const int e0 = blockIdx.y * ET;
-  const int64_t ta = blockIdx.z * tch, tb = min64(ta + tch, Tn);
-  float acc[EPT][4];
+  constexpr int CGR = 256 / EGR;            // column groups (8 columns each)
+  constexpr int COLS = CGR * 8;             // columns per block
+  constexpr int TT = 16384 / (COLS * (int)sizeof(T)) > 0 ? 16384 / (COLS * (int)sizeof(T)) : 1;  // tokens per tile
+  constexpr int VPR = COLS * (int)sizeof(T) / 16;  // 16-byte vectors per token row of the tile
+  __shared__ __align__(16) uint8_t xs_raw[2][TT * COLS * sizeof(T)];
+  __shared__ __align__(16) float ds[2][TT][EGR * 8];
+  const int cg = threadIdx.x % CGR, eg = threadIdx.x / CGR;
+  const int c0 = blockIdx.x * COLS;
+  const int col = c0 + cg * 8;
+  const int64_t ta = blockIdx.y * tch, tb = min64(ta + tch, Tn);
+  const int ntiles = (int)ceil_div(tb - ta, TT);
+  float acc[8][8];
 #pragma unroll
-  for (int i = 0; i < EPT; ++i)
+  for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
-  for (int64_t t0 = ta; t0 < tb; t0 += WG_TT) {
-    const int nt = (int)min64(WG_TT, tb - t0);
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+  auto issue = [&](int it, int buf) {
+    const int64_t t0 = ta + (int64_t)it * TT;
+    T* xs = reinterpret_cast<T*>(xs_raw[buf]);
+    for (int v = threadIdx.x; v < TT * VPR; v += 256) {
+      const int r = v / VPR, cv = v % VPR;
+      const int64_t t = t0 + r;
+      const int cc = cv * (16 / (int)sizeof(T));
+      const bool ok = t < tb && c0 + cc < d;
+      cpa16(xs + r * COLS + cc, ok ? (const void*)(x + t * d + c0 + cc) : (const void*)x, ok);
+    }
+    for (int v = threadIdx.x; v < TT * EGR * 8; v += 256) {
+      const int r = v / (EGR * 8), e = v % (EGR * 8);
+      const int64_t t = t0 + r;
+      ds[buf][r][e] = (t < tb && e < E) ? dlogits[t * E + e] : 0.f;
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (ntiles > 0) issue(0, 0);
+  for (int it = 0; it < ntiles; ++it) {
+    const int buf = it & 1;
+    if (it + 1 < ntiles) {
+      issue(it + 1, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
     __syncthreads();
-    for (int i = threadIdx.x; i < WG_TT * WG_COLS; i += 256) {
-      const int r = i / WG_COLS, c = i % WG_COLS;
-      xs[r][c] = (r < nt && c0 + c < d) ? to_f32(x[(t0 + r) * d + c0 + c]) : 0.f;
-    }
-    for (int i = threadIdx.x; i < WG_TT * ET; i += 256) {
-      const int r = i / ET, e = i % ET;
-      ds[r][e] = (r < nt && e0 + e < E) ? dlogits[(t0 + r) * E + e0 + e] : 0.f;
+    const T* xs = reinterpret_cast<const T*>(xs_raw[buf]);
+#pragma unroll
+    for (int r = 0; r < TT; ++r) {
+      float xv[8];
+      load8(xs + r * COLS + cg * 8, xv);
+      const float4 e0 = *reinterpret_cast<const float4*>(&ds[buf][r][eg * 8]);
+      const float4 e1 = *reinterpret_cast<const float4*>(&ds[buf][r][eg * 8 + 4]);
+      const float ev[8] = {e0.x, e0.y, e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[q][j] = fmaf(ev[q], xv[j], acc[q][j]);
     }
     __syncthreads();
-#pragma unroll 4
-    for (int r = 0; r < WG_TT; ++r) {
-      const float4 xv = *reinterpret_cast<const float4*>(&xs[r][4 * tx]);
-      float dv[EPT];
-      if constexpr (EPT % 4 == 0) {
-#pragma unroll
-        for (int q = 0; q < EPT; q += 4) {
-          const float4 t4 = *reinterpret_cast<const float4*>(&ds[r][ty * EPT + q]);
-          dv[q] = t4.x; dv[q + 1] = t4.y; dv[q + 2] = t4.z; dv[q + 3] = t4.w;
-        }
-      } else {
-#pragma unroll
-        for (int q = 0; q < EPT; ++q) dv[q] = ds[r][ty * EPT + q];
-      }
-#pragma unroll
-      for (int q = 0; q < EPT; ++q) {
-        acc[q][0] = fmaf(dv[q], xv.x, acc[q][0]);
-        acc[q][1] = fmaf(dv[q], xv.y, acc[q][1]);
-        acc[q][2] = fmaf(dv[q], xv.z, acc[q][2]);
-        acc[q][3] = fmaf(dv[q], xv.w, acc[q][3]);
-      }
-    }
   }
+  if (col < d) {
 #pragma unroll
-  for (int q = 0; q < EPT; ++q) {
-    const int e = e0 + ty * EPT + q;
-    if (e >= E) continue;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int col = c0 + 4 * tx + j;
-      if (col < d) part[((int64_t)blockIdx.z * E + e) * d + col] = acc[q][j];
+    for (int q = 0; q < 8; ++q) {
+      const int e = eg * 8 + q;
+      if (e < E) store8(part + ((int64_t)blockIdx.y * E + e) * d + col, acc[q]);
     }
   }
 }
 
 // dx[t, :] = dtype(acc[t, :] + sum_e dl[t, e] Wg[e, :]) — the router's share of
-// the token gradient, fused with the fp32 -> dtype finalisation.  Block: 64
-// tokens x 128 columns; thread = 8 tokens x 4 columns; experts in chunks of 32
-// (W_g chunk and dl^T chunk staged in shared memory as fp32).
+// the token gradient fused with the fp32 -> dtype finalisation.  Thread tile:
+// 8 consecutive columns (one 16-byte W_g load per expert, L1/L2-resident) x 8
+// tokens; block = 32 column groups (256 columns) x 8 token groups (64 tokens);
+// a warp shares its token group, so the dlogits reads are smem broadcasts.
 template <typename T, typename A>
 __global__ void __launch_bounds__(256) router_dx_kernel(const A* __restrict__ acc, const float* __restrict__ dl,
                                                         const T* __restrict__ wg, int64_t Tn, int d, int E,
                                                         T* __restrict__ out) {
-  __shared__ __align__(16) float ws_[32][128];
-  __shared__ __align__(16) float dsT[32][64];
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  __shared__ __align__(16) float wsm[32][256];  // W_g chunk: 32 experts x 256 columns (fp32)
+  __shared__ float dsm[32][64 + 1];             // dlogits chunk: 32 experts x 64 tokens
+  const int cg = threadIdx.x & 31, tg = threadIdx.x >> 5;
   const int64_t t0 = (int64_t)blockIdx.y * 64;
-  const int c0 = blockIdx.x * 128;
-  const int col = c0 + 4 * tx;
-  float a[8][4];
+  const int c0 = blockIdx.x * 256;
+  const int col = c0 + cg * 8;
+  float a[8][8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    const int64_t t = t0 + ty * 8 + i;
+    const int64_t t = t0 + tg * 8 + i;
+    if (t < Tn && col < d) load8(acc + t * d + col, a[i]);
+    else
 #pragma unroll
-    for (int j = 0; j < 4; ++j) a[i][j] = (t < Tn && col + j < d) ? to_f32(acc[t * d + col + j]) : 0.f;
+      for (int j = 0; j < 8; ++j) a[i][j] = 0.f;
   }
   for (int e0 = 0; e0 < E; e0 += 32) {
     __syncthreads();
-    for (int i = threadIdx.x; i < 32 * 128; i += 256) {
-      const int e = i / 128, c = i % 128;
-      ws_[e][c] = (e0 + e < E && c0 + c < d) ? to_f32(wg[(int64_t)(e0 + e) * d + c0 + c]) : 0.f;
+    for (int v = threadIdx.x; v < 32 * 32; v += 256) {  // 32 experts x 32 vectors of 8 columns
+      const int e = v / 32, cv = v % 32;
+      float w[8];
+      if (e0 + e < E && c0 + cv * 8 < d) load8(wg + (int64_t)(e0 + e) * d + c0 + cv * 8, w);
+      else
+#pragma unroll
+        for (int j = 0; j < 8; ++j) w[j] = 0.f;
+      store8(&wsm[e][cv * 8], w);
     }
-    for (int i = threadIdx.x; i < 32 * 64; i += 256) {
-      const int r = i / 32, e = i % 32;
-      dsT[e][r] = (t0 + r < Tn && e0 + e < E) ? dl[(t0 + r) * E + e0 + e] : 0.f;
+    for (int v = threadIdx.x; v < 64 * 32; v += 256) {
+      const int r = v / 32, e = v % 32;
+      dsm[e][r] = (t0 + r < Tn && e0 + e < E) ? dl[(t0 + r) * E + e0 + e] : 0.f;
     }
     __syncthreads();
+    const int ne = min(32, E - e0);
 #pragma unroll 4
-    for (int e = 0; e < 32; ++e) {
-      const float4 w = *reinterpret_cast<const float4*>(&ws_[e][4 * tx]);
-      const float4 p0 = *reinterpret_cast<const float4*>(&dsT[e][ty * 8]);
-      const float4 p1 = *reinterpret_cast<const float4*>(&dsT[e][ty * 8 + 4]);
-      const float pv[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+    for (int e = 0; e < ne; ++e) {
+      float w[8];
+      load8(&wsm[e][cg * 8], w);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        a[i][0] = fmaf(pv[i], w.x, a[i][0]);
-        a[i][1] = fmaf(pv[i], w.y, a[i][1]);
-        a[i][2] = fmaf(pv[i], w.z, a[i][2]);
-        a[i][3] = fmaf(pv[i], w.w, a[i][3]);
+        const float p = dsm[e][tg * 8 + i];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a[i][j] = fmaf(p, w[j], a[i][j]);
       }
     }
   }
+  if (col >= d) return;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    const int64_t t = t0 + ty * 8 + i;
-    if (t >= Tn) continue;
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (col + j < d) out[t * d + col + j] = from_f32<T>(a[i][j]);
+    const int64_t t = t0 + tg * 8 + i;
+    if (t < Tn) store8(out + t * d + col, a[i]);
   }
 }
 
@@ -276,25 +321,29 @@ moe_status launch_dg_reduce(const float* part, int nparts, const int32_t* tim, i
   return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
 }
 
-static int dwg_et(int E) { return E <= 8 ? 8 : (E <= 16 ? 16 : (E <= 32 ? 32 : 64)); }
+static int dwg_egr(int E) {
+  const int g = (int)ceil_div(E, 8);
+  return g <= 1 ? 1 : (g <= 2 ? 2 : (g <= 4 ? 4 : 8));
+}
 
-int dwg_chunks(int64_t T, int d) {
-  // token chunks so that (column blocks x chunks) >= ~3 waves of 148 SMs, >= 128 tokens per chunk
-  const int64_t colb = ceil_div(d, WG_COLS);
+int dwg_chunks(int64_t T, int d, int E) {
+  // column blocks x token chunks >= ~3 waves of 148 SMs, >= 64 tokens per chunk
+  const int64_t colb = ceil_div(d, 8 * (256 / dwg_egr(E)));
   int64_t nch = ceil_div(3 * 148, colb);
-  nch = std::min<int64_t>(nch, std::max<int64_t>(1, T / 128));
+  nch = std::min<int64_t>(nch, std::max<int64_t>(1, T / 64));
   return (int)std::max<int64_t>(1, std::min<int64_t>(nch, 256));
 }
 
 template <typename T>
 static void launch_dwg_partial(const float* dl, const T* x, int64_t Tn, int d, int E, int nch, int64_t tch, float* part,
                                cudaStream_t st) {
-  const int et = dwg_et(E);
-  dim3 grid((unsigned)ceil_div(d, WG_COLS), (unsigned)ceil_div(E, et), nch);
-  if (et == 8) MOE_LAUNCH((dwg_partial_kernel<T, 8>), grid, 256, 0, st, dl, x, Tn, d, E, tch, part);
-  else if (et == 16) MOE_LAUNCH((dwg_partial_kernel<T, 16>), grid, 256, 0, st, dl, x, Tn, d, E, tch, part);
-  else if (et == 32) MOE_LAUNCH((dwg_partial_kernel<T, 32>), grid, 256, 0, st, dl, x, Tn, d, E, tch, part);
-  else MOE_LAUNCH((dwg_partial_kernel<T, 64>), grid, 256, 0, st, dl, x, Tn, d, E, tch, part);
+  const int egr = dwg_egr(E);
+  const int cols_per_block = 8 * (256 / egr);
+  dim3 grid((unsigned)ceil_div(d, cols_per_block), nch);
+  if (egr == 1) MOE_LAUNCH((dwg_partial_kernel<T, 1>), grid, 256, 0, st, dl, x, Tn, d, E, tch, part);
+  else if (egr == 2) MOE_LAUNCH((dwg_partial_kernel<T, 2>), grid, 256, 0, st, dl, x, Tn, d, E, tch, part);
+  else if (egr == 4) MOE_LAUNCH((dwg_partial_kernel<T, 4>), grid, 256, 0, st, dl, x, Tn, d, E, tch, part);
+  else MOE_LAUNCH((dwg_partial_kernel<T, 8>), grid, 256, 0, st, dl, x, Tn, d, E, tch, part);
 }
 
 moe_status launch_router_bwd(const moe_problem* p, const float* logits, const int32_t* ids, const float* dg,
@@ -305,7 +354,7 @@ moe_status launch_router_bwd(const moe_problem* p, const float* logits, const in
     MOE_LAUNCH(router_bwd_kernel, (unsigned)ceil_div(T * 32, 256), 256, 0, st, logits, ids, dg, T, E, p->k,
                p->renormalize, dlogits);
   }
-  const int nch = dwg_chunks(T, d);
+  const int nch = dwg_chunks(T, d, E);
   const int64_t tch = ceil_div(std::max<int64_t>(T, 1), nch);
   const int64_t n = (int64_t)E * d;
   if (p->dtype == MOE_BF16) {
@@ -324,16 +373,18 @@ moe_status launch_finalize(const moe_problem* p, const void* acc, const float* d
   if (p->T == 0) return MOE_OK;
   typedef __nv_bfloat16 bf;
   if (dl) {
-    dim3 g2((unsigned)ceil_div(p->d, 128), (unsigned)ceil_div(p->T, 64));
+    dim3 g2((unsigned)ceil_div(p->d, 256), (unsigned)ceil_div(p->T, 64));
+    const size_t sm2 = 0;
     if (p->dtype == MOE_BF16) {
       if (acc_is_dtype)
-        MOE_LAUNCH((router_dx_kernel<bf, bf>), g2, 256, 0, st, (const bf*)acc, dl, (const bf*)wg, p->T, p->d, p->E, (bf*)out);
-      else
-        MOE_LAUNCH((router_dx_kernel<bf, float>), g2, 256, 0, st, (const float*)acc, dl, (const bf*)wg, p->T, p->d, p->E,
+        MOE_LAUNCH((router_dx_kernel<bf, bf>), g2, 256, sm2, st, (const bf*)acc, dl, (const bf*)wg, p->T, p->d, p->E,
                    (bf*)out);
+      else
+        MOE_LAUNCH((router_dx_kernel<bf, float>), g2, 256, sm2, st, (const float*)acc, dl, (const bf*)wg, p->T, p->d,
+                   p->E, (bf*)out);
     } else {
-      MOE_LAUNCH((router_dx_kernel<float, float>), g2, 256, 0, st, (const float*)acc, dl, (const float*)wg, p->T, p->d,
-                 p->E, (float*)out);
+      MOE_LAUNCH((router_dx_kernel<float, float>), g2, 256, sm2, st, (const float*)acc, dl, (const float*)wg, p->T,
+                 p->d, p->E, (float*)out);
     }
     return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
   }
