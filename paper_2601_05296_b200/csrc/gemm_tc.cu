@@ -49,13 +49,17 @@ constexpr int TA_BYTES = 128 * TBK * 2;    // 16 KB: 128 rows of A per CTA
 constexpr int TC_THREADS = 384;            // 12 warps
 constexpr int GATHER_THREADS = 128;
 
-template <int CG>
+template <int CG, int KIND = 0>
 struct CgCfg {
   static constexpr int TM = 128 * CG;                   // tile rows per CTA group
   static constexpr int B_BYTES = (TBN / CG) * TBK * 2;  // B per CTA per stage
   static constexpr int STAGE = TA_BYTES + B_BYTES;
-  static constexpr int STAGES = CG == 1 ? 4 : 6;
-  static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 1024 /*barriers*/ + 2 * 260 * 4;
+  // BWD_DH double-buffers its epilogue inputs (A, B chunks): one stage less
+  static constexpr bool DH = (KIND == 2);
+  static constexpr int STAGES = (CG == 1 ? 4 : 6) - (DH ? 1 : 0);
+  static constexpr int STG_WARP = DH ? 10240 : 6144;    // epilogue staging bytes per warp
+  static constexpr int STG_OFF = STAGES * STAGE + 1024 /*barriers*/ + 2176 /*offsets, tile starts*/;
+  static constexpr int SMEM = STG_OFF + 4 * STG_WARP + 1024 /*align*/;
 };
 
 struct TcParams {
@@ -172,12 +176,76 @@ __device__ __forceinline__ void load_bf16x32(const __nv_bfloat16* src, float* v)
   }
 }
 
+// ---------------------------------------------------------------- epilogue staging
+// Each epilogue warp owns 32 accumulator rows (one per lane).  Its 32-column
+// chunks go through a small swizzled shared tile so that global loads,
+// stores and red.adds are issued row-coalesced (8 lanes x 16 B per 128 B line)
+// instead of one 16-byte access per lane on 32 different lines.
+// bf16 tile: 32 rows x 64 B, 16-byte chunk q of row i at i*64 + ((q ^ ((i>>1)&3)) << 4)
+// fp32 tile: 32 rows x 128 B, chunk q (0..7) of row i at i*128 + ((q ^ (i&7)) << 4)
+__device__ __forceinline__ uint32_t stg16_off(int i, int q) { return i * 64 + ((q ^ ((i >> 1) & 3)) << 4); }
+__device__ __forceinline__ uint32_t stg32_off(int i, int q) { return i * 128 + ((q ^ (i & 7)) << 4); }
+
+__device__ __forceinline__ void stg_put_bf16(uint8_t* stg, int i, const float* v) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint4 u;
+    u.x = ptx::pack_bf16(v[8 * q + 0], v[8 * q + 1]);
+    u.y = ptx::pack_bf16(v[8 * q + 2], v[8 * q + 3]);
+    u.z = ptx::pack_bf16(v[8 * q + 4], v[8 * q + 5]);
+    u.w = ptx::pack_bf16(v[8 * q + 6], v[8 * q + 7]);
+    *reinterpret_cast<uint4*>(stg + stg16_off(i, q)) = u;
+  }
+}
+__device__ __forceinline__ void stg_get_bf16(const uint8_t* stg, int i, float* v) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint4 u = *reinterpret_cast<const uint4*>(stg + stg16_off(i, q));
+    float2 f;
+    f = ptx::unpack_bf16(u.x); v[8 * q + 0] = f.x; v[8 * q + 1] = f.y;
+    f = ptx::unpack_bf16(u.y); v[8 * q + 2] = f.x; v[8 * q + 3] = f.y;
+    f = ptx::unpack_bf16(u.z); v[8 * q + 4] = f.x; v[8 * q + 5] = f.y;
+    f = ptx::unpack_bf16(u.w); v[8 * q + 6] = f.x; v[8 * q + 7] = f.y;
+  }
+}
+// rows [0, nvalid) of the tile <-> global rows base + row * ld (32 bf16 columns each)
+__device__ __forceinline__ void stg_store_bf16(const uint8_t* stg, int lane, __nv_bfloat16* base, int64_t ld,
+                                               int nvalid) {
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    const int row = it * 8 + (lane >> 2), q = lane & 3;
+    if (row < nvalid)
+      *reinterpret_cast<uint4*>(base + row * ld + q * 8) = *reinterpret_cast<const uint4*>(stg + stg16_off(row, q));
+  }
+}
+__device__ __forceinline__ void stg_load_bf16(uint8_t* stg, int lane, const __nv_bfloat16* base, int64_t ld,
+                                              int nvalid) {
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    const int row = it * 8 + (lane >> 2), q = lane & 3;
+    uint4 u = make_uint4(0, 0, 0, 0);
+    if (row < nvalid) u = *reinterpret_cast<const uint4*>(base + row * ld + q * 8);
+    *reinterpret_cast<uint4*>(stg + stg16_off(row, q)) = u;
+  }
+}
+
+__device__ __forceinline__ void stg_load_bf16_async(uint8_t* stg, int lane, const __nv_bfloat16* base, int64_t ld,
+                                                    int nvalid) {
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    const int row = it * 8 + (lane >> 2), q = lane & 3;
+    const bool ok = row < nvalid;
+    ptx::cp_async16(ptx::smem_u32(stg + stg16_off(row, q)), ok ? (const void*)(base + row * ld + q * 8) : (const void*)base,
+                    ok ? 16u : 0u);
+  }
+}
+
 template <int KIND, bool CPA, int CG>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
                const __grid_constant__ CUtensorMap mB0, const __grid_constant__ CUtensorMap mB1, const TcParams P) {
   using K = KindTraits<KIND>;
-  using C = CgCfg<CG>;
+  using C = CgCfg<CG, KIND>;
   static_assert(CG == 1 || CPA, "the CTA-pair path uses the cp.async gather engine");
   constexpr int STAGES = C::STAGES;
   constexpr int NB = TBN / CG;     // B columns (rows of the B tile) held by this CTA
@@ -497,6 +565,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
     // ============================ epilogue ============================
     const int wq = warp & 3;
     const int row = rowoff + wq * 32 + lane;  // row of the tile owned by this thread
+    uint8_t* stg = smem + C::STG_OFF + wq * C::STG_WARP;  // this warp's staging tiles
     int as = 0;
     uint32_t aphase = 0;
     TileInfo t;
@@ -568,35 +637,44 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
           }
         }
       } else if constexpr (KIND == TC_FWD_UP) {
-        const int r = t.m0 + row;
-        const bool valid = r < t.seg1;
+        const int r0w = t.m0 + rowoff + wq * 32;  // first row of this warp
+        const int nvalid = max(0, min(32, t.seg1 - r0w));
+        uint8_t* T0 = stg;
+        uint8_t* T1 = stg + 2048;
+        uint8_t* T2 = stg + 4096;
         uint32_t bv[32];
 #pragma unroll 1
         for (int c = 0; c < 128; c += 32) {
           ptx::tmem_ld32(tb + c, v);
           ptx::tmem_ld32(tb + 128 + c, bv);
           ptx::tmem_wait_ld();
-          if (valid) {
-            float a[32], b[32], u[32];
+          float a[32], b[32], u[32];
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              a[i] = __uint_as_float(v[i]);
-              b[i] = __uint_as_float(bv[i]);
-              u[i] = a[i] * sigmoidf_(a[i]) * b[i];
-            }
-            const int64_t o = (int64_t)r * P.h + t.n0 + c;
-            store_bf16x32(P.a_save + o, a);
-            store_bf16x32(P.b_save + o, b);
-            store_bf16x32(P.u + o, u);
+          for (int i = 0; i < 32; ++i) {
+            a[i] = __uint_as_float(v[i]);
+            b[i] = __uint_as_float(bv[i]);
+            u[i] = a[i] * sigmoidf_(a[i]) * b[i];
           }
+          stg_put_bf16(T0, lane, a);
+          stg_put_bf16(T1, lane, b);
+          stg_put_bf16(T2, lane, u);
+          __syncwarp();
+          if (nvalid > 0) {
+            const int64_t o = (int64_t)r0w * P.h + t.n0 + c;
+            stg_store_bf16(T0, lane, P.a_save + o, P.h, nvalid);
+            stg_store_bf16(T1, lane, P.b_save + o, P.h, nvalid);
+            stg_store_bf16(T2, lane, P.u + o, P.h, nvalid);
+          }
+          __syncwarp();
         }
       } else if constexpr (KIND == TC_FWD_DOWN || KIND == TC_BWD_DX) {
         const int r = t.m0 + row;
-        const bool valid = r < t.seg1;
+        const int r0w = t.m0 + rowoff + wq * 32;
+        const int nvalid = max(0, min(32, t.seg1 - r0w));
         const int N = P.d;
         float w = 1.f;
-        int64_t tok = 0;
-        if (valid) {
+        int tok = 0;
+        if (r < t.seg1) {
           tok = P.eti[r];
           if constexpr (KIND == TC_FWD_DOWN) w = P.topw[P.row_slot[r]];
         }
@@ -605,61 +683,123 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
           if (t.n0 + c >= N) break;
           ptx::tmem_ld32(tb + c, v);
           ptx::tmem_wait_ld();
-          if (valid) {
-            float* dst = P.acc_out + tok * N + t.n0 + c;
 #pragma unroll
-            for (int i = 0; i < 32; i += 4)
-              ptx::red_add_v4(dst + i, w * __uint_as_float(v[i]), w * __uint_as_float(v[i + 1]),
-                              w * __uint_as_float(v[i + 2]), w * __uint_as_float(v[i + 3]));
+          for (int q = 0; q < 8; ++q)
+            *reinterpret_cast<float4*>(stg + stg32_off(lane, q)) =
+                make_float4(w * __uint_as_float(v[4 * q]), w * __uint_as_float(v[4 * q + 1]),
+                            w * __uint_as_float(v[4 * q + 2]), w * __uint_as_float(v[4 * q + 3]));
+          __syncwarp();
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            const int rr = it * 4 + (lane >> 3), q = lane & 7;
+            const int tr = __shfl_sync(0xffffffffu, tok, rr);
+            if (rr < nvalid) {
+              const float4 f = *reinterpret_cast<const float4*>(stg + stg32_off(rr, q));
+              ptx::red_add_v4(P.acc_out + (int64_t)tr * N + t.n0 + c + 4 * q, f.x, f.y, f.z, f.w);
+            }
           }
+          __syncwarp();
         }
       } else if constexpr (KIND == TC_BWD_DH) {
+        // A, B chunks of 32 columns are prefetched one chunk ahead with cp.async
+        // into double-buffered staging tiles (buf: A at +0, B at +2048); dA and
+        // dB overwrite the consumed input tiles, wU goes to its own tile.
         const int r = t.m0 + row;
         const bool valid = r < t.seg1;
+        const int r0w = t.m0 + rowoff + wq * 32;
+        const int nvalid = max(0, min(32, t.seg1 - r0w));
         const float w = valid ? P.topw[P.row_slot[r]] : 0.f;
+        uint8_t* TU = stg + 8192;
+        const int nchunk = min(TBN, P.h - t.n0) / 32;
+        const int64_t o0 = (int64_t)r0w * P.h + t.n0;
         float rowsum = 0.f;
+        stg_load_bf16_async(stg, lane, P.a_save + o0, P.h, nvalid);
+        stg_load_bf16_async(stg + 2048, lane, P.b_save + o0, P.h, nvalid);
+        asm volatile("cp.async.commit_group;" ::: "memory");
 #pragma unroll 1
-        for (int c = 0; c < TBN; c += 32) {
-          if (t.n0 + c >= P.h) break;
-          ptx::tmem_ld32(tb + c, v);
-          ptx::tmem_wait_ld();
-          if (valid) {
-            const int64_t o = (int64_t)r * P.h + t.n0 + c;
-            float a[32], b[32];
-            load_bf16x32(P.a_save + o, a);
-            load_bf16x32(P.b_save + o, b);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const float dH = __uint_as_float(v[i]);
-              const float s = sigmoidf_(a[i]);
-              const float S = a[i] * s;
-              const float U = S * b[i];
-              rowsum = fmaf(dH, U, rowsum);
-              const float dU = w * dH;
-              const float dA = dU * b[i] * s * (1.f + a[i] * (1.f - s));
-              const float dB = dU * S;
-              a[i] = dA;
-              b[i] = dB;
-              v[i] = __float_as_uint(w * U);
-            }
-            store_bf16x32(P.a_save + o, a);
-            store_bf16x32(P.b_save + o, b);
-            store_bf16x32(P.u + o, reinterpret_cast<float*>(v));
+        for (int ci = 0; ci < nchunk; ++ci) {
+          uint8_t* TA = stg + (ci & 1) * 4096;
+          uint8_t* TB = TA + 2048;
+          if (ci + 1 < nchunk) {  // prefetch the next chunk into the other buffer
+            uint8_t* NA = stg + ((ci + 1) & 1) * 4096;
+            stg_load_bf16_async(NA, lane, P.a_save + o0 + (ci + 1) * 32, P.h, nvalid);
+            stg_load_bf16_async(NA + 2048, lane, P.b_save + o0 + (ci + 1) * 32, P.h, nvalid);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+          } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
           }
+          __syncwarp();
+#pragma unroll 1
+          for (int hf = 0; hf < 2; ++hf) {  // two 16-column halves keep the register footprint small
+            uint32_t v16[16];
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+                "%14, %15}, [%16];"
+                : "=r"(v16[0]), "=r"(v16[1]), "=r"(v16[2]), "=r"(v16[3]), "=r"(v16[4]), "=r"(v16[5]), "=r"(v16[6]),
+                  "=r"(v16[7]), "=r"(v16[8]), "=r"(v16[9]), "=r"(v16[10]), "=r"(v16[11]), "=r"(v16[12]),
+                  "=r"(v16[13]), "=r"(v16[14]), "=r"(v16[15])
+                : "r"(tb + ci * 32 + hf * 16));
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int qq = 0; qq < 2; ++qq) {
+              const int q = hf * 2 + qq;
+              const uint4 ua = *reinterpret_cast<const uint4*>(TA + stg16_off(lane, q));
+              const uint4 ub = *reinterpret_cast<const uint4*>(TB + stg16_off(lane, q));
+              const uint32_t* pa = reinterpret_cast<const uint32_t*>(&ua);
+              const uint32_t* pb = reinterpret_cast<const uint32_t*>(&ub);
+              uint32_t oa[4], ob[4], ou[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 a2 = ptx::unpack_bf16(pa[e]);
+                const float2 b2 = ptx::unpack_bf16(pb[e]);
+                float ra[2], rb[2], ru[2];
+                const float av[2] = {a2.x, a2.y}, bvv[2] = {b2.x, b2.y};
+#pragma unroll
+                for (int z = 0; z < 2; ++z) {
+                  const float dH = __uint_as_float(v16[qq * 8 + e * 2 + z]);
+                  const float a = av[z], b = bvv[z];
+                  const float sg = sigmoidf_(a);
+                  const float S = a * sg;
+                  const float U = S * b;
+                  rowsum = fmaf(dH, U, rowsum);
+                  const float dU = w * dH;
+                  ra[z] = dU * b * sg * (1.f + a * (1.f - sg));
+                  rb[z] = dU * S;
+                  ru[z] = w * U;
+                }
+                oa[e] = ptx::pack_bf16(ra[0], ra[1]);
+                ob[e] = ptx::pack_bf16(rb[0], rb[1]);
+                ou[e] = ptx::pack_bf16(ru[0], ru[1]);
+              }
+              *reinterpret_cast<uint4*>(TA + stg16_off(lane, q)) = make_uint4(oa[0], oa[1], oa[2], oa[3]);
+              *reinterpret_cast<uint4*>(TB + stg16_off(lane, q)) = make_uint4(ob[0], ob[1], ob[2], ob[3]);
+              *reinterpret_cast<uint4*>(TU + stg16_off(lane, q)) = make_uint4(ou[0], ou[1], ou[2], ou[3]);
+            }
+          }
+          __syncwarp();
+          if (nvalid > 0) {
+            const int64_t o = o0 + ci * 32;
+            stg_store_bf16(TA, lane, P.a_save + o, P.h, nvalid);
+            stg_store_bf16(TB, lane, P.b_save + o, P.h, nvalid);
+            stg_store_bf16(TU, lane, P.u + o, P.h, nvalid);
+          }
+          __syncwarp();
         }
         if (valid) P.dg_part[(int64_t)r * P.dg_parts + t.n_tile] = rowsum;
       } else {  // DW3 / DW12: store the weight-gradient tile
-        const int m = t.m0 + row;
         const int M = (KIND == TC_DW3) ? P.d : 2 * P.h;
-        __nv_bfloat16* dst;
+        const int m0w = t.m0 + rowoff + wq * 32;
+        const int nvalid = max(0, min(32, M - m0w));
+        __nv_bfloat16* base;
         int N;
         if constexpr (KIND == TC_DW3) {
           N = P.h;
-          dst = P.out0 + (int64_t)t.e * P.d * P.h + (int64_t)m * P.h;
-        } else {
+          base = P.out0 + (int64_t)t.e * P.d * P.h + (int64_t)m0w * P.h;
+        } else {  // a warp's 32 rows lie entirely in dW1 or in dW2 (h % 128 == 0)
           N = P.d;
-          dst = (m < P.h) ? P.out0 + (int64_t)t.e * P.h * P.d + (int64_t)m * P.d
-                          : P.out1 + (int64_t)t.e * P.h * P.d + (int64_t)(m - P.h) * P.d;
+          base = (m0w < P.h) ? P.out0 + (int64_t)t.e * P.h * P.d + (int64_t)m0w * P.d
+                             : P.out1 + (int64_t)t.e * P.h * P.d + (int64_t)(m0w - P.h) * P.d;
         }
 #pragma unroll 1
         for (int c = 0; c < TBN; c += 32) {
@@ -674,7 +814,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
 #pragma unroll
             for (int i = 0; i < 32; ++i) f[i] = 0.f;
           }
-          if (m < M) store_bf16x32(dst + t.n0 + c, f);
+          stg_put_bf16(stg, lane, f);
+          __syncwarp();
+          if (nvalid > 0) stg_store_bf16(stg, lane, base + t.n0 + c, N, nvalid);
+          __syncwarp();
         }
       }
       ptx::tc_fence_before();
@@ -757,7 +900,7 @@ static moe_status launch_tc_impl(const CUtensorMap& a0, const CUtensorMap& a1, c
   static bool attr = false;
   auto kern = tc_gemm_kernel<KIND, CPA, CG>;
   if (!attr) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CgCfg<CG>::SMEM) != cudaSuccess)
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CgCfg<CG, KIND>::SMEM) != cudaSuccess)
       return MOE_ERR_CUDA;
     attr = true;
   }
@@ -766,7 +909,7 @@ static moe_status launch_tc_impl(const CUtensorMap& a0, const CUtensorMap& a1, c
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(groups * CG);
   cfg.blockDim = dim3(TC_THREADS);
-  cfg.dynamicSmemBytes = CgCfg<CG>::SMEM;
+  cfg.dynamicSmemBytes = CgCfg<CG, KIND>::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attrs[1];
   attrs[0].id = cudaLaunchAttributeClusterDimension;
