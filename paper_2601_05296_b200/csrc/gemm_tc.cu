@@ -142,8 +142,26 @@ __device__ __forceinline__ bool decode_tile(int tile, const TcParams& P, const i
     t.seg1 = s_offs[t.e + 1];
     const int mt_e = (t.seg1 - t.seg0 + TM - 1) / TM;
     const int local = tile - s_tstart[t.e];
-    t.n_tile = local / mt_e;
-    t.m0 = t.seg0 + (local - t.n_tile * mt_e) * TM;
+    // grouped rasterisation: blocks of RG m-tiles x all n-tiles, m fastest, so
+    // a block's gathered rows (RG*TM rows) stay L2-resident while the weight
+    // tiles stream once per block (large segments would otherwise re-stream
+    // their rows from HBM for every n-tile)
+    constexpr int RG = 8;
+    const int nfull = mt_e / RG;
+    const int big = nfull * RG * P.n_tiles;
+    int mi;
+    if (local < big) {
+      const int g = local / (RG * P.n_tiles);
+      const int rem = local - g * RG * P.n_tiles;
+      t.n_tile = rem / RG;
+      mi = g * RG + (rem - t.n_tile * RG);
+    } else {
+      const int gl = mt_e - nfull * RG;
+      const int rem = local - big;
+      t.n_tile = rem / gl;
+      mi = nfull * RG + (rem - t.n_tile * gl);
+    }
+    t.m0 = t.seg0 + mi * TM;
     t.n0 = t.n_tile * K::NT;
     const int Kdim = (KIND == TC_FWD_UP || KIND == TC_BWD_DH) ? P.d : (KIND == TC_FWD_DOWN ? P.h : 2 * P.h);
     t.nk = Kdim / TBK;
