@@ -150,6 +150,8 @@ def main():
     ap.add_argument("--no-memory", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=10.0)
     ap.add_argument("--ep", action="store_true", help="use the expert-parallel path even at N = 1")
+    ap.add_argument("--checkpoint", default="ab", choices=["ab", "none"],
+                    help="activation checkpoint policy: ab = save A, B (paper); none = recompute A, B in backward")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -203,11 +205,14 @@ def main():
         def step():
             return ep.step(x, wg, w1, w2, w3, dy)
     else:
+        ck = args.checkpoint
+
         def step():
             logits, ids, w = M.route(x, wg, k, renorm)
             disp = M.dispatch_build(ids, cfg.E, dtype=x.dtype)
-            y, a, b = M.ffn_fwd(x, w1, w2, w3, w, disp, renorm)
-            g = M.ffn_bwd(dy, x, w1, w2, w3, w, disp, a, b, w_gate=wg, logits=logits, renormalize=renorm)
+            y, a, b = M.ffn_fwd(x, w1, w2, w3, w, disp, renorm, checkpoint=ck)
+            g = M.ffn_bwd(dy, x, w1, w2, w3, w, disp, a, b, w_gate=wg, logits=logits, renormalize=renorm,
+                          checkpoint=ck)
             return y, g
 
     for _ in range(args.warmup):
@@ -255,14 +260,14 @@ def main():
     if True:
         dom = max(prof, key=lambda n: prof[n][0])
         tot_ms, n_l = prof[dom]
-        flops = GEMM_FLOP_FACTOR[dom] * R * cfg.d * cfg.h
+        flops = GEMM_FLOP_FACTOR[dom] * R * cfg.d * cfg.h  # per launch (FWD_UP runs twice per step under --checkpoint none)
         achieved = flops / (tot_ms / n_l / 1e3) / 1e12
         peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
         traffic = None
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tp):
             traffic = json.load(open(tp)).get(args.workload, {}).get(dom)
-        all_flops = 18 * R * cfg.d * cfg.h
+        all_flops = (18 + (4 if args.checkpoint == "none" else 0)) * R * cfg.d * cfg.h
         roof = {"bound": "tensor", "kernel": f"tc_gemm_kernel<{dom}>", "achieved": round(achieved, 1),
                 "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                 "peak_source": f"{peaks['source']} bf16 sustained (kernel timed inside the step)",
@@ -343,7 +348,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded, moe_inputs)",
             "config": {"workload": cfg.name, "T_per_gpu": cfg.T, "d": cfg.d, "h": cfg.h, "E": cfg.E, "k": cfg.k,
-                       "renormalize": renorm,
+                       "renormalize": renorm, "checkpoint": args.checkpoint,
                        "parallelism": f"ep{world}" if ep is not None else "single-GPU",
                        "l2": "no flush: inputs larger than L2 (weights %.2f GB + X %.0f MB vs 126 MB L2)" % (
                            3 * w1.numel() * 2 * (world if world > 1 else 1) / 1e9, x.numel() * 2 / 1e6)},
@@ -388,6 +393,7 @@ def measure_memory(M, x, wg, w1, w2, w3, dy, k, renorm):
     out = {"method": "torch.autograd.graph.saved_tensors_hooks, unique storages excl. parameters (P:289); "
                      "peak = max_memory_allocated delta over fwd+bwd"}
     out["ours"] = one(lambda xx, a, b, c, d_: M.moe_layer(xx, a, b, c, d_, k, renorm))
+    out["ours_checkpoint_none"] = one(lambda xx, a, b, c, d_: M.moe_layer(xx, a, b, c, d_, k, renorm, "none"))
     try:
         out["materialized_baseline"] = one(lambda xx, a, b, c, d_: materialized_moe(xx, a, b, c, d_, k, renorm))
         out["saved_ratio"] = round(out["materialized_baseline"]["saved_gb"] / out["ours"]["saved_gb"], 3)

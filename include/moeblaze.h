@@ -72,7 +72,16 @@ typedef struct {
   int32_t check_routing;  /* 1: moe_dispatch_build validates ids (range, per-token
                              uniqueness) and records violations in the device status
                              word at ws offset 0 (int32; 0 = ok, else MOE_ERR_BAD_ROUTING) */
+  int32_t checkpoint;     /* activation-checkpoint policy:
+                             MOE_CKPT_AB (0, default) = the paper's smart checkpoint: save
+                             the pre-activations A, B, recompute SiLU in backward;
+                             MOE_CKPT_NONE (1) = save nothing but X and the routing: A, B
+                             live in ws during moe_ffn_fwd (a_save/b_save may be NULL) and
+                             moe_ffn_bwd recomputes them with the fused up-projection
+                             (+4 T*k*d*h flops; results bit-identical to MOE_CKPT_AB) */
 } moe_problem;
+
+enum { MOE_CKPT_AB = 0, MOE_CKPT_NONE = 1 };
 
 /* The compact dispatch index structures of §4.1.  R = T*k.
  *   expert_counts[E]         tokens routed to each expert (expert_lengths)
@@ -130,7 +139,8 @@ moe_status moe_dispatch_build(const moe_problem* p, const int32_t* topk_ids, con
  *     U_r = SiLU(A_r) * B_r               (transient, in ws)
  *     y[t] += topk_w[row_slot[r]] * (U_r W3_e)     (combine fused into the down GEMM)
  *   a_save, b_save [T*k, h] dtype: the checkpointed pre-activations A, B in
- *   expert-sorted row order, written.  y [T,d] dtype, written. */
+ *   expert-sorted row order, written (ignored, may be NULL,
+ *   under MOE_CKPT_NONE).  y [T,d] dtype, written. */
 moe_status moe_ffn_fwd(const moe_problem* p, const void* x, const void* w1, const void* w2,
                        const void* w3, const float* topk_w, const moe_dispatch* disp,
                        void* a_save, void* b_save, void* y,
@@ -143,7 +153,8 @@ moe_status moe_ffn_fwd(const moe_problem* p, const void* x, const void* w1, cons
  *   dA_r = w_r dH_r * B_r * SiLU'(A_r);  dB_r = w_r dH_r * SiLU(A_r)
  *   dw1[e] = sum_r dA_r^T X[eti[r]],  dw2[e] = sum_r dB_r^T X[eti[r]]
  *   dx[t]  = sum_{r: eti[r]=t} (dA_r W1_e^T + dB_r W2_e^T)  [+ router path]
- * a_save/b_save are read (A, B) and OVERWRITTEN with dA, dB (in place).
+ * a_save/b_save are read (A, B) and OVERWRITTEN with dA, dB (in place); under
+ * MOE_CKPT_NONE they are ignored (may be NULL) and A, B are recomputed in ws.
  * dw1/dw2/dw3 are written (experts with no rows get zeros), not accumulated.
  * d_topk_w [T,k] fp32 may be NULL only if router is NULL.
  * router != NULL: also computes the router backward (renorm-aware) and adds

@@ -28,7 +28,7 @@ GEMM_KINDS = ("FWD_UP", "FWD_DOWN", "BWD_DH", "BWD_DX", "DW3", "DW12")
 class MoeProblem(ctypes.Structure):
     _fields_ = [("T", ctypes.c_int64), ("d", ctypes.c_int32), ("h", ctypes.c_int32), ("E", ctypes.c_int32),
                 ("k", ctypes.c_int32), ("dtype", ctypes.c_int32), ("renormalize", ctypes.c_int32),
-                ("check_routing", ctypes.c_int32)]
+                ("check_routing", ctypes.c_int32), ("checkpoint", ctypes.c_int32)]
 
 
 class MoeDispatch(ctypes.Structure):
@@ -107,9 +107,13 @@ def _dtype_code(dt):
     raise MoEError(f"unsupported dtype {dt} (bf16 or fp32)")
 
 
-def problem(T, d, h, E, k, dtype, renormalize=False, check_routing=False):
+MOE_CKPT_AB, MOE_CKPT_NONE = 0, 1
+CHECKPOINT = {"ab": MOE_CKPT_AB, "none": MOE_CKPT_NONE}
+
+
+def problem(T, d, h, E, k, dtype, renormalize=False, check_routing=False, checkpoint="ab"):
     return MoeProblem(int(T), int(d), int(h), int(E), int(k), _dtype_code(dtype), int(bool(renormalize)),
-                      int(bool(check_routing)))
+                      int(bool(check_routing)), CHECKPOINT[checkpoint])
 
 
 def workspace_size(p, op):

@@ -34,6 +34,7 @@ static moe_status validate(const moe_problem* p) {
   if (p->dtype != MOE_BF16 && p->dtype != MOE_FP32) return MOE_ERR_INVALID_ARG;
   if (p->dtype == MOE_BF16 && (p->d % 128 != 0 || p->h % 128 != 0)) return MOE_ERR_UNSUPPORTED;
   if (p->dtype == MOE_FP32 && (p->d % 8 != 0)) return MOE_ERR_UNSUPPORTED;
+  if (p->checkpoint != MOE_CKPT_AB && p->checkpoint != MOE_CKPT_NONE) return MOE_ERR_INVALID_ARG;
   return MOE_OK;
 }
 
@@ -44,7 +45,7 @@ static size_t esize(const moe_problem* p) { return p->dtype == MOE_BF16 ? 2 : 4;
 // dg partial columns per routed row: the max over the GEMM backends
 static int dg_parts(const moe_problem* p) { return (int)ceil_div(p->h, 64); }
 
-struct FwdWs { void* u; float* yacc; size_t total; };
+struct FwdWs { void* u; float* yacc; void* a; void* b; size_t total; };
 static FwdWs fwd_layout(const moe_problem* p, void* base) {
   const int64_t R = p->T * p->k;
   char* b = (char*)base;
@@ -52,6 +53,11 @@ static FwdWs fwd_layout(const moe_problem* p, void* base) {
   FwdWs w;
   w.u = b + o; o += align256((size_t)R * p->h * esize(p));
   w.yacc = (float*)(b + o); o += align256((size_t)p->T * p->d * 4);
+  w.a = w.b = nullptr;
+  if (p->checkpoint == MOE_CKPT_NONE) {  // A, B are transient: not checkpointed
+    w.a = b + o; o += align256((size_t)R * p->h * esize(p));
+    w.b = b + o; o += align256((size_t)R * p->h * esize(p));
+  }
   w.total = o;
   return w;
 }
@@ -67,7 +73,7 @@ static RouterWs router_layout(const moe_problem* p, void* base) {
   return w;
 }
 
-struct BwdWs { void* wu; float* dxacc; float* dgpart; float* dlogits; float* dwgpart; float* dg; size_t total; };
+struct BwdWs { void* wu; float* dxacc; float* dgpart; float* dlogits; float* dwgpart; float* dg; void* a; void* b; size_t total; };
 static BwdWs bwd_layout(const moe_problem* p, void* base) {
   const int64_t R = p->T * p->k;
   char* b = (char*)base;
@@ -79,6 +85,11 @@ static BwdWs bwd_layout(const moe_problem* p, void* base) {
   w.dlogits = (float*)(b + o); o += align256((size_t)p->T * p->E * 4);
   w.dwgpart = (float*)(b + o); o += align256((size_t)dwg_chunks(p->T, p->d, p->E) * p->E * p->d * 4);
   w.dg = (float*)(b + o); o += align256((size_t)R * 4);
+  w.a = w.b = nullptr;
+  if (p->checkpoint == MOE_CKPT_NONE) {  // recomputed pre-activations
+    w.a = b + o; o += align256((size_t)R * p->h * esize(p));
+    w.b = b + o; o += align256((size_t)R * p->h * esize(p));
+  }
   w.total = o;
   return w;
 }
@@ -148,8 +159,9 @@ moe_status moe_ffn_fwd(const moe_problem* p, const void* x, const void* w1, cons
   moe_status s = validate(p);
   if (s != MOE_OK) return s;
   if (!disp || !w1 || !w2 || !w3) return MOE_ERR_INVALID_ARG;
-  if (p->T > 0 && (!x || !y || !topk_w || !a_save || !b_save || !ws || !disp->expert_offsets || !disp->expert_token_indices ||
-                   !disp->row_slot))
+  const bool ckpt = p->checkpoint == MOE_CKPT_AB;
+  if (p->T > 0 && (!x || !y || !topk_w || (ckpt && (!a_save || !b_save)) || !ws || !disp->expert_offsets ||
+                   !disp->expert_token_indices || !disp->row_slot))
     return MOE_ERR_INVALID_ARG;
   if (!aligned16(x) || !aligned16(w1) || !aligned16(w2) || !aligned16(w3) || !aligned16(a_save) ||
       !aligned16(b_save) || !aligned16(y))
@@ -158,6 +170,10 @@ moe_status moe_ffn_fwd(const moe_problem* p, const void* x, const void* w1, cons
   if (ws_bytes < w.total) return MOE_ERR_WORKSPACE;
   cudaStream_t st = (cudaStream_t)stream;
   if (p->T == 0) return MOE_OK;
+  if (!ckpt) {
+    a_save = w.a;
+    b_save = w.b;
+  }
   MOE_CUDA_CHECK(cudaMemsetAsync(w.yacc, 0, (size_t)p->T * p->d * 4, st));
   GemmCall c{};
   c.x = x; c.w1 = w1; c.w2 = w2; c.w3 = w3; c.topw = topk_w;
@@ -180,7 +196,8 @@ moe_status moe_ffn_bwd(const moe_problem* p, const void* dy, const void* x, cons
   if (!disp || !dw1 || !dw2 || !dw3 || !w1 || !w2 || !w3) return MOE_ERR_INVALID_ARG;
   if (router && (!router->w_gate || !router->dw_gate)) return MOE_ERR_INVALID_ARG;
   if (router && p->T > 0 && (!router->logits || !router->topk_ids)) return MOE_ERR_INVALID_ARG;
-  if (p->T > 0 && (!dy || !x || !dx || !topk_w || !a_save || !b_save || !ws || !disp->expert_offsets ||
+  const bool ckpt = p->checkpoint == MOE_CKPT_AB;
+  if (p->T > 0 && (!dy || !x || !dx || !topk_w || (ckpt && (!a_save || !b_save)) || !ws || !disp->expert_offsets ||
                    !disp->expert_token_indices || !disp->token_index_map || !disp->row_slot))
     return MOE_ERR_INVALID_ARG;
   if (!aligned16(dy) || !aligned16(x) || !aligned16(a_save) || !aligned16(b_save) || !aligned16(dx) ||
@@ -190,6 +207,10 @@ moe_status moe_ffn_bwd(const moe_problem* p, const void* dy, const void* x, cons
   if (ws_bytes < w.total) return MOE_ERR_WORKSPACE;
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t R = p->T * p->k;
+  if (!ckpt) {
+    a_save = w.a;
+    b_save = w.b;
+  }
   GemmCall c{};
   c.x = x; c.dy = dy; c.w1 = w1; c.w2 = w2; c.w3 = w3; c.topw = topk_w;
   c.offs = disp->expert_offsets; c.eti = disp->expert_token_indices; c.row_slot = disp->row_slot;
@@ -198,6 +219,10 @@ moe_status moe_ffn_bwd(const moe_problem* p, const void* dy, const void* x, cons
   c.T = p->T; c.R = R; c.d = p->d; c.h = p->h; c.E = p->E; c.bf16 = p->dtype == MOE_BF16;
   if (p->T > 0) {
     MOE_CUDA_CHECK(cudaMemsetAsync(w.dxacc, 0, (size_t)p->T * p->d * 4, st));
+    if (!ckpt) {  // MOE_CKPT_NONE: recompute A, B (and U into the wU buffer) with the fused up-projection
+      c.which = GEMM_FWD_UP;
+      if ((s = run_gemm(c, st)) != MOE_OK) return s;
+    }
     c.which = GEMM_BWD_DH;  // dH, SwiGLU bwd: dA/dB in place, wU, dg partials
     if ((s = run_gemm(c, st)) != MOE_OK) return s;
   }

@@ -13,8 +13,8 @@ import torch
 from . import _lib as L
 
 
-def _problem(T, d, h, E, k, dtype, renormalize=False, check_routing=False):
-    return L.problem(T, d, h, E, k, dtype, renormalize, check_routing)
+def _problem(T, d, h, E, k, dtype, renormalize=False, check_routing=False, checkpoint="ab"):
+    return L.problem(T, d, h, E, k, dtype, renormalize, check_routing, checkpoint)
 
 
 @dataclass
@@ -60,15 +60,17 @@ def dispatch_build(ids, E, check_routing=False, stream=None, dtype=torch.bfloat1
     return disp
 
 
-def ffn_fwd(x, w1, w2, w3, topk_w, disp: Dispatch, renormalize=False, stream=None):
-    """moe_ffn_fwd (§3.1, Alg. 1 FusedForward): returns y, A, B (A, B checkpointed)."""
+def ffn_fwd(x, w1, w2, w3, topk_w, disp: Dispatch, renormalize=False, stream=None, checkpoint="ab"):
+    """moe_ffn_fwd (§3.1, Alg. 1 FusedForward): returns y, A, B (A, B checkpointed;
+    None, None under checkpoint="none", where backward recomputes them)."""
     T, d = x.shape
     E, h, _ = w1.shape
     k = topk_w.shape[1]
-    p = _problem(T, d, h, E, k, x.dtype, renormalize)
+    p = _problem(T, d, h, E, k, x.dtype, renormalize, checkpoint=checkpoint)
     R = T * k
-    a = torch.empty(R, h, dtype=x.dtype, device=x.device)
-    b = torch.empty(R, h, dtype=x.dtype, device=x.device)
+    save = checkpoint == "ab"
+    a = torch.empty(R, h, dtype=x.dtype, device=x.device) if save else None
+    b = torch.empty(R, h, dtype=x.dtype, device=x.device) if save else None
     y = torch.empty(T, d, dtype=x.dtype, device=x.device)
     ws = L.workspace(p, L.MOE_OP_FFN_FWD, x.device)
     L.moe_ffn_fwd(p, x, w1, w2, w3, topk_w, disp.c(), a, b, y, ws, stream)
@@ -76,13 +78,14 @@ def ffn_fwd(x, w1, w2, w3, topk_w, disp: Dispatch, renormalize=False, stream=Non
 
 
 def ffn_bwd(dy, x, w1, w2, w3, topk_w, disp: Dispatch, a_save, b_save, w_gate=None, logits=None,
-            renormalize=False, stream=None):
+            renormalize=False, stream=None, checkpoint="ab"):
     """moe_ffn_bwd (§3.2, Alg. 1 FusedBackward).  a_save/b_save are overwritten
-    with dA/dB.  With w_gate/logits: router backward too (dx includes it)."""
+    with dA/dB (checkpoint="none": pass None, A and B are recomputed).  With
+    w_gate/logits: router backward too (dx includes it)."""
     T, d = x.shape
     E, h, _ = w1.shape
     k = topk_w.shape[1]
-    p = _problem(T, d, h, E, k, x.dtype, renormalize)
+    p = _problem(T, d, h, E, k, x.dtype, renormalize, checkpoint=checkpoint)
     dx = torch.empty_like(x)
     dw1 = torch.empty_like(w1)
     dw2 = torch.empty_like(w2)
@@ -101,37 +104,44 @@ def ffn_bwd(dy, x, w1, w2, w3, topk_w, disp: Dispatch, a_save, b_save, w_gate=No
 class MoEBlazeFunction(torch.autograd.Function):
     """y = MoE(x): route -> dispatch -> fused expert forward; backward recomputes
     SiLU from the checkpointed A, B.  Saved for backward: x, logits,
-    ids, w, the index structures, A, B — no routed-token buffer."""
+    ids, w, the index structures, A, B — no routed-token buffer.  With
+    checkpoint="none" A, B are not saved either (recomputed in backward)."""
 
     @staticmethod
-    def forward(ctx, x, w_gate, w1, w2, w3, k, renormalize):
+    def forward(ctx, x, w_gate, w1, w2, w3, k, renormalize, checkpoint="ab"):
         logits, ids, w = route(x, w_gate, k, renormalize)
         disp = dispatch_build(ids, w_gate.shape[0], dtype=x.dtype)
-        y, a, b = ffn_fwd(x, w1, w2, w3, w, disp, renormalize)
-        ctx.save_for_backward(x, w_gate, w1, w2, w3, logits, ids, w, disp.counts, disp.offs, disp.eti, disp.tim,
-                              disp.row_slot, a, b)
+        y, a, b = ffn_fwd(x, w1, w2, w3, w, disp, renormalize, checkpoint=checkpoint)
+        saved = [x, w_gate, w1, w2, w3, logits, ids, w, disp.counts, disp.offs, disp.eti, disp.tim, disp.row_slot]
+        if checkpoint == "ab":
+            saved += [a, b]
+        ctx.save_for_backward(*saved)
         ctx.renormalize = renormalize
+        ctx.checkpoint = checkpoint
         return y
 
     @staticmethod
     def backward(ctx, dy):
-        (x, w_gate, w1, w2, w3, logits, ids, w, counts, offs, eti, tim, row_slot, a, b) = ctx.saved_tensors
+        t = ctx.saved_tensors
+        (x, w_gate, w1, w2, w3, logits, ids, w, counts, offs, eti, tim, row_slot) = t[:13]
+        a, b = (t[13], t[14]) if ctx.checkpoint == "ab" else (None, None)
         disp = Dispatch(counts, offs, eti, tim, row_slot, ids)
         g = ffn_bwd(dy.contiguous(), x, w1, w2, w3, w, disp, a, b, w_gate=w_gate, logits=logits,
-                    renormalize=ctx.renormalize)
-        return g["dx"], g["dw_gate"], g["dw1"], g["dw2"], g["dw3"], None, None
+                    renormalize=ctx.renormalize, checkpoint=ctx.checkpoint)
+        return g["dx"], g["dw_gate"], g["dw1"], g["dw2"], g["dw3"], None, None, None
 
 
-def moe_layer(x, w_gate, w1, w2, w3, k, renormalize=False):
-    return MoEBlazeFunction.apply(x, w_gate, w1, w2, w3, k, renormalize)
+def moe_layer(x, w_gate, w1, w2, w3, k, renormalize=False, checkpoint="ab"):
+    """checkpoint: "ab" (paper: save A, B, recompute SiLU) | "none" (save X only, recompute A, B)."""
+    return MoEBlazeFunction.apply(x, w_gate, w1, w2, w3, k, renormalize, checkpoint)
 
 
 class MoEBlazeLayer(torch.nn.Module):
     """Dropless top-k SwiGLU MoE layer on the MoEBlaze path."""
 
-    def __init__(self, d, h, E, k, renormalize=False, dtype=torch.bfloat16, device="cuda"):
+    def __init__(self, d, h, E, k, renormalize=False, dtype=torch.bfloat16, device="cuda", checkpoint="ab"):
         super().__init__()
-        self.k, self.renormalize = k, renormalize
+        self.k, self.renormalize, self.checkpoint = k, renormalize, checkpoint
         kw = dict(dtype=dtype, device=device)
         self.w_gate = torch.nn.Parameter(torch.randn(E, d, **kw) / d ** 0.5)
         self.w1 = torch.nn.Parameter(torch.randn(E, h, d, **kw) / d ** 0.5)
@@ -139,4 +149,4 @@ class MoEBlazeLayer(torch.nn.Module):
         self.w3 = torch.nn.Parameter(torch.randn(E, d, h, **kw) / h ** 0.5)
 
     def forward(self, x):
-        return moe_layer(x, self.w_gate, self.w1, self.w2, self.w3, self.k, self.renormalize)
+        return moe_layer(x, self.w_gate, self.w1, self.w2, self.w3, self.k, self.renormalize, self.checkpoint)

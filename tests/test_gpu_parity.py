@@ -165,3 +165,32 @@ def test_autograd_layer_matches_functional(M):
     assert torch.equal(y, out["y"])
     assert torch.equal(x.grad, out["dx"])
     assert torch.equal(params[1].grad, out["dw1"])
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_checkpoint_none_recompute_is_bit_identical(M, dtype):
+    """checkpoint="none" (NEXT-3): A, B are not saved; backward recomputes them
+    with the same kernel, so every gradient is bit-identical to the paper's
+    A,B-checkpoint policy, and the autograd saved set loses the 2*T*k*h
+    pre-activations."""
+    T, d, h, E, k = (512, 256, 384, 8, 2) if dtype == "bf16" else (256, 64, 128, 4, 2)
+    inp = make_inputs(T, d, h, E, k, dtype=dtype, seed=11, device=DEV)
+    outs = {}
+    for ck in ("ab", "none"):
+        x = inp["x"].clone().requires_grad_(True)
+        params = [inp[n].clone().requires_grad_(True) for n in ("w_gate", "w1", "w2", "w3")]
+        saved = {}
+
+        def pack(t):
+            saved[t.untyped_storage().data_ptr()] = t.untyped_storage().nbytes()
+            return t
+
+        with torch.autograd.graph.saved_tensors_hooks(pack, lambda t: t):
+            y = M.moe_layer(x, *params, k, False, ck)
+        y.backward(inp["dy"])
+        torch.cuda.synchronize()
+        outs[ck] = (y, x.grad, [p.grad for p in params], sum(saved.values()))
+    for a_, b_ in zip([outs["ab"][0], outs["ab"][1]] + outs["ab"][2], [outs["none"][0], outs["none"][1]] + outs["none"][2]):
+        assert torch.equal(a_, b_)
+    esz = 2 if dtype == "bf16" else 4
+    assert outs["ab"][3] - outs["none"][3] == 2 * T * k * h * esz
