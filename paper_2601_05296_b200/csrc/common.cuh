@@ -36,6 +36,9 @@ template <> __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(flo
 }
 
 __device__ __forceinline__ float sigmoidf_(float a) { return 1.0f / (1.0f + __expf(-a)); }
+// ~2-ulp sigmoid (MUFU.EX2 + MUFU.RCP, no IEEE division sequence) for the bf16
+// tensor-core epilogues, whose outputs are rounded to bf16 (2^-9) anyway.
+__device__ __forceinline__ float sigmoid_fast(float a) { return __fdividef(1.0f, 1.0f + __expf(-a)); }
 
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 __host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -56,8 +56,9 @@ struct CgCfg {
   static constexpr int STAGE = TA_BYTES + B_BYTES;
   // BWD_DH double-buffers its epilogue inputs (A, B chunks): one stage less
   static constexpr bool DH = (KIND == 2);
-  static constexpr int STAGES = (CG == 1 ? 4 : 6) - (DH ? 1 : 0);
-  static constexpr int STG_WARP = DH ? 10240 : 6144;    // epilogue staging bytes per warp
+  static constexpr int STAGES = DH ? (CG == 1 ? 2 : 3) : (CG == 1 ? 4 : 6);
+  static constexpr int DH_NBUF = 7;                     // BWD_DH: ring of A/B input chunks per warp
+  static constexpr int STG_WARP = DH ? (DH_NBUF * 4096 + 2048) : 6144;  // epilogue staging bytes per warp
   static constexpr int STG_OFF = STAGES * STAGE + 1024 /*barriers*/ + 2176 /*offsets, tile starts*/;
   static constexpr int SMEM = STG_OFF + 4 * STG_WARP + 1024 /*align*/;
 };
@@ -588,6 +589,23 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
     uint32_t aphase = 0;
     TileInfo t;
     for (int tile = cluster_id; decode_tile<KIND, CG>(tile, P, s_offs, s_tstart, t); tile += n_clusters) {
+      if constexpr (KIND == TC_BWD_DH) {
+        // the epilogue inputs (A, B rows of this tile) do not depend on the
+        // accumulator: start streaming the first chunks before waiting for it
+        const int r0w = t.m0 + rowoff + wq * 32;
+        const int nvalid = max(0, min(32, t.seg1 - r0w));
+        const int nchunk = min(TBN, P.h - t.n0) / 32;
+        const int64_t o0 = (int64_t)r0w * P.h + t.n0;
+#pragma unroll
+        for (int ci = 0; ci < C::DH_NBUF - 1; ++ci) {
+          if (ci < nchunk) {
+            uint8_t* NA = stg + ci * 4096;
+            stg_load_bf16_async(NA, lane, P.a_save + o0 + ci * 32, P.h, nvalid);
+            stg_load_bf16_async(NA + 2048, lane, P.b_save + o0 + ci * 32, P.h, nvalid);
+          }
+          asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+      }
       ptx::mbar_wait(&tfull[as], aphase);
       ptx::tc_fence_after();
       const uint32_t tb = tmem_base + ((uint32_t)(wq * 32) << 16) + as * TBN;
@@ -671,7 +689,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
           for (int i = 0; i < 32; ++i) {
             a[i] = __uint_as_float(v[i]);
             b[i] = __uint_as_float(bv[i]);
-            u[i] = a[i] * sigmoidf_(a[i]) * b[i];
+            u[i] = a[i] * sigmoid_fast(a[i]) * b[i];
           }
           stg_put_bf16(T0, lane, a);
           stg_put_bf16(T1, lane, b);
@@ -719,81 +737,76 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
           __syncwarp();
         }
       } else if constexpr (KIND == TC_BWD_DH) {
-        // A, B chunks of 32 columns are prefetched one chunk ahead with cp.async
-        // into double-buffered staging tiles (buf: A at +0, B at +2048); dA and
-        // dB overwrite the consumed input tiles, wU goes to its own tile.
+        // A, B chunks of 32 columns stream through a ring of DH_NBUF cp.async
+        // staging buffers (A at +0, B at +2048 of each 4 KB slot; the first
+        // slots are filled before the accumulator is ready); dA and dB
+        // overwrite the consumed input slot, wU goes to its own tile.  The
+        // next chunk's TMEM read is issued before this chunk is processed.
         const int r = t.m0 + row;
         const bool valid = r < t.seg1;
         const int r0w = t.m0 + rowoff + wq * 32;
         const int nvalid = max(0, min(32, t.seg1 - r0w));
         const float w = valid ? P.topw[P.row_slot[r]] : 0.f;
-        uint8_t* TU = stg + 8192;
+        constexpr int NBUF = C::DH_NBUF;
+        uint8_t* TU = stg + NBUF * 4096;
         const int nchunk = min(TBN, P.h - t.n0) / 32;
         const int64_t o0 = (int64_t)r0w * P.h + t.n0;
         float rowsum = 0.f;
-        stg_load_bf16_async(stg, lane, P.a_save + o0, P.h, nvalid);
-        stg_load_bf16_async(stg + 2048, lane, P.b_save + o0, P.h, nvalid);
-        asm volatile("cp.async.commit_group;" ::: "memory");
+        if (nchunk > 0) ptx::tmem_ld32(tb, v);
 #pragma unroll 1
         for (int ci = 0; ci < nchunk; ++ci) {
-          uint8_t* TA = stg + (ci & 1) * 4096;
+          uint8_t* TA = stg + (ci % NBUF) * 4096;
           uint8_t* TB = TA + 2048;
-          if (ci + 1 < nchunk) {  // prefetch the next chunk into the other buffer
-            uint8_t* NA = stg + ((ci + 1) & 1) * 4096;
-            stg_load_bf16_async(NA, lane, P.a_save + o0 + (ci + 1) * 32, P.h, nvalid);
-            stg_load_bf16_async(NA + 2048, lane, P.b_save + o0 + (ci + 1) * 32, P.h, nvalid);
-            asm volatile("cp.async.commit_group;" ::: "memory");
-            asm volatile("cp.async.wait_group 1;" ::: "memory");
-          } else {
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
-          }
-          __syncwarp();
-#pragma unroll 1
-          for (int hf = 0; hf < 2; ++hf) {  // two 16-column halves keep the register footprint small
-            uint32_t v16[16];
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
-                "%14, %15}, [%16];"
-                : "=r"(v16[0]), "=r"(v16[1]), "=r"(v16[2]), "=r"(v16[3]), "=r"(v16[4]), "=r"(v16[5]), "=r"(v16[6]),
-                  "=r"(v16[7]), "=r"(v16[8]), "=r"(v16[9]), "=r"(v16[10]), "=r"(v16[11]), "=r"(v16[12]),
-                  "=r"(v16[13]), "=r"(v16[14]), "=r"(v16[15])
-                : "r"(tb + ci * 32 + hf * 16));
-            ptx::tmem_wait_ld();
-#pragma unroll
-            for (int qq = 0; qq < 2; ++qq) {
-              const int q = hf * 2 + qq;
-              const uint4 ua = *reinterpret_cast<const uint4*>(TA + stg16_off(lane, q));
-              const uint4 ub = *reinterpret_cast<const uint4*>(TB + stg16_off(lane, q));
-              const uint32_t* pa = reinterpret_cast<const uint32_t*>(&ua);
-              const uint32_t* pb = reinterpret_cast<const uint32_t*>(&ub);
-              uint32_t oa[4], ob[4], ou[4];
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 a2 = ptx::unpack_bf16(pa[e]);
-                const float2 b2 = ptx::unpack_bf16(pb[e]);
-                float ra[2], rb[2], ru[2];
-                const float av[2] = {a2.x, a2.y}, bvv[2] = {b2.x, b2.y};
-#pragma unroll
-                for (int z = 0; z < 2; ++z) {
-                  const float dH = __uint_as_float(v16[qq * 8 + e * 2 + z]);
-                  const float a = av[z], b = bvv[z];
-                  const float sg = sigmoidf_(a);
-                  const float S = a * sg;
-                  const float U = S * b;
-                  rowsum = fmaf(dH, U, rowsum);
-                  const float dU = w * dH;
-                  ra[z] = dU * b * sg * (1.f + a * (1.f - sg));
-                  rb[z] = dU * S;
-                  ru[z] = w * U;
-                }
-                oa[e] = ptx::pack_bf16(ra[0], ra[1]);
-                ob[e] = ptx::pack_bf16(rb[0], rb[1]);
-                ou[e] = ptx::pack_bf16(ru[0], ru[1]);
-              }
-              *reinterpret_cast<uint4*>(TA + stg16_off(lane, q)) = make_uint4(oa[0], oa[1], oa[2], oa[3]);
-              *reinterpret_cast<uint4*>(TB + stg16_off(lane, q)) = make_uint4(ob[0], ob[1], ob[2], ob[3]);
-              *reinterpret_cast<uint4*>(TU + stg16_off(lane, q)) = make_uint4(ou[0], ou[1], ou[2], ou[3]);
+          {  // keep NBUF-1 chunks in flight: one commit group per iteration (possibly empty)
+            const int nx = ci + NBUF - 1;
+            if (nx < nchunk) {
+              uint8_t* NA = stg + (nx % NBUF) * 4096;
+              stg_load_bf16_async(NA, lane, P.a_save + o0 + nx * 32, P.h, nvalid);
+              stg_load_bf16_async(NA + 2048, lane, P.b_save + o0 + nx * 32, P.h, nvalid);
             }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            asm volatile("cp.async.wait_group %0;" ::"n"(NBUF - 1) : "memory");
+          }
+          // accumulator chunk ci was loaded (asynchronously) one iteration ago
+          ptx::tmem_wait_ld();
+          uint32_t dh[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) dh[i] = v[i];
+          if (ci + 1 < nchunk) ptx::tmem_ld32(tb + (ci + 1) * 32, v);  // overlap the next TMEM read
+          __syncwarp();
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint4 ua = *reinterpret_cast<const uint4*>(TA + stg16_off(lane, q));
+            const uint4 ub = *reinterpret_cast<const uint4*>(TB + stg16_off(lane, q));
+            const uint32_t* pa = reinterpret_cast<const uint32_t*>(&ua);
+            const uint32_t* pb = reinterpret_cast<const uint32_t*>(&ub);
+            uint32_t oa[4], ob[4], ou[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 a2 = ptx::unpack_bf16(pa[e]);
+              const float2 b2 = ptx::unpack_bf16(pb[e]);
+              float ra[2], rb[2], ru[2];
+              const float av[2] = {a2.x, a2.y}, bvv[2] = {b2.x, b2.y};
+#pragma unroll
+              for (int z = 0; z < 2; ++z) {
+                const float dH = __uint_as_float(dh[q * 8 + e * 2 + z]);
+                const float a = av[z], b = bvv[z];
+                const float sg = sigmoid_fast(a);
+                const float S = a * sg;
+                const float U = S * b;
+                rowsum = fmaf(dH, U, rowsum);
+                const float dU = w * dH;
+                ra[z] = dU * b * sg * (1.f + a * (1.f - sg));
+                rb[z] = dU * S;
+                ru[z] = w * U;
+              }
+              oa[e] = ptx::pack_bf16(ra[0], ra[1]);
+              ob[e] = ptx::pack_bf16(rb[0], rb[1]);
+              ou[e] = ptx::pack_bf16(ru[0], ru[1]);
+            }
+            *reinterpret_cast<uint4*>(TA + stg16_off(lane, q)) = make_uint4(oa[0], oa[1], oa[2], oa[3]);
+            *reinterpret_cast<uint4*>(TB + stg16_off(lane, q)) = make_uint4(ob[0], ob[1], ob[2], ob[3]);
+            *reinterpret_cast<uint4*>(TU + stg16_off(lane, q)) = make_uint4(ou[0], ou[1], ou[2], ou[3]);
           }
           __syncwarp();
           if (nvalid > 0) {
