@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(256) dwg_partial_kernel(const float* __restric
   const int cg = threadIdx.x % CGR, eg = threadIdx.x / CGR;
   const int c0 = blockIdx.x * COLS;
   const int col = c0 + cg * 8;
+  const int ebase = blockIdx.z * EGR * 8;  // expert block (E > 64 uses several)
   const int64_t ta = blockIdx.y * tch, tb = min64(ta + tch, Tn);
   const int ntiles = (int)ceil_div(tb - ta, TT);
   float acc[8][8];
@@ -131,7 +132,7 @@ __global__ void __launch_bounds__(256) dwg_partial_kernel(const float* __restric
     for (int v = threadIdx.x; v < TT * EGR * 8; v += 256) {
       const int r = v / (EGR * 8), e = v % (EGR * 8);
       const int64_t t = t0 + r;
-      ds[buf][r][e] = (t < tb && e < E) ? dlogits[t * E + e] : 0.f;
+      ds[buf][r][e] = (t < tb && ebase + e < E) ? dlogits[t * E + ebase + e] : 0.f;
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
@@ -163,7 +164,7 @@ __global__ void __launch_bounds__(256) dwg_partial_kernel(const float* __restric
   if (col < d) {
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      const int e = eg * 8 + q;
+      const int e = ebase + eg * 8 + q;
       if (e < E) store8(part + ((int64_t)blockIdx.y * E + e) * d + col, acc[q]);
     }
   }
@@ -339,7 +340,7 @@ static void launch_dwg_partial(const float* dl, const T* x, int64_t Tn, int d, i
                                cudaStream_t st) {
   const int egr = dwg_egr(E);
   const int cols_per_block = 8 * (256 / egr);
-  dim3 grid((unsigned)ceil_div(d, cols_per_block), nch);
+  dim3 grid((unsigned)ceil_div(d, cols_per_block), nch, (unsigned)ceil_div(E, egr * 8));
   if (egr == 1) MOE_LAUNCH((dwg_partial_kernel<T, 1>), grid, 256, 0, st, dl, x, Tn, d, E, tch, part);
   else if (egr == 2) MOE_LAUNCH((dwg_partial_kernel<T, 2>), grid, 256, 0, st, dl, x, Tn, d, E, tch, part);
   else if (egr == 4) MOE_LAUNCH((dwg_partial_kernel<T, 4>), grid, 256, 0, st, dl, x, Tn, d, E, tch, part);

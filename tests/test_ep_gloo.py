@@ -102,7 +102,8 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("P,renorm,routing", [(2, False, "balanced"), (2, True, "skewed"), (4, False, "balanced")])
+@pytest.mark.parametrize("P,renorm,routing", [(2, False, "balanced"), (2, True, "skewed"), (4, False, "balanced"),
+                                             (4, False, "degenerate")])
 def test_ep_matches_single_process_oracle(P, renorm, routing):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

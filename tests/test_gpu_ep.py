@@ -29,19 +29,20 @@ def staged_a2a(send, send_split, recv_split, group=None):
     return out.to(send.device)
 
 
-def _inputs(P):
+def _inputs(P, routing="balanced"):
     c = CFG
-    W = make_inputs(c["T"], c["d"], c["h"], c["E"], c["k"], dtype="bf16", seed=100)
-    XS = [make_inputs(c["T"], c["d"], c["h"], c["E"], c["k"], dtype="bf16", seed=r) for r in range(P)]
+    W = make_inputs(c["T"], c["d"], c["h"], c["E"], c["k"], dtype="bf16", seed=100, routing=routing)
+    XS = [make_inputs(c["T"], c["d"], c["h"], c["E"], c["k"], dtype="bf16", seed=r, routing=routing)
+          for r in range(P)]
     return W, [(X["x"], X["dy"]) for X in XS]
 
 
-def _worker(rank, P, port, q):
+def _worker(rank, P, port, q, routing):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=P)
     from paper_2601_05296_b200.ep import ExpertParallelMoE
-    W, XS = _inputs(P)
+    W, XS = _inputs(P, routing)
     dev = torch.device("cuda", 0)
     ep = ExpertParallelMoE(CFG["E"], CFG["k"], False, a2a=staged_a2a)
     lo, hi = ep.local_experts
@@ -64,12 +65,13 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("P", [1, 2])
-def test_ep_cuda_matches_single_gpu(P):
+@pytest.mark.parametrize("P,routing", [(1, "balanced"), (2, "balanced"), (2, "degenerate")])
+def test_ep_cuda_matches_single_gpu(P, routing):
+    """degenerate routing: every token picks experts 0,1, so rank 1 receives no rows."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, P, port, q)) for r in range(P)]
+    procs = [ctx.Process(target=_worker, args=(r, P, port, q, routing)) for r in range(P)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=300) for _ in range(P)], key=lambda t: t[0])
@@ -77,7 +79,7 @@ def test_ep_cuda_matches_single_gpu(P):
         p.join(timeout=60)
         assert p.exitcode == 0
     import paper_2601_05296_b200 as M
-    W, XS = _inputs(P)
+    W, XS = _inputs(P, routing)
     dev = torch.device("cuda", 0)
     x = torch.cat([a for a, _ in XS]).to(dev)
     dy = torch.cat([b for _, b in XS]).to(dev)

@@ -194,3 +194,33 @@ def test_checkpoint_none_recompute_is_bit_identical(M, dtype):
         assert torch.equal(a_, b_)
     esz = 2 if dtype == "bf16" else 4
     assert outs["ab"][3] - outs["none"][3] == 2 * T * k * h * esz
+
+
+EDGE_CASES = [
+    # T, d, h, E, k, routing
+    (1, 128, 128, 1, 1, "balanced"),        # one token, one expert
+    (3, 128, 128, 256, 16, "balanced"),     # max E and k, nearly all experts empty
+    (130, 128, 128, 256, 16, "skewed"),     # max E and k, ragged
+    (257, 256, 128, 2, 2, "balanced"),      # k = E: every token to every expert
+    (129, 128, 256, 16, 1, "degenerate"),   # all rows to expert 0
+    (1023, 384, 640, 12, 5, "skewed"),      # odd sizes (d, h multiples of 128 only)
+]
+
+
+@pytest.mark.parametrize("T,d,h,E,k,routing", EDGE_CASES)
+def test_layer_edge_shapes(M, T, d, h, E, k, routing):
+    inp, out = _run_layer(M, T, d, h, E, k, "bf16", False, routing, seed=T + E)
+    X, WG, W1, W2, W3, DY = (f64(inp[n]) for n in ("x", "w_gate", "w1", "w2", "w3", "dy"))
+    fwd = O.layer_forward(X, WG, W1, W2, W3, k, False, logits=f64(out["logits"]))
+    assert np.array_equal(i64(out["ids"]), fwd["ids"])
+    bwd = O.layer_backward(fwd, DY, X, WG, W1, W2, W3, False)
+    errs = {n: normwise(out[n], fwd[n] if n in ("A", "B", "y") else bwd[n])
+            for n in ("A", "B", "y", "dA", "dB", "dg", "dx", "dw1", "dw2", "dw3", "dw_gate")}
+    bad = {n: v for n, v in errs.items() if not v <= BF16_TOL}
+    assert not bad, errs
+    counts = i64(out["disp"].counts)
+    empty = np.nonzero(counts == 0)[0]
+    if len(empty):  # experts with no rows: exact zero gradients
+        sel = torch.from_numpy(empty).to(DEV)
+        assert torch.count_nonzero(out["dw1"][sel]).item() == 0
+        assert torch.count_nonzero(out["dw3"][sel]).item() == 0
