@@ -37,8 +37,14 @@ import numpy as np
 __all__ = [
     "softmax_rows", "topk_from_logits", "route", "dispatch_brute", "dispatch_argsort",
     "ffn_forward", "ffn_backward", "router_backward", "layer_forward", "layer_backward",
-    "silu", "sigmoid",
+    "silu", "sigmoid", "ACTIVATIONS",
 ]
+
+# FFN variants: the paper evaluates SwiGLU experts (§5,
+# P:188-192) and non-gated experts E_i(x) = W2,i sigma(W1,i x) (§2.2) with
+# sigma = SiLU or ReLU.  Non-gated experts use w1 (gate/
+# first layer) and w3 (second layer); w2 is unused and B does not exist.
+ACTIVATIONS = ("swiglu", "silu", "relu")
 
 
 def sigmoid(a):
@@ -151,7 +157,26 @@ def _f64(a):
     return np.asarray(a, dtype=np.float64)
 
 
-def ffn_forward(x, w1, w2, w3, ids, w, disp):
+def _act(a, activation):
+    """sigma of the non-gated FFN: SiLU(u) = u sigma(u) or ReLU."""
+    if activation == "silu":
+        return silu(a)
+    if activation == "relu":
+        return np.maximum(a, 0.0)
+    raise ValueError(activation)
+
+
+def _act_grad(a, activation):
+    """d sigma / d a: SiLU' = sigma(a)(1 + a(1 - sigma(a))); ReLU' = 1[a > 0]."""
+    if activation == "silu":
+        s = sigmoid(a)
+        return s * (1.0 + a * (1.0 - s))
+    if activation == "relu":
+        return (a > 0).astype(np.float64)
+    raise ValueError(activation)
+
+
+def ffn_forward(x, w1, w2, w3, ids, w, disp, activation="swiglu"):
     """Expert computation + output aggregation, forward (Alg. 1
     FusedForward P:221-233, SwiGLU P:190-192, aggregation P:89-93).
 
@@ -163,8 +188,12 @@ def ffn_forward(x, w1, w2, w3, ids, w, disp):
         y_t += w[t,j] * O_r                        (P:91)
     Returns y [T,d] and the checkpointed pre-activations A, B [T*k, h] in
     expert-sorted row order.
+    Non-gated (activation = "silu" | "relu"): U_r = sigma(A_r), no B
+    (returned as None), w2 unused.
     """
-    x, w1, w2, w3, w = _f64(x), _f64(w1), _f64(w2), _f64(w3), _f64(w)
+    gated = activation == "swiglu"
+    x, w1, w3, w = _f64(x), _f64(w1), _f64(w3), _f64(w)
+    w2 = _f64(w2) if gated else None
     T, d = x.shape
     E, h, _ = w1.shape
     k = ids.shape[1]
@@ -172,7 +201,7 @@ def ffn_forward(x, w1, w2, w3, ids, w, disp):
     R = T * k
     y = np.zeros((T, d))
     A = np.zeros((R, h))
-    B = np.zeros((R, h))
+    B = np.zeros((R, h)) if gated else None
     for e in range(E):
         lo, hi = int(offs[e]), int(offs[e + 1])
         if hi == lo:
@@ -181,17 +210,20 @@ def ffn_forward(x, w1, w2, w3, ids, w, disp):
         slots = row_slot[lo:hi].astype(np.int64)
         xe = x[toks]
         a = xe @ w1[e].T
-        b = xe @ w2[e].T
-        u = silu(a) * b
+        if gated:
+            b = xe @ w2[e].T
+            u = silu(a) * b
+            B[lo:hi] = b
+        else:
+            u = _act(a, activation)
         o = u @ w3[e].T
         wr = w.reshape(-1)[slots]
         np.add.at(y, toks, wr[:, None] * o)
         A[lo:hi] = a
-        B[lo:hi] = b
     return dict(y=y, A=A, B=B)
 
 
-def ffn_backward(dy, x, w1, w2, w3, ids, w, disp, A, B):
+def ffn_backward(dy, x, w1, w2, w3, ids, w, disp, A, B, activation="swiglu"):
     """Expert backward (Alg. 1 FusedBackward P:236-253, §3.2), with
     the routing weight of P:91 carried through, plus the gate-weight gradient.
 
@@ -207,20 +239,25 @@ def ffn_backward(dy, x, w1, w2, w3, ids, w, disp, A, B):
         dx_t  += dA_r W1_e^T + dB_r W2_e^T            (l.30 FusedBwdX)
     SiLU'(a) = sigma(a) (1 + a (1 - sigma(a))).
     Returns dx [T,d], dw1, dw2 [E,h,d], dw3 [E,d,h], dg [T,k], dA, dB [R,h].
+    Non-gated: U = sigma(A), dA = dU * sigma'(A); dw2, dB are None and
+    dx_t += dA_r W1_e^T only.
     """
-    dy, x, w1, w2, w3, w = _f64(dy), _f64(x), _f64(w1), _f64(w2), _f64(w3), _f64(w)
-    A, B = _f64(A), _f64(B)
+    gated = activation == "swiglu"
+    dy, x, w1, w3, w = _f64(dy), _f64(x), _f64(w1), _f64(w3), _f64(w)
+    w2 = _f64(w2) if gated else None
+    A = _f64(A)
+    B = _f64(B) if gated else None
     T, d = x.shape
     E, h, _ = w1.shape
     k = ids.shape[1]
     offs, eti, row_slot = disp["offs"], disp["eti"], disp["row_slot"]
     dx = np.zeros((T, d))
     dw1 = np.zeros_like(w1)
-    dw2 = np.zeros_like(w2)
+    dw2 = np.zeros_like(w2) if gated else None
     dw3 = np.zeros_like(w3)
     dg = np.zeros(T * k)
     dA = np.zeros_like(A)
-    dB = np.zeros_like(B)
+    dB = np.zeros_like(B) if gated else None
     for e in range(E):
         lo, hi = int(offs[e]), int(offs[e + 1])
         if hi == lo:
@@ -228,23 +265,31 @@ def ffn_backward(dy, x, w1, w2, w3, ids, w, disp, A, B):
         toks = eti[lo:hi].astype(np.int64)
         slots = row_slot[lo:hi].astype(np.int64)
         wr = w.reshape(-1)[slots][:, None]
-        a, b = A[lo:hi], B[lo:hi]
-        sg = sigmoid(a)
-        s = a * sg
-        u = s * b
+        a = A[lo:hi]
+        if gated:
+            b = B[lo:hi]
+            sg = sigmoid(a)
+            s = a * sg
+            u = s * b
+        else:
+            u = _act(a, activation)
         go = dy[toks]
         dhu = go @ w3[e]                      # [n, h]  (w3[e] is [d, h])
         dg[slots] = np.sum(dhu * u, axis=1)
         dw3[e] = go.T @ (wr * u)              # [d, h]
         du = wr * dhu
-        da = du * b * sg * (1.0 + a * (1.0 - sg))
-        db = du * s
         xe = x[toks]
+        if gated:
+            da = du * b * sg * (1.0 + a * (1.0 - sg))
+            db = du * s
+            dw2[e] = db.T @ xe
+            dB[lo:hi] = db
+            np.add.at(dx, toks, da @ w1[e] + db @ w2[e])
+        else:
+            da = du * _act_grad(a, activation)
+            np.add.at(dx, toks, da @ w1[e])
         dw1[e] = da.T @ xe                    # [h, d]
-        dw2[e] = db.T @ xe
-        np.add.at(dx, toks, da @ w1[e] + db @ w2[e])
         dA[lo:hi] = da
-        dB[lo:hi] = db
     return dict(dx=dx, dw1=dw1, dw2=dw2, dw3=dw3, dg=dg.reshape(T, k), dA=dA, dB=dB)
 
 
@@ -273,7 +318,7 @@ def router_backward(dg, x, w_gate, logits, ids, renormalize=False):
     return dict(dlogits=dlogits, dw_gate=dlogits.T @ x, dx=dlogits @ w_gate)
 
 
-def layer_forward(x, w_gate, w1, w2, w3, k, renormalize=False, logits=None, dispatch="argsort"):
+def layer_forward(x, w_gate, w1, w2, w3, k, renormalize=False, logits=None, dispatch="argsort", activation="swiglu"):
     """Whole layer forward.  `logits` given => forced routing on those logits
     (used with the GPU's fp32 logits so near-ties resolve identically)."""
     if logits is None:
@@ -283,13 +328,14 @@ def layer_forward(x, w_gate, w1, w2, w3, k, renormalize=False, logits=None, disp
         r = dict(logits=_f64(logits), probs=p, ids=ids, w=w)
     E = _f64(w_gate).shape[0]
     disp = (dispatch_brute if dispatch == "brute" else dispatch_argsort)(r["ids"], E)
-    f = ffn_forward(x, w1, w2, w3, r["ids"], r["w"], disp)
-    return dict(**r, disp=disp, **f)
+    f = ffn_forward(x, w1, w2, w3, r["ids"], r["w"], disp, activation)
+    return dict(**r, disp=disp, activation=activation, **f)
 
 
 def layer_backward(fwd, dy, x, w_gate, w1, w2, w3, renormalize=False):
     """Whole layer backward: expert part + router part; dx includes both."""
-    b = ffn_backward(dy, x, w1, w2, w3, fwd["ids"], fwd["w"], fwd["disp"], fwd["A"], fwd["B"])
+    b = ffn_backward(dy, x, w1, w2, w3, fwd["ids"], fwd["w"], fwd["disp"], fwd["A"], fwd["B"],
+                     fwd.get("activation", "swiglu"))
     rb = router_backward(b["dg"], x, w_gate, fwd["logits"], fwd["ids"], renormalize)
     out = dict(b)
     out["dx_ffn"] = b["dx"]

@@ -198,3 +198,65 @@ def test_paper_memory_formulas():
     assert math.isclose(L * d * k * 2 / 1e9, 98.304)
     assert 90 < L * d * k * 2 / 2**30 < 95
     assert math.isclose(2 * L * h / 1e9, 98.304)
+
+
+# ---------------------------------------------------------------- non-gated experts (NEXT-2)
+@pytest.mark.parametrize("act", ["silu", "relu"])
+def test_nongated_single_expert_is_textbook_mlp(act):
+    """E = k = 1: y = W2 sigma(W1 x) via torch.nn.functional, fp64."""
+    P = _problem(E=1, k=1)
+    f = O.layer_forward(P["x"], P["w_gate"], P["w1"], P["w2"], P["w3"], 1, activation=act)
+    x, w1, w3 = (torch.from_numpy(np.ascontiguousarray(a)) for a in (P["x"], P["w1"][0], P["w3"][0]))
+    sig = F.silu if act == "silu" else F.relu
+    ref = F.linear(sig(F.linear(x, w1)), w3).numpy()
+    assert np.allclose(f["y"], ref, rtol=1e-12, atol=1e-12)
+    assert f["B"] is None
+
+
+@pytest.mark.parametrize("act", ["silu", "relu"])
+@pytest.mark.parametrize("renorm", [False, True])
+def test_nongated_backward_vs_dense_masked_autograd(act, renorm):
+    T, d, h, E, k = 21, 12, 16, 5, 2
+    P = _problem(T, d, h, E, k, seed=4)
+    fwd = O.layer_forward(P["x"], P["w_gate"], P["w1"], P["w2"], P["w3"], k, renorm, activation=act)
+    bwd = O.layer_backward(fwd, P["dy"], P["x"], P["w_gate"], P["w1"], P["w2"], P["w3"], renorm)
+    t = {n: torch.tensor(v, requires_grad=True) for n, v in P.items() if n != "dy"}
+    logits = t["x"] @ t["w_gate"].T
+    p = torch.softmax(logits, 1)
+    ids = torch.from_numpy(np.argsort(-logits.detach().numpy(), axis=1, kind="stable")[:, :k].copy())
+    G = p * torch.zeros_like(p).scatter_(1, ids, 1.0)
+    if renorm:
+        G = G / G.sum(1, keepdim=True)
+    sig = F.silu if act == "silu" else F.relu
+    y = sum(G[:, e:e + 1] * F.linear(sig(F.linear(t["x"], t["w1"][e])), t["w3"][e]) for e in range(E))
+    assert np.allclose(y.detach().numpy(), fwd["y"], rtol=1e-12, atol=1e-12)
+    (y * torch.from_numpy(P["dy"])).sum().backward()
+    for mine, ref in (("dx", "x"), ("dw1", "w1"), ("dw3", "w3"), ("dw_gate", "w_gate")):
+        g = t[ref].grad.numpy()
+        assert np.abs(bwd[mine] - g).max() / max(np.abs(g).max(), 1e-6) < 1e-10, (act, mine)
+    assert bwd["dw2"] is None and np.abs(t["w2"].grad.numpy() if t["w2"].grad is not None else 0).max() == 0
+
+
+def test_nongated_silu_finite_differences():
+    T, d, h, E, k = 10, 6, 8, 3, 2
+    P = _problem(T, d, h, E, k, seed=13)
+    fwd = O.layer_forward(P["x"], P["w_gate"], P["w1"], P["w2"], P["w3"], k, activation="silu")
+    bwd = O.layer_backward(fwd, P["dy"], P["x"], P["w_gate"], P["w1"], P["w2"], P["w3"])
+    rng = np.random.default_rng(3)
+    eps = 1e-6
+    for name, gname in (("x", "dx"), ("w1", "dw1"), ("w3", "dw3"), ("w_gate", "dw_gate")):
+        done = 0
+        while done < 8:
+            idx = tuple(rng.integers(0, s) for s in P[name].shape)
+            vals, idsl = [], []
+            for sgn in (1, -1):
+                Q = {n: v.copy() for n, v in P.items()}
+                Q[name][idx] += sgn * eps
+                f = O.layer_forward(Q["x"], Q["w_gate"], Q["w1"], Q["w2"], Q["w3"], k, activation="silu")
+                vals.append(float(np.sum(f["y"] * P["dy"])))
+                idsl.append(f["ids"])
+            if not all(np.array_equal(i, fwd["ids"]) for i in idsl):
+                continue
+            fd = (vals[0] - vals[1]) / (2 * eps)
+            assert abs(fd - bwd[gname][idx]) <= 1e-6 * max(1.0, abs(fd)), (name, idx)
+            done += 1
