@@ -79,9 +79,15 @@ typedef struct {
                              live in ws during moe_ffn_fwd (a_save/b_save may be NULL) and
                              moe_ffn_bwd recomputes them with the fused up-projection
                              (+4 T*k*d*h flops; results bit-identical to MOE_CKPT_AB) */
+  int32_t activation;     /* expert FFN: MOE_ACT_SWIGLU (0, default) =
+                             SiLU(x W1) * (x W2) W3; MOE_ACT_SILU (1) / MOE_ACT_RELU (2)
+                             = the non-gated expert W2 sigma(W1 x) of P:75 (the paper's SiLU /
+                             ReLU experiments): uses w1 and w3 only; w2, b_save and
+                             dw2 are unused (may be NULL); A alone is checkpointed */
 } moe_problem;
 
 enum { MOE_CKPT_AB = 0, MOE_CKPT_NONE = 1 };
+enum { MOE_ACT_SWIGLU = 0, MOE_ACT_SILU = 1, MOE_ACT_RELU = 2 };
 
 /* The compact dispatch index structures of §4.1.  R = T*k.
  *   expert_counts[E]         tokens routed to each expert (expert_lengths)

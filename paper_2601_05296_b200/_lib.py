@@ -28,7 +28,7 @@ GEMM_KINDS = ("FWD_UP", "FWD_DOWN", "BWD_DH", "BWD_DX", "DW3", "DW12")
 class MoeProblem(ctypes.Structure):
     _fields_ = [("T", ctypes.c_int64), ("d", ctypes.c_int32), ("h", ctypes.c_int32), ("E", ctypes.c_int32),
                 ("k", ctypes.c_int32), ("dtype", ctypes.c_int32), ("renormalize", ctypes.c_int32),
-                ("check_routing", ctypes.c_int32), ("checkpoint", ctypes.c_int32)]
+                ("check_routing", ctypes.c_int32), ("checkpoint", ctypes.c_int32), ("activation", ctypes.c_int32)]
 
 
 class MoeDispatch(ctypes.Structure):
@@ -111,9 +111,12 @@ MOE_CKPT_AB, MOE_CKPT_NONE = 0, 1
 CHECKPOINT = {"ab": MOE_CKPT_AB, "none": MOE_CKPT_NONE}
 
 
-def problem(T, d, h, E, k, dtype, renormalize=False, check_routing=False, checkpoint="ab"):
+ACTIVATION = {"swiglu": 0, "silu": 1, "relu": 2}
+
+
+def problem(T, d, h, E, k, dtype, renormalize=False, check_routing=False, checkpoint="ab", activation="swiglu"):
     return MoeProblem(int(T), int(d), int(h), int(E), int(k), _dtype_code(dtype), int(bool(renormalize)),
-                      int(bool(check_routing)), CHECKPOINT[checkpoint])
+                      int(bool(check_routing)), CHECKPOINT[checkpoint], ACTIVATION[activation])
 
 
 def workspace_size(p, op):

@@ -35,6 +35,7 @@ static moe_status validate(const moe_problem* p) {
   if (p->dtype == MOE_BF16 && (p->d % 128 != 0 || p->h % 128 != 0)) return MOE_ERR_UNSUPPORTED;
   if (p->dtype == MOE_FP32 && (p->d % 8 != 0)) return MOE_ERR_UNSUPPORTED;
   if (p->checkpoint != MOE_CKPT_AB && p->checkpoint != MOE_CKPT_NONE) return MOE_ERR_INVALID_ARG;
+  if (p->activation < MOE_ACT_SWIGLU || p->activation > MOE_ACT_RELU) return MOE_ERR_INVALID_ARG;
   return MOE_OK;
 }
 
@@ -158,10 +159,11 @@ moe_status moe_ffn_fwd(const moe_problem* p, const void* x, const void* w1, cons
                        size_t ws_bytes, void* stream) {
   moe_status s = validate(p);
   if (s != MOE_OK) return s;
-  if (!disp || !w1 || !w2 || !w3) return MOE_ERR_INVALID_ARG;
+  const bool gated = p->activation == MOE_ACT_SWIGLU;
+  if (!disp || !w1 || (gated && !w2) || !w3) return MOE_ERR_INVALID_ARG;
   const bool ckpt = p->checkpoint == MOE_CKPT_AB;
-  if (p->T > 0 && (!x || !y || !topk_w || (ckpt && (!a_save || !b_save)) || !ws || !disp->expert_offsets ||
-                   !disp->expert_token_indices || !disp->row_slot))
+  if (p->T > 0 && (!x || !y || !topk_w || (ckpt && (!a_save || (gated && !b_save))) || !ws ||
+                   !disp->expert_offsets || !disp->expert_token_indices || !disp->row_slot))
     return MOE_ERR_INVALID_ARG;
   if (!aligned16(x) || !aligned16(w1) || !aligned16(w2) || !aligned16(w3) || !aligned16(a_save) ||
       !aligned16(b_save) || !aligned16(y))
@@ -180,6 +182,7 @@ moe_status moe_ffn_fwd(const moe_problem* p, const void* x, const void* w1, cons
   c.offs = disp->expert_offsets; c.eti = disp->expert_token_indices; c.row_slot = disp->row_slot;
   c.a_save = a_save; c.b_save = b_save; c.u = w.u; c.acc_out = w.yacc;
   c.T = p->T; c.R = p->T * p->k; c.d = p->d; c.h = p->h; c.E = p->E; c.bf16 = p->dtype == MOE_BF16;
+  c.act = p->activation;
   c.which = GEMM_FWD_UP;
   if ((s = run_gemm(c, st)) != MOE_OK) return s;
   c.which = GEMM_FWD_DOWN;
@@ -193,12 +196,13 @@ moe_status moe_ffn_bwd(const moe_problem* p, const void* dy, const void* x, cons
                        void* ws, size_t ws_bytes, void* stream) {
   moe_status s = validate(p);
   if (s != MOE_OK) return s;
-  if (!disp || !dw1 || !dw2 || !dw3 || !w1 || !w2 || !w3) return MOE_ERR_INVALID_ARG;
+  const bool gated = p->activation == MOE_ACT_SWIGLU;
+  if (!disp || !dw1 || (gated && (!dw2 || !w2)) || !dw3 || !w1 || !w3) return MOE_ERR_INVALID_ARG;
   if (router && (!router->w_gate || !router->dw_gate)) return MOE_ERR_INVALID_ARG;
   if (router && p->T > 0 && (!router->logits || !router->topk_ids)) return MOE_ERR_INVALID_ARG;
   const bool ckpt = p->checkpoint == MOE_CKPT_AB;
-  if (p->T > 0 && (!dy || !x || !dx || !topk_w || (ckpt && (!a_save || !b_save)) || !ws || !disp->expert_offsets ||
-                   !disp->expert_token_indices || !disp->token_index_map || !disp->row_slot))
+  if (p->T > 0 && (!dy || !x || !dx || !topk_w || (ckpt && (!a_save || (gated && !b_save))) || !ws ||
+                   !disp->expert_offsets || !disp->expert_token_indices || !disp->token_index_map || !disp->row_slot))
     return MOE_ERR_INVALID_ARG;
   if (!aligned16(dy) || !aligned16(x) || !aligned16(a_save) || !aligned16(b_save) || !aligned16(dx) ||
       !aligned16(dw1) || !aligned16(dw2) || !aligned16(dw3))
@@ -217,6 +221,7 @@ moe_status moe_ffn_bwd(const moe_problem* p, const void* dy, const void* x, cons
   c.a_save = a_save; c.b_save = b_save; c.u = w.wu; c.acc_out = w.dxacc; c.dg_part = w.dgpart;
   c.dw_a = dw3; c.dw_b = nullptr;
   c.T = p->T; c.R = R; c.d = p->d; c.h = p->h; c.E = p->E; c.bf16 = p->dtype == MOE_BF16;
+  c.act = p->activation;
   if (p->T > 0) {
     MOE_CUDA_CHECK(cudaMemsetAsync(w.dxacc, 0, (size_t)p->T * p->d * 4, st));
     if (!ckpt) {  // MOE_CKPT_NONE: recompute A, B (and U into the wU buffer) with the fused up-projection

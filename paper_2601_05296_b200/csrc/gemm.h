@@ -20,7 +20,14 @@ struct GemmCall {
   int64_t T, R;
   int d, h, E;
   bool bf16;
+  int act;  // MOE_ACT_*: 0 = SwiGLU (gated), 1 = SiLU, 2 = ReLU (non-gated)
 };
+
+// non-gated activation sigma and its derivative
+__device__ __forceinline__ float act_fwd(int act, float a, float sg) { return act == 2 ? fmaxf(a, 0.f) : a * sg; }
+__device__ __forceinline__ float act_grad(int act, float a, float sg) {
+  return act == 2 ? (a > 0.f ? 1.f : 0.f) : sg * (1.f + a * (1.f - sg));
+}
 
 moe_status run_gemm(const GemmCall& c, cudaStream_t st);
 int gemm_dg_parts(const GemmCall& c);  // dg partial columns per row written by BWD_DH

@@ -32,6 +32,7 @@ struct SimtArgs {
   float* dg_part;                        // [R, nparts]
   T* dw_a; T* dw_b;                      // DW3: dw3 ; DW12: dw1, dw2
   int64_t R; int d, h, E;
+  int act;                               // 0 SwiGLU (gated); 1 SiLU, 2 ReLU (non-gated)
 };
 
 template <typename T, int MODE>
@@ -53,8 +54,9 @@ __global__ void __launch_bounds__(ST) simt_rows_kernel(SimtArgs<T> g) {
   const int e = find_segment(tstart, E, mt);
   const int seg0 = g.offs[e], seg1 = g.offs[e + 1];
   const int r0 = seg0 + (mt - tstart[e]) * SB;
+  const bool gated = g.act == 0;
   const int N = (MODE == FWD_UP || MODE == BWD_DH) ? g.h : g.d;
-  const int K = (MODE == FWD_UP || MODE == BWD_DH) ? g.d : (MODE == FWD_DOWN ? g.h : 2 * g.h);
+  const int K = (MODE == FWD_UP || MODE == BWD_DH) ? g.d : (MODE == FWD_DOWN ? g.h : (gated ? 2 : 1) * g.h);
   const int n0 = blockIdx.y * SB;
   const int64_t hd = (int64_t)g.h * g.d;
   float acc[2][4][4];
@@ -85,7 +87,7 @@ __global__ void __launch_bounds__(ST) simt_rows_kernel(SimtArgs<T> g) {
       if (kg < K && n < N) {
         if (MODE == FWD_UP) {
           v0 = to_f32(g.w1[e * hd + (int64_t)n * g.d + kg]);
-          v1 = to_f32(g.w2[e * hd + (int64_t)n * g.d + kg]);
+          v1 = gated ? to_f32(g.w2[e * hd + (int64_t)n * g.d + kg]) : 0.f;
         } else if (MODE == FWD_DOWN) {
           v0 = to_f32(g.w3[e * hd + (int64_t)n * g.h + kg]);
         } else if (MODE == BWD_DH) {
@@ -132,19 +134,29 @@ __global__ void __launch_bounds__(ST) simt_rows_kernel(SimtArgs<T> g) {
         float a = acc[0][i][j], b = acc[1][i][j];
         int64_t o = (int64_t)r * g.h + n;
         g.a_save[o] = from_f32<T>(a);
-        g.b_save[o] = from_f32<T>(b);
-        g.u[o] = from_f32<T>(a * sigmoidf_(a) * b);
+        if (gated) {
+          g.b_save[o] = from_f32<T>(b);
+          g.u[o] = from_f32<T>(a * sigmoidf_(a) * b);
+        } else {
+          g.u[o] = from_f32<T>(act_fwd(g.act, a, sigmoidf_(a)));
+        }
       } else if (MODE == FWD_DOWN) {
         atomicAdd(&g.acc_out[t * g.d + n], w * acc[0][i][j]);
       } else if (MODE == BWD_DH) {
         int64_t o = (int64_t)r * g.h + n;
-        float a = to_f32(g.a_save[o]), b = to_f32(g.b_save[o]);
-        float s = sigmoidf_(a), S = a * s, U = S * b, dH = acc[0][i][j];
-        rowsum[i] += dH * U;
-        float dU = w * dH;
-        g.a_save[o] = from_f32<T>(dU * b * s * (1.f + a * (1.f - s)));
-        g.b_save[o] = from_f32<T>(dU * S);
-        g.u[o] = from_f32<T>(w * U);
+        const float a = to_f32(g.a_save[o]), dH = acc[0][i][j], s = sigmoidf_(a), dU = w * dH;
+        if (gated) {
+          const float b = to_f32(g.b_save[o]), S = a * s, U = S * b;
+          rowsum[i] += dH * U;
+          g.a_save[o] = from_f32<T>(dU * b * s * (1.f + a * (1.f - s)));
+          g.b_save[o] = from_f32<T>(dU * S);
+          g.u[o] = from_f32<T>(w * U);
+        } else {
+          const float U = act_fwd(g.act, a, s);
+          rowsum[i] += dH * U;
+          g.a_save[o] = from_f32<T>(dU * act_grad(g.act, a, s));
+          g.u[o] = from_f32<T>(w * U);
+        }
       } else {
         atomicAdd(&g.acc_out[t * g.d + n], acc[0][i][j]);
       }
@@ -172,7 +184,7 @@ __global__ void __launch_bounds__(ST) simt_wgrad_kernel(SimtArgs<T> g) {
   __shared__ float Bs[SK][SB + 4];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   const int e = blockIdx.z;
-  const int M = MODE == DW3 ? g.d : 2 * g.h;
+  const int M = MODE == DW3 ? g.d : (g.act == 0 ? 2 : 1) * g.h;
   const int N = MODE == DW3 ? g.h : g.d;
   const int m0 = blockIdx.y * SB, n0 = blockIdx.x * SB;
   const int seg0 = g.offs[e], seg1 = g.offs[e + 1];
@@ -241,7 +253,7 @@ static moe_status simt_launch_all(int which, const SimtArgs<T>& g, cudaStream_t 
     case 2: MOE_LAUNCH((simt_rows_kernel<T, BWD_DH>), dim3(mtiles, ceil_div(g.h, SB)), ST, 0, st, g); break;
     case 3: MOE_LAUNCH((simt_rows_kernel<T, BWD_DX>), dim3(mtiles, ceil_div(g.d, SB)), ST, 0, st, g); break;
     case 4: MOE_LAUNCH((simt_wgrad_kernel<T, DW3>), dim3(ceil_div(g.h, SB), ceil_div(g.d, SB), g.E), ST, 0, st, g); break;
-    case 5: MOE_LAUNCH((simt_wgrad_kernel<T, DW12>), dim3(ceil_div(g.d, SB), ceil_div(2 * g.h, SB), g.E), ST, 0, st, g); break;
+    case 5: MOE_LAUNCH((simt_wgrad_kernel<T, DW12>), dim3(ceil_div(g.d, SB), ceil_div((g.act == 0 ? 2 : 1) * g.h, SB), g.E), ST, 0, st, g); break;
   }
   MOE_CUDA_CHECK(cudaGetLastError());
   return MOE_OK;
@@ -252,13 +264,13 @@ moe_status simt_gemm(const GemmCall& c, cudaStream_t st) {
     using T = __nv_bfloat16;
     SimtArgs<T> g{(const T*)c.x, (const T*)c.dy, (const T*)c.w1, (const T*)c.w2, (const T*)c.w3, c.topw, c.offs, c.eti,
                   c.row_slot, (T*)c.a_save, (T*)c.b_save, (T*)c.u, c.acc_out, c.dg_part, (T*)c.dw_a, (T*)c.dw_b,
-                  c.R, c.d, c.h, c.E};
+                  c.R, c.d, c.h, c.E, c.act};
     return simt_launch_all<T>(c.which, g, st);
   }
   using T = float;
   SimtArgs<T> g{(const T*)c.x, (const T*)c.dy, (const T*)c.w1, (const T*)c.w2, (const T*)c.w3, c.topw, c.offs, c.eti,
                 c.row_slot, (T*)c.a_save, (T*)c.b_save, (T*)c.u, c.acc_out, c.dg_part, (T*)c.dw_a, (T*)c.dw_b,
-                c.R, c.d, c.h, c.E};
+                c.R, c.d, c.h, c.E, c.act};
   return simt_launch_all<T>(c.which, g, st);
 }
 

@@ -86,6 +86,7 @@ struct TcParams {
   float* route_w;
   int k, renorm, route_n;
   uint32_t route_idesc;
+  int act;  // MOE_ACT_*: 0 SwiGLU (gated: stacked [W1;W2], A and B); 1 SiLU / 2 ReLU (non-gated)
 };
 
 template <int KIND>
@@ -163,8 +164,9 @@ __device__ __forceinline__ bool decode_tile(int tile, const TcParams& P, const i
       mi = nfull * RG + (rem - t.n_tile * gl);
     }
     t.m0 = t.seg0 + mi * TM;
-    t.n0 = t.n_tile * K::NT;
-    const int Kdim = (KIND == TC_FWD_UP || KIND == TC_BWD_DH) ? P.d : (KIND == TC_FWD_DOWN ? P.h : 2 * P.h);
+    t.n0 = t.n_tile * ((KIND == TC_FWD_UP && P.act == 0) ? 128 : 256);
+    const int Kdim = (KIND == TC_FWD_UP || KIND == TC_BWD_DH) ? P.d
+                     : (KIND == TC_FWD_DOWN ? P.h : (P.act == 0 ? 2 : 1) * P.h);
     t.nk = Kdim / TBK;
   }
   return true;
@@ -375,12 +377,15 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
           if (lane == 1) load(sB, &mB0, k0, 0);
         } else if constexpr (KIND == TC_FWD_UP) {
           if (!CPA) ptx::tma_gather4(sA + 512 * lane, &mA0, bar, k0, gi0, gi1, gi2, gi3);
+          const bool gated = P.act == 0;
           if constexpr (CG == 1) {
+            // gated: B = [W1 tile ; W2 tile] (128 + 128 rows); non-gated: 256 rows of W1
             if (lane == 0) load(sB, &mB0, k0, t.e * P.h + t.n0);
-            if (lane == 1) load(sB + C::B_BYTES / 2, &mB1, k0, t.e * P.h + t.n0);
+            if (lane == 1) load(sB + C::B_BYTES / 2, gated ? &mB1 : &mB0, k0, t.e * P.h + t.n0 + (gated ? 0 : 128));
           } else {
-            // the pair's B = [W1 tile ; W2 tile]: CTA 0 holds the W1 rows, CTA 1 the W2 rows
-            if (lane == 0) load(sB, crank ? &mB1 : &mB0, k0, t.e * P.h + t.n0);
+            // gated: CTA 0 holds the W1 rows, CTA 1 the W2 rows; non-gated: W1 rows n0 + 128 * rank
+            if (lane == 0)
+              load(sB, (gated && crank) ? &mB1 : &mB0, k0, t.e * P.h + t.n0 + (gated ? 0 : 128 * (int)crank));
           }
         } else if constexpr (KIND == TC_FWD_DOWN) {
           if (lane == 0) load(sA, &mA0, k0, t.m0 + rowoff);
@@ -420,7 +425,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
             }
           }
           const int m = t.m0 + rowoff;
-          const bool second = m >= P.h;
+          const bool second = m >= P.h;  // (only for the gated FFN, where M = 2h)
           if (lane >= 2 && lane < 4)
             load(sA + (lane - 2) * 8192, second ? &mA1 : &mA0, (second ? m - P.h : m) + 64 * (lane - 2), t.seg0 + k0);
         }
@@ -601,7 +606,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
           if (ci < nchunk) {
             uint8_t* NA = stg + ci * 4096;
             stg_load_bf16_async(NA, lane, P.a_save + o0 + ci * 32, P.h, nvalid);
-            stg_load_bf16_async(NA + 2048, lane, P.b_save + o0 + ci * 32, P.h, nvalid);
+            if (P.act == 0) stg_load_bf16_async(NA + 2048, lane, P.b_save + o0 + ci * 32, P.h, nvalid);
           }
           asm volatile("cp.async.commit_group;" ::: "memory");
         }
@@ -679,8 +684,31 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
         uint8_t* T1 = stg + 2048;
         uint8_t* T2 = stg + 4096;
         uint32_t bv[32];
+        if (P.act != 0) {  // non-gated: 256 columns of A, U = sigma(A)
 #pragma unroll 1
-        for (int c = 0; c < 128; c += 32) {
+          for (int c = 0; c < TBN; c += 32) {
+            if (t.n0 + c >= P.h) break;
+            ptx::tmem_ld32(tb + c, v);
+            ptx::tmem_wait_ld();
+            float a[32], u[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              a[i] = __uint_as_float(v[i]);
+              u[i] = act_fwd(P.act, a[i], sigmoid_fast(a[i]));
+            }
+            stg_put_bf16(T0, lane, a);
+            stg_put_bf16(T2, lane, u);
+            __syncwarp();
+            if (nvalid > 0) {
+              const int64_t o = (int64_t)r0w * P.h + t.n0 + c;
+              stg_store_bf16(T0, lane, P.a_save + o, P.h, nvalid);
+              stg_store_bf16(T2, lane, P.u + o, P.h, nvalid);
+            }
+            __syncwarp();
+          }
+        }
+#pragma unroll 1
+        for (int c = 0; c < (P.act == 0 ? 128 : 0); c += 32) {
           ptx::tmem_ld32(tb + c, v);
           ptx::tmem_ld32(tb + 128 + c, bv);
           ptx::tmem_wait_ld();
@@ -762,7 +790,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
             if (nx < nchunk) {
               uint8_t* NA = stg + (nx % NBUF) * 4096;
               stg_load_bf16_async(NA, lane, P.a_save + o0 + nx * 32, P.h, nvalid);
-              stg_load_bf16_async(NA + 2048, lane, P.b_save + o0 + nx * 32, P.h, nvalid);
+              if (P.act == 0) stg_load_bf16_async(NA + 2048, lane, P.b_save + o0 + nx * 32, P.h, nvalid);
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
             asm volatile("cp.async.wait_group %0;" ::"n"(NBUF - 1) : "memory");
@@ -792,13 +820,21 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
                 const float dH = __uint_as_float(dh[q * 8 + e * 2 + z]);
                 const float a = av[z], b = bvv[z];
                 const float sg = sigmoid_fast(a);
-                const float S = a * sg;
-                const float U = S * b;
-                rowsum = fmaf(dH, U, rowsum);
                 const float dU = w * dH;
-                ra[z] = dU * b * sg * (1.f + a * (1.f - sg));
-                rb[z] = dU * S;
-                ru[z] = w * U;
+                if (P.act == 0) {
+                  const float S = a * sg;
+                  const float U = S * b;
+                  rowsum = fmaf(dH, U, rowsum);
+                  ra[z] = dU * b * sg * (1.f + a * (1.f - sg));
+                  rb[z] = dU * S;
+                  ru[z] = w * U;
+                } else {  // non-gated: U = sigma(A), dA = dU sigma'(A)
+                  const float U = act_fwd(P.act, a, sg);
+                  rowsum = fmaf(dH, U, rowsum);
+                  ra[z] = dU * act_grad(P.act, a, sg);
+                  rb[z] = 0.f;
+                  ru[z] = w * U;
+                }
               }
               oa[e] = ptx::pack_bf16(ra[0], ra[1]);
               ob[e] = ptx::pack_bf16(rb[0], rb[1]);
@@ -812,14 +848,14 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
           if (nvalid > 0) {
             const int64_t o = o0 + ci * 32;
             stg_store_bf16(TA, lane, P.a_save + o, P.h, nvalid);
-            stg_store_bf16(TB, lane, P.b_save + o, P.h, nvalid);
+            if (P.act == 0) stg_store_bf16(TB, lane, P.b_save + o, P.h, nvalid);
             stg_store_bf16(TU, lane, P.u + o, P.h, nvalid);
           }
           __syncwarp();
         }
         if (valid) P.dg_part[(int64_t)r * P.dg_parts + t.n_tile] = rowsum;
       } else {  // DW3 / DW12: store the weight-gradient tile
-        const int M = (KIND == TC_DW3) ? P.d : 2 * P.h;
+        const int M = (KIND == TC_DW3) ? P.d : (P.act == 0 ? 2 : 1) * P.h;
         const int m0w = t.m0 + rowoff + wq * 32;
         const int nvalid = max(0, min(32, M - m0w));
         __nv_bfloat16* base;
@@ -990,6 +1026,8 @@ moe_status tc_gemm(const GemmCall& c, cudaStream_t st) {
   const int d = c.d, h = c.h, E = c.E;
   const uint32_t bw = engine() == ENG_PAIR ? 128 : 256;  // K-major W3 box rows held per CTA
   TcParams P{};
+  P.act = c.act;
+  const bool gated = c.act == 0;
   P.x = (const bf*)c.x; P.dy = (const bf*)c.dy;
   P.offs = c.offs; P.eti = c.eti; P.row_slot = c.row_slot; P.topw = c.topw;
   P.a_save = (bf*)c.a_save; P.b_save = (bf*)c.b_save; P.u = (bf*)c.u;
@@ -1006,9 +1044,9 @@ moe_status tc_gemm(const GemmCall& c, cudaStream_t st) {
       if (R == 0) return MOE_OK;
       ok &= make_map(&a0, c.x, T, d, 64, 1);
       ok &= make_map(&b0, c.w1, (uint64_t)E * h, d, 64, 128);
-      ok &= make_map(&b1, c.w2, (uint64_t)E * h, d, 64, 128);
+      ok &= make_map(&b1, gated ? c.w2 : c.w1, (uint64_t)E * h, d, 64, 128);
       if (!ok) return MOE_ERR_CUDA;
-      P.n_tiles = h / 128;
+      P.n_tiles = gated ? h / 128 : (int)ceil_div(h, TBN);
       return launch_tc<TC_FWD_UP>(a0, a0, b0, b1, P, rows_tiles(P.n_tiles), st);
     }
     case GEMM_FWD_DOWN: {
@@ -1030,9 +1068,9 @@ moe_status tc_gemm(const GemmCall& c, cudaStream_t st) {
     case GEMM_BWD_DX: {
       if (R == 0) return MOE_OK;
       ok &= make_map(&a0, c.a_save, R, h, 64, 128);
-      ok &= make_map(&a1, c.b_save, R, h, 64, 128);
+      ok &= make_map(&a1, gated ? c.b_save : c.a_save, R, h, 64, 128);
       ok &= make_map(&b0, c.w1, (uint64_t)E * h, d, 64, 64);
-      ok &= make_map(&b1, c.w2, (uint64_t)E * h, d, 64, 64);
+      ok &= make_map(&b1, gated ? c.w2 : c.w1, (uint64_t)E * h, d, 64, 64);
       if (!ok) return MOE_ERR_CUDA;
       P.n_tiles = (int)ceil_div(d, TBN);
       return launch_tc<TC_BWD_DX>(a0, a1, b0, b1, P, rows_tiles(P.n_tiles), st);
@@ -1054,19 +1092,19 @@ moe_status tc_gemm(const GemmCall& c, cudaStream_t st) {
     case GEMM_DW12: {
       if (R == 0) {
         MOE_CUDA_CHECK(cudaMemsetAsync(c.dw_a, 0, (size_t)E * d * h * 2, st));
-        MOE_CUDA_CHECK(cudaMemsetAsync(c.dw_b, 0, (size_t)E * d * h * 2, st));
+        if (gated) MOE_CUDA_CHECK(cudaMemsetAsync(c.dw_b, 0, (size_t)E * d * h * 2, st));
         return MOE_OK;
       }
+      const int64_t M = (gated ? 2 : 1) * (int64_t)h;  // [dW1 ; dW2] rows, or dW1 only
       ok &= make_map(&a0, c.a_save, R, h, 64, 64);
-      ok &= make_map(&a1, c.b_save, R, h, 64, 64);
+      ok &= make_map(&a1, gated ? c.b_save : c.a_save, R, h, 64, 64);
       ok &= make_map(&b0, c.x, T, d, 64, 1);
       if (!ok) return MOE_ERR_CUDA;
       P.n_tiles = (int)ceil_div(d, TBN);
-      P.m_tiles = (int)ceil_div(2 * h, 128);
-      P.m_tiles2 = (int)ceil_div(2 * h, 256);
+      P.m_tiles = (int)ceil_div(M, 128);
+      P.m_tiles2 = (int)ceil_div(M, 256);
       const int64_t nt = P.n_tiles;
-      return launch_tc<TC_DW12>(a0, a1, b0, b0, P, [=](int TM) { return (int64_t)E * ceil_div(2 * h, TM) * nt; },
-                                st);
+      return launch_tc<TC_DW12>(a0, a1, b0, b0, P, [=](int TM) { return (int64_t)E * ceil_div(M, TM) * nt; }, st);
     }
   }
   return MOE_ERR_INVALID_ARG;

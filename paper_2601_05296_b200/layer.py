@@ -13,8 +13,8 @@ import torch
 from . import _lib as L
 
 
-def _problem(T, d, h, E, k, dtype, renormalize=False, check_routing=False, checkpoint="ab"):
-    return L.problem(T, d, h, E, k, dtype, renormalize, check_routing, checkpoint)
+def _problem(T, d, h, E, k, dtype, renormalize=False, check_routing=False, checkpoint="ab", activation="swiglu"):
+    return L.problem(T, d, h, E, k, dtype, renormalize, check_routing, checkpoint, activation)
 
 
 @dataclass
@@ -60,17 +60,21 @@ def dispatch_build(ids, E, check_routing=False, stream=None, dtype=torch.bfloat1
     return disp
 
 
-def ffn_fwd(x, w1, w2, w3, topk_w, disp: Dispatch, renormalize=False, stream=None, checkpoint="ab"):
+def ffn_fwd(x, w1, w2, w3, topk_w, disp: Dispatch, renormalize=False, stream=None, checkpoint="ab",
+            activation="swiglu"):
     """moe_ffn_fwd (§3.1, Alg. 1 FusedForward): returns y, A, B (A, B checkpointed;
-    None, None under checkpoint="none", where backward recomputes them)."""
+    None, None under checkpoint="none", where backward recomputes them).
+    activation "silu" | "relu": the non-gated expert W2 sigma(W1 x); w2
+    may be None and B is None."""
     T, d = x.shape
     E, h, _ = w1.shape
     k = topk_w.shape[1]
-    p = _problem(T, d, h, E, k, x.dtype, renormalize, checkpoint=checkpoint)
+    p = _problem(T, d, h, E, k, x.dtype, renormalize, checkpoint=checkpoint, activation=activation)
     R = T * k
     save = checkpoint == "ab"
+    gated = activation == "swiglu"
     a = torch.empty(R, h, dtype=x.dtype, device=x.device) if save else None
-    b = torch.empty(R, h, dtype=x.dtype, device=x.device) if save else None
+    b = torch.empty(R, h, dtype=x.dtype, device=x.device) if (save and gated) else None
     y = torch.empty(T, d, dtype=x.dtype, device=x.device)
     ws = L.workspace(p, L.MOE_OP_FFN_FWD, x.device)
     L.moe_ffn_fwd(p, x, w1, w2, w3, topk_w, disp.c(), a, b, y, ws, stream)
@@ -78,17 +82,17 @@ def ffn_fwd(x, w1, w2, w3, topk_w, disp: Dispatch, renormalize=False, stream=Non
 
 
 def ffn_bwd(dy, x, w1, w2, w3, topk_w, disp: Dispatch, a_save, b_save, w_gate=None, logits=None,
-            renormalize=False, stream=None, checkpoint="ab"):
+            renormalize=False, stream=None, checkpoint="ab", activation="swiglu"):
     """moe_ffn_bwd (§3.2, Alg. 1 FusedBackward).  a_save/b_save are overwritten
     with dA/dB (checkpoint="none": pass None, A and B are recomputed).  With
     w_gate/logits: router backward too (dx includes it)."""
     T, d = x.shape
     E, h, _ = w1.shape
     k = topk_w.shape[1]
-    p = _problem(T, d, h, E, k, x.dtype, renormalize, checkpoint=checkpoint)
+    p = _problem(T, d, h, E, k, x.dtype, renormalize, checkpoint=checkpoint, activation=activation)
     dx = torch.empty_like(x)
     dw1 = torch.empty_like(w1)
-    dw2 = torch.empty_like(w2)
+    dw2 = torch.empty_like(w2) if activation == "swiglu" else None
     dw3 = torch.empty_like(w3)
     dg = torch.empty(T, k, dtype=torch.float32, device=x.device)
     router = None
@@ -108,32 +112,37 @@ class MoEBlazeFunction(torch.autograd.Function):
     checkpoint="none" A, B are not saved either (recomputed in backward)."""
 
     @staticmethod
-    def forward(ctx, x, w_gate, w1, w2, w3, k, renormalize, checkpoint="ab"):
+    def forward(ctx, x, w_gate, w1, w2, w3, k, renormalize, checkpoint="ab", activation="swiglu"):
         logits, ids, w = route(x, w_gate, k, renormalize)
         disp = dispatch_build(ids, w_gate.shape[0], dtype=x.dtype)
-        y, a, b = ffn_fwd(x, w1, w2, w3, w, disp, renormalize, checkpoint=checkpoint)
-        saved = [x, w_gate, w1, w2, w3, logits, ids, w, disp.counts, disp.offs, disp.eti, disp.tim, disp.row_slot]
+        y, a, b = ffn_fwd(x, w1, w2, w3, w, disp, renormalize, checkpoint=checkpoint, activation=activation)
+        gated = activation == "swiglu"
+        saved = [x, w_gate, w1, w2 if gated else w1, w3, logits, ids, w, disp.counts, disp.offs, disp.eti, disp.tim,
+                 disp.row_slot]
         if checkpoint == "ab":
-            saved += [a, b]
+            saved += [a, b if gated else a]
         ctx.save_for_backward(*saved)
         ctx.renormalize = renormalize
         ctx.checkpoint = checkpoint
+        ctx.activation = activation
         return y
 
     @staticmethod
     def backward(ctx, dy):
         t = ctx.saved_tensors
         (x, w_gate, w1, w2, w3, logits, ids, w, counts, offs, eti, tim, row_slot) = t[:13]
-        a, b = (t[13], t[14]) if ctx.checkpoint == "ab" else (None, None)
+        gated = ctx.activation == "swiglu"
+        a, b = (t[13], t[14] if gated else None) if ctx.checkpoint == "ab" else (None, None)
         disp = Dispatch(counts, offs, eti, tim, row_slot, ids)
-        g = ffn_bwd(dy.contiguous(), x, w1, w2, w3, w, disp, a, b, w_gate=w_gate, logits=logits,
-                    renormalize=ctx.renormalize, checkpoint=ctx.checkpoint)
-        return g["dx"], g["dw_gate"], g["dw1"], g["dw2"], g["dw3"], None, None, None
+        g = ffn_bwd(dy.contiguous(), x, w1, w2 if gated else None, w3, w, disp, a, b, w_gate=w_gate, logits=logits,
+                    renormalize=ctx.renormalize, checkpoint=ctx.checkpoint, activation=ctx.activation)
+        return g["dx"], g["dw_gate"], g["dw1"], g["dw2"], g["dw3"], None, None, None, None
 
 
-def moe_layer(x, w_gate, w1, w2, w3, k, renormalize=False, checkpoint="ab"):
-    """checkpoint: "ab" (paper: save A, B, recompute SiLU) | "none" (save X only, recompute A, B)."""
-    return MoEBlazeFunction.apply(x, w_gate, w1, w2, w3, k, renormalize, checkpoint)
+def moe_layer(x, w_gate, w1, w2, w3, k, renormalize=False, checkpoint="ab", activation="swiglu"):
+    """checkpoint: "ab" (paper: save A (,B), recompute the activation) | "none" (recompute A, B).
+    activation: "swiglu" | "silu" | "relu" (non-gated W2 sigma(W1 x); w2 unused)."""
+    return MoEBlazeFunction.apply(x, w_gate, w1, w2, w3, k, renormalize, checkpoint, activation)
 
 
 class MoEBlazeLayer(torch.nn.Module):

@@ -224,3 +224,43 @@ def test_layer_edge_shapes(M, T, d, h, E, k, routing):
         sel = torch.from_numpy(empty).to(DEV)
         assert torch.count_nonzero(out["dw1"][sel]).item() == 0
         assert torch.count_nonzero(out["dw3"][sel]).item() == 0
+
+
+NONGATED_CASES = [
+    # name, T, d, h, E, k, dtype, act
+    ("silu_fp32", 256, 64, 128, 4, 2, "fp32", "silu"),
+    ("relu_fp32", 200, 64, 96, 6, 3, "fp32", "relu"),
+    ("silu_bf16", 512, 256, 384, 8, 2, "bf16", "silu"),      # h % 256 == 128 (half n-tile)
+    ("relu_bf16", 1000, 128, 512, 16, 4, "bf16", "relu"),
+    ("silu_bf16_k1", 333, 256, 256, 4, 1, "bf16", "silu"),
+]
+
+
+@pytest.mark.parametrize("case", NONGATED_CASES, ids=[c[0] for c in NONGATED_CASES])
+@pytest.mark.parametrize("ckpt", ["ab", "none"])
+def test_nongated_fwd_bwd_parity(M, case, ckpt):
+    """Non-gated experts W2 sigma(W1 x) (NEXT-2): y, dX, dW1, dW3, dW_g, dg
+    vs the oracle (w2 is not used: passed as None)."""
+    name, T, d, h, E, k, dtype, act = case
+    inp = make_inputs(T, d, h, E, k, dtype=dtype, seed=T, device=DEV)
+    x, wg, w1, w3, dy = (inp[n] for n in ("x", "w_gate", "w1", "w3", "dy"))
+    logits, ids, w = M.route(x, wg, k)
+    disp = M.dispatch_build(ids, E, dtype=x.dtype)
+    y, a, b = M.ffn_fwd(x, w1, None, w3, w, disp, checkpoint=ckpt, activation=act)
+    assert b is None
+    a0 = a.clone() if a is not None else None
+    g = M.ffn_bwd(dy, x, w1, None, w3, w, disp, a, b, w_gate=wg, logits=logits, checkpoint=ckpt, activation=act)
+    torch.cuda.synchronize()
+    assert g["dw2"] is None
+    tol = FP32_TOL if dtype == "fp32" else BF16_TOL
+    X, WG, W1, W3, DY = (f64(inp[n]) for n in ("x", "w_gate", "w1", "w3", "dy"))
+    fwd = O.layer_forward(X, WG, W1, None, W3, k, logits=f64(logits), activation=act)
+    bwd = O.layer_backward(fwd, DY, X, WG, W1, None, W3)
+    errs = {"y": normwise(y, fwd["y"]), "dx": normwise(g["dx"], bwd["dx"]), "dw1": normwise(g["dw1"], bwd["dw1"]),
+            "dw3": normwise(g["dw3"], bwd["dw3"]), "dw_gate": normwise(g["dw_gate"], bwd["dw_gate"]),
+            "dg": normwise(g["dg"], bwd["dg"])}
+    if a0 is not None:
+        errs["A"] = normwise(a0, fwd["A"])
+        errs["dA"] = normwise(a, bwd["dA"])
+    bad = {n: v for n, v in errs.items() if not v <= tol}
+    assert not bad, (name, ckpt, errs)
