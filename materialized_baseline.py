@@ -11,7 +11,7 @@ import torch
 import torch.nn.functional as F
 
 
-def materialized_moe(x, w_gate, w1, w2, w3, k, renormalize=False):
+def materialized_moe(x, w_gate, w1, w2, w3, k, renormalize=False, activation="swiglu"):
     T, d = x.shape
     E = w_gate.shape[0]
     logits = x.float() @ w_gate.float().t()
@@ -27,8 +27,11 @@ def materialized_moe(x, w_gate, w1, w2, w3, k, renormalize=False):
     offs = torch.cumsum(counts, 0).to(torch.int32)
     xr = x[eti]                                            # routed-token buffer [T*k, d]
     a = F.grouped_mm(xr, w1.transpose(1, 2), offs=offs)    # [R, h]
-    b = F.grouped_mm(xr, w2.transpose(1, 2), offs=offs)
-    u = F.silu(a) * b
+    if activation == "swiglu":
+        b = F.grouped_mm(xr, w2.transpose(1, 2), offs=offs)
+        u = F.silu(a) * b
+    else:                                                  # non-gated expert
+        u = F.silu(a) if activation == "silu" else F.relu(a)
     o = F.grouped_mm(u, w3.transpose(1, 2), offs=offs)     # expert outputs [R, d] before combine
     wr = w.reshape(-1)[order].to(o.dtype)
     y = torch.zeros(T, d, dtype=o.dtype, device=x.device).index_add_(0, eti, o * wr[:, None])
