@@ -84,6 +84,16 @@ typedef struct {
                              = the non-gated expert W2 sigma(W1 x) of P:75 (the paper's SiLU /
                              ReLU experiments): uses w1 and w3 only; w2, b_save and
                              dw2 are unused (may be NULL); A alone is checkpointed */
+  int32_t deterministic;  /* combine of the k expert outputs of a token (SURVEY §8(f) NEXT-4,
+                             P:111 vs P:134): 0 (default) = fused red.add of w*O into an fp32
+                             [T,d] accumulator in the down-GEMM epilogue (bitwise reproducible
+                             for k <= 2, order-dependent in the last bit for k >= 3);
+                             1 = ordered: the epilogue stores each routed row's fp32 result at
+                             its expert-sorted row index ([T*k, d] fp32 transient ws) and a
+                             token-side pass sums a token's rows in slot order j = 0..k-1
+                             through token_index_map (bitwise reproducible for every k; for
+                             k <= 2 bit-identical to mode 0).  Applies to y and dx.  k = 1
+                             ignores it: each token has one row, stored directly. */
 } moe_problem;
 
 enum { MOE_CKPT_AB = 0, MOE_CKPT_NONE = 1 };
@@ -118,7 +128,8 @@ typedef struct {
 } moe_router_bwd;
 
 /* Bytes of device scratch `ws` that `op` needs for problem `p` (closed form;
- * it has no T*k*d term: no routed-token buffer exists). */
+ * with deterministic = 0 it has no T*k*d term: no routed-token buffer exists;
+ * deterministic = 1 adds the transient [T*k, d] fp32 row-result buffer). */
 moe_status moe_workspace_size(const moe_problem* p, moe_op op, size_t* bytes);
 
 /* Gating.  logits = X W_g^T accumulated in fp32; ids[t,:] = the k

@@ -28,7 +28,8 @@ GEMM_KINDS = ("FWD_UP", "FWD_DOWN", "BWD_DH", "BWD_DX", "DW3", "DW12")
 class MoeProblem(ctypes.Structure):
     _fields_ = [("T", ctypes.c_int64), ("d", ctypes.c_int32), ("h", ctypes.c_int32), ("E", ctypes.c_int32),
                 ("k", ctypes.c_int32), ("dtype", ctypes.c_int32), ("renormalize", ctypes.c_int32),
-                ("check_routing", ctypes.c_int32), ("checkpoint", ctypes.c_int32), ("activation", ctypes.c_int32)]
+                ("check_routing", ctypes.c_int32), ("checkpoint", ctypes.c_int32), ("activation", ctypes.c_int32),
+                ("deterministic", ctypes.c_int32)]
 
 
 class MoeDispatch(ctypes.Structure):
@@ -114,9 +115,10 @@ CHECKPOINT = {"ab": MOE_CKPT_AB, "none": MOE_CKPT_NONE}
 ACTIVATION = {"swiglu": 0, "silu": 1, "relu": 2}
 
 
-def problem(T, d, h, E, k, dtype, renormalize=False, check_routing=False, checkpoint="ab", activation="swiglu"):
+def problem(T, d, h, E, k, dtype, renormalize=False, check_routing=False, checkpoint="ab", activation="swiglu",
+            deterministic=False):
     return MoeProblem(int(T), int(d), int(h), int(E), int(k), _dtype_code(dtype), int(bool(renormalize)),
-                      int(bool(check_routing)), CHECKPOINT[checkpoint], ACTIVATION[activation])
+                      int(bool(check_routing)), CHECKPOINT[checkpoint], ACTIVATION[activation], int(bool(deterministic)))
 
 
 def workspace_size(p, op):

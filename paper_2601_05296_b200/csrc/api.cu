@@ -19,7 +19,8 @@ moe_status launch_dg_reduce(const float*, int, const int32_t*, int64_t, float*, 
 int dwg_chunks(int64_t T, int d, int E);
 moe_status launch_router_bwd(const moe_problem*, const float*, const int32_t*, const float*, const void*, float*,
                              float*, void*, cudaStream_t);
-moe_status launch_finalize(const moe_problem*, const void*, const float*, const void*, void*, cudaStream_t, bool);
+moe_status launch_finalize(const moe_problem*, const void*, const float*, const void*, void*, cudaStream_t, bool,
+                           const int32_t*);
 moe_status launch_ep_row_meta(const int32_t*, const int32_t*, const float*, int64_t, int, float*, int32_t*, cudaStream_t);
 moe_status launch_gather_rows(const void*, const int32_t*, int64_t, int64_t, void*, cudaStream_t);
 moe_status launch_combine_rows(const moe_problem*, const void*, const int32_t*, void*, cudaStream_t);
@@ -36,6 +37,7 @@ static moe_status validate(const moe_problem* p) {
   if (p->dtype == MOE_FP32 && (p->d % 8 != 0)) return MOE_ERR_UNSUPPORTED;
   if (p->checkpoint != MOE_CKPT_AB && p->checkpoint != MOE_CKPT_NONE) return MOE_ERR_INVALID_ARG;
   if (p->activation < MOE_ACT_SWIGLU || p->activation > MOE_ACT_RELU) return MOE_ERR_INVALID_ARG;
+  if (p->deterministic != 0 && p->deterministic != 1) return MOE_ERR_INVALID_ARG;
   return MOE_OK;
 }
 
@@ -46,6 +48,19 @@ static size_t esize(const moe_problem* p) { return p->dtype == MOE_BF16 ? 2 : 4;
 // dg partial columns per routed row: the max over the GEMM backends
 static int dg_parts(const moe_problem* p) { return (int)ceil_div(p->h, 64); }
 
+// Output mode of the down-projection GEMMs (gemm.h OutMode) and the fp32 rows
+// of the accumulator it needs.  k = 1: every token has exactly one routed row,
+// so it is stored, not added (bit-identical to red.add onto zero) -- straight
+// into the output when nothing else is added to it.  deterministic: one fp32
+// row per routed row, summed per token in slot order by the finalize pass.
+static int out_mode(const moe_problem* p, bool more_terms) {
+  if (p->k == 1) return more_terms ? OUT_TOK : OUT_TOKN;
+  return p->deterministic ? OUT_ROWS : OUT_RED;
+}
+static int64_t acc_rows(const moe_problem* p, int mode) {
+  return mode == OUT_TOKN ? 0 : (mode == OUT_ROWS ? p->T * p->k : p->T);
+}
+
 struct FwdWs { void* u; float* yacc; void* a; void* b; size_t total; };
 static FwdWs fwd_layout(const moe_problem* p, void* base) {
   const int64_t R = p->T * p->k;
@@ -53,7 +68,7 @@ static FwdWs fwd_layout(const moe_problem* p, void* base) {
   size_t o = 0;
   FwdWs w;
   w.u = b + o; o += align256((size_t)R * p->h * esize(p));
-  w.yacc = (float*)(b + o); o += align256((size_t)p->T * p->d * 4);
+  w.yacc = (float*)(b + o); o += align256((size_t)acc_rows(p, out_mode(p, false)) * p->d * 4);
   w.a = w.b = nullptr;
   if (p->checkpoint == MOE_CKPT_NONE) {  // A, B are transient: not checkpointed
     w.a = b + o; o += align256((size_t)R * p->h * esize(p));
@@ -81,7 +96,7 @@ static BwdWs bwd_layout(const moe_problem* p, void* base) {
   size_t o = 0;
   BwdWs w;
   w.wu = b + o; o += align256((size_t)R * p->h * esize(p));
-  w.dxacc = (float*)(b + o); o += align256((size_t)p->T * p->d * 4);
+  w.dxacc = (float*)(b + o); o += align256((size_t)acc_rows(p, out_mode(p, true)) * p->d * 4);  // router or not
   w.dgpart = (float*)(b + o); o += align256((size_t)R * dg_parts(p) * 4);
   w.dlogits = (float*)(b + o); o += align256((size_t)p->T * p->E * 4);
   w.dwgpart = (float*)(b + o); o += align256((size_t)dwg_chunks(p->T, p->d, p->E) * p->E * p->d * 4);
@@ -163,7 +178,8 @@ moe_status moe_ffn_fwd(const moe_problem* p, const void* x, const void* w1, cons
   if (!disp || !w1 || (gated && !w2) || !w3) return MOE_ERR_INVALID_ARG;
   const bool ckpt = p->checkpoint == MOE_CKPT_AB;
   if (p->T > 0 && (!x || !y || !topk_w || (ckpt && (!a_save || (gated && !b_save))) || !ws ||
-                   !disp->expert_offsets || !disp->expert_token_indices || !disp->row_slot))
+                   !disp->expert_offsets || !disp->expert_token_indices || !disp->row_slot ||
+                   (p->deterministic && p->k > 1 && !disp->token_index_map)))
     return MOE_ERR_INVALID_ARG;
   if (!aligned16(x) || !aligned16(w1) || !aligned16(w2) || !aligned16(w3) || !aligned16(a_save) ||
       !aligned16(b_save) || !aligned16(y))
@@ -176,8 +192,10 @@ moe_status moe_ffn_fwd(const moe_problem* p, const void* x, const void* w1, cons
     a_save = w.a;
     b_save = w.b;
   }
-  MOE_CUDA_CHECK(cudaMemsetAsync(w.yacc, 0, (size_t)p->T * p->d * 4, st));
+  const int mode = out_mode(p, false);
+  if (mode == OUT_RED) MOE_CUDA_CHECK(cudaMemsetAsync(w.yacc, 0, (size_t)p->T * p->d * 4, st));
   GemmCall c{};
+  c.out_mode = mode; c.out_tok = y;
   c.x = x; c.w1 = w1; c.w2 = w2; c.w3 = w3; c.topw = topk_w;
   c.offs = disp->expert_offsets; c.eti = disp->expert_token_indices; c.row_slot = disp->row_slot;
   c.a_save = a_save; c.b_save = b_save; c.u = w.u; c.acc_out = w.yacc;
@@ -187,7 +205,8 @@ moe_status moe_ffn_fwd(const moe_problem* p, const void* x, const void* w1, cons
   if ((s = run_gemm(c, st)) != MOE_OK) return s;
   c.which = GEMM_FWD_DOWN;
   if ((s = run_gemm(c, st)) != MOE_OK) return s;
-  return launch_finalize(p, w.yacc, nullptr, nullptr, y, st, false);
+  if (mode == OUT_TOKN) return MOE_OK;
+  return launch_finalize(p, w.yacc, nullptr, nullptr, y, st, false, mode == OUT_ROWS ? disp->token_index_map : nullptr);
 }
 
 moe_status moe_ffn_bwd(const moe_problem* p, const void* dy, const void* x, const void* w1, const void* w2,
@@ -222,8 +241,10 @@ moe_status moe_ffn_bwd(const moe_problem* p, const void* dy, const void* x, cons
   c.dw_a = dw3; c.dw_b = nullptr;
   c.T = p->T; c.R = R; c.d = p->d; c.h = p->h; c.E = p->E; c.bf16 = p->dtype == MOE_BF16;
   c.act = p->activation;
+  const int mode = out_mode(p, router != nullptr);
+  c.out_mode = mode; c.out_tok = dx;
   if (p->T > 0) {
-    MOE_CUDA_CHECK(cudaMemsetAsync(w.dxacc, 0, (size_t)p->T * p->d * 4, st));
+    if (mode == OUT_RED) MOE_CUDA_CHECK(cudaMemsetAsync(w.dxacc, 0, (size_t)p->T * p->d * 4, st));
     if (!ckpt) {  // MOE_CKPT_NONE: recompute A, B (and U into the wU buffer) with the fused up-projection
       c.which = GEMM_FWD_UP;
       if ((s = run_gemm(c, st)) != MOE_OK) return s;
@@ -246,6 +267,7 @@ moe_status moe_ffn_bwd(const moe_problem* p, const void* dy, const void* x, cons
   if ((s = run_gemm(c, st)) != MOE_OK) return s;
   float* dg = d_topk_w ? d_topk_w : w.dg;
   if ((s = launch_dg_reduce(w.dgpart, gemm_dg_parts(c), disp->token_index_map, R, dg, st)) != MOE_OK) return s;
+  if (mode == OUT_TOKN) return MOE_OK;  // k = 1 without router: dx already written by BWD_DX
   const float* dl = nullptr;
   if (router) {
     if ((s = launch_router_bwd(p, router->logits, router->topk_ids, dg, x, w.dlogits, w.dwgpart, router->dw_gate,
@@ -253,7 +275,8 @@ moe_status moe_ffn_bwd(const moe_problem* p, const void* dy, const void* x, cons
       return s;
     dl = w.dlogits;
   }
-  return launch_finalize(p, w.dxacc, dl, router ? router->w_gate : nullptr, dx, st, false);
+  return launch_finalize(p, w.dxacc, dl, router ? router->w_gate : nullptr, dx, st, false,
+                         mode == OUT_ROWS ? disp->token_index_map : nullptr);
 }
 
 moe_status moe_router_backward(const moe_problem* p, const float* d_topk_w, const void* x, const moe_router_bwd* router,
@@ -273,7 +296,7 @@ moe_status moe_router_backward(const moe_problem* p, const float* d_topk_w, cons
   if ((s = launch_router_bwd(p, router->logits, router->topk_ids, d_topk_w, x, w.dlogits, w.dwgpart, router->dw_gate,
                              st)) != MOE_OK)
     return s;
-  return launch_finalize(p, dx_partial, w.dlogits, router->w_gate, dx, st, true);
+  return launch_finalize(p, dx_partial, w.dlogits, router->w_gate, dx, st, true, nullptr);
 }
 
 moe_status moe_ep_row_meta(const moe_problem* p, const moe_dispatch* disp, const float* topk_w, int32_t experts_per_rank,

@@ -170,13 +170,34 @@ __global__ void __launch_bounds__(256) dwg_partial_kernel(const float* __restric
   }
 }
 
+// The token-side accumulator of 8 columns: acc[t] ([T,d], fused red.add or
+// k = 1 store), or with tim != NULL the ordered combine of NEXT-4: acc holds
+// one fp32 row per routed row ([R,d], expert-sorted) and token t sums its k
+// rows in slot order j = 0..k-1 (fixed order -> bitwise reproducible).
+template <typename A>
+__device__ __forceinline__ void load_acc8(const A* acc, const int32_t* tim, int k, int64_t t, int d, int col, float* a) {
+  if (!tim) {
+    load8(acc + t * d + col, a);
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a[j] = 0.f;
+  for (int j = 0; j < k; ++j) {
+    float v[8];
+    load8(acc + (int64_t)tim[t * k + j] * d + col, v);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) a[q] += v[q];
+  }
+}
+
 // dx[t, :] = dtype(acc[t, :] + sum_e dl[t, e] Wg[e, :]) — the router's share of
 // the token gradient fused with the fp32 -> dtype finalisation.  Thread tile:
 // 8 consecutive columns (one 16-byte W_g load per expert, L1/L2-resident) x 8
 // tokens; block = 32 column groups (256 columns) x 8 token groups (64 tokens);
 // a warp shares its token group, so the dlogits reads are smem broadcasts.
 template <typename T, typename A>
-__global__ void __launch_bounds__(256) router_dx_kernel(const A* __restrict__ acc, const float* __restrict__ dl,
+__global__ void __launch_bounds__(256) router_dx_kernel(const A* __restrict__ acc, const int32_t* __restrict__ tim,
+                                                        int k, const float* __restrict__ dl,
                                                         const T* __restrict__ wg, int64_t Tn, int d, int E,
                                                         T* __restrict__ out) {
   __shared__ __align__(16) float wsm[32][256];  // W_g chunk: 32 experts x 256 columns (fp32)
@@ -189,7 +210,7 @@ __global__ void __launch_bounds__(256) router_dx_kernel(const A* __restrict__ ac
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int64_t t = t0 + tg * 8 + i;
-    if (t < Tn && col < d) load8(acc + t * d + col, a[i]);
+    if (t < Tn && col < d) load_acc8(acc, tim, k, t, d, col, a[i]);
     else
 #pragma unroll
       for (int j = 0; j < 8; ++j) a[i][j] = 0.f;
@@ -242,7 +263,8 @@ __global__ void dwg_reduce_kernel(const float* __restrict__ part, int nch, int64
 
 // out[t, :] = dtype(acc[t, :] + sum_e dl[t, e] Wg[e, :]); block: 16 tokens x 256 cols
 template <typename T, typename A>
-__global__ void __launch_bounds__(256) finalize_kernel(const A* __restrict__ acc, const float* __restrict__ dl,
+__global__ void __launch_bounds__(256) finalize_kernel(const A* __restrict__ acc, const int32_t* __restrict__ tim,
+                                                       int k, const float* __restrict__ dl,
                                                        const T* __restrict__ wg, int64_t Tn, int d, int E,
                                                        T* __restrict__ out) {
   extern __shared__ float sdl[];  // [16][E]
@@ -251,7 +273,14 @@ __global__ void __launch_bounds__(256) finalize_kernel(const A* __restrict__ acc
   const int nt = (int)min64(16, Tn - t0);
   float a[16];
 #pragma unroll
-  for (int r = 0; r < 16; ++r) a[r] = (r < nt && col < d) ? to_f32(acc[(t0 + r) * d + col]) : 0.f;
+  for (int r = 0; r < 16; ++r) {
+    a[r] = 0.f;
+    if (r < nt && col < d) {
+      if (!tim) a[r] = to_f32(acc[(t0 + r) * d + col]);
+      else
+        for (int j = 0; j < k; ++j) a[r] += to_f32(acc[(int64_t)tim[(t0 + r) * k + j] * d + col]);
+    }
+  }
   if (dl) {
     for (int i = threadIdx.x; i < 16 * E; i += 256) {
       int r = i / E, e = i % E;
@@ -369,8 +398,9 @@ moe_status launch_router_bwd(const moe_problem* p, const float* logits, const in
 }
 
 // acc_is_dtype: the accumulator is a [T,d] tensor of the run dtype (EP path) instead of fp32
+// tim != NULL: acc is the [R,d] fp32 row-result buffer, summed per token in slot order (NEXT-4)
 moe_status launch_finalize(const moe_problem* p, const void* acc, const float* dl, const void* wg, void* out,
-                           cudaStream_t st, bool acc_is_dtype) {
+                           cudaStream_t st, bool acc_is_dtype, const int32_t* tim) {
   if (p->T == 0) return MOE_OK;
   typedef __nv_bfloat16 bf;
   if (dl) {
@@ -378,13 +408,13 @@ moe_status launch_finalize(const moe_problem* p, const void* acc, const float* d
     const size_t sm2 = 0;
     if (p->dtype == MOE_BF16) {
       if (acc_is_dtype)
-        MOE_LAUNCH((router_dx_kernel<bf, bf>), g2, 256, sm2, st, (const bf*)acc, dl, (const bf*)wg, p->T, p->d, p->E,
+        MOE_LAUNCH((router_dx_kernel<bf, bf>), g2, 256, sm2, st, (const bf*)acc, tim, p->k, dl, (const bf*)wg, p->T, p->d, p->E,
                    (bf*)out);
       else
-        MOE_LAUNCH((router_dx_kernel<bf, float>), g2, 256, sm2, st, (const float*)acc, dl, (const bf*)wg, p->T, p->d,
+        MOE_LAUNCH((router_dx_kernel<bf, float>), g2, 256, sm2, st, (const float*)acc, tim, p->k, dl, (const bf*)wg, p->T, p->d,
                    p->E, (bf*)out);
     } else {
-      MOE_LAUNCH((router_dx_kernel<float, float>), g2, 256, sm2, st, (const float*)acc, dl, (const float*)wg, p->T,
+      MOE_LAUNCH((router_dx_kernel<float, float>), g2, 256, sm2, st, (const float*)acc, tim, p->k, dl, (const float*)wg, p->T,
                  p->d, p->E, (float*)out);
     }
     return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
@@ -393,12 +423,12 @@ moe_status launch_finalize(const moe_problem* p, const void* acc, const float* d
   size_t sm = 0;
   if (p->dtype == MOE_BF16) {
     if (acc_is_dtype)
-      MOE_LAUNCH((finalize_kernel<bf, bf>), grid, 256, sm, st, (const bf*)acc, dl, (const bf*)wg, p->T, p->d, p->E, (bf*)out);
+      MOE_LAUNCH((finalize_kernel<bf, bf>), grid, 256, sm, st, (const bf*)acc, tim, p->k, dl, (const bf*)wg, p->T, p->d, p->E, (bf*)out);
     else
-      MOE_LAUNCH((finalize_kernel<bf, float>), grid, 256, sm, st, (const float*)acc, dl, (const bf*)wg, p->T, p->d, p->E,
+      MOE_LAUNCH((finalize_kernel<bf, float>), grid, 256, sm, st, (const float*)acc, tim, p->k, dl, (const bf*)wg, p->T, p->d, p->E,
                  (bf*)out);
   } else {
-    MOE_LAUNCH((finalize_kernel<float, float>), grid, 256, sm, st, (const float*)acc, dl, (const float*)wg, p->T, p->d,
+    MOE_LAUNCH((finalize_kernel<float, float>), grid, 256, sm, st, (const float*)acc, tim, p->k, dl, (const float*)wg, p->T, p->d,
                p->E, (float*)out);
   }
   return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;

@@ -21,7 +21,16 @@ struct GemmCall {
   int d, h, E;
   bool bf16;
   int act;  // MOE_ACT_*: 0 = SwiGLU (gated), 1 = SiLU, 2 = ReLU (non-gated)
+  int out_mode;   // FWD_DOWN / BWD_DX epilogue target, OutMode
+  void* out_tok;  // OUT_TOKN: [T, d] output in the run dtype
 };
+
+// Where FWD_DOWN / BWD_DX put a routed row's result v (row r, token t = eti[r]):
+//   OUT_RED  acc_out[t] += v    fp32 [T,d], red.add (default combine)
+//   OUT_ROWS acc_out[r]  = v    fp32 [R,d], ordered token-side sum later (NEXT-4)
+//   OUT_TOK  acc_out[t]  = v    fp32 [T,d], k = 1 (one row per token)
+//   OUT_TOKN out_tok[t]  = dtype(v), k = 1 with nothing left to add
+enum OutMode { OUT_RED = 0, OUT_ROWS = 1, OUT_TOK = 2, OUT_TOKN = 3 };
 
 // non-gated activation sigma and its derivative
 __device__ __forceinline__ float act_fwd(int act, float a, float sg) { return act == 2 ? fmaxf(a, 0.f) : a * sg; }

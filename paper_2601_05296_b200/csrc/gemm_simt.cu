@@ -33,7 +33,19 @@ struct SimtArgs {
   T* dw_a; T* dw_b;                      // DW3: dw3 ; DW12: dw1, dw2
   int64_t R; int d, h, E;
   int act;                               // 0 SwiGLU (gated); 1 SiLU, 2 ReLU (non-gated)
+  int out_mode;                          // FWD_DOWN / BWD_DX target (gemm.h OutMode)
+  T* out_tok;                            // OUT_TOKN destination [T, d]
 };
+
+template <typename T>
+__device__ __forceinline__ void simt_out(const SimtArgs<T>& g, int64_t r, int64_t t, int n, float v) {
+  switch (g.out_mode) {
+    case OUT_RED: atomicAdd(&g.acc_out[t * g.d + n], v); break;
+    case OUT_ROWS: g.acc_out[r * g.d + n] = v; break;
+    case OUT_TOK: g.acc_out[t * g.d + n] = v; break;
+    default: g.out_tok[t * g.d + n] = from_f32<T>(v); break;
+  }
+}
 
 template <typename T, int MODE>
 __global__ void __launch_bounds__(ST) simt_rows_kernel(SimtArgs<T> g) {
@@ -141,7 +153,7 @@ __global__ void __launch_bounds__(ST) simt_rows_kernel(SimtArgs<T> g) {
           g.u[o] = from_f32<T>(act_fwd(g.act, a, sigmoidf_(a)));
         }
       } else if (MODE == FWD_DOWN) {
-        atomicAdd(&g.acc_out[t * g.d + n], w * acc[0][i][j]);
+        simt_out(g, r, t, n, w * acc[0][i][j]);
       } else if (MODE == BWD_DH) {
         int64_t o = (int64_t)r * g.h + n;
         const float a = to_f32(g.a_save[o]), dH = acc[0][i][j], s = sigmoidf_(a), dU = w * dH;
@@ -158,7 +170,7 @@ __global__ void __launch_bounds__(ST) simt_rows_kernel(SimtArgs<T> g) {
           g.u[o] = from_f32<T>(w * U);
         }
       } else {
-        atomicAdd(&g.acc_out[t * g.d + n], acc[0][i][j]);
+        simt_out(g, r, t, n, acc[0][i][j]);
       }
     }
   }
@@ -264,13 +276,13 @@ moe_status simt_gemm(const GemmCall& c, cudaStream_t st) {
     using T = __nv_bfloat16;
     SimtArgs<T> g{(const T*)c.x, (const T*)c.dy, (const T*)c.w1, (const T*)c.w2, (const T*)c.w3, c.topw, c.offs, c.eti,
                   c.row_slot, (T*)c.a_save, (T*)c.b_save, (T*)c.u, c.acc_out, c.dg_part, (T*)c.dw_a, (T*)c.dw_b,
-                  c.R, c.d, c.h, c.E, c.act};
+                  c.R, c.d, c.h, c.E, c.act, c.out_mode, (T*)c.out_tok};
     return simt_launch_all<T>(c.which, g, st);
   }
   using T = float;
   SimtArgs<T> g{(const T*)c.x, (const T*)c.dy, (const T*)c.w1, (const T*)c.w2, (const T*)c.w3, c.topw, c.offs, c.eti,
                 c.row_slot, (T*)c.a_save, (T*)c.b_save, (T*)c.u, c.acc_out, c.dg_part, (T*)c.dw_a, (T*)c.dw_b,
-                c.R, c.d, c.h, c.E, c.act};
+                c.R, c.d, c.h, c.E, c.act, c.out_mode, (T*)c.out_tok};
   return simt_launch_all<T>(c.which, g, st);
 }
 

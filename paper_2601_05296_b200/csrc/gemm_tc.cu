@@ -87,6 +87,8 @@ struct TcParams {
   int k, renorm, route_n;
   uint32_t route_idesc;
   int act;  // MOE_ACT_*: 0 SwiGLU (gated: stacked [W1;W2], A and B); 1 SiLU / 2 ReLU (non-gated)
+  int out_mode;                  // FWD_DOWN / BWD_DX target (gemm.h OutMode)
+  __nv_bfloat16* out_tok;        // OUT_TOKN destination [T, d]
 };
 
 template <int KIND>
@@ -753,13 +755,33 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
                 make_float4(w * __uint_as_float(v[4 * q]), w * __uint_as_float(v[4 * q + 1]),
                             w * __uint_as_float(v[4 * q + 2]), w * __uint_as_float(v[4 * q + 3]));
           __syncwarp();
+          if (P.out_mode == OUT_TOKN) {  // k = 1: one row per token, final dtype, 16-byte stores
 #pragma unroll
-          for (int it = 0; it < 8; ++it) {
-            const int rr = it * 4 + (lane >> 3), q = lane & 7;
-            const int tr = __shfl_sync(0xffffffffu, tok, rr);
-            if (rr < nvalid) {
-              const float4 f = *reinterpret_cast<const float4*>(stg + stg32_off(rr, q));
-              ptx::red_add_v4(P.acc_out + (int64_t)tr * N + t.n0 + c + 4 * q, f.x, f.y, f.z, f.w);
+            for (int it = 0; it < 4; ++it) {
+              const int rr = it * 8 + (lane >> 2), q = lane & 3;
+              const int tr = __shfl_sync(0xffffffffu, tok, rr);
+              if (rr < nvalid) {
+                const float4 f0 = *reinterpret_cast<const float4*>(stg + stg32_off(rr, 2 * q));
+                const float4 f1 = *reinterpret_cast<const float4*>(stg + stg32_off(rr, 2 * q + 1));
+                uint4 o;
+                o.x = ptx::pack_bf16(f0.x, f0.y); o.y = ptx::pack_bf16(f0.z, f0.w);
+                o.z = ptx::pack_bf16(f1.x, f1.y); o.w = ptx::pack_bf16(f1.z, f1.w);
+                *reinterpret_cast<uint4*>(P.out_tok + (int64_t)tr * N + t.n0 + c + 8 * q) = o;
+              }
+            }
+          } else {
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+              const int rr = it * 4 + (lane >> 3), q = lane & 7;
+              const int tr = __shfl_sync(0xffffffffu, tok, rr);
+              if (rr < nvalid) {
+                const float4 f = *reinterpret_cast<const float4*>(stg + stg32_off(rr, q));
+                if (P.out_mode == OUT_RED)
+                  ptx::red_add_v4(P.acc_out + (int64_t)tr * N + t.n0 + c + 4 * q, f.x, f.y, f.z, f.w);
+                else  // OUT_ROWS: expert-sorted row r0w + rr; OUT_TOK: token tr
+                  *reinterpret_cast<float4*>(P.acc_out + (int64_t)(P.out_mode == OUT_ROWS ? r0w + rr : tr) * N +
+                                             t.n0 + c + 4 * q) = f;
+              }
             }
           }
           __syncwarp();
@@ -1032,6 +1054,7 @@ moe_status tc_gemm(const GemmCall& c, cudaStream_t st) {
   P.offs = c.offs; P.eti = c.eti; P.row_slot = c.row_slot; P.topw = c.topw;
   P.a_save = (bf*)c.a_save; P.b_save = (bf*)c.b_save; P.u = (bf*)c.u;
   P.acc_out = c.acc_out; P.dg_part = c.dg_part;
+  P.out_mode = c.out_mode; P.out_tok = (bf*)c.out_tok;
   P.out0 = (bf*)c.dw_a; P.out1 = (bf*)c.dw_b;
   P.T = (int)T; P.d = d; P.h = h; P.E = E;
   P.dg_parts = tc_dg_parts(h);

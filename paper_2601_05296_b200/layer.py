@@ -13,8 +13,9 @@ import torch
 from . import _lib as L
 
 
-def _problem(T, d, h, E, k, dtype, renormalize=False, check_routing=False, checkpoint="ab", activation="swiglu"):
-    return L.problem(T, d, h, E, k, dtype, renormalize, check_routing, checkpoint, activation)
+def _problem(T, d, h, E, k, dtype, renormalize=False, check_routing=False, checkpoint="ab", activation="swiglu",
+             deterministic=False):
+    return L.problem(T, d, h, E, k, dtype, renormalize, check_routing, checkpoint, activation, deterministic)
 
 
 @dataclass
@@ -61,15 +62,17 @@ def dispatch_build(ids, E, check_routing=False, stream=None, dtype=torch.bfloat1
 
 
 def ffn_fwd(x, w1, w2, w3, topk_w, disp: Dispatch, renormalize=False, stream=None, checkpoint="ab",
-            activation="swiglu"):
+            activation="swiglu", deterministic=False):
     """moe_ffn_fwd (§3.1, Alg. 1 FusedForward): returns y, A, B (A, B checkpointed;
     None, None under checkpoint="none", where backward recomputes them).
     activation "silu" | "relu": the non-gated expert W2 sigma(W1 x); w2
-    may be None and B is None."""
+    may be None and B is None.  deterministic: ordered token-side combine
+    (bitwise reproducible for every k; NEXT-4)."""
     T, d = x.shape
     E, h, _ = w1.shape
     k = topk_w.shape[1]
-    p = _problem(T, d, h, E, k, x.dtype, renormalize, checkpoint=checkpoint, activation=activation)
+    p = _problem(T, d, h, E, k, x.dtype, renormalize, checkpoint=checkpoint, activation=activation,
+                 deterministic=deterministic)
     R = T * k
     save = checkpoint == "ab"
     gated = activation == "swiglu"
@@ -82,14 +85,15 @@ def ffn_fwd(x, w1, w2, w3, topk_w, disp: Dispatch, renormalize=False, stream=Non
 
 
 def ffn_bwd(dy, x, w1, w2, w3, topk_w, disp: Dispatch, a_save, b_save, w_gate=None, logits=None,
-            renormalize=False, stream=None, checkpoint="ab", activation="swiglu"):
+            renormalize=False, stream=None, checkpoint="ab", activation="swiglu", deterministic=False):
     """moe_ffn_bwd (§3.2, Alg. 1 FusedBackward).  a_save/b_save are overwritten
     with dA/dB (checkpoint="none": pass None, A and B are recomputed).  With
     w_gate/logits: router backward too (dx includes it)."""
     T, d = x.shape
     E, h, _ = w1.shape
     k = topk_w.shape[1]
-    p = _problem(T, d, h, E, k, x.dtype, renormalize, checkpoint=checkpoint, activation=activation)
+    p = _problem(T, d, h, E, k, x.dtype, renormalize, checkpoint=checkpoint, activation=activation,
+                 deterministic=deterministic)
     dx = torch.empty_like(x)
     dw1 = torch.empty_like(w1)
     dw2 = torch.empty_like(w2) if activation == "swiglu" else None
@@ -112,10 +116,12 @@ class MoEBlazeFunction(torch.autograd.Function):
     checkpoint="none" A, B are not saved either (recomputed in backward)."""
 
     @staticmethod
-    def forward(ctx, x, w_gate, w1, w2, w3, k, renormalize, checkpoint="ab", activation="swiglu"):
+    def forward(ctx, x, w_gate, w1, w2, w3, k, renormalize, checkpoint="ab", activation="swiglu",
+                deterministic=False):
         logits, ids, w = route(x, w_gate, k, renormalize)
         disp = dispatch_build(ids, w_gate.shape[0], dtype=x.dtype)
-        y, a, b = ffn_fwd(x, w1, w2, w3, w, disp, renormalize, checkpoint=checkpoint, activation=activation)
+        y, a, b = ffn_fwd(x, w1, w2, w3, w, disp, renormalize, checkpoint=checkpoint, activation=activation,
+                          deterministic=deterministic)
         gated = activation == "swiglu"
         saved = [x, w_gate, w1, w2 if gated else w1, w3, logits, ids, w, disp.counts, disp.offs, disp.eti, disp.tim,
                  disp.row_slot]
@@ -125,6 +131,7 @@ class MoEBlazeFunction(torch.autograd.Function):
         ctx.renormalize = renormalize
         ctx.checkpoint = checkpoint
         ctx.activation = activation
+        ctx.deterministic = deterministic
         return y
 
     @staticmethod
@@ -135,27 +142,34 @@ class MoEBlazeFunction(torch.autograd.Function):
         a, b = (t[13], t[14] if gated else None) if ctx.checkpoint == "ab" else (None, None)
         disp = Dispatch(counts, offs, eti, tim, row_slot, ids)
         g = ffn_bwd(dy.contiguous(), x, w1, w2 if gated else None, w3, w, disp, a, b, w_gate=w_gate, logits=logits,
-                    renormalize=ctx.renormalize, checkpoint=ctx.checkpoint, activation=ctx.activation)
-        return g["dx"], g["dw_gate"], g["dw1"], g["dw2"], g["dw3"], None, None, None, None
+                    renormalize=ctx.renormalize, checkpoint=ctx.checkpoint, activation=ctx.activation,
+                    deterministic=ctx.deterministic)
+        return g["dx"], g["dw_gate"], g["dw1"], g["dw2"], g["dw3"], None, None, None, None, None
 
 
-def moe_layer(x, w_gate, w1, w2, w3, k, renormalize=False, checkpoint="ab", activation="swiglu"):
+def moe_layer(x, w_gate, w1, w2, w3, k, renormalize=False, checkpoint="ab", activation="swiglu",
+              deterministic=False):
     """checkpoint: "ab" (paper: save A (,B), recompute the activation) | "none" (recompute A, B).
-    activation: "swiglu" | "silu" | "relu" (non-gated W2 sigma(W1 x); w2 unused)."""
-    return MoEBlazeFunction.apply(x, w_gate, w1, w2, w3, k, renormalize, checkpoint, activation)
+    activation: "swiglu" | "silu" | "relu" (non-gated W2 sigma(W1 x); w2 unused).
+    deterministic: ordered combine of a token's k expert outputs (bitwise reproducible for k >= 3)."""
+    return MoEBlazeFunction.apply(x, w_gate, w1, w2, w3, k, renormalize, checkpoint, activation, deterministic)
 
 
 class MoEBlazeLayer(torch.nn.Module):
-    """Dropless top-k SwiGLU MoE layer on the MoEBlaze path."""
+    """Dropless top-k MoE layer on the MoEBlaze path: SwiGLU
+    experts or non-gated SiLU/ReLU experts (no w2)."""
 
-    def __init__(self, d, h, E, k, renormalize=False, dtype=torch.bfloat16, device="cuda", checkpoint="ab"):
+    def __init__(self, d, h, E, k, renormalize=False, dtype=torch.bfloat16, device="cuda", checkpoint="ab",
+                 activation="swiglu", deterministic=False):
         super().__init__()
         self.k, self.renormalize, self.checkpoint = k, renormalize, checkpoint
+        self.activation, self.deterministic = activation, deterministic
         kw = dict(dtype=dtype, device=device)
         self.w_gate = torch.nn.Parameter(torch.randn(E, d, **kw) / d ** 0.5)
         self.w1 = torch.nn.Parameter(torch.randn(E, h, d, **kw) / d ** 0.5)
-        self.w2 = torch.nn.Parameter(torch.randn(E, h, d, **kw) / d ** 0.5)
+        self.w2 = torch.nn.Parameter(torch.randn(E, h, d, **kw) / d ** 0.5) if activation == "swiglu" else None
         self.w3 = torch.nn.Parameter(torch.randn(E, d, h, **kw) / h ** 0.5)
 
     def forward(self, x):
-        return moe_layer(x, self.w_gate, self.w1, self.w2, self.w3, self.k, self.renormalize, self.checkpoint)
+        return moe_layer(x, self.w_gate, self.w1, self.w2, self.w3, self.k, self.renormalize, self.checkpoint,
+                         self.activation, self.deterministic)

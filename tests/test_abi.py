@@ -1,5 +1,6 @@
 """C-ABI library: loads, exports every symbol include/moeblaze.h declares,
 validates arguments and sizes its workspace without a GPU (CPU test)."""
+import torch
 import ctypes
 import os
 import re
@@ -52,18 +53,34 @@ def _problem(L, T=1024, d=256, h=512, E=8, k=2, dtype=0, renorm=0):
 
 def test_workspace_has_no_routed_token_term(lib):
     """By construction (SURVEY §8(c) audit 1): the fwd/bwd workspace is a closed
-    form with no T*k*d term.  Its growth in d is the same for k = 1 and k = 8
-    (only the [T, d] fp32 accumulators and router terms depend on d)."""
+    form with no T*k*d term.  Its growth in d is the same for k = 2 and k = 8
+    (only the [T, d] fp32 accumulators and router terms depend on d); k = 1
+    stores each token's single row directly and needs no more than that."""
     from paper_2601_05296_b200 import _lib as L
     for (T, d, h, E) in [(1024, 256, 512, 8), (4096, 512, 256, 64), (2048, 1024, 1024, 16)]:
         for op in (L.MOE_OP_FFN_FWD, L.MOE_OP_FFN_BWD):
             grow = []
-            for k in (1, 8):
+            for k in (1, 2, 8):
                 s1 = L.workspace_size(_problem(L, T, d, h, E, k), op)
                 s2 = L.workspace_size(_problem(L, T, 2 * d, h, E, k), op)
                 grow.append(s2 - s1)
-            assert abs(grow[1] - grow[0]) <= 2048, (T, d, h, E, op, grow)
-            assert grow[0] <= T * d * 4 + 64 * E * d * 4 + 4096
+            assert abs(grow[2] - grow[1]) <= 2048, (T, d, h, E, op, grow)
+            assert grow[0] <= grow[1] + 2048
+            assert grow[1] <= T * d * 4 + 64 * E * d * 4 + 4096
+
+
+def test_deterministic_workspace_is_the_row_buffer(lib):
+    """deterministic = 1 (NEXT-4) replaces the [T, d] fp32 accumulator by the
+    transient [T*k, d] fp32 row-result buffer -- exactly that, nothing else."""
+    from paper_2601_05296_b200 import _lib as L
+    for (T, d, h, E, k) in [(1024, 256, 512, 8, 2), (4096, 512, 256, 64, 6), (300, 128, 128, 16, 8)]:
+        for op in (L.MOE_OP_FFN_FWD, L.MOE_OP_FFN_BWD):
+            base = L.workspace_size(L.problem(T, d, h, E, k, torch.bfloat16), op)
+            det = L.workspace_size(L.problem(T, d, h, E, k, torch.bfloat16, deterministic=True), op)
+            assert abs((det - base) - (T * k - T) * d * 4) <= 512, (T, d, h, E, k, op, det - base)
+        one = [L.workspace_size(L.problem(T, d, h, E, 1, torch.bfloat16, deterministic=det), L.MOE_OP_FFN_FWD)
+               for det in (False, True)]
+        assert one[0] == one[1]  # k = 1 ignores the flag
 
 
 def test_argument_validation(lib):
@@ -76,8 +93,11 @@ def test_argument_validation(lib):
         _problem(L, d=100),             # bf16 needs d % 128 == 0
         _problem(L, h=96),
     ]
+    nd = _problem(L)
+    nd.deterministic = 2            # only 0 / 1
+    bad.append(nd)
     codes = [lib.moe_workspace_size(ctypes.byref(p), 2, ctypes.byref(n)) for p in bad]
-    assert codes == [1, 1, 1, 2, 2]
+    assert codes == [1, 1, 1, 2, 2, 1]
     ok = _problem(L, T=0)
     assert lib.moe_workspace_size(ctypes.byref(ok), 3, ctypes.byref(n)) == 0
     fp32 = _problem(L, d=64, h=96, dtype=1)

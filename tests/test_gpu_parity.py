@@ -101,14 +101,15 @@ LAYER_CASES = [
 ]
 
 
-def _run_layer(M, T, d, h, E, k, dtype, renorm, routing, seed=0):
+def _run_layer(M, T, d, h, E, k, dtype, renorm, routing, seed=0, det=False):
     inp = make_inputs(T, d, h, E, k, dtype=dtype, seed=seed, routing=routing, device=DEV)
     x, wg, w1, w2, w3, dy = (inp[n] for n in ("x", "w_gate", "w1", "w2", "w3", "dy"))
     logits, ids, w = M.route(x, wg, k, renorm)
     disp = M.dispatch_build(ids, E, dtype=x.dtype)
-    y, a, b = M.ffn_fwd(x, w1, w2, w3, w, disp, renorm)
+    y, a, b = M.ffn_fwd(x, w1, w2, w3, w, disp, renorm, deterministic=det)
     a0, b0 = a.clone(), b.clone()
-    g = M.ffn_bwd(dy, x, w1, w2, w3, w, disp, a, b, w_gate=wg, logits=logits, renormalize=renorm)
+    g = M.ffn_bwd(dy, x, w1, w2, w3, w, disp, a, b, w_gate=wg, logits=logits, renormalize=renorm,
+                  deterministic=det)
     torch.cuda.synchronize()
     out = dict(logits=logits, ids=ids, w=w, y=y, A=a0, B=b0, dA=a, dB=b, disp=disp, **g)
     return inp, out
@@ -264,3 +265,38 @@ def test_nongated_fwd_bwd_parity(M, case, ckpt):
         errs["dA"] = normwise(a, bwd["dA"])
     bad = {n: v for n, v in errs.items() if not v <= tol}
     assert not bad, (name, ckpt, errs)
+
+
+DET_CASES = [
+    # T, d, h, E, k, dtype, routing
+    (1000, 128, 256, 16, 6, "bf16", "skewed"),
+    (130, 128, 128, 256, 16, "bf16", "skewed"),
+    (200, 64, 96, 6, 3, "fp32", "skewed"),
+    (257, 256, 128, 2, 2, "bf16", "balanced"),   # k = 2: red.add of two terms is already exact
+    (256, 64, 128, 4, 2, "fp32", "balanced"),
+    (333, 256, 256, 4, 1, "bf16", "balanced"),   # k = 1: flag ignored (direct store)
+    (100, 64, 64, 4, 1, "fp32", "skewed"),
+]
+_DET_KEYS = ("y", "dx", "dA", "dB", "dg", "dw1", "dw2", "dw3", "dw_gate")
+
+
+@pytest.mark.parametrize("T,d,h,E,k,dtype,routing", DET_CASES)
+def test_deterministic_combine(M, T, d, h, E, k, dtype, routing):
+    """deterministic=True (NEXT-4): fp32 row results are summed per token
+    in slot order, so repeated runs are bitwise identical for every k; the
+    result is within tolerance of the oracle, and for k <= 2 bit-identical to
+    the fused red.add combine (a + b == b + a exactly)."""
+    inp, o1 = _run_layer(M, T, d, h, E, k, dtype, False, routing, seed=7 * T + k, det=True)
+    _, o2 = _run_layer(M, T, d, h, E, k, dtype, False, routing, seed=7 * T + k, det=True)
+    _, o0 = _run_layer(M, T, d, h, E, k, dtype, False, routing, seed=7 * T + k, det=False)
+    for n in _DET_KEYS:
+        assert torch.equal(o1[n], o2[n]), n
+        if k <= 2:
+            assert torch.equal(o1[n], o0[n]), n
+    X, WG, W1, W2, W3, DY = (f64(inp[n]) for n in ("x", "w_gate", "w1", "w2", "w3", "dy"))
+    fwd = O.layer_forward(X, WG, W1, W2, W3, k, False, logits=f64(o1["logits"]))
+    bwd = O.layer_backward(fwd, DY, X, WG, W1, W2, W3, False)
+    tol = FP32_TOL if dtype == "fp32" else BF16_TOL
+    errs = {n: normwise(o1[n], fwd[n] if n == "y" else bwd[n]) for n in _DET_KEYS}
+    bad = {n: v for n, v in errs.items() if not v <= tol}
+    assert not bad, errs
