@@ -35,6 +35,13 @@ FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustain
 GEMM_FLOP_FACTOR = {"FWD_UP": 4, "FWD_DOWN": 2, "BWD_DH": 2, "BWD_DX": 4, "DW3": 2, "DW12": 4}
 
 
+def flop_factor(kind, gated=True):
+    """Algorithmic flops per launch / (R d h).  Non-gated experts have one
+    up-projection: FWD_UP, DW12 and BWD_DX halve."""
+    f = GEMM_FLOP_FACTOR[kind]
+    return f if gated or kind not in ("FWD_UP", "DW12", "BWD_DX") else f // 2
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -93,7 +100,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------ oracle timing
-def oracle_tokens_per_s(inp_host, cfg, budget_s=15.0, min_tokens=64, fixed_tokens=None):
+def oracle_tokens_per_s(inp_host, cfg, budget_s=15.0, min_tokens=64, fixed_tokens=None, activation="swiglu"):
     """Time the fp64 oracle (as it stands) on a bounded token sample of the
     workload, full weights.  Returns (tokens/s, sample tokens, seconds, threads)."""
     import numpy as np
@@ -108,8 +115,9 @@ def oracle_tokens_per_s(inp_host, cfg, budget_s=15.0, min_tokens=64, fixed_token
 
     def run(S):
         t0 = time.perf_counter()
-        fwd = O.layer_forward(X[:S], WG, W1, W2, W3, k)
-        O.layer_backward(fwd, DY[:S], X[:S], WG, W1, W2, W3)
+        w2 = W2 if activation == "swiglu" else None
+        fwd = O.layer_forward(X[:S], WG, W1, w2, W3, k, activation=activation)
+        O.layer_backward(fwd, DY[:S], X[:S], WG, W1, w2, W3)
         return time.perf_counter() - t0
 
     if fixed_tokens:
@@ -152,6 +160,10 @@ def main():
     ap.add_argument("--ep", action="store_true", help="use the expert-parallel path even at N = 1")
     ap.add_argument("--checkpoint", default="ab", choices=["ab", "none"],
                     help="activation checkpoint policy: ab = save A, B (paper); none = recompute A, B in backward")
+    ap.add_argument("--activation", default="swiglu", choices=["swiglu", "silu", "relu"],
+                    help="expert FFN: SwiGLU (P:190) or the non-gated W2 sigma(W1 x) of P:75")
+    ap.add_argument("--deterministic", action="store_true",
+                    help="ordered token-side combine of the k expert outputs (bitwise reproducible, NEXT-4)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -192,8 +204,14 @@ def main():
     x, wg, w1, w2, w3, dy = (inp[n] for n in ("x", "w_gate", "w1", "w2", "w3", "dy"))
     renorm = args.renormalize
 
+    act, det = args.activation, args.deterministic
+    gated = act == "swiglu"
+    if not gated:
+        w2 = None
     ep = None
     if use_ep:
+        if not gated or det:
+            raise SystemExit("--activation/--deterministic are single-GPU options (the EP receiver runs k = 1)")
         from paper_2601_05296_b200.ep import ExpertParallelMoE
         ep = ExpertParallelMoE(cfg.E, k, renorm, group=None)
         # each rank keeps only its experts' weights; the router is replicated
@@ -210,9 +228,9 @@ def main():
         def step():
             logits, ids, w = M.route(x, wg, k, renorm)
             disp = M.dispatch_build(ids, cfg.E, dtype=x.dtype)
-            y, a, b = M.ffn_fwd(x, w1, w2, w3, w, disp, renorm, checkpoint=ck)
+            y, a, b = M.ffn_fwd(x, w1, w2, w3, w, disp, renorm, checkpoint=ck, activation=act, deterministic=det)
             g = M.ffn_bwd(dy, x, w1, w2, w3, w, disp, a, b, w_gate=wg, logits=logits, renormalize=renorm,
-                          checkpoint=ck)
+                          checkpoint=ck, activation=act, deterministic=det)
             return y, g
 
     for _ in range(args.warmup):
@@ -260,14 +278,15 @@ def main():
     if True:
         dom = max(prof, key=lambda n: prof[n][0])
         tot_ms, n_l = prof[dom]
-        flops = GEMM_FLOP_FACTOR[dom] * R * cfg.d * cfg.h  # per launch (FWD_UP runs twice per step under --checkpoint none)
+        flops = flop_factor(dom, gated) * R * cfg.d * cfg.h  # per launch (FWD_UP runs twice per step under --checkpoint none)
         achieved = flops / (tot_ms / n_l / 1e3) / 1e12
         peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
         traffic = None
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tp):
             traffic = json.load(open(tp)).get(args.workload, {}).get(dom)
-        all_flops = (18 + (4 if args.checkpoint == "none" else 0)) * R * cfg.d * cfg.h
+        all_flops = ((18 if gated else 12) + (flop_factor("FWD_UP", gated) if args.checkpoint == "none" else 0)) \
+            * R * cfg.d * cfg.h
         roof = {"bound": "tensor", "kernel": f"tc_gemm_kernel<{dom}>", "achieved": round(achieved, 1),
                 "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                 "peak_source": f"{peaks['source']} bf16 sustained (kernel timed inside the step)",
@@ -284,7 +303,7 @@ def main():
     if True:
         x_h = x.detach().cpu().pin_memory()
         dy_h = dy.detach().cpu().pin_memory()
-        params = [torch.nn.Parameter(t) for t in (wg, w1, w2, w3)]
+        params = [torch.nn.Parameter(t) if t is not None else None for t in (wg, w1, w2, w3)]
 
         def layer_step(xd, dyd):
             if ep is not None:
@@ -292,8 +311,9 @@ def main():
                 return y, g["dx"]
             xl = xd.detach().requires_grad_(True)
             for p in params:
-                p.grad = None
-            y = M.moe_layer(xl, *params, k, renorm, args.checkpoint)
+                if p is not None:
+                    p.grad = None
+            y = M.moe_layer(xl, *params, k, renorm, args.checkpoint, act, det)
             y.backward(dyd)
             return y, xl.grad
 
@@ -328,14 +348,14 @@ def main():
     # ----------------------------------------------------------------- activation memory (P:289 method)
     mem = None
     if ep is None and not args.no_memory:
-        mem = measure_memory(M, x, wg, w1, w2, w3, dy, k, renorm)
+        mem = measure_memory(M, x, wg, w1, w2, w3, dy, k, renorm, act, det)
 
     # ----------------------------------------------------------------- CPU oracle baseline (rank 0, N = 1)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
             host = host_f64({n: inp[n] for n in ("x", "w_gate", "w1", "w2", "w3", "dy")})
-            tps, S, secs, threads = oracle_tokens_per_s(host, cfg, budget_s=args.cpu_budget_s)
+            tps, S, secs, threads = oracle_tokens_per_s(host, cfg, budget_s=args.cpu_budget_s, activation=act)
             cpu = {"value": round(tps, 3), "unit": UNIT, "cores": threads, "kind": "oracle",
                    "sample": f"{S} of {cfg.T} tokens of the {cfg.name} layer, full weights, fwd+bwd incl. router, "
                              f"fp64 NumPy, {secs:.1f} s", "host_cpus": os.cpu_count()}
@@ -349,10 +369,12 @@ def main():
             "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded, moe_inputs)",
             "config": {"workload": cfg.name, "T_per_gpu": cfg.T, "d": cfg.d, "h": cfg.h, "E": cfg.E, "k": cfg.k,
-                       "renormalize": renorm, "checkpoint": args.checkpoint,
+                       "renormalize": renorm, "checkpoint": args.checkpoint, "activation": act,
+                       "deterministic": det,
                        "parallelism": f"ep{world}" if ep is not None else "single-GPU",
                        "l2": "no flush: inputs larger than L2 (weights %.2f GB + X %.0f MB vs 126 MB L2)" % (
-                           3 * w1.numel() * 2 * (world if world > 1 else 1) / 1e9, x.numel() * 2 / 1e6)},
+                           (3 if gated else 2) * w1.numel() * 2 * (world if world > 1 else 1) / 1e9,
+                           x.numel() * 2 / 1e6)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "gpu_launches_per_step": launches / args.steps, "clocks": clk,
             "peak_activation_gb": mem["ours"]["peak_gb"] if mem else None, "memory": mem,
@@ -362,7 +384,7 @@ def main():
         dist.destroy_process_group()
 
 
-def measure_memory(M, x, wg, w1, w2, w3, dy, k, renorm):
+def measure_memory(M, x, wg, w1, w2, w3, dy, k, renorm, act="swiglu", det=False):
     """Saved-activation bytes via autograd saved-tensor hooks, deduped by
     storage and excluding parameters, plus the peak allocation delta over one
     fwd+bwd — for our layer and for the materialise-everything baseline."""
@@ -370,8 +392,8 @@ def measure_memory(M, x, wg, w1, w2, w3, dy, k, renorm):
     from materialized_baseline import materialized_moe
 
     def one(fn):
-        params = [torch.nn.Parameter(t.detach().clone()) for t in (wg, w1, w2, w3)]
-        pids = {p.untyped_storage().data_ptr() for p in params}
+        params = [torch.nn.Parameter(t.detach().clone()) if t is not None else None for t in (wg, w1, w2, w3)]
+        pids = {p.untyped_storage().data_ptr() for p in params if p is not None}
         xd = x.detach().clone().requires_grad_(True)
         seen = {}
 
@@ -393,10 +415,10 @@ def measure_memory(M, x, wg, w1, w2, w3, dy, k, renorm):
 
     out = {"method": "torch.autograd.graph.saved_tensors_hooks, unique storages excl. parameters (P:289); "
                      "peak = max_memory_allocated delta over fwd+bwd"}
-    out["ours"] = one(lambda xx, a, b, c, d_: M.moe_layer(xx, a, b, c, d_, k, renorm))
-    out["ours_checkpoint_none"] = one(lambda xx, a, b, c, d_: M.moe_layer(xx, a, b, c, d_, k, renorm, "none"))
+    out["ours"] = one(lambda xx, a, b, c, d_: M.moe_layer(xx, a, b, c, d_, k, renorm, "ab", act, det))
+    out["ours_checkpoint_none"] = one(lambda xx, a, b, c, d_: M.moe_layer(xx, a, b, c, d_, k, renorm, "none", act, det))
     try:
-        out["materialized_baseline"] = one(lambda xx, a, b, c, d_: materialized_moe(xx, a, b, c, d_, k, renorm))
+        out["materialized_baseline"] = one(lambda xx, a, b, c, d_: materialized_moe(xx, a, b, c, d_, k, renorm, act))
         out["saved_ratio"] = round(out["materialized_baseline"]["saved_gb"] / out["ours"]["saved_gb"], 3)
     except Exception as exc:
         out["materialized_baseline"] = {"error": repr(exc)[:300]}
@@ -413,19 +435,21 @@ def run_reference(args, cfg, rank, world):
     host = host_f64(inp)
     # per-step sample sized so the whole W + K run stays within ~3 minutes
     budget = 150.0 / (args.steps + args.warmup)
-    _, S, t, threads = oracle_tokens_per_s(host, cfg, budget_s=budget)
+    _, S, t, threads = oracle_tokens_per_s(host, cfg, budget_s=budget, activation=args.activation)
     for _ in range(args.warmup):
-        oracle_tokens_per_s(host, cfg, fixed_tokens=S)
+        oracle_tokens_per_s(host, cfg, fixed_tokens=S, activation=args.activation)
     times = []
     for _ in range(args.steps):
-        times.append(oracle_tokens_per_s(host, cfg, fixed_tokens=S)[2])
+        times.append(oracle_tokens_per_s(host, cfg, fixed_tokens=S, activation=args.activation)[2])
     tot = sum(times)
     value = S * args.steps / tot
     out = {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * tot / args.steps, 2),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic (seeded, moe_inputs)",
-           "config": {"workload": cfg.name, "T_per_gpu": cfg.T, "d": cfg.d, "h": cfg.h, "E": cfg.E, "k": cfg.k},
+           "config": {"workload": cfg.name, "T_per_gpu": cfg.T, "d": cfg.d, "h": cfg.h, "E": cfg.E, "k": cfg.k,
+                      "renormalize": args.renormalize, "checkpoint": args.checkpoint, "activation": args.activation,
+                      "deterministic": args.deterministic},
            "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": threads, "kind": "oracle",
                             "sample": f"{S} of {cfg.T} tokens per step, full weights, fwd+bwd incl. router, "
                                       "fp64 NumPy oracle"},

@@ -14,7 +14,9 @@ import os
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libmoeblaze.so")
+# MOEBLAZE_LIB: an alternative in-tree build of the same library (compile-time
+# tuning variants, tools/tune_*.sh); never a different implementation
+LIB_PATH = os.environ.get("MOEBLAZE_LIB") or os.path.join(_PKG, "libmoeblaze.so")
 
 MOE_BF16, MOE_FP32 = 0, 1
 MOE_OP_ROUTE, MOE_OP_DISPATCH, MOE_OP_FFN_FWD, MOE_OP_FFN_BWD, MOE_OP_ROUTER_BWD = 0, 1, 2, 3, 4

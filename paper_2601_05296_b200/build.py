@@ -30,8 +30,8 @@ def _deps_mtime():
     return max(os.path.getmtime(f) for f in files)
 
 
-def _compile(src, extra):
-    obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+def _compile(src, extra, obj_dir=OBJ):
+    obj = os.path.join(obj_dir, os.path.basename(src) + ".o")
     cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
@@ -39,24 +39,29 @@ def _compile(src, extra):
     return obj, r.stderr
 
 
-def build(force=False, jobs=None, verbose=False, extra=()):
-    if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= _deps_mtime():
-        return OUT
-    os.makedirs(OBJ, exist_ok=True)
+def build(force=False, jobs=None, verbose=False, extra=(), out=None):
+    """out/extra: a tuning variant (extra -D flags) written to another .so."""
+    out = out or OUT
+    if os.environ.get("MOEBLAZE_LIB") and out == OUT:
+        return os.environ["MOEBLAZE_LIB"]
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= _deps_mtime():
+        return out
+    obj_dir = OBJ if out == OUT else out + ".objs"
+    os.makedirs(obj_dir, exist_ok=True)
     srcs = sources()
     jobs = jobs or min(len(srcs), os.cpu_count() or 4)
     with cf.ThreadPoolExecutor(jobs) as ex:
-        results = list(ex.map(lambda s: _compile(s, list(extra)), srcs))
+        results = list(ex.map(lambda s: _compile(s, list(extra), obj_dir), srcs))
     for obj, err in results:
         if verbose and err.strip():
             print(err, file=sys.stderr)
-    tmp = OUT + ".tmp"
+    tmp = out + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *[o for o, _ in results], "-cudart=static"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
@@ -64,5 +69,7 @@ if __name__ == "__main__":
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--jobs", type=int, default=None)
     ap.add_argument("-v", "--verbose", action="store_true")
+    ap.add_argument("--out", default=None, help="write a tuning variant to this path")
+    ap.add_argument("-D", action="append", default=[], help="extra -D definitions for a tuning variant")
     a = ap.parse_args()
-    print(build(force=a.force, jobs=a.jobs, verbose=a.verbose))
+    print(build(force=a.force, jobs=a.jobs, verbose=a.verbose, extra=[f"-D{d}" for d in a.D], out=a.out))

@@ -44,6 +44,12 @@ namespace moeb {
 
 enum TcKind { TC_FWD_UP = 0, TC_FWD_DOWN = 1, TC_BWD_DH = 2, TC_BWD_DX = 3, TC_DW3 = 4, TC_DW12 = 5, TC_ROUTE = 6 };
 
+#ifndef MOEB_DH_STAGES
+#define MOEB_DH_STAGES 4  // BWD_DH mainloop stages in the CTA-pair engine (smem shared with the epilogue ring)
+#endif
+#ifndef MOEB_DH_NBUF
+#define MOEB_DH_NBUF 4    // BWD_DH epilogue ring depth (A/B chunks of 32 columns per warp)
+#endif
 constexpr int TBN = 256, TBK = 64;         // MMA N per tile, K block
 constexpr int TA_BYTES = 128 * TBK * 2;    // 16 KB: 128 rows of A per CTA
 constexpr int TC_THREADS = 384;            // 12 warps
@@ -54,10 +60,11 @@ struct CgCfg {
   static constexpr int TM = 128 * CG;                   // tile rows per CTA group
   static constexpr int B_BYTES = (TBN / CG) * TBK * 2;  // B per CTA per stage
   static constexpr int STAGE = TA_BYTES + B_BYTES;
-  // BWD_DH double-buffers its epilogue inputs (A, B chunks): one stage less
+  // BWD_DH shares smem between its mainloop ring and the epilogue A/B ring (tools/tune_variants.sh:
+  // 4 stages + 4-deep ring beat 3 + 7 by 11 % on the Mixtral layer)
   static constexpr bool DH = (KIND == 2);
-  static constexpr int STAGES = DH ? (CG == 1 ? 2 : 3) : (CG == 1 ? 4 : 6);
-  static constexpr int DH_NBUF = 7;                     // BWD_DH: ring of A/B input chunks per warp
+  static constexpr int STAGES = DH ? (CG == 1 ? 2 : MOEB_DH_STAGES) : (CG == 1 ? 4 : 6);
+  static constexpr int DH_NBUF = MOEB_DH_NBUF;          // BWD_DH: ring of A/B input chunks per warp
   static constexpr int STG_WARP = DH ? (DH_NBUF * 4096 + 2048) : 6144;  // epilogue staging bytes per warp
   static constexpr int STG_OFF = STAGES * STAGE + 1024 /*barriers*/ + 2176 /*offsets, tile starts*/;
   static constexpr int SMEM = STG_OFF + 4 * STG_WARP + 1024 /*align*/;
@@ -547,31 +554,27 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
       uint32_t aphase = 0;
       TileInfo t;
       const uint32_t idesc = (KIND == TC_ROUTE) ? P.route_idesc : IDESC;
+      const uint32_t tb = __shfl_sync(0xffffffffu, tmem_base, 0);
+      const uint32_t s0 = ptx::smem_u32(smem);
+      const uint32_t empty0 = ptx::smem_u32(empty);
       for (int tile = cluster_id; decode_tile<KIND, CG>(tile, P, s_offs, s_tstart, t); tile += n_clusters) {
         if constexpr (CG == 2) ptx::mbar_wait_cluster(&tempty[as], aphase ^ 1);
         else ptx::mbar_wait(&tempty[as], aphase ^ 1);
         ptx::tc_fence_after();
-        const uint32_t d_tmem = tmem_base + as * TBN;
+        const uint32_t d_tmem = tb + as * TBN;
         for (int kb = 0; kb < t.nk; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           if (CPA && K::gathered) ptx::fence_proxy_async();  // cp.async (generic proxy) -> tcgen05 reads
           ptx::tc_fence_after();
-          if (lane == 0) {
-            const uint32_t sA = ptx::smem_u32(smem + stage * C::STAGE);
-            const uint32_t sB = sA + TA_BYTES;
-#pragma unroll
-            for (int ks = 0; ks < TBK / 16; ++ks) {
-              const uint64_t ad = K::a_mn ? ptx::umma_desc_sw128(sA + ks * 2048, 8192, 1024)
-                                          : ptx::umma_desc_sw128(sA + ks * 32, 16, 1024);
-              const uint64_t bd = K::b_mn ? ptx::umma_desc_sw128(sB + ks * 2048, 8192, 1024)
-                                          : ptx::umma_desc_sw128(sB + ks * 32, 16, 1024);
-              if constexpr (CG == 2) ptx::umma_bf16_cg2(d_tmem, ad, bd, idesc, (kb | ks) != 0);
-              else ptx::umma_bf16(d_tmem, ad, bd, idesc, (kb | ks) != 0);
-            }
-            if constexpr (CG == 2) ptx::umma_commit_cg2(&empty[stage], 0x3);
-            else ptx::umma_commit(&empty[stage]);
-          }
-          __syncwarp();
+          // whole warp converged; elect.sync inside the asm issues from one thread
+          // (the descriptors' low words: (smem >> 4) | LBO field, see ptx::umma_kblock)
+          constexpr uint32_t LBO_A = K::a_mn ? (8192u >> 4) << 16 : (16u >> 4) << 16;
+          constexpr uint32_t LBO_B = K::b_mn ? (8192u >> 4) << 16 : (16u >> 4) << 16;
+          constexpr uint32_t STEP_A = K::a_mn ? 2048u >> 4 : 32u >> 4;
+          constexpr uint32_t STEP_B = K::b_mn ? 2048u >> 4 : 32u >> 4;
+          const uint32_t sA = s0 + stage * C::STAGE;
+          ptx::umma_kblock<CG, STEP_A, STEP_B>(d_tmem, (sA >> 4) | LBO_A, ((sA + TA_BYTES) >> 4) | LBO_B, idesc,
+                                               kb != 0, empty0 + 8 * stage, 0x3);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
         if (lane == 0) {

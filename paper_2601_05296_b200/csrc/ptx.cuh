@@ -183,6 +183,97 @@ __device__ __forceinline__ void umma_bf16_cg2(uint32_t d_tmem, uint64_t a_desc, 
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// Warp-converged issue: the whole warp executes these with warp-uniform
+// operands and elect.sync picks the one issuing thread inside the asm.  Keeping
+// the warp converged lets ptxas hold the descriptors in uniform registers; an
+// `if (lane == 0)` around the MMA made it wrap every UTCHMMA in an
+// ELECT/R2UR.BROADCAST/BRA.U.ANY waterfall (~20 instructions per MMA), which
+// capped the tensor pipe at ~67 % busy (profiles/SUMMARY_r01.md).
+__device__ __forceinline__ void umma_bf16_e(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_bf16_cg2_e(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                                uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_cg2_e(uint32_t bar_addr, uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::
+          "r"(bar_addr), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_e(uint32_t bar_addr) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar_addr)
+      : "memory");
+}
+// One K block (4 x K16 MMAs) plus the commit that frees its smem stage, issued
+// by one elected thread of a converged warp.  SW128 descriptors: the high word
+// (SBO = 1024, version, layout) is the constant DESC_HI; the low word is
+// (smem >> 4) | LBO field, advancing by STEP_A / STEP_B per K16 slice (no carry:
+// smem addresses < 256 KB).  CG = 2: cta_group::2 with a multicast commit.
+constexpr uint32_t DESC_HI = (1024u >> 4) | (1u << 14) | (2u << 29);
+template <int CG, uint32_t STEP_A, uint32_t STEP_B>
+__device__ __forceinline__ void umma_kblock(uint32_t d_tmem, uint32_t a_lo, uint32_t b_lo, uint32_t idesc,
+                                            uint32_t accumulate, uint32_t bar_addr, uint16_t mask) {
+  if constexpr (CG == 2) {
+    asm volatile(
+        "{\n\t.reg .pred p, q, e;\n\t.reg .b32 a1, a2, a3, b1, b2, b3;\n\t"
+        ".reg .b64 da0, da1, da2, da3, db0, db1, db2, db3;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "setp.eq.b32 q, 0, 0;\n\t"
+        "add.u32 a1, %1, %7;\n\tadd.u32 a2, %1, %8;\n\tadd.u32 a3, %1, %9;\n\t"
+        "add.u32 b1, %2, %10;\n\tadd.u32 b2, %2, %11;\n\tadd.u32 b3, %2, %12;\n\t"
+        "mov.b64 da0, {%1, %6};\n\tmov.b64 da1, {a1, %6};\n\tmov.b64 da2, {a2, %6};\n\tmov.b64 da3, {a3, %6};\n\t"
+        "mov.b64 db0, {%2, %6};\n\tmov.b64 db1, {b1, %6};\n\tmov.b64 db2, {b2, %6};\n\tmov.b64 db3, {b3, %6};\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], da0, db0, %3, p;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], da1, db1, %3, q;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], da2, db2, %3, q;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], da3, db3, %3, q;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%5], %13;\n\t}"
+        ::"r"(d_tmem), "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(accumulate), "r"(bar_addr), "n"(DESC_HI),
+        "n"(STEP_A), "n"(2 * STEP_A), "n"(3 * STEP_A), "n"(STEP_B), "n"(2 * STEP_B), "n"(3 * STEP_B), "h"(mask)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p, q, e;\n\t.reg .b32 a1, a2, a3, b1, b2, b3;\n\t"
+        ".reg .b64 da0, da1, da2, da3, db0, db1, db2, db3;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "setp.eq.b32 q, 0, 0;\n\t"
+        "add.u32 a1, %1, %7;\n\tadd.u32 a2, %1, %8;\n\tadd.u32 a3, %1, %9;\n\t"
+        "add.u32 b1, %2, %10;\n\tadd.u32 b2, %2, %11;\n\tadd.u32 b3, %2, %12;\n\t"
+        "mov.b64 da0, {%1, %6};\n\tmov.b64 da1, {a1, %6};\n\tmov.b64 da2, {a2, %6};\n\tmov.b64 da3, {a3, %6};\n\t"
+        "mov.b64 db0, {%2, %6};\n\tmov.b64 db1, {b1, %6};\n\tmov.b64 db2, {b2, %6};\n\tmov.b64 db3, {b3, %6};\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da0, db0, %3, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da1, db1, %3, q;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da2, db2, %3, q;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da3, db3, %3, q;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t}"
+        ::"r"(d_tmem), "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(accumulate), "r"(bar_addr), "n"(DESC_HI),
+        "n"(STEP_A), "n"(2 * STEP_A), "n"(3 * STEP_A), "n"(STEP_B), "n"(2 * STEP_B), "n"(3 * STEP_B)
+        : "memory");
+    (void)mask;
+  }
+}
 // Arrive (once) on the mbarrier at the same smem offset in every CTA of `mask`.
 __device__ __forceinline__ void umma_commit_cg2(uint64_t* bar, uint16_t mask) {
   asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::
