@@ -94,12 +94,21 @@ typedef struct {
                              through token_index_map (bitwise reproducible for every k; for
                              k <= 2 bit-identical to mode 0).  Applies to y and dx.  k = 1
                              ignores it: each token has one row, stored directly. */
+  int64_t rows;           /* routed (token, expert) rows R.  0 (default): R = T*k, every slot of
+                             topk_ids holds an expert id.  > 0: "sparse slots" -- topk_ids entries
+                             equal to -1 are empty slots (no expert), skipped by the dispatch
+                             (token_index_map = -1 there, d_topk_w = 0), and R = rows is the
+                             number of non-empty slots (a_save/b_save hold R rows).  Used by the
+                             expert-parallel receiver, whose received token rows carry only the
+                             slots of this rank's experts (SURVEY §8(f) NEXT-1 dedup).
+                             0 <= rows <= T*k. */
 } moe_problem;
 
 enum { MOE_CKPT_AB = 0, MOE_CKPT_NONE = 1 };
 enum { MOE_ACT_SWIGLU = 0, MOE_ACT_SILU = 1, MOE_ACT_RELU = 2 };
 
-/* The compact dispatch index structures of §4.1.  R = T*k.
+/* The compact dispatch index structures of §4.1.  R = T*k (or
+ * p->rows with sparse slots; token_index_map is then -1 at empty slots).
  *   expert_counts[E]         tokens routed to each expert (expert_lengths)
  *   expert_offsets[E+1]      exclusive prefix sum of counts; offsets[E] = R
  *   expert_token_indices[R]  token ids grouped by expert, ascending inside an
@@ -175,12 +184,27 @@ moe_status moe_ffn_fwd(const moe_problem* p, const void* x, const void* w1, cons
  * dw1/dw2/dw3 are written (experts with no rows get zeros), not accumulated.
  * d_topk_w [T,k] fp32 may be NULL only if router is NULL.
  * router != NULL: also computes the router backward (renorm-aware) and adds
- * dlogits W_g into dx; router->dw_gate is written. */
+ * dlogits W_g into dx; router->dw_gate is written.
+ * Launch order on `stream`: dH GEMM (dA, dB, wU, gate-grad partials) -> d_topk_w
+ * -> dX GEMM -> router backward / dx finalise -> [sync->dx_ready recorded] ->
+ * dW3 GEMM -> [sync->x_ready waited] -> dW1/dW2 GEMM (the only kernel after the
+ * optional up-projection recompute that reads x).  `sync` may be NULL. */
+typedef struct {
+  void* x_ready;   /* cudaEvent_t or NULL: the stream waits on it (cudaStreamWaitEvent) before
+                      the first kernel that reads x after the dX GEMM; lets an expert-parallel
+                      receiver overlap the arrival of x with the dH / dX GEMMs.  With
+                      MOE_CKPT_NONE x is read at the start (recompute), so x must be ready
+                      before the call. */
+  void* dx_ready;  /* cudaEvent_t or NULL: recorded once dx and d_topk_w are final, before the
+                      weight-gradient GEMMs; lets the caller return dx rows while dW1..3 run. */
+} moe_bwd_sync;
+
 moe_status moe_ffn_bwd(const moe_problem* p, const void* dy, const void* x, const void* w1,
                        const void* w2, const void* w3, const float* topk_w,
                        const moe_dispatch* disp, void* a_save, void* b_save,
                        void* dx, void* dw1, void* dw2, void* dw3, float* d_topk_w,
-                       const moe_router_bwd* router, void* ws, size_t ws_bytes, void* stream);
+                       const moe_router_bwd* router, const moe_bwd_sync* sync,
+                       void* ws, size_t ws_bytes, void* stream);
 
 /* Router backward on its own (used by the expert-parallel path, where the
  * gate-weight gradient d_topk_w arrives from the expert owners):
@@ -191,21 +215,44 @@ moe_status moe_router_backward(const moe_problem* p, const float* d_topk_w, cons
                                const moe_router_bwd* router, const void* dx_partial, void* dx,
                                void* ws, size_t ws_bytes, void* stream);
 
-/* Expert-parallel helpers (the paper's "future work").
- * moe_ep_row_meta: for every routed row r (expert-sorted order) row_w[r] =
- *   topk_w[row_slot[r]] and row_local_expert[r] = ids[row_slot[r]] mod
- *   experts_per_rank: the per-row payload that travels with the row to the
- *   rank owning its expert (ranks own contiguous expert ranges).
+/* Expert-parallel helpers (the paper's "future work"; SURVEY §8(e),
+ * §8(f) NEXT-1).  P = n_ranks ranks; rank q owns the experts
+ * [q*experts_per_rank, (q+1)*experts_per_rank).  A token's row travels ONCE to
+ * every rank that owns at least one of its k experts (per-destination dedup),
+ * carrying the k slots restricted to that rank; the receiver's expert outputs
+ * for the token come back already summed over its experts (one row per
+ * (token, rank) pair instead of one per (token, expert) pair).
+ *
+ * moe_ep_dest: dest[t*P + q] = q if some ids[t, j] is owned by rank q, else -1.
+ *   topk_ids [T,k] (p->T, p->k; p->E = global experts) -> dest [T, P] int32.
+ *   moe_dispatch_build over dest (T tokens, "k" = E = P, sparse slots, rows =
+ *   number of (token, rank) pairs or any upper bound up to T*P) then yields the
+ *   send plan: counts[q] rows to rank q, expert_token_indices = the tokens to
+ *   send, grouped by rank, ascending (the send order), token_index_map [T,P] =
+ *   send position of (t, q) or -1, row_slot = t*P + q.
+ * moe_ep_send_meta: for send row i < n_send (send_row_slot = that row_slot):
+ *   send_ids[i*k + j] = ids[t,j] - q*experts_per_rank if rank q owns ids[t,j]
+ *   else -1, send_w[i*k + j] = topk_w[t,j] (0 for -1): the receiver's sparse
+ *   topk_ids / topk_w.
+ * moe_ep_slot_grad: dg[t*k + j] = dg_back[send_pos[t*P + q]*k + j] with q the
+ *   owner of ids[t,j]: the gate-weight gradients returned by the owners,
+ *   back in (token, slot) order.  dg_back [n_send, k] fp32.
  * moe_gather_rows: dst[i, :] = src[index[i], :] for i < n (rows of `width`
  *   elements of `elem_bytes` in {2,4}; row bytes a multiple of 4); builds the
- *   all-to-all send buffer in expert_token_indices order.  index entries must
- *   be in [0, n_src).
- * moe_combine_rows: out[t, :] = sum_{j<k} rows[tim[t*k+j], :] (fixed j order,
- *   fp32 accumulation, dtype output): the token-side combine of returned
- *   expert rows through token_index_map ("gather its k expert
- *   outputs"). */
-moe_status moe_ep_row_meta(const moe_problem* p, const moe_dispatch* disp, const float* topk_w,
-                           int32_t experts_per_rank, float* row_w, int32_t* row_local_expert, void* stream);
+ *   all-to-all send buffer in send order.  index entries must be in [0, n_src).
+ * moe_combine_rows: out[t, :] = sum_{j<k, tim[t*k+j] >= 0} rows[tim[t*k+j], :]
+ *   (fixed j order, fp32 accumulation, dtype output; -1 entries skipped): the
+ *   token-side combine of returned rows through token_index_map (P:130-135
+ *   "gather its k expert outputs"); with the send plan (k = P) it sums a
+ *   token's per-rank partial outputs. */
+moe_status moe_ep_dest(const moe_problem* p, const int32_t* topk_ids, int32_t experts_per_rank,
+                       int32_t n_ranks, int32_t* dest, void* stream);
+moe_status moe_ep_send_meta(const moe_problem* p, const int32_t* topk_ids, const float* topk_w,
+                            int32_t experts_per_rank, int32_t n_ranks, const int32_t* send_row_slot,
+                            int64_t n_send, int32_t* send_ids, float* send_w, void* stream);
+moe_status moe_ep_slot_grad(const moe_problem* p, const int32_t* topk_ids, int32_t experts_per_rank,
+                            int32_t n_ranks, const int32_t* send_pos, const float* dg_back, float* dg,
+                            void* stream);
 moe_status moe_gather_rows(const void* src, int64_t n_src, const int32_t* index, int64_t n,
                            int64_t width, int32_t elem_bytes, void* dst, void* stream);
 moe_status moe_combine_rows(const moe_problem* p, const void* rows, const int32_t* token_index_map,

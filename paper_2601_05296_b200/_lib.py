@@ -23,7 +23,8 @@ MOE_OP_ROUTE, MOE_OP_DISPATCH, MOE_OP_FFN_FWD, MOE_OP_FFN_BWD, MOE_OP_ROUTER_BWD
 
 EXPORTS = ("moe_workspace_size", "moe_route", "moe_dispatch_build", "moe_ffn_fwd", "moe_ffn_bwd",
            "moe_gather_rows", "moe_combine_rows", "moe_status_string", "moe_launch_count", "moe_version",
-           "moe_profile_enable", "moe_profile_reset", "moe_profile_read", "moe_router_backward", "moe_ep_row_meta")
+           "moe_profile_enable", "moe_profile_reset", "moe_profile_read", "moe_router_backward", "moe_ep_dest",
+           "moe_ep_send_meta", "moe_ep_slot_grad")
 GEMM_KINDS = ("FWD_UP", "FWD_DOWN", "BWD_DH", "BWD_DX", "DW3", "DW12")
 
 
@@ -31,13 +32,17 @@ class MoeProblem(ctypes.Structure):
     _fields_ = [("T", ctypes.c_int64), ("d", ctypes.c_int32), ("h", ctypes.c_int32), ("E", ctypes.c_int32),
                 ("k", ctypes.c_int32), ("dtype", ctypes.c_int32), ("renormalize", ctypes.c_int32),
                 ("check_routing", ctypes.c_int32), ("checkpoint", ctypes.c_int32), ("activation", ctypes.c_int32),
-                ("deterministic", ctypes.c_int32)]
+                ("deterministic", ctypes.c_int32), ("rows", ctypes.c_int64)]
 
 
 class MoeDispatch(ctypes.Structure):
     _fields_ = [("expert_counts", ctypes.c_void_p), ("expert_offsets", ctypes.c_void_p),
                 ("expert_token_indices", ctypes.c_void_p), ("token_index_map", ctypes.c_void_p),
                 ("row_slot", ctypes.c_void_p), ("token_expert_indices", ctypes.c_void_p)]
+
+
+class MoeBwdSync(ctypes.Structure):
+    _fields_ = [("x_ready", ctypes.c_void_p), ("dx_ready", ctypes.c_void_p)]
 
 
 class MoeRouterBwd(ctypes.Structure):
@@ -67,13 +72,16 @@ def load():
     lib.moe_dispatch_build.argtypes = [P(MoeProblem), V, P(MoeDispatch), V, SZ, V]
     lib.moe_ffn_fwd.argtypes = [P(MoeProblem), V, V, V, V, V, P(MoeDispatch), V, V, V, V, SZ, V]
     lib.moe_ffn_bwd.argtypes = [P(MoeProblem), V, V, V, V, V, V, P(MoeDispatch), V, V, V, V, V, V, V,
-                                P(MoeRouterBwd), V, SZ, V]
+                                P(MoeRouterBwd), P(MoeBwdSync), V, SZ, V]
     lib.moe_gather_rows.argtypes = [V, I64, V, I64, I64, I32, V, V]
     lib.moe_combine_rows.argtypes = [P(MoeProblem), V, V, V, V]
     lib.moe_router_backward.argtypes = [P(MoeProblem), V, V, P(MoeRouterBwd), V, V, V, SZ, V]
-    lib.moe_ep_row_meta.argtypes = [P(MoeProblem), P(MoeDispatch), V, I32, V, V, V]
+    lib.moe_ep_dest.argtypes = [P(MoeProblem), V, I32, I32, V, V]
+    lib.moe_ep_send_meta.argtypes = [P(MoeProblem), V, V, I32, I32, V, I64, V, V, V]
+    lib.moe_ep_slot_grad.argtypes = [P(MoeProblem), V, I32, I32, V, V, V, V]
     for fn in ("moe_workspace_size", "moe_route", "moe_dispatch_build", "moe_ffn_fwd", "moe_ffn_bwd",
-               "moe_gather_rows", "moe_combine_rows", "moe_router_backward", "moe_ep_row_meta"):
+               "moe_gather_rows", "moe_combine_rows", "moe_router_backward", "moe_ep_dest", "moe_ep_send_meta",
+               "moe_ep_slot_grad"):
         getattr(lib, fn).restype = I32
     lib.moe_status_string.argtypes = [I32]
     lib.moe_status_string.restype = ctypes.c_char_p
@@ -81,7 +89,8 @@ def load():
     lib.moe_version.restype = I32
     lib.moe_profile_enable.argtypes = [I32]
     lib.moe_profile_read.argtypes = [I32, P(ctypes.c_double), P(I64)]
-    for fn in ("moe_profile_enable", "moe_profile_reset", "moe_profile_read", "moe_router_backward", "moe_ep_row_meta"):
+    for fn in ("moe_profile_enable", "moe_profile_reset", "moe_profile_read", "moe_router_backward", "moe_ep_dest",
+           "moe_ep_send_meta", "moe_ep_slot_grad"):
         getattr(lib, fn).restype = I32
     _lib = lib
     return lib
@@ -118,9 +127,11 @@ ACTIVATION = {"swiglu": 0, "silu": 1, "relu": 2}
 
 
 def problem(T, d, h, E, k, dtype, renormalize=False, check_routing=False, checkpoint="ab", activation="swiglu",
-            deterministic=False):
+            deterministic=False, rows=0):
+    """rows > 0: sparse slots (topk_ids -1 = empty slot), R = rows routed rows."""
     return MoeProblem(int(T), int(d), int(h), int(E), int(k), _dtype_code(dtype), int(bool(renormalize)),
-                      int(bool(check_routing)), CHECKPOINT[checkpoint], ACTIVATION[activation], int(bool(deterministic)))
+                      int(bool(check_routing)), CHECKPOINT[checkpoint], ACTIVATION[activation], int(bool(deterministic)),
+                      int(rows))
 
 
 def workspace_size(p, op):
@@ -161,10 +172,16 @@ def moe_ffn_fwd(p, x, w1, w2, w3, topk_w, disp, a_save, b_save, y, ws, stream=No
 
 
 def moe_ffn_bwd(p, dy, x, w1, w2, w3, topk_w, disp, a_save, b_save, dx, dw1, dw2, dw3, d_topk_w, router, ws,
-                stream=None):
+                stream=None, x_ready=None, dx_ready=None):
+    """x_ready / dx_ready: torch.cuda.Event or None (moe_bwd_sync)."""
+    sync = None
+    if x_ready is not None or dx_ready is not None:
+        sync = MoeBwdSync(x_ready.cuda_event if x_ready is not None else None,
+                          dx_ready.cuda_event if dx_ready is not None else None)
     _check(load().moe_ffn_bwd(ctypes.byref(p), _ptr(dy), _ptr(x), _ptr(w1), _ptr(w2), _ptr(w3), _ptr(topk_w),
                               ctypes.byref(disp), _ptr(a_save), _ptr(b_save), _ptr(dx), _ptr(dw1), _ptr(dw2),
                               _ptr(dw3), _ptr(d_topk_w), ctypes.byref(router) if router is not None else None,
+                              ctypes.byref(sync) if sync is not None else None,
                               _ptr(ws), ws.numel(), _stream(stream)), "moe_ffn_bwd")
 
 
@@ -174,9 +191,20 @@ def moe_router_backward(p, d_topk_w, x, router, dx_partial, dx, ws, stream=None)
            "moe_router_backward")
 
 
-def moe_ep_row_meta(p, disp, topk_w, experts_per_rank, row_w, row_local_expert, stream=None):
-    _check(load().moe_ep_row_meta(ctypes.byref(p), ctypes.byref(disp), _ptr(topk_w), int(experts_per_rank),
-                                  _ptr(row_w), _ptr(row_local_expert), _stream(stream)), "moe_ep_row_meta")
+def moe_ep_dest(p, topk_ids, experts_per_rank, n_ranks, dest, stream=None):
+    _check(load().moe_ep_dest(ctypes.byref(p), _ptr(topk_ids), int(experts_per_rank), int(n_ranks), _ptr(dest),
+                              _stream(stream)), "moe_ep_dest")
+
+
+def moe_ep_send_meta(p, topk_ids, topk_w, experts_per_rank, n_ranks, send_row_slot, send_ids, send_w, stream=None):
+    _check(load().moe_ep_send_meta(ctypes.byref(p), _ptr(topk_ids), _ptr(topk_w), int(experts_per_rank),
+                                   int(n_ranks), _ptr(send_row_slot), send_row_slot.numel(), _ptr(send_ids),
+                                   _ptr(send_w), _stream(stream)), "moe_ep_send_meta")
+
+
+def moe_ep_slot_grad(p, topk_ids, experts_per_rank, n_ranks, send_pos, dg_back, dg, stream=None):
+    _check(load().moe_ep_slot_grad(ctypes.byref(p), _ptr(topk_ids), int(experts_per_rank), int(n_ranks),
+                                   _ptr(send_pos), _ptr(dg_back), _ptr(dg), _stream(stream)), "moe_ep_slot_grad")
 
 
 def moe_gather_rows(src, index, dst, stream=None):

@@ -21,7 +21,10 @@ moe_status launch_router_bwd(const moe_problem*, const float*, const int32_t*, c
                              float*, void*, cudaStream_t);
 moe_status launch_finalize(const moe_problem*, const void*, const float*, const void*, void*, cudaStream_t, bool,
                            const int32_t*);
-moe_status launch_ep_row_meta(const int32_t*, const int32_t*, const float*, int64_t, int, float*, int32_t*, cudaStream_t);
+moe_status launch_ep_dest(const int32_t*, int64_t, int, int, int, int32_t*, cudaStream_t);
+moe_status launch_ep_send_meta(const int32_t*, const float*, int, int, int, const int32_t*, int64_t, int32_t*, float*,
+                               cudaStream_t);
+moe_status launch_ep_slot_grad(const int32_t*, int64_t, int, int, int, const int32_t*, const float*, float*, cudaStream_t);
 moe_status launch_gather_rows(const void*, const int32_t*, int64_t, int64_t, void*, cudaStream_t);
 moe_status launch_combine_rows(const moe_problem*, const void*, const int32_t*, void*, cudaStream_t);
 
@@ -38,8 +41,13 @@ static moe_status validate(const moe_problem* p) {
   if (p->checkpoint != MOE_CKPT_AB && p->checkpoint != MOE_CKPT_NONE) return MOE_ERR_INVALID_ARG;
   if (p->activation < MOE_ACT_SWIGLU || p->activation > MOE_ACT_RELU) return MOE_ERR_INVALID_ARG;
   if (p->deterministic != 0 && p->deterministic != 1) return MOE_ERR_INVALID_ARG;
+  if (p->rows < 0 || p->rows > p->T * (int64_t)p->k) return MOE_ERR_INVALID_ARG;
   return MOE_OK;
 }
+
+// routed rows R: T*k, or p->rows with sparse slots (empty slots = -1 in topk_ids)
+static int64_t routed_rows(const moe_problem* p) { return p->rows > 0 ? p->rows : p->T * p->k; }
+static bool sparse_slots(const moe_problem* p) { return p->rows > 0; }
 
 static bool aligned16(const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; }
 
@@ -54,16 +62,16 @@ static int dg_parts(const moe_problem* p) { return (int)ceil_div(p->h, 64); }
 // into the output when nothing else is added to it.  deterministic: one fp32
 // row per routed row, summed per token in slot order by the finalize pass.
 static int out_mode(const moe_problem* p, bool more_terms) {
-  if (p->k == 1) return more_terms ? OUT_TOK : OUT_TOKN;
+  if (p->k == 1 && !sparse_slots(p)) return more_terms ? OUT_TOK : OUT_TOKN;  // sparse: a token may have no row
   return p->deterministic ? OUT_ROWS : OUT_RED;
 }
 static int64_t acc_rows(const moe_problem* p, int mode) {
-  return mode == OUT_TOKN ? 0 : (mode == OUT_ROWS ? p->T * p->k : p->T);
+  return mode == OUT_TOKN ? 0 : (mode == OUT_ROWS ? routed_rows(p) : p->T);
 }
 
 struct FwdWs { void* u; float* yacc; void* a; void* b; size_t total; };
 static FwdWs fwd_layout(const moe_problem* p, void* base) {
-  const int64_t R = p->T * p->k;
+  const int64_t R = routed_rows(p);
   char* b = (char*)base;
   size_t o = 0;
   FwdWs w;
@@ -91,7 +99,7 @@ static RouterWs router_layout(const moe_problem* p, void* base) {
 
 struct BwdWs { void* wu; float* dxacc; float* dgpart; float* dlogits; float* dwgpart; float* dg; void* a; void* b; size_t total; };
 static BwdWs bwd_layout(const moe_problem* p, void* base) {
-  const int64_t R = p->T * p->k;
+  const int64_t R = routed_rows(p);
   char* b = (char*)base;
   size_t o = 0;
   BwdWs w;
@@ -100,7 +108,7 @@ static BwdWs bwd_layout(const moe_problem* p, void* base) {
   w.dgpart = (float*)(b + o); o += align256((size_t)R * dg_parts(p) * 4);
   w.dlogits = (float*)(b + o); o += align256((size_t)p->T * p->E * 4);
   w.dwgpart = (float*)(b + o); o += align256((size_t)dwg_chunks(p->T, p->d, p->E) * p->E * p->d * 4);
-  w.dg = (float*)(b + o); o += align256((size_t)R * 4);
+  w.dg = (float*)(b + o); o += align256((size_t)p->T * p->k * 4);
   w.a = w.b = nullptr;
   if (p->checkpoint == MOE_CKPT_NONE) {  // recomputed pre-activations
     w.a = b + o; o += align256((size_t)R * p->h * esize(p));
@@ -166,7 +174,7 @@ moe_status moe_dispatch_build(const moe_problem* p, const int32_t* topk_ids, con
   cudaStream_t st = (cudaStream_t)stream;
   int32_t* status = (int32_t*)ws;
   if (p->check_routing) MOE_CUDA_CHECK(cudaMemsetAsync(status, 0, sizeof(int32_t), st));
-  return launch_dispatch(p, topk_ids, out, (int32_t*)((char*)ws + 256), status, st);
+  return launch_dispatch(p, topk_ids, out, (int32_t*)((char*)ws + 256), status, st);  // rows checked if check_routing
 }
 
 moe_status moe_ffn_fwd(const moe_problem* p, const void* x, const void* w1, const void* w2, const void* w3,
@@ -179,7 +187,7 @@ moe_status moe_ffn_fwd(const moe_problem* p, const void* x, const void* w1, cons
   const bool ckpt = p->checkpoint == MOE_CKPT_AB;
   if (p->T > 0 && (!x || !y || !topk_w || (ckpt && (!a_save || (gated && !b_save))) || !ws ||
                    !disp->expert_offsets || !disp->expert_token_indices || !disp->row_slot ||
-                   (p->deterministic && p->k > 1 && !disp->token_index_map)))
+                   (out_mode(p, false) == OUT_ROWS && !disp->token_index_map)))
     return MOE_ERR_INVALID_ARG;
   if (!aligned16(x) || !aligned16(w1) || !aligned16(w2) || !aligned16(w3) || !aligned16(a_save) ||
       !aligned16(b_save) || !aligned16(y))
@@ -199,7 +207,7 @@ moe_status moe_ffn_fwd(const moe_problem* p, const void* x, const void* w1, cons
   c.x = x; c.w1 = w1; c.w2 = w2; c.w3 = w3; c.topw = topk_w;
   c.offs = disp->expert_offsets; c.eti = disp->expert_token_indices; c.row_slot = disp->row_slot;
   c.a_save = a_save; c.b_save = b_save; c.u = w.u; c.acc_out = w.yacc;
-  c.T = p->T; c.R = p->T * p->k; c.d = p->d; c.h = p->h; c.E = p->E; c.bf16 = p->dtype == MOE_BF16;
+  c.T = p->T; c.R = routed_rows(p); c.d = p->d; c.h = p->h; c.E = p->E; c.bf16 = p->dtype == MOE_BF16;
   c.act = p->activation;
   c.which = GEMM_FWD_UP;
   if ((s = run_gemm(c, st)) != MOE_OK) return s;
@@ -212,13 +220,14 @@ moe_status moe_ffn_fwd(const moe_problem* p, const void* x, const void* w1, cons
 moe_status moe_ffn_bwd(const moe_problem* p, const void* dy, const void* x, const void* w1, const void* w2,
                        const void* w3, const float* topk_w, const moe_dispatch* disp, void* a_save, void* b_save,
                        void* dx, void* dw1, void* dw2, void* dw3, float* d_topk_w, const moe_router_bwd* router,
-                       void* ws, size_t ws_bytes, void* stream) {
+                       const moe_bwd_sync* sync, void* ws, size_t ws_bytes, void* stream) {
   moe_status s = validate(p);
   if (s != MOE_OK) return s;
   const bool gated = p->activation == MOE_ACT_SWIGLU;
   if (!disp || !dw1 || (gated && (!dw2 || !w2)) || !dw3 || !w1 || !w3) return MOE_ERR_INVALID_ARG;
   if (router && (!router->w_gate || !router->dw_gate)) return MOE_ERR_INVALID_ARG;
   if (router && p->T > 0 && (!router->logits || !router->topk_ids)) return MOE_ERR_INVALID_ARG;
+  if (router && sparse_slots(p)) return MOE_ERR_INVALID_ARG;  // the router sees every slot of its own tokens
   const bool ckpt = p->checkpoint == MOE_CKPT_AB;
   if (p->T > 0 && (!dy || !x || !dx || !topk_w || (ckpt && (!a_save || (gated && !b_save))) || !ws ||
                    !disp->expert_offsets || !disp->expert_token_indices || !disp->token_index_map || !disp->row_slot))
@@ -229,7 +238,9 @@ moe_status moe_ffn_bwd(const moe_problem* p, const void* dy, const void* x, cons
   BwdWs w = bwd_layout(p, ws);
   if (ws_bytes < w.total) return MOE_ERR_WORKSPACE;
   cudaStream_t st = (cudaStream_t)stream;
-  const int64_t R = p->T * p->k;
+  cudaEvent_t x_ready = sync ? (cudaEvent_t)sync->x_ready : nullptr;
+  cudaEvent_t dx_ready = sync ? (cudaEvent_t)sync->dx_ready : nullptr;
+  const int64_t R = routed_rows(p);
   if (!ckpt) {
     a_save = w.a;
     b_save = w.b;
@@ -238,7 +249,6 @@ moe_status moe_ffn_bwd(const moe_problem* p, const void* dy, const void* x, cons
   c.x = x; c.dy = dy; c.w1 = w1; c.w2 = w2; c.w3 = w3; c.topw = topk_w;
   c.offs = disp->expert_offsets; c.eti = disp->expert_token_indices; c.row_slot = disp->row_slot;
   c.a_save = a_save; c.b_save = b_save; c.u = w.wu; c.acc_out = w.dxacc; c.dg_part = w.dgpart;
-  c.dw_a = dw3; c.dw_b = nullptr;
   c.T = p->T; c.R = R; c.d = p->d; c.h = p->h; c.E = p->E; c.bf16 = p->dtype == MOE_BF16;
   c.act = p->activation;
   const int mode = out_mode(p, router != nullptr);
@@ -251,32 +261,34 @@ moe_status moe_ffn_bwd(const moe_problem* p, const void* dy, const void* x, cons
     }
     c.which = GEMM_BWD_DH;  // dH, SwiGLU bwd: dA/dB in place, wU, dg partials
     if ((s = run_gemm(c, st)) != MOE_OK) return s;
+    float* dg = d_topk_w ? d_topk_w : w.dg;
+    if ((s = launch_dg_reduce(w.dgpart, gemm_dg_parts(c), disp->token_index_map, p->T * p->k, dg, st)) != MOE_OK)
+      return s;
+    c.which = GEMM_BWD_DX;   // dXacc += [dA|dB][W1;W2]
+    if ((s = run_gemm(c, st)) != MOE_OK) return s;
+    if (mode != OUT_TOKN) {  // (k = 1 without router: dx already written by the dX GEMM)
+      const float* dl = nullptr;
+      if (router) {
+        if ((s = launch_router_bwd(p, router->logits, router->topk_ids, dg, x, w.dlogits, w.dwgpart, router->dw_gate,
+                                   st)) != MOE_OK)
+          return s;
+        dl = w.dlogits;
+      }
+      if ((s = launch_finalize(p, w.dxacc, dl, router ? router->w_gate : nullptr, dx, st, false,
+                               mode == OUT_ROWS ? disp->token_index_map : nullptr)) != MOE_OK)
+        return s;
+    }
+  } else if (router) {
+    MOE_CUDA_CHECK(cudaMemsetAsync(router->dw_gate, 0, (size_t)p->E * p->d * esize(p), st));
   }
+  if (dx_ready) MOE_CUDA_CHECK(cudaEventRecord(dx_ready, st));
   c.which = GEMM_DW3;      // dW3 = dY^T (wU)
+  c.dw_a = dw3; c.dw_b = nullptr;
   if ((s = run_gemm(c, st)) != MOE_OK) return s;
+  if (x_ready) MOE_CUDA_CHECK(cudaStreamWaitEvent(st, x_ready, 0));
   c.which = GEMM_DW12;     // dW1, dW2 = [dA|dB]^T X
   c.dw_a = dw1; c.dw_b = dw2;
-  if ((s = run_gemm(c, st)) != MOE_OK) return s;
-  if (p->T == 0) {
-    if (router) {
-      MOE_CUDA_CHECK(cudaMemsetAsync(router->dw_gate, 0, (size_t)p->E * p->d * esize(p), st));
-    }
-    return MOE_OK;
-  }
-  c.which = GEMM_BWD_DX;   // dXacc += [dA|dB][W1;W2]
-  if ((s = run_gemm(c, st)) != MOE_OK) return s;
-  float* dg = d_topk_w ? d_topk_w : w.dg;
-  if ((s = launch_dg_reduce(w.dgpart, gemm_dg_parts(c), disp->token_index_map, R, dg, st)) != MOE_OK) return s;
-  if (mode == OUT_TOKN) return MOE_OK;  // k = 1 without router: dx already written by BWD_DX
-  const float* dl = nullptr;
-  if (router) {
-    if ((s = launch_router_bwd(p, router->logits, router->topk_ids, dg, x, w.dlogits, w.dwgpart, router->dw_gate,
-                               st)) != MOE_OK)
-      return s;
-    dl = w.dlogits;
-  }
-  return launch_finalize(p, w.dxacc, dl, router ? router->w_gate : nullptr, dx, st, false,
-                         mode == OUT_ROWS ? disp->token_index_map : nullptr);
+  return run_gemm(c, st);
 }
 
 moe_status moe_router_backward(const moe_problem* p, const float* d_topk_w, const void* x, const moe_router_bwd* router,
@@ -299,16 +311,38 @@ moe_status moe_router_backward(const moe_problem* p, const float* d_topk_w, cons
   return launch_finalize(p, dx_partial, w.dlogits, router->w_gate, dx, st, true, nullptr);
 }
 
-moe_status moe_ep_row_meta(const moe_problem* p, const moe_dispatch* disp, const float* topk_w, int32_t experts_per_rank,
-                           float* row_w, int32_t* row_local_expert, void* stream) {
+moe_status moe_ep_dest(const moe_problem* p, const int32_t* topk_ids, int32_t experts_per_rank, int32_t n_ranks,
+                       int32_t* dest, void* stream) {
   moe_status s = validate(p);
   if (s != MOE_OK) return s;
-  if (!disp || experts_per_rank < 1) return MOE_ERR_INVALID_ARG;
-  const int64_t R = p->T * p->k;
-  if (R > 0 && (!disp->row_slot || !disp->token_expert_indices || !topk_w || !row_w || !row_local_expert))
+  if (experts_per_rank < 1 || n_ranks < 1 || (int64_t)experts_per_rank * n_ranks != p->E || sparse_slots(p))
     return MOE_ERR_INVALID_ARG;
-  return launch_ep_row_meta(disp->row_slot, disp->token_expert_indices, topk_w, R, experts_per_rank, row_w,
-                            row_local_expert, (cudaStream_t)stream);
+  if (p->T > 0 && (!topk_ids || !dest)) return MOE_ERR_INVALID_ARG;
+  return launch_ep_dest(topk_ids, p->T, p->k, experts_per_rank, n_ranks, dest, (cudaStream_t)stream);
+}
+
+moe_status moe_ep_send_meta(const moe_problem* p, const int32_t* topk_ids, const float* topk_w, int32_t experts_per_rank,
+                            int32_t n_ranks, const int32_t* send_row_slot, int64_t n_send, int32_t* send_ids,
+                            float* send_w, void* stream) {
+  moe_status s = validate(p);
+  if (s != MOE_OK) return s;
+  if (experts_per_rank < 1 || n_ranks < 1 || (int64_t)experts_per_rank * n_ranks != p->E || sparse_slots(p))
+    return MOE_ERR_INVALID_ARG;
+  if (n_send < 0 || n_send > p->T * (int64_t)n_ranks) return MOE_ERR_INVALID_ARG;
+  if (n_send > 0 && (!topk_ids || !topk_w || !send_row_slot || !send_ids || !send_w)) return MOE_ERR_INVALID_ARG;
+  return launch_ep_send_meta(topk_ids, topk_w, p->k, experts_per_rank, n_ranks, send_row_slot, n_send, send_ids, send_w,
+                             (cudaStream_t)stream);
+}
+
+moe_status moe_ep_slot_grad(const moe_problem* p, const int32_t* topk_ids, int32_t experts_per_rank, int32_t n_ranks,
+                            const int32_t* send_pos, const float* dg_back, float* dg, void* stream) {
+  moe_status s = validate(p);
+  if (s != MOE_OK) return s;
+  if (experts_per_rank < 1 || n_ranks < 1 || (int64_t)experts_per_rank * n_ranks != p->E || sparse_slots(p))
+    return MOE_ERR_INVALID_ARG;
+  if (p->T > 0 && (!topk_ids || !send_pos || !dg_back || !dg)) return MOE_ERR_INVALID_ARG;
+  return launch_ep_slot_grad(topk_ids, p->T, p->k, experts_per_rank, n_ranks, send_pos, dg_back, dg,
+                             (cudaStream_t)stream);
 }
 
 moe_status moe_gather_rows(const void* src, int64_t n_src, const int32_t* index, int64_t n, int64_t width,

@@ -35,7 +35,7 @@ int dispatch_tile_entries(int64_t R) {
 
 // launch 1: tile_counts[tile*E + e]; status word validation
 __global__ void __launch_bounds__(DT_THREADS)
-dispatch_hist_kernel(const int32_t* __restrict__ ids, int64_t R, int k, int E, int tile, int check,
+dispatch_hist_kernel(const int32_t* __restrict__ ids, int64_t R, int k, int E, int tile, int check, int sparse,
                      int32_t* __restrict__ tile_counts, int32_t* __restrict__ status) {
   extern __shared__ int32_t hs[];  // [DT_WARPS][E]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -47,7 +47,7 @@ dispatch_hist_kernel(const int32_t* __restrict__ ids, int64_t R, int k, int E, i
     const int64_t f = base + lane;
     const bool valid = f < f1;
     int e = valid ? ids[f] : -1;
-    if (check && valid) {
+    if (check && valid && !(sparse && e == -1)) {  // sparse slots: -1 = empty slot, not an error
       bool bad = (e < 0 || e >= E);
       // per-token uniqueness: compare with the other slots of the same token
       const int64_t t = f / k;
@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(DT_THREADS)
 dispatch_scatter_kernel(const int32_t* __restrict__ ids, int64_t R, int k, int E, int tile, int ntiles,
                         const int32_t* __restrict__ tile_counts, int32_t* __restrict__ counts,
                         int32_t* __restrict__ offs, int32_t* __restrict__ eti, int32_t* __restrict__ tim,
-                        int32_t* __restrict__ row_slot) {
+                        int32_t* __restrict__ row_slot, int64_t rows_decl, int32_t* __restrict__ status) {
   extern __shared__ int32_t ss[];
   int32_t* base = ss;                 // [E]   running global base of each expert for this tile
   int32_t* wc = base + E;             // [DT_WARPS][E] warp counts of the current round
@@ -113,7 +113,10 @@ dispatch_scatter_kernel(const int32_t* __restrict__ ids, int64_t R, int k, int E
       }
       carry += __shfl_sync(0xffffffffu, incl, 31);
     }
-    if (my == 0 && lane == 0) offs[E] = carry;
+    if (my == 0 && lane == 0) {
+      offs[E] = carry;
+      if (status && rows_decl > 0 && carry > rows_decl) *status = MOE_ERR_BAD_ROUTING;  // more rows than declared
+    }
   }
   __syncthreads();
   const int64_t f0 = (int64_t)my * tile;
@@ -147,6 +150,8 @@ dispatch_scatter_kernel(const int32_t* __restrict__ ids, int64_t R, int k, int E
       tim[f] = pos;
       eti[pos] = (int32_t)(f / k);
       if (row_slot) row_slot[pos] = (int32_t)f;
+    } else if (valid) {
+      tim[f] = -1;  // empty (sparse) or invalid slot: no routed row
     }
     __syncthreads();
   }
@@ -165,10 +170,11 @@ moe_status launch_dispatch(const moe_problem* p, const int32_t* ids, const moe_d
   const int ntiles = (int)ceil_div(R, tile);
   size_t sm1 = sizeof(int32_t) * DT_WARPS * E;
   MOE_LAUNCH(dispatch_hist_kernel, ntiles, DT_THREADS, sm1, st, ids, R, p->k, E, tile, p->check_routing,
-             ws_tile_counts, status);
+             p->rows > 0 ? 1 : 0, ws_tile_counts, status);
   size_t sm2 = sizeof(int32_t) * (E + DT_WARPS * E + E);
   MOE_LAUNCH(dispatch_scatter_kernel, ntiles, DT_THREADS, sm2, st, ids, R, p->k, E, tile, ntiles, ws_tile_counts,
-             out->expert_counts, out->expert_offsets, out->expert_token_indices, out->token_index_map, out->row_slot);
+             out->expert_counts, out->expert_offsets, out->expert_token_indices, out->token_index_map, out->row_slot,
+             p->rows, p->check_routing ? status : nullptr);
   MOE_CUDA_CHECK(cudaGetLastError());
   return MOE_OK;
 }

@@ -16,9 +16,12 @@ __global__ void dg_reduce_kernel(const float* __restrict__ part, int nparts, con
                                  int64_t R, float* __restrict__ dg) {
   int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= R) return;
-  const float* p = part + (int64_t)tim[f] * nparts;
+  const int r = tim[f];
   float s = 0.f;
-  for (int i = 0; i < nparts; ++i) s += p[i];
+  if (r >= 0) {  // r < 0: empty slot (sparse slots) -> no routed row, zero gradient
+    const float* p = part + (int64_t)r * nparts;
+    for (int i = 0; i < nparts; ++i) s += p[i];
+  }
   dg[f] = s;
 }
 
@@ -183,8 +186,10 @@ __device__ __forceinline__ void load_acc8(const A* acc, const int32_t* tim, int 
 #pragma unroll
   for (int j = 0; j < 8; ++j) a[j] = 0.f;
   for (int j = 0; j < k; ++j) {
+    const int r = tim[t * k + j];
+    if (r < 0) continue;  // empty slot
     float v[8];
-    load8(acc + (int64_t)tim[t * k + j] * d + col, v);
+    load8(acc + (int64_t)r * d + col, v);
 #pragma unroll
     for (int q = 0; q < 8; ++q) a[q] += v[q];
   }
@@ -278,7 +283,10 @@ __global__ void __launch_bounds__(256) finalize_kernel(const A* __restrict__ acc
     if (r < nt && col < d) {
       if (!tim) a[r] = to_f32(acc[(t0 + r) * d + col]);
       else
-        for (int j = 0; j < k; ++j) a[r] += to_f32(acc[(int64_t)tim[(t0 + r) * k + j] * d + col]);
+        for (int j = 0; j < k; ++j) {
+          const int rr = tim[(t0 + r) * k + j];
+          if (rr >= 0) a[r] += to_f32(acc[(int64_t)rr * d + col]);
+        }
     }
   }
   if (dl) {
@@ -302,15 +310,47 @@ __global__ void __launch_bounds__(256) finalize_kernel(const A* __restrict__ acc
   }
 }
 
-// per-row EP payload: gate weight and local expert id of every routed row
-__global__ void ep_row_meta_kernel(const int32_t* __restrict__ row_slot, const int32_t* __restrict__ ids,
-                                   const float* __restrict__ topw, int64_t R, int epr, float* __restrict__ row_w,
-                                   int32_t* __restrict__ row_e) {
-  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= R) return;
-  const int s = row_slot[r];
-  row_w[r] = topw[s];
-  row_e[r] = ids[s] % epr;
+// ---- expert-parallel plan (NEXT-1: one row per (token, destination rank))
+// dest[t, q] = q if rank q owns one of the token's experts, else -1
+__global__ void ep_dest_kernel(const int32_t* __restrict__ ids, int64_t T, int k, int epr, int P,
+                               int32_t* __restrict__ dest) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  uint32_t mask[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // P <= 256 ranks
+  for (int j = 0; j < k; ++j) {
+    const int q = ids[t * k + j] / epr;
+    mask[q >> 5] |= 1u << (q & 31);
+  }
+  for (int q = 0; q < P; ++q) dest[t * P + q] = ((mask[q >> 5] >> (q & 31)) & 1u) ? q : -1;
+}
+
+// send row i (row_slot = t*P + q): the token's slots restricted to rank q, local expert ids
+__global__ void ep_send_meta_kernel(const int32_t* __restrict__ ids, const float* __restrict__ topw, int k, int epr,
+                                    int P, const int32_t* __restrict__ row_slot, int64_t n,
+                                    int32_t* __restrict__ send_ids, float* __restrict__ send_w) {
+  const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // f = i*k + j
+  if (f >= n * k) return;
+  const int64_t i = f / k;
+  const int j = (int)(f - i * k);
+  const int rs = row_slot[i];
+  const int64_t t = rs / P;
+  const int q = rs - (int)(t * P);
+  const int e = ids[t * k + j];
+  const bool mine = e / epr == q;
+  send_ids[f] = mine ? e - q * epr : -1;
+  send_w[f] = mine ? topw[t * k + j] : 0.f;
+}
+
+// dg[t, j] = dg_back[send_pos[t, owner(ids[t,j])], j]
+__global__ void ep_slot_grad_kernel(const int32_t* __restrict__ ids, int64_t T, int k, int epr, int P,
+                                    const int32_t* __restrict__ send_pos, const float* __restrict__ dg_back,
+                                    float* __restrict__ dg) {
+  const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= T * k) return;
+  const int64_t t = f / k;
+  const int j = (int)(f - t * k);
+  const int q = ids[f] / epr;
+  dg[f] = dg_back[(int64_t)send_pos[t * P + q] * k + j];
 }
 
 // 4-byte row gather for rows that are not a multiple of 16 bytes
@@ -332,16 +372,25 @@ __global__ void gather_rows_kernel(const uint4* __restrict__ src, const int32_t*
   dst[i] = src[(int64_t)index[row] * vec_per_row + c];
 }
 
+// out[t, 8c .. 8c+7] = sum_j rows[tim[t,j], ...] (fixed j order, -1 skipped); d % 8 == 0
 template <typename T>
 __global__ void combine_rows_kernel(const T* __restrict__ rows, const int32_t* __restrict__ tim, int64_t Tn, int d,
                                     int k, T* __restrict__ out) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= Tn * d) return;
-  int64_t t = i / d;
-  int c = (int)(i % d);
-  float s = 0.f;
-  for (int j = 0; j < k; ++j) s += to_f32(rows[(int64_t)tim[t * k + j] * d + c]);
-  out[i] = from_f32<T>(s);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int cpr = d / 8;
+  if (i >= Tn * cpr) return;
+  const int64_t t = i / cpr;
+  const int col = (int)(i - t * cpr) * 8;
+  float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int j = 0; j < k; ++j) {
+    const int r = tim[t * k + j];
+    if (r < 0) continue;
+    float v[8];
+    load8(rows + (int64_t)r * d + col, v);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) a[q] += v[q];
+  }
+  store8(out + t * d + col, a);
 }
 
 // ----------------------------------------------------------------- launchers
@@ -434,10 +483,25 @@ moe_status launch_finalize(const moe_problem* p, const void* acc, const float* d
   return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
 }
 
-moe_status launch_ep_row_meta(const int32_t* row_slot, const int32_t* ids, const float* topw, int64_t R, int epr,
-                              float* row_w, int32_t* row_e, cudaStream_t st) {
-  if (R == 0) return MOE_OK;
-  MOE_LAUNCH(ep_row_meta_kernel, (unsigned)ceil_div(R, 256), 256, 0, st, row_slot, ids, topw, R, epr, row_w, row_e);
+moe_status launch_ep_dest(const int32_t* ids, int64_t T, int k, int epr, int P, int32_t* dest, cudaStream_t st) {
+  if (T == 0) return MOE_OK;
+  MOE_LAUNCH(ep_dest_kernel, (unsigned)ceil_div(T, 256), 256, 0, st, ids, T, k, epr, P, dest);
+  return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
+}
+
+moe_status launch_ep_send_meta(const int32_t* ids, const float* topw, int k, int epr, int P, const int32_t* row_slot,
+                               int64_t n, int32_t* send_ids, float* send_w, cudaStream_t st) {
+  if (n == 0) return MOE_OK;
+  MOE_LAUNCH(ep_send_meta_kernel, (unsigned)ceil_div(n * k, 256), 256, 0, st, ids, topw, k, epr, P, row_slot, n,
+             send_ids, send_w);
+  return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
+}
+
+moe_status launch_ep_slot_grad(const int32_t* ids, int64_t T, int k, int epr, int P, const int32_t* send_pos,
+                               const float* dg_back, float* dg, cudaStream_t st) {
+  if (T == 0) return MOE_OK;
+  MOE_LAUNCH(ep_slot_grad_kernel, (unsigned)ceil_div(T * k, 256), 256, 0, st, ids, T, k, epr, P, send_pos, dg_back,
+             dg);
   return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
 }
 
@@ -457,7 +521,7 @@ moe_status launch_gather_rows(const void* src, const int32_t* index, int64_t n, 
 }
 
 moe_status launch_combine_rows(const moe_problem* p, const void* rows, const int32_t* tim, void* out, cudaStream_t st) {
-  const int64_t n = p->T * p->d;
+  const int64_t n = p->T * (p->d / 8);
   if (n == 0) return MOE_OK;
   if (p->dtype == MOE_BF16)
     MOE_LAUNCH(combine_rows_kernel<__nv_bfloat16>, (unsigned)ceil_div(n, 256), 256, 0, st,

@@ -1,38 +1,51 @@
-"""Expert-parallel MoEBlaze layer over torch.distributed (SURVEY §8(e)).
+"""Expert-parallel MoEBlaze layer over torch.distributed (SURVEY §8(e), §8(f) NEXT-1).
 
 The paper is single-GPU and names distribution as future work.  The
 layer shards naturally by expert: rank r owns experts [r*E/P, (r+1)*E/P);
 tokens stay data-parallel (T per rank); the router W_g is replicated.
 
+Per-destination dedup (NEXT-1).  A token whose k experts live on m <= min(k, P)
+ranks travels m times, not k times: the send plan is the MoEBlaze dispatch
+itself, applied one level up -- moe_ep_dest marks, per token, the ranks owning
+any of its experts (dest [T, P], -1 elsewhere) and moe_dispatch_build over dest
+(sparse slots) yields the send order (tokens grouped by rank, ascending), the
+per-rank row counts and the inverse map send_pos [T, P] (P:123-135 with
+"experts" = ranks).  Each sent row carries the token's k slots restricted to
+the receiving rank (moe_ep_send_meta: local expert id or -1, gate weight), so
+the receiver runs the SAME fused kernels as a sparse-slot problem (p.rows = its
+routed (token, expert) rows): FWD_DOWN's red.add combine then sums the token's
+local experts before anything travels back -- one return row per (token, rank).
+
 Forward, per rank:
-  1. route + dispatch build over the GLOBAL experts (moe_route,
-     moe_dispatch_build): expert_token_indices is then grouped by owner rank.
-  2. split sizes per destination from expert_token_offsets (one D2H) and the
-     per-expert counts all-to-all (C1) -> receive sizes.
-  3. send buffer = X rows in expert_token_indices order (moe_gather_rows) +
-     each row's gate weight and local expert id (moe_ep_row_meta): exactly the
-     routed rows, no padding, freed after the exchange (C2, NCCL all-to-all).
-  4. the receiver runs the SAME kernels on its received rows as a k = 1
-     problem (moe_dispatch_build over local expert ids, moe_ffn_fwd): each
-     received row's output w*O comes back (C3) in the sender's order, and
-     moe_combine_rows sums the k returned rows per token through
-     token_index_map.
-Backward mirrors it: dY rows and X rows travel again (C4; keeping the received
-X would be a saved permuted activation), moe_ffn_bwd on the receiver, dX rows
-and gate-grads return (C5), moe_combine_rows + moe_router_backward on the
-source, and all_reduce of dW_g (C6).  Expert weight grads stay local.
+  1. moe_route + moe_dispatch_build over the global experts (per-expert counts).
+  2. send plan (moe_ep_dest + moe_dispatch_build); C1: all-to-all of the
+     [rows, pairs per local expert] counts; ONE device->host read of the split
+     sizes (the only host sync of the step).
+  3. C2: X rows in send order (moe_gather_rows) + the packed slot metadata.
+  4. receiver: sparse dispatch over the received slots, moe_ffn_fwd; C3 returns
+     one row per (token, rank); moe_combine_rows sums them through send_pos.
+Backward:
+  C4a: dY rows to the owners (needed first); C4b: X rows again (keeping the
+  received X would be a saved permuted activation) on a side stream, overlapped
+  with the dH / dX GEMMs -- moe_ffn_bwd waits for it only before the dW1/dW2
+  GEMM (moe_bwd_sync.x_ready).  C5: dX rows and gate-weight gradients return on
+  the side stream as soon as moe_ffn_bwd records dx_ready, overlapped with the
+  dW3 / dW1,dW2 GEMMs.  moe_combine_rows + moe_ep_slot_grad + moe_router_backward
+  on the source; C6: all_reduce of dW_g.  Expert weight grads stay local.
 
 `ops` (the compute) and `a2a` (the exchange) are injectable so the host-side
-bookkeeping is testable with gloo on CPU; the product binds CudaOps (the C
-ABI) and NCCL.
+bookkeeping is testable with gloo on CPU; the product binds CudaOps (the C ABI)
+and NCCL.
 """
 from __future__ import annotations
+
+import contextlib
 
 import torch
 import torch.distributed as dist
 
 from . import _lib as L
-from .layer import Dispatch, dispatch_build, ffn_bwd, ffn_fwd, route
+from .layer import Dispatch, route
 
 
 class CudaOps:
@@ -41,17 +54,39 @@ class CudaOps:
     def route(self, x, wg, k, renorm):
         return route(x, wg, k, renorm)
 
-    def dispatch(self, ids, E, dtype):
-        return dispatch_build(ids, E, dtype=dtype)
+    def dispatch(self, ids, E, dtype, rows=0):
+        """moe_dispatch_build; rows > 0: sparse slots (-1 = empty), R <= rows."""
+        T, k = ids.shape
+        dev = ids.device
+        R = rows if rows > 0 else T * k
+        p = L.problem(T, 128, 128, E, k, dtype, rows=rows)
+        disp = Dispatch(torch.empty(E, dtype=torch.int32, device=dev), torch.empty(E + 1, dtype=torch.int32, device=dev),
+                        torch.empty(max(R, 1), dtype=torch.int32, device=dev)[:R],
+                        torch.empty(T, k, dtype=torch.int32, device=dev),
+                        torch.empty(max(R, 1), dtype=torch.int32, device=dev)[:R], ids)
+        ws = L.workspace(p, L.MOE_OP_DISPATCH, dev)
+        L.moe_dispatch_build(p, ids, disp.c(), ws)
+        return disp
 
-    def row_meta(self, disp, w, experts_per_rank, dtype):
-        T, k = w.shape
-        R = T * k
-        p = L.problem(T, 128, 128, max(experts_per_rank, k), k, dtype)
-        row_w = torch.empty(R, dtype=torch.float32, device=w.device)
-        row_e = torch.empty(R, dtype=torch.int32, device=w.device)
-        L.moe_ep_row_meta(p, disp.c(), w, experts_per_rank, row_w, row_e)
-        return row_w, row_e
+    def ep_dest(self, ids, E, El, P):
+        T, k = ids.shape
+        dest = torch.empty(T, P, dtype=torch.int32, device=ids.device)
+        L.moe_ep_dest(L.problem(T, 128, 128, E, k, torch.bfloat16), ids, El, P, dest)
+        return dest
+
+    def send_meta(self, ids, w, E, El, P, send_row_slot):
+        T, k = ids.shape
+        n = send_row_slot.numel()
+        sid = torch.empty(n, k, dtype=torch.int32, device=ids.device)
+        sw = torch.empty(n, k, dtype=torch.float32, device=ids.device)
+        L.moe_ep_send_meta(L.problem(T, 128, 128, E, k, torch.bfloat16), ids, w, El, P, send_row_slot, sid, sw)
+        return sid, sw
+
+    def slot_grad(self, ids, E, El, P, send_pos, dg_back):
+        T, k = ids.shape
+        dg = torch.empty(T, k, dtype=torch.float32, device=ids.device)
+        L.moe_ep_slot_grad(L.problem(T, 128, 128, E, k, torch.bfloat16), ids, El, P, send_pos, dg_back, dg)
+        return dg
 
     def gather_rows(self, src, index):
         n = index.numel()
@@ -59,11 +94,30 @@ class CudaOps:
         L.moe_gather_rows(src, index.reshape(-1), dst)
         return dst
 
-    def ffn_fwd(self, x, w1, w2, w3, w, disp):
-        return ffn_fwd(x, w1, w2, w3, w, disp)
+    def ffn_fwd(self, x, w1, w2, w3, w, disp, rows):
+        T, d = x.shape
+        E, h, _ = w1.shape
+        k = w.shape[1]
+        p = L.problem(T, d, h, E, k, x.dtype, rows=rows)
+        a = torch.empty(rows, h, dtype=x.dtype, device=x.device)
+        b = torch.empty(rows, h, dtype=x.dtype, device=x.device)
+        y = torch.empty(T, d, dtype=x.dtype, device=x.device)
+        ws = L.workspace(p, L.MOE_OP_FFN_FWD, x.device)
+        L.moe_ffn_fwd(p, x, w1, w2, w3, w, disp.c(), a, b, y, ws)
+        return y, a, b
 
-    def ffn_bwd(self, dy, x, w1, w2, w3, w, disp, a, b):
-        return ffn_bwd(dy, x, w1, w2, w3, w, disp, a, b)
+    def ffn_bwd(self, dy, x, w1, w2, w3, w, disp, a, b, rows, x_ready=None, dx_ready=None):
+        T, d = dy.shape
+        E, h, _ = w1.shape
+        k = w.shape[1]
+        p = L.problem(T, d, h, E, k, dy.dtype, rows=rows)
+        dx = torch.empty_like(dy)
+        dw1, dw2, dw3 = torch.empty_like(w1), torch.empty_like(w2), torch.empty_like(w3)
+        dg = torch.empty(T, k, dtype=torch.float32, device=dy.device)
+        ws = L.workspace(p, L.MOE_OP_FFN_BWD, dy.device)
+        L.moe_ffn_bwd(p, dy, x, w1, w2, w3, w, disp.c(), a, b, dx, dw1, dw2, dw3, dg, None, ws,
+                      x_ready=x_ready, dx_ready=dx_ready)
+        return dict(dx=dx, dw1=dw1, dw2=dw2, dw3=dw3, dg=dg)
 
     def combine(self, rows, tim, T, d, k):
         out = torch.empty(T, d, dtype=rows.dtype, device=rows.device)
@@ -91,9 +145,13 @@ def nccl_a2a(send, send_split, recv_split, group=None):
 
 
 class ExpertParallelMoE:
-    """One MoE layer, expert-parallel over `group`."""
+    """One MoE layer, expert-parallel over `group`, with per-destination dedup.
 
-    def __init__(self, E, k, renormalize=False, group=None, ops=None, a2a=None):
+    overlap: run C4b (X rows) and C5 (dX rows, gate grads) on a side CUDA
+    stream against the backward GEMMs (default: on for CUDA tensors over NCCL).
+    """
+
+    def __init__(self, E, k, renormalize=False, group=None, ops=None, a2a=None, overlap=None):
         self.P = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         if E % self.P:
@@ -103,56 +161,111 @@ class ExpertParallelMoE:
         self.local_experts = (self.rank * self.El, (self.rank + 1) * self.El)
         self.ops = ops or CudaOps()
         self._a2a = a2a or nccl_a2a
-        self.last_rows_received = 0
+        self.overlap = overlap
+        self.last_rows_received = 0   # (token, expert) rows computed here
+        self.last_rows_sent = 0       # token rows sent (X), after dedup
+        self.last_pairs_sent = 0      # (token, expert) pairs they carry
 
     def a2a(self, send, send_split, recv_split):
         return self._a2a(send, send_split, recv_split, self.group)
 
+    def _use_streams(self, x):
+        if self.overlap is not None:
+            return bool(self.overlap) and x.is_cuda
+        return x.is_cuda and dist.get_backend(self.group) == "nccl"
+
     def forward(self, x, wg, w1l, w2l, w3l):
-        ops, P, El, k = self.ops, self.P, self.El, self.k
+        ops, P, El, k, E = self.ops, self.P, self.El, self.k, self.E
         T, d = x.shape
         logits, ids, w = ops.route(x, wg, k, self.renorm)
-        disp = ops.dispatch(ids, self.E, x.dtype)
-        row_w, row_e = ops.row_meta(disp, w, El, x.dtype)
-        # C1: per-expert counts to the owner ranks; split sizes to the host (one sync)
-        recv_counts = self.a2a(disp.counts, [El] * P, [El] * P)
-        offs_h = disp.offs.cpu().tolist()
-        send_split = [offs_h[(q + 1) * El] - offs_h[q * El] for q in range(P)]
-        rc = recv_counts.cpu().view(P, El)
-        recv_split = rc.sum(1).tolist()
-        self.last_rows_received = int(sum(recv_split))
-        # C2: routed rows (exactly T*k rows in expert order; a comm buffer, not an activation)
-        xs = ops.gather_rows(x, disp.eti)
-        x_recv = self.a2a(xs, send_split, recv_split)
-        del xs
-        w_recv = self.a2a(row_w, send_split, recv_split).view(-1, 1)
-        e_recv = self.a2a(row_e, send_split, recv_split).view(-1, 1)
-        disp_l = ops.dispatch(e_recv, El, x.dtype)
-        y_rows, a_l, b_l = ops.ffn_fwd(x_recv, w1l, w2l, w3l, w_recv, disp_l)
+        disp = ops.dispatch(ids, E, x.dtype)
+        # send plan: one row per (token, owning rank)
+        dest = ops.ep_dest(ids, E, El, P)
+        plan = ops.dispatch(dest, P, x.dtype, rows=T * min(k, P))
+        # C1: [rows to q, pairs per local expert of q] -> owners; one host read of all split sizes
+        cnt = torch.cat([plan.counts.view(P, 1), disp.counts.view(P, El)], 1).reshape(-1).contiguous()
+        rc = self.a2a(cnt, [El + 1] * P, [El + 1] * P)
+        host = torch.cat([plan.counts, rc]).cpu()
+        send_split = host[:P].tolist()
+        rc_h = host[P:].view(P, El + 1)
+        recv_split = rc_h[:, 0].tolist()
+        n_pairs = int(rc_h[:, 1:].sum())
+        n_send = int(sum(send_split))
+        self.last_rows_received = n_pairs
+        self.last_rows_sent = n_send
+        self.last_pairs_sent = T * k
+        send_tok = plan.eti[:n_send]
+        sid, sw = ops.send_meta(ids, w, E, El, P, plan.row_slot[:n_send])
+        # C2: token rows + their slot metadata (local expert id or -1, gate weight) in one int32 payload
+        x_recv = self.a2a(ops.gather_rows(x, send_tok), send_split, recv_split)
+        meta = self.a2a(torch.cat([sid, sw.view(torch.int32)], 1), send_split, recv_split)
+        ids_l = meta[:, :k].contiguous()
+        w_l = meta[:, k:].contiguous().view(sw.dtype)
+        U = x_recv.shape[0]
+        disp_l = ops.dispatch(ids_l, El, x.dtype, rows=n_pairs) if n_pairs else None
+        if n_pairs:
+            y_rows, a_l, b_l = ops.ffn_fwd(x_recv, w1l, w2l, w3l, w_l, disp_l, n_pairs)
+        else:
+            y_rows, a_l, b_l = x_recv.new_zeros(U, d), None, None
         del x_recv
-        # C3: expert outputs back to their tokens, combined through token_index_map
+        # C3: per-(token, rank) partial outputs back; token-side sum through send_pos
         y_back = self.a2a(y_rows, recv_split, send_split)
-        y = ops.combine(y_back, disp.tim, T, d, k)
-        ctx = dict(x=x, wg=wg, w1l=w1l, w2l=w2l, w3l=w3l, logits=logits, ids=ids, w=w, disp=disp,
-                   send_split=send_split, recv_split=recv_split, w_recv=w_recv, disp_l=disp_l, a_l=a_l, b_l=b_l)
+        y = ops.combine(y_back, plan.tim, T, d, P)
+        ctx = dict(x=x, wg=wg, w1l=w1l, w2l=w2l, w3l=w3l, logits=logits, ids=ids, w=w, plan=plan, send_tok=send_tok,
+                   send_split=send_split, recv_split=recv_split, w_l=w_l, disp_l=disp_l, a_l=a_l, b_l=b_l,
+                   n_pairs=n_pairs)
         return y, ctx
 
     def backward(self, ctx, dy):
-        ops = self.ops
-        x, disp = ctx["x"], ctx["disp"]
+        ops, P, El, E, k = self.ops, self.P, self.El, self.E, self.k
+        x, plan = ctx["x"], ctx["plan"]
         T, d = x.shape
         ss, rs = ctx["send_split"], ctx["recv_split"]
-        # C4: dY rows and (again) X rows to the expert owners
-        dy_recv = self.a2a(ops.gather_rows(dy, disp.eti), ss, rs)
-        x_recv = self.a2a(ops.gather_rows(x, disp.eti), ss, rs)
-        g = ops.ffn_bwd(dy_recv, x_recv, ctx["w1l"], ctx["w2l"], ctx["w3l"], ctx["w_recv"], ctx["disp_l"],
-                        ctx["a_l"], ctx["b_l"])
-        del dy_recv, x_recv
-        # C5: token-gradient rows and gate-weight gradients back to the sources
-        dx_back = self.a2a(g["dx"], rs, ss)
-        dg_back = self.a2a(g["dg"].reshape(-1, 1), rs, ss)
-        dx_part = ops.combine(dx_back, disp.tim, T, d, self.k)
-        dg = ops.gather_rows(dg_back, disp.tim.reshape(-1)).view(T, self.k)
+        n_pairs = ctx["n_pairs"]
+        w1l, w2l, w3l = ctx["w1l"], ctx["w2l"], ctx["w3l"]
+        streams = self._use_streams(x)
+        main = torch.cuda.current_stream() if streams else None
+        side = torch.cuda.Stream(device=x.device) if streams else None
+        sctx = (lambda: torch.cuda.stream(side)) if streams else contextlib.nullcontext
+        # C4a: dY rows to the expert owners (the dH GEMM needs them first)
+        dy_recv = self.a2a(ops.gather_rows(dy, ctx["send_tok"]), ss, rs)
+        # C4b: X rows again, on the side stream (only the dW1/dW2 GEMM reads them)
+        x_send = ops.gather_rows(x, ctx["send_tok"])
+        x_ready = dx_ready = None
+        if streams:
+            side.wait_stream(main)
+        with sctx():
+            x_recv = self.a2a(x_send, ss, rs)
+        if streams:
+            x_ready = torch.cuda.Event()
+            x_ready.record(side)
+            x_recv.record_stream(main)
+            x_send.record_stream(side)
+            dx_ready = torch.cuda.Event()
+        U = dy_recv.shape[0]
+        if n_pairs:
+            g = ops.ffn_bwd(dy_recv, x_recv, w1l, w2l, w3l, ctx["w_l"], ctx["disp_l"], ctx["a_l"], ctx["b_l"],
+                            n_pairs, x_ready=x_ready, dx_ready=dx_ready)
+        else:  # nothing routed here: zero expert grads
+            g = dict(dx=dy_recv.new_zeros(U, d), dg=torch.zeros(U, k, dtype=ctx["w_l"].dtype, device=dy.device),
+                     dw1=torch.zeros_like(w1l), dw2=torch.zeros_like(w2l), dw3=torch.zeros_like(w3l))
+            if streams:
+                dx_ready.record(main)
+                main.wait_event(x_ready)
+        # C5: per-(token, rank) dX partials and the gate-weight gradients back, on the side stream
+        with sctx():
+            if streams:
+                side.wait_event(dx_ready)
+                g["dx"].record_stream(side)
+                g["dg"].record_stream(side)
+            dx_back = self.a2a(g["dx"], rs, ss)
+            dg_back = self.a2a(g["dg"], rs, ss)
+        if streams:
+            main.wait_stream(side)
+            dx_back.record_stream(main)
+            dg_back.record_stream(main)
+        dx_part = ops.combine(dx_back, plan.tim, T, d, P)
+        dg = ops.slot_grad(ctx["ids"], E, El, P, plan.tim, dg_back)
         dx, dwg = ops.router_backward(dg, x, ctx["wg"], ctx["logits"], ctx["ids"], dx_part, self.renorm)
         # C6: replicated router
         acc = dwg.float() if dwg.element_size() < 4 else dwg  # reduce 16-bit grads in fp32

@@ -105,3 +105,31 @@ def test_argument_validation(lib):
     # null pointers are rejected synchronously, nothing is launched
     assert lib.moe_route(ctypes.byref(_problem(L)), None, None, None, None, None, None, 0, None) == 1
     assert lib.moe_status_string(4) == b"workspace too small"
+
+
+def test_sparse_slot_rows_validation(lib):
+    """moe_problem.rows (sparse slots, NEXT-1 EP receivers): 0 <= rows <= T*k;
+    the workspace scales with rows, not T*k (no routed-token term either way)."""
+    from paper_2601_05296_b200 import _lib as L
+    n = ctypes.c_size_t(0)
+    for rows, code in ((-1, 1), (1024 * 2 + 1, 1), (1, 0), (1024 * 2, 0)):
+        p = L.problem(1024, 256, 512, 8, 2, torch.bfloat16, rows=rows)
+        assert lib.moe_workspace_size(ctypes.byref(p), L.MOE_OP_FFN_FWD, ctypes.byref(n)) == code, rows
+    dense = L.workspace_size(L.problem(1024, 256, 512, 8, 2, torch.bfloat16), L.MOE_OP_FFN_FWD)
+    half = L.workspace_size(L.problem(1024, 256, 512, 8, 2, torch.bfloat16, rows=1024), L.MOE_OP_FFN_FWD)
+    assert abs((dense - half) - 1024 * 512 * 2) <= 512  # the transient U buffer holds R = rows rows
+
+
+def test_ep_helpers_validation(lib):
+    """moe_ep_* reject a rank split that does not tile the experts and sparse
+    source problems, synchronously (nothing launched: no GPU needed)."""
+    from paper_2601_05296_b200 import _lib as L
+    p = L.problem(16, 128, 128, 8, 2, torch.bfloat16)
+    assert lib.moe_ep_dest(ctypes.byref(p), None, 3, 2, None, None) == 1        # 3*2 != 8
+    assert lib.moe_ep_dest(ctypes.byref(p), None, 4, 2, None, None) == 1        # null pointers, T > 0
+    p0 = L.problem(0, 128, 128, 8, 2, torch.bfloat16)
+    assert lib.moe_ep_dest(ctypes.byref(p0), None, 4, 2, None, None) == 0       # T = 0: nothing to do
+    assert lib.moe_ep_send_meta(ctypes.byref(p), None, None, 4, 2, None, 33, None, None, None) == 1  # n > T*P
+    assert lib.moe_ep_send_meta(ctypes.byref(p0), None, None, 4, 2, None, 0, None, None, None) == 0
+    ps = L.problem(16, 128, 128, 8, 2, torch.bfloat16, rows=8)
+    assert lib.moe_ep_slot_grad(ctypes.byref(ps), None, 4, 2, None, None, None, None) == 1  # sparse source

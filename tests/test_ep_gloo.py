@@ -17,10 +17,12 @@ import torch.multiprocessing as mp
 
 import oracle as O
 from moe_inputs import make_inputs
+from tests._util import dispatch_sparse as _dispatch_sparse
 
 
 class OracleOps:
-    """Test-only compute for the EP orchestrator: the fp64 oracle on CPU."""
+    """Test-only compute for the EP orchestrator: the fp64 oracle on CPU, plus
+    numpy restatements of the EP helpers' definitions (include/moeblaze.h)."""
 
     class D:
         def __init__(self, d, ids):
@@ -36,27 +38,44 @@ class OracleOps:
         r = O.route(x.numpy(), wg.numpy(), k, renorm)
         return torch.from_numpy(r["logits"]), torch.from_numpy(r["ids"]), torch.from_numpy(r["w"])
 
-    def dispatch(self, ids, E, dtype):
+    def dispatch(self, ids, E, dtype, rows=0):
+        if rows:
+            return OracleOps.D(_dispatch_sparse(ids.numpy(), E), ids)
         return OracleOps.D(O.dispatch_argsort(ids.numpy(), E), ids)
 
-    def row_meta(self, disp, w, epr, dtype):
-        rs = disp.row_slot
-        return w.reshape(-1)[rs].clone(), (disp.ids.reshape(-1)[rs] % epr).to(torch.int32)
+    def ep_dest(self, ids, E, El, P):
+        owner = ids.long() // El
+        dest = torch.full((ids.shape[0], P), -1, dtype=torch.int32)
+        for q in range(P):
+            dest[(owner == q).any(1), q] = q
+        return dest
+
+    def send_meta(self, ids, w, E, El, P, row_slot):
+        t, q = row_slot.long() // P, row_slot.long() % P
+        e = ids[t].long()
+        mine = (e // El) == q[:, None]
+        return torch.where(mine, e - q[:, None] * El, -1).to(torch.int32), torch.where(mine, w[t], 0.0)
+
+    def slot_grad(self, ids, E, El, P, send_pos, dg_back):
+        T, k = ids.shape
+        pos = send_pos.long().gather(1, ids.long() // El)
+        return dg_back[pos, torch.arange(k)[None, :].expand(T, k)]
 
     def gather_rows(self, src, index):
         return src[index.reshape(-1).long()].clone()
 
-    def ffn_fwd(self, x, w1, w2, w3, w, disp):
+    def ffn_fwd(self, x, w1, w2, w3, w, disp, rows):
         f = O.ffn_forward(x.numpy(), w1.numpy(), w2.numpy(), w3.numpy(), disp.ids.numpy(), w.numpy(), disp.raw)
-        return torch.from_numpy(f["y"]), torch.from_numpy(f["A"]), torch.from_numpy(f["B"])
+        return torch.from_numpy(f["y"]), torch.from_numpy(f["A"][:rows]), torch.from_numpy(f["B"][:rows])
 
-    def ffn_bwd(self, dy, x, w1, w2, w3, w, disp, a, b):
+    def ffn_bwd(self, dy, x, w1, w2, w3, w, disp, a, b, rows, x_ready=None, dx_ready=None):
         g = O.ffn_backward(dy.numpy(), x.numpy(), w1.numpy(), w2.numpy(), w3.numpy(), disp.ids.numpy(), w.numpy(),
                            disp.raw, a.numpy(), b.numpy())
         return {n: torch.from_numpy(np.ascontiguousarray(g[n])) for n in ("dx", "dw1", "dw2", "dw3", "dg")}
 
     def combine(self, rows, tim, T, d, k):
-        return rows[tim.reshape(T, k).long()].sum(1)
+        t = tim.reshape(T, k).long()
+        return torch.where((t >= 0)[..., None], rows[t.clamp(min=0)], 0.0).sum(1)
 
     def router_backward(self, dg, x, wg, logits, ids, dx_partial, renorm):
         rb = O.router_backward(dg.numpy(), x.numpy(), wg.numpy(), logits.numpy(), ids.numpy(), renorm)
@@ -70,26 +89,26 @@ def gloo_a2a(send, send_split, recv_split, group=None):
 
 
 CFG = dict(T=40, d=16, h=24, E=8, k=2)
+CFG6 = dict(T=40, d=16, h=24, E=8, k=6)   # k > P: tokens hit several experts per rank (dedup)
 
 
-def _inputs(rank, P, renorm, routing):
-    c = CFG
+def _inputs(rank, P, renorm, routing, c=CFG):
     W = make_inputs(c["T"], c["d"], c["h"], c["E"], c["k"], dtype="fp32", seed=100, routing=routing)
     X = [make_inputs(c["T"], c["d"], c["h"], c["E"], c["k"], dtype="fp32", seed=r, routing=routing) for r in range(P)]
     f = lambda t: t.double()  # noqa: E731
     return {n: f(W[n]) for n in ("w_gate", "w1", "w2", "w3")}, [(f(X[r]["x"]), f(X[r]["dy"])) for r in range(P)]
 
 
-def _worker(rank, P, port, renorm, routing, q):
+def _worker(rank, P, port, renorm, routing, q, c=CFG):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=P)
     from paper_2601_05296_b200.ep import ExpertParallelMoE
-    W, XS = _inputs(rank, P, renorm, routing)
-    ep = ExpertParallelMoE(CFG["E"], CFG["k"], renorm, ops=OracleOps(), a2a=gloo_a2a)
+    W, XS = _inputs(rank, P, renorm, routing, c)
+    ep = ExpertParallelMoE(c["E"], c["k"], renorm, ops=OracleOps(), a2a=gloo_a2a)
     lo, hi = ep.local_experts
     x, dy = XS[rank]
     y, g = ep.step(x, W["w_gate"], W["w1"][lo:hi], W["w2"][lo:hi], W["w3"][lo:hi], dy)
-    q.put((rank, y.numpy(), {n: v.numpy() for n, v in g.items()}, (lo, hi)))
+    q.put((rank, y.numpy(), {n: v.numpy() for n, v in g.items()}, (lo, hi), ep.last_rows_sent))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -102,13 +121,16 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("P,renorm,routing", [(2, False, "balanced"), (2, True, "skewed"), (4, False, "balanced"),
-                                             (4, False, "degenerate")])
-def test_ep_matches_single_process_oracle(P, renorm, routing):
+@pytest.mark.parametrize("P,renorm,routing,c", [(2, False, "balanced", CFG), (2, True, "skewed", CFG),
+                                               (4, False, "balanced", CFG), (4, False, "degenerate", CFG),
+                                               (2, False, "balanced", CFG6), (4, True, "skewed", CFG6)])
+def test_ep_matches_single_process_oracle(P, renorm, routing, c):
+    """Every rank's y, dx, dg, dW_g and local expert grads equal the fp64 oracle
+    over the concatenated tokens; each token row is sent once per owning rank."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, P, port, renorm, routing, q)) for r in range(P)]
+    procs = [ctx.Process(target=_worker, args=(r, P, port, renorm, routing, q, c)) for r in range(P)]
     for p in procs:
         p.start()
     res = [q.get(timeout=120) for _ in range(P)]
@@ -116,15 +138,20 @@ def test_ep_matches_single_process_oracle(P, renorm, routing):
         p.join(timeout=60)
         assert p.exitcode == 0
     res.sort(key=lambda t: t[0])
-    W, XS = _inputs(0, P, renorm, routing)
+    W, XS = _inputs(0, P, renorm, routing, c)
     Xall = torch.cat([x for x, _ in XS]).numpy()
     DYall = torch.cat([dy for _, dy in XS]).numpy()
     Wn = {n: v.numpy() for n, v in W.items()}
-    fwd = O.layer_forward(Xall, Wn["w_gate"], Wn["w1"], Wn["w2"], Wn["w3"], CFG["k"], renorm)
+    fwd = O.layer_forward(Xall, Wn["w_gate"], Wn["w1"], Wn["w2"], Wn["w3"], c["k"], renorm)
     bwd = O.layer_backward(fwd, DYall, Xall, Wn["w_gate"], Wn["w1"], Wn["w2"], Wn["w3"], renorm)
-    T = CFG["T"]
-    for rank, y, g, (lo, hi) in res:
+    T = c["T"]
+    El = c["E"] // P
+    for rank, y, g, (lo, hi), n_sent in res:
         sl = slice(rank * T, (rank + 1) * T)
+        owners = fwd["ids"][sl] // El
+        assert n_sent == sum(len(set(row)) for row in owners.tolist())  # per-destination dedup
+        if c["k"] > P:
+            assert n_sent < T * c["k"]
         np.testing.assert_allclose(y, fwd["y"][sl], rtol=1e-10, atol=1e-12)
         np.testing.assert_allclose(g["dx"], bwd["dx"][sl], rtol=1e-10, atol=1e-12)
         np.testing.assert_allclose(g["dg"], bwd["dg"][sl], rtol=1e-10, atol=1e-12)
