@@ -175,6 +175,9 @@ def moe_ffn_bwd(p, dy, x, w1, w2, w3, topk_w, disp, a_save, b_save, dx, dw1, dw2
                 stream=None, x_ready=None, dx_ready=None):
     """x_ready / dx_ready: torch.cuda.Event or None (moe_bwd_sync)."""
     sync = None
+    for ev in (x_ready, dx_ready):
+        if ev is not None and not ev.cuda_event:
+            raise MoEError("moe_ffn_bwd: sync events must be created (recorded once) before the call")
     if x_ready is not None or dx_ready is not None:
         sync = MoeBwdSync(x_ready.cuda_event if x_ready is not None else None,
                           dx_ready.cuda_event if dx_ready is not None else None)

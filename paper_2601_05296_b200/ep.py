@@ -241,7 +241,10 @@ class ExpertParallelMoE:
             x_ready.record(side)
             x_recv.record_stream(main)
             x_send.record_stream(side)
+            # torch creates the CUDA event lazily at its first record: create it
+            # now so the library gets a real handle to re-record after dX is final
             dx_ready = torch.cuda.Event()
+            dx_ready.record(main)
         U = dy_recv.shape[0]
         if n_pairs:
             g = ops.ffn_bwd(dy_recv, x_recv, w1l, w2l, w3l, ctx["w_l"], ctx["disp_l"], ctx["a_l"], ctx["b_l"],

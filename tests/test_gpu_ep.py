@@ -37,14 +37,18 @@ def _inputs(P, routing="balanced"):
     return W, [(X["x"], X["dy"]) for X in XS]
 
 
-def _worker(rank, P, port, q, routing):
+def _worker(rank, P, port, q, routing, backend="gloo"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
-    dist.init_process_group("gloo", rank=rank, world_size=P)
+    dev = torch.device("cuda", 0)
+    if backend == "nccl":  # one rank: real NCCL all-to-all and the side-stream overlap of C4b / C5
+        dist.init_process_group("nccl", rank=rank, world_size=P, device_id=dev)
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=P)
     from paper_2601_05296_b200.ep import ExpertParallelMoE
     W, XS = _inputs(P, routing)
-    dev = torch.device("cuda", 0)
-    ep = ExpertParallelMoE(CFG["E"], CFG["k"], False, a2a=staged_a2a)
+    ep = ExpertParallelMoE(CFG["E"], CFG["k"], False, a2a=staged_a2a if backend == "gloo" else None)
+    assert ep._use_streams(XS[rank][0].to(dev)) == (backend == "nccl")
     lo, hi = ep.local_experts
     x, dy = (t.to(dev) for t in XS[rank])
     wl = [W[n][lo:hi].contiguous().to(dev) for n in ("w1", "w2", "w3")]
@@ -65,13 +69,16 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("P,routing", [(1, "balanced"), (2, "balanced"), (2, "degenerate")])
-def test_ep_cuda_matches_single_gpu(P, routing):
-    """degenerate routing: every token picks experts 0,1, so rank 1 receives no rows."""
+@pytest.mark.parametrize("P,routing,backend", [(1, "balanced", "gloo"), (2, "balanced", "gloo"),
+                                               (2, "degenerate", "gloo"), (1, "balanced", "nccl"),
+                                               (1, "skewed", "nccl")])
+def test_ep_cuda_matches_single_gpu(P, routing, backend):
+    """degenerate routing: every token picks experts 0,1, so rank 1 receives no rows.
+    nccl (P = 1): the product path, with C4b / C5 on the side stream."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, P, port, q, routing)) for r in range(P)]
+    procs = [ctx.Process(target=_worker, args=(r, P, port, q, routing, backend)) for r in range(P)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=300) for _ in range(P)], key=lambda t: t[0])
