@@ -16,11 +16,12 @@ moe_status launch_route(const moe_problem*, const void*, const void*, float*, in
 moe_status launch_dispatch(const moe_problem*, const int32_t*, const moe_dispatch*, int32_t*, int32_t*, cudaStream_t);
 size_t dispatch_ws_bytes(const moe_problem*);
 moe_status launch_dg_reduce(const float*, int, const int32_t*, int64_t, float*, cudaStream_t);
-int dwg_chunks(int64_t T, int d, int E);
+int dwg_chunks(const moe_problem* p);
 moe_status launch_router_bwd(const moe_problem*, const float*, const int32_t*, const float*, const void*, float*,
-                             float*, void*, cudaStream_t);
-moe_status launch_finalize(const moe_problem*, const void*, const float*, const void*, void*, cudaStream_t, bool,
-                           const int32_t*);
+                             __nv_bfloat16*, float*, void*, cudaStream_t);
+moe_status launch_finalize(const moe_problem*, const void*, const float*, const __nv_bfloat16*, const void*, void*,
+                           cudaStream_t, bool, const int32_t*);
+int router_ep8(int E);
 moe_status launch_ep_dest(const int32_t*, int64_t, int, int, int, int32_t*, cudaStream_t);
 moe_status launch_ep_send_meta(const int32_t*, const float*, int, int, int, const int32_t*, int64_t, int32_t*, float*,
                                cudaStream_t);
@@ -86,18 +87,24 @@ static FwdWs fwd_layout(const moe_problem* p, void* base) {
   return w;
 }
 
-struct RouterWs { float* dlogits; float* dwgpart; size_t total; };
+// dl hi/lo split (bf16 runs): [2, T, ep8] bf16, the router tensor-core operands
+static size_t dlhl_bytes(const moe_problem* p) {
+  return p->dtype == MOE_BF16 ? align256((size_t)2 * p->T * router_ep8(p->E) * 2) : 0;
+}
+
+struct RouterWs { float* dlogits; __nv_bfloat16* dlhl; float* dwgpart; size_t total; };
 static RouterWs router_layout(const moe_problem* p, void* base) {
   char* b = (char*)base;
   size_t o = 0;
   RouterWs w;
   w.dlogits = (float*)(b + o); o += align256((size_t)p->T * p->E * 4);
-  w.dwgpart = (float*)(b + o); o += align256((size_t)dwg_chunks(p->T, p->d, p->E) * p->E * p->d * 4);
+  w.dlhl = (__nv_bfloat16*)(b + o); o += dlhl_bytes(p);
+  w.dwgpart = (float*)(b + o); o += align256((size_t)dwg_chunks(p) * p->E * p->d * 4);
   w.total = o;
   return w;
 }
 
-struct BwdWs { void* wu; float* dxacc; float* dgpart; float* dlogits; float* dwgpart; float* dg; void* a; void* b; size_t total; };
+struct BwdWs { void* wu; float* dxacc; float* dgpart; float* dlogits; __nv_bfloat16* dlhl; float* dwgpart; float* dg; void* a; void* b; size_t total; };
 static BwdWs bwd_layout(const moe_problem* p, void* base) {
   const int64_t R = routed_rows(p);
   char* b = (char*)base;
@@ -107,7 +114,8 @@ static BwdWs bwd_layout(const moe_problem* p, void* base) {
   w.dxacc = (float*)(b + o); o += align256((size_t)acc_rows(p, out_mode(p, true)) * p->d * 4);  // router or not
   w.dgpart = (float*)(b + o); o += align256((size_t)R * dg_parts(p) * 4);
   w.dlogits = (float*)(b + o); o += align256((size_t)p->T * p->E * 4);
-  w.dwgpart = (float*)(b + o); o += align256((size_t)dwg_chunks(p->T, p->d, p->E) * p->E * p->d * 4);
+  w.dlhl = (__nv_bfloat16*)(b + o); o += dlhl_bytes(p);
+  w.dwgpart = (float*)(b + o); o += align256((size_t)dwg_chunks(p) * p->E * p->d * 4);
   w.dg = (float*)(b + o); o += align256((size_t)p->T * p->k * 4);
   w.a = w.b = nullptr;
   if (p->checkpoint == MOE_CKPT_NONE) {  // recomputed pre-activations
@@ -214,7 +222,8 @@ moe_status moe_ffn_fwd(const moe_problem* p, const void* x, const void* w1, cons
   c.which = GEMM_FWD_DOWN;
   if ((s = run_gemm(c, st)) != MOE_OK) return s;
   if (mode == OUT_TOKN) return MOE_OK;
-  return launch_finalize(p, w.yacc, nullptr, nullptr, y, st, false, mode == OUT_ROWS ? disp->token_index_map : nullptr);
+  return launch_finalize(p, w.yacc, nullptr, nullptr, nullptr, y, st, false,
+                         mode == OUT_ROWS ? disp->token_index_map : nullptr);
 }
 
 moe_status moe_ffn_bwd(const moe_problem* p, const void* dy, const void* x, const void* w1, const void* w2,
@@ -269,12 +278,12 @@ moe_status moe_ffn_bwd(const moe_problem* p, const void* dy, const void* x, cons
     if (mode != OUT_TOKN) {  // (k = 1 without router: dx already written by the dX GEMM)
       const float* dl = nullptr;
       if (router) {
-        if ((s = launch_router_bwd(p, router->logits, router->topk_ids, dg, x, w.dlogits, w.dwgpart, router->dw_gate,
-                                   st)) != MOE_OK)
+        if ((s = launch_router_bwd(p, router->logits, router->topk_ids, dg, x, w.dlogits, w.dlhl, w.dwgpart,
+                                   router->dw_gate, st)) != MOE_OK)
           return s;
         dl = w.dlogits;
       }
-      if ((s = launch_finalize(p, w.dxacc, dl, router ? router->w_gate : nullptr, dx, st, false,
+      if ((s = launch_finalize(p, w.dxacc, dl, w.dlhl, router ? router->w_gate : nullptr, dx, st, false,
                                mode == OUT_ROWS ? disp->token_index_map : nullptr)) != MOE_OK)
         return s;
     }
@@ -305,10 +314,10 @@ moe_status moe_router_backward(const moe_problem* p, const float* d_topk_w, cons
     MOE_CUDA_CHECK(cudaMemsetAsync(router->dw_gate, 0, (size_t)p->E * p->d * esize(p), st));
     return MOE_OK;
   }
-  if ((s = launch_router_bwd(p, router->logits, router->topk_ids, d_topk_w, x, w.dlogits, w.dwgpart, router->dw_gate,
-                             st)) != MOE_OK)
+  if ((s = launch_router_bwd(p, router->logits, router->topk_ids, d_topk_w, x, w.dlogits, w.dlhl, w.dwgpart,
+                             router->dw_gate, st)) != MOE_OK)
     return s;
-  return launch_finalize(p, dx_partial, w.dlogits, router->w_gate, dx, st, true, nullptr);
+  return launch_finalize(p, dx_partial, w.dlogits, w.dlhl, router->w_gate, dx, st, true, nullptr);
 }
 
 moe_status moe_ep_dest(const moe_problem* p, const int32_t* topk_ids, int32_t experts_per_rank, int32_t n_ranks,

@@ -26,9 +26,11 @@ __global__ void dg_reduce_kernel(const float* __restrict__ part, int nparts, con
 }
 
 // one warp per token
+// dlhl != NULL (bf16 runs): also dl = hi + lo as two bf16 [T, ep8] tensors (zero
+// columns E..ep8-1), the tensor-core operands of router_tc.cu
 __global__ void router_bwd_kernel(const float* __restrict__ logits, const int32_t* __restrict__ ids,
                                   const float* __restrict__ dg, int64_t T, int E, int k, int renorm,
-                                  float* __restrict__ dlogits) {
+                                  float* __restrict__ dlogits, __nv_bfloat16* __restrict__ dlhl, int ep8) {
   const int lane = threadIdx.x & 31;
   const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (t >= T) return;
@@ -58,8 +60,19 @@ __global__ void router_bwd_kernel(const float* __restrict__ logits, const int32_
     for (int j = 0; j < k; ++j)
       if (ids[t * k + j] == e) dp = renorm ? (dg[t * k + j] - dgw) / psum : dg[t * k + j];
     float p = expf(l[e] - m) * inv;
-    dlogits[t * E + e] = p * (dp - pdp);
+    const float v = p * (dp - pdp);
+    dlogits[t * E + e] = v;
+    if (dlhl) {
+      const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+      dlhl[t * ep8 + e] = hi;
+      dlhl[(T + t) * ep8 + e] = __float2bfloat16_rn(v - __bfloat162float(hi));
+    }
   }
+  if (dlhl)
+    for (int e = E + lane; e < ep8; e += 32) {
+      dlhl[t * ep8 + e] = __float2bfloat16_rn(0.f);
+      dlhl[(T + t) * ep8 + e] = __float2bfloat16_rn(0.f);
+    }
 }
 
 // 8 consecutive elements of a row as fp32 (16-byte load for bf16, 2 x 16 for fp32)
@@ -405,7 +418,20 @@ static int dwg_egr(int E) {
   return g <= 1 ? 1 : (g <= 2 ? 2 : (g <= 4 ? 4 : 8));
 }
 
-int dwg_chunks(int64_t T, int d, int E) {
+int router_dwg_tc_splits(int64_t T, int d);
+int router_ep8(int E);
+moe_status launch_router_dwg_tc(const __nv_bfloat16* dlhl, const void* x, int64_t T, int d, int E, float* part,
+                                cudaStream_t st);
+moe_status launch_router_dx_tc(bool load, const void* acc, bool acc_is_dtype, const int32_t* tim, int k,
+                               const __nv_bfloat16* dlhl, const void* wg, int64_t T, int d, int E, void* out,
+                               cudaStream_t st);
+
+// token chunks of the dW_g partial sums: bf16 runs use the tensor-core split
+// (router_tc.cu); fp32 runs the CUDA-core kernel below
+int dwg_chunks(const moe_problem* p) {
+  const int64_t T = p->T;
+  const int d = p->d, E = p->E;
+  if (p->dtype == MOE_BF16) return router_dwg_tc_splits(T, d);
   // column blocks x token chunks >= ~3 waves of 148 SMs, >= 64 tokens per chunk
   const int64_t colb = ceil_div(d, 8 * (256 / dwg_egr(E)));
   int64_t nch = ceil_div(3 * 148, colb);
@@ -425,19 +451,23 @@ static void launch_dwg_partial(const float* dl, const T* x, int64_t Tn, int d, i
   else MOE_LAUNCH((dwg_partial_kernel<T, 8>), grid, 256, 0, st, dl, x, Tn, d, E, tch, part);
 }
 
+// dlhl: bf16 runs, [2, T, router_ep8(E)] hi / lo split of dlogits (written here)
 moe_status launch_router_bwd(const moe_problem* p, const float* logits, const int32_t* ids, const float* dg,
-                             const void* x, float* dlogits, float* dwg_part, void* dwg, cudaStream_t st) {
+                             const void* x, float* dlogits, __nv_bfloat16* dlhl, float* dwg_part, void* dwg,
+                             cudaStream_t st) {
   const int64_t T = p->T;
   const int E = p->E, d = p->d;
+  const bool bf = p->dtype == MOE_BF16;
   if (T > 0) {
     MOE_LAUNCH(router_bwd_kernel, (unsigned)ceil_div(T * 32, 256), 256, 0, st, logits, ids, dg, T, E, p->k,
-               p->renormalize, dlogits);
+               p->renormalize, dlogits, bf ? dlhl : nullptr, router_ep8(E));
   }
-  const int nch = dwg_chunks(T, d, E);
+  const int nch = dwg_chunks(p);
   const int64_t tch = ceil_div(std::max<int64_t>(T, 1), nch);
   const int64_t n = (int64_t)E * d;
   if (p->dtype == MOE_BF16) {
-    launch_dwg_partial<__nv_bfloat16>(dlogits, (const __nv_bfloat16*)x, T, d, E, nch, tch, dwg_part, st);
+    moe_status s = launch_router_dwg_tc(dlhl, x, T, d, E, dwg_part, st);  // tensor cores, split-T partials
+    if (s != MOE_OK) return s;
     MOE_LAUNCH(dwg_reduce_kernel<__nv_bfloat16>, (unsigned)ceil_div(n, 256), 256, 0, st, dwg_part, nch, n, (__nv_bfloat16*)dwg);
   } else {
     launch_dwg_partial<float>(dlogits, (const float*)x, T, d, E, nch, tch, dwg_part, st);
@@ -446,26 +476,20 @@ moe_status launch_router_bwd(const moe_problem* p, const float* logits, const in
   return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
 }
 
-// acc_is_dtype: the accumulator is a [T,d] tensor of the run dtype (EP path) instead of fp32
-// tim != NULL: acc is the [R,d] fp32 row-result buffer, summed per token in slot order (NEXT-4)
-moe_status launch_finalize(const moe_problem* p, const void* acc, const float* dl, const void* wg, void* out,
-                           cudaStream_t st, bool acc_is_dtype, const int32_t* tim) {
+// out = dtype(acc [+ dlogits W_g]).  acc_is_dtype: the accumulator is a [T,d]
+// tensor of the run dtype (EP path) instead of fp32; tim != NULL: acc is the
+// [R,d] fp32 row-result buffer, summed per token in slot order (NEXT-4).
+// bf16 with the router term: tensor cores (router_tc.cu) from the hi/lo split dlhl.
+moe_status launch_finalize(const moe_problem* p, const void* acc, const float* dl, const __nv_bfloat16* dlhl,
+                           const void* wg, void* out, cudaStream_t st, bool acc_is_dtype, const int32_t* tim) {
   if (p->T == 0) return MOE_OK;
   typedef __nv_bfloat16 bf;
-  if (dl) {
+  if (dl && p->dtype == MOE_BF16)
+    return launch_router_dx_tc(true, acc, acc_is_dtype, tim, p->k, dlhl, wg, p->T, p->d, p->E, out, st);
+  if (dl) {  // fp32 storage: CUDA-core FMA (true fp32)
     dim3 g2((unsigned)ceil_div(p->d, 256), (unsigned)ceil_div(p->T, 64));
-    const size_t sm2 = 0;
-    if (p->dtype == MOE_BF16) {
-      if (acc_is_dtype)
-        MOE_LAUNCH((router_dx_kernel<bf, bf>), g2, 256, sm2, st, (const bf*)acc, tim, p->k, dl, (const bf*)wg, p->T, p->d, p->E,
-                   (bf*)out);
-      else
-        MOE_LAUNCH((router_dx_kernel<bf, float>), g2, 256, sm2, st, (const float*)acc, tim, p->k, dl, (const bf*)wg, p->T, p->d,
-                   p->E, (bf*)out);
-    } else {
-      MOE_LAUNCH((router_dx_kernel<float, float>), g2, 256, sm2, st, (const float*)acc, tim, p->k, dl, (const float*)wg, p->T,
-                 p->d, p->E, (float*)out);
-    }
+    MOE_LAUNCH((router_dx_kernel<float, float>), g2, 256, 0, st, (const float*)acc, tim, p->k, dl, (const float*)wg,
+               p->T, p->d, p->E, (float*)out);
     return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
   }
   dim3 grid((unsigned)ceil_div(p->d, 256), (unsigned)ceil_div(p->T, 16));
