@@ -47,8 +47,18 @@ enum TcKind { TC_FWD_UP = 0, TC_FWD_DOWN = 1, TC_BWD_DH = 2, TC_BWD_DX = 3, TC_D
 #ifndef MOEB_DH_STAGES
 #define MOEB_DH_STAGES 4  // BWD_DH mainloop stages in the CTA-pair engine (smem shared with the epilogue ring)
 #endif
+#ifndef MOEB_DH_TMA
+#define MOEB_DH_TMA 1     // BWD_DH epilogue I/O by TMA boxes (1) or per-lane cp.async / stores (0)
+#endif
 #ifndef MOEB_DH_NBUF
 #define MOEB_DH_NBUF 4    // BWD_DH epilogue ring depth (A/B chunks of 32 columns per warp)
+#endif
+// timing-only experiments (never in the product build): bit masks over TcKind
+#ifndef MOEB_EXP_NOEPI
+#define MOEB_EXP_NOEPI 0  // kinds whose epilogue is skipped (measures the mainloop alone)
+#endif
+#ifndef MOEB_EXP_NOMMA
+#define MOEB_EXP_NOMMA 0  // kinds whose MMAs are skipped (measures loads + epilogue)
 #endif
 constexpr int TBN = 256, TBK = 64;         // MMA N per tile, K block
 constexpr int TA_BYTES = 128 * TBK * 2;    // 16 KB: 128 rows of A per CTA
@@ -65,8 +75,11 @@ struct CgCfg {
   static constexpr bool DH = (KIND == 2);
   static constexpr int STAGES = DH ? (CG == 1 ? 2 : MOEB_DH_STAGES) : (CG == 1 ? 4 : 6);
   static constexpr int DH_NBUF = MOEB_DH_NBUF;          // BWD_DH: ring of A/B input chunks per warp
-  static constexpr int STG_WARP = DH ? (DH_NBUF * 4096 + 2048) : 6144;  // epilogue staging bytes per warp
-  static constexpr int STG_OFF = STAGES * STAGE + 1024 /*barriers*/ + 2176 /*offsets, tile starts*/;
+  // epilogue staging bytes per warp (BWD_DH: the A/B ring + two wU tiles)
+  static constexpr int STG_WARP = DH ? (DH_NBUF * 4096 + 4096) : 6144;
+  // 1024-aligned: the BWD_DH tiles are TMA boxes in the 64-byte swizzle, whose pattern is
+  // taken from the smem address bits
+  static constexpr int STG_OFF = (STAGES * STAGE + 1024 /*barriers*/ + 2176 /*offsets, tile starts*/ + 1023) / 1024 * 1024;
   static constexpr int SMEM = STG_OFF + 4 * STG_WARP + 1024 /*align*/;
 };
 
@@ -139,8 +152,17 @@ __device__ __forceinline__ bool decode_tile(int tile, const TcParams& P, const i
     if (tile >= P.E * per_e) return false;
     t.e = tile / per_e;
     const int rem = tile - t.e * per_e;
-    const int mt = rem / P.n_tiles;
-    t.n_tile = rem - mt * P.n_tiles;
+    int mt;
+    if constexpr (KIND == TC_DW3) {
+      // m fastest: the concurrent tiles share the B n-tile (wU rows, h wide: the
+      // larger operand) and re-read the small gathered dY from L2
+      t.n_tile = rem / P.m_tiles;
+      mt = rem - t.n_tile * P.m_tiles;
+    } else {
+      // n fastest: DW12's A ([dA|dB], 2h wide) is the larger operand
+      mt = rem / P.n_tiles;
+      t.n_tile = rem - mt * P.n_tiles;
+    }
     t.m0 = mt * TM;
     t.n0 = t.n_tile * TBN;
     t.seg0 = s_offs[t.e];
@@ -153,25 +175,33 @@ __device__ __forceinline__ bool decode_tile(int tile, const TcParams& P, const i
     t.seg1 = s_offs[t.e + 1];
     const int mt_e = (t.seg1 - t.seg0 + TM - 1) / TM;
     const int local = tile - s_tstart[t.e];
-    // grouped rasterisation: blocks of RG m-tiles x all n-tiles, m fastest, so
-    // a block's gathered rows (RG*TM rows) stay L2-resident while the weight
-    // tiles stream once per block (large segments would otherwise re-stream
-    // their rows from HBM for every n-tile)
+    // grouped rasterisation: blocks of ~RG m-tiles x all n-tiles, m fastest, so
+    // a block's rows stay L2-resident while the weight tiles stream once per
+    // block.  The segment's m-tiles are split into ng = max(1, mt_e / RG) groups
+    // of near-equal size (sizes differ by at most one, the larger first): a
+    // remainder never forms a small group of its own, which would re-stream the
+    // expert's whole weight for a handful of rows (9 m-tiles = one group of 9,
+    // not 8 + 1)
     constexpr int RG = 8;
-    const int nfull = mt_e / RG;
-    const int big = nfull * RG * P.n_tiles;
-    int mi;
+    const int nt = P.n_tiles;
+    const int ng = max(1, mt_e / RG);
+    const int gsz = mt_e / ng, extra = mt_e - gsz * ng;  // `extra` groups have gsz + 1 m-tiles
+    const int big = extra * (gsz + 1) * nt;
+    int sz, mstart, within;
     if (local < big) {
-      const int g = local / (RG * P.n_tiles);
-      const int rem = local - g * RG * P.n_tiles;
-      t.n_tile = rem / RG;
-      mi = g * RG + (rem - t.n_tile * RG);
+      sz = gsz + 1;
+      const int g = local / (sz * nt);
+      within = local - g * sz * nt;
+      mstart = g * sz;
     } else {
-      const int gl = mt_e - nfull * RG;
-      const int rem = local - big;
-      t.n_tile = rem / gl;
-      mi = nfull * RG + (rem - t.n_tile * gl);
+      sz = gsz;
+      const int l2 = local - big;
+      const int g = l2 / (sz * nt);
+      within = l2 - g * sz * nt;
+      mstart = extra * (gsz + 1) + g * sz;
     }
+    t.n_tile = within / sz;
+    const int mi = mstart + (within - t.n_tile * sz);
     t.m0 = t.seg0 + mi * TM;
     t.n0 = t.n_tile * ((KIND == TC_FWD_UP && P.act == 0) ? 128 : 256);
     const int Kdim = (KIND == TC_FWD_UP || KIND == TC_BWD_DH) ? P.d
@@ -290,6 +320,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
   uint64_t* tfull = gfull + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* ebar = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE + 512);  // BWD_DH: [4 warps][DH_NBUF] TMA loads
   int* s_offs = reinterpret_cast<int*>(smem + STAGES * C::STAGE + 1024);
   int* s_tstart = s_offs + 260;
 
@@ -323,6 +354,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
       ptx::mbar_init(&tfull[s], 1);
       ptx::mbar_init(&tempty[s], 4 * CG);
     }
+    if constexpr (KIND == TC_BWD_DH && CPA && MOEB_DH_TMA)
+      for (int s = 0; s < 4 * C::DH_NBUF; ++s) ptx::mbar_init(&ebar[s], 1);
     ptx::fence_mbar_init();
     ptx::fence_proxy_async();
   }
@@ -573,8 +606,16 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
           constexpr uint32_t STEP_A = K::a_mn ? 2048u >> 4 : 32u >> 4;
           constexpr uint32_t STEP_B = K::b_mn ? 2048u >> 4 : 32u >> 4;
           const uint32_t sA = s0 + stage * C::STAGE;
-          ptx::umma_kblock<CG, STEP_A, STEP_B>(d_tmem, (sA >> 4) | LBO_A, ((sA + TA_BYTES) >> 4) | LBO_B, idesc,
-                                               kb != 0, empty0 + 8 * stage, 0x3);
+          if constexpr ((MOEB_EXP_NOMMA >> KIND) & 1) {
+            if (lane == 0) {
+              if constexpr (CG == 2) ptx::umma_commit_cg2(&empty[stage], 0x3);
+              else ptx::umma_commit(&empty[stage]);
+            }
+            __syncwarp();
+          } else {
+            ptx::umma_kblock<CG, STEP_A, STEP_B>(d_tmem, (sA >> 4) | LBO_A, ((sA + TA_BYTES) >> 4) | LBO_B, idesc,
+                                                 kb != 0, empty0 + 8 * stage, 0x3);
+          }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
         if (lane == 0) {
@@ -597,9 +638,31 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
     uint8_t* stg = smem + C::STG_OFF + wq * C::STG_WARP;  // this warp's staging tiles
     int as = 0;
     uint32_t aphase = 0;
+    uint32_t gch = 0;  // BWD_DH (TMA epilogue): this warp's running chunk count (ring slot / parity)
+    constexpr int DH_PF = C::DH_NBUF - 2;  // chunks loaded ahead (slot reuse distance 2: wait_read<1>)
+    // BWD_DH epilogue TMA: 32 x 32 bf16 boxes (64-byte swizzle = the stg16_off layout) of
+    // A (mA0), B (mA1) loaded and dA, dB, wU (mB1) stored by lane 0
+    auto dh_load = [&](uint32_t g, int col, int row0) {
+      const int slot = (int)(g % C::DH_NBUF);
+      uint64_t* bar = &ebar[wq * C::DH_NBUF + slot];
+      uint8_t* NA = stg + slot * 4096;
+      ptx::mbar_arrive_expect_tx(bar, P.act == 0 ? 4096u : 2048u);
+      ptx::tma_load_2d(NA, &mA0, bar, col, row0);
+      if (P.act == 0) ptx::tma_load_2d(NA + 2048, &mA1, bar, col, row0);
+    };
     TileInfo t;
     for (int tile = cluster_id; decode_tile<KIND, CG>(tile, P, s_offs, s_tstart, t); tile += n_clusters) {
-      if constexpr (KIND == TC_BWD_DH) {
+      if constexpr (KIND == TC_BWD_DH && CPA && MOEB_DH_TMA) {
+        // the epilogue inputs (A, B rows of this tile) do not depend on the
+        // accumulator: start their TMA loads before waiting for it
+        const int r0w = t.m0 + rowoff + wq * 32;
+        const int nchunk = min(TBN, P.h - t.n0) / 32;
+        if (lane == 0) {
+          ptx::bulk_wait_read<1>();
+          for (int ci = 0; ci < DH_PF && ci < nchunk; ++ci) dh_load(gch + ci, t.n0 + 32 * ci, r0w);
+        }
+        __syncwarp();
+      } else if constexpr (KIND == TC_BWD_DH) {
         // the epilogue inputs (A, B rows of this tile) do not depend on the
         // accumulator: start streaming the first chunks before waiting for it
         const int r0w = t.m0 + rowoff + wq * 32;
@@ -620,7 +683,15 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
       ptx::tc_fence_after();
       const uint32_t tb = tmem_base + ((uint32_t)(wq * 32) << 16) + as * TBN;
       uint32_t v[32];
-      if constexpr (KIND == TC_ROUTE) {
+      if constexpr ((MOEB_EXP_NOEPI >> KIND) & 1) {
+        if constexpr (KIND == TC_BWD_DH && CPA && MOEB_DH_TMA) {
+          const int nchunk = min(TBN, P.h - t.n0) / 32;
+          for (int ci = 0; ci < DH_PF && ci < nchunk; ++ci, ++gch)
+            ptx::mbar_wait(&ebar[wq * C::DH_NBUF + (int)(gch % C::DH_NBUF)], (gch / C::DH_NBUF) & 1);
+        } else if constexpr (KIND == TC_BWD_DH) {
+          asm volatile("cp.async.wait_all;" ::: "memory");
+        }
+      } else if constexpr (KIND == TC_ROUTE) {
         // one token row per thread: logits out, softmax, top-k (desc, ties -> lower id)
         const int r = t.m0 + row;
         const bool valid = r < P.T;
@@ -789,6 +860,101 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
           }
           __syncwarp();
         }
+      } else if constexpr (KIND == TC_BWD_DH && CPA && MOEB_DH_TMA) {
+        // A, B chunks of 32 columns arrive by TMA in a ring of DH_NBUF slots (A at +0,
+        // B at +2048 of each 4 KB slot; DH_PF chunks ahead, the first ones issued before
+        // the accumulator was ready); dA, dB overwrite the consumed slot, wU goes to one
+        // of two tiles, and lane 0 stores the three 32 x 32 boxes by TMA (rows past the
+        // segment belong to the next expert: a partial row group is stored by hand).
+        const int r = t.m0 + row;
+        const bool valid = r < t.seg1;
+        const int r0w = t.m0 + rowoff + wq * 32;
+        const int nvalid = max(0, min(32, t.seg1 - r0w));
+        const float w = valid ? P.topw[P.row_slot[r]] : 0.f;
+        constexpr int NBUF = C::DH_NBUF;
+        const int nchunk = min(TBN, P.h - t.n0) / 32;
+        const int64_t o0 = (int64_t)r0w * P.h + t.n0;
+        float rowsum = 0.f;
+        if (nchunk > 0) ptx::tmem_ld32(tb, v);
+#pragma unroll 1
+        for (int ci = 0; ci < nchunk; ++ci, ++gch) {
+          const int slot = (int)(gch % NBUF);
+          uint8_t* TA = stg + slot * 4096;
+          uint8_t* TB = TA + 2048;
+          uint8_t* TU = stg + NBUF * 4096 + (gch & 1) * 2048;
+          if (lane == 0) {
+            ptx::bulk_wait_read<1>();  // chunk gch-2's stores have read their slot and wU tile
+            if (ci + DH_PF < nchunk) dh_load(gch + DH_PF, t.n0 + 32 * (ci + DH_PF), r0w);
+          }
+          __syncwarp();
+          ptx::mbar_wait(&ebar[wq * NBUF + slot], (gch / NBUF) & 1);
+          // accumulator chunk ci was loaded (asynchronously) one iteration ago
+          ptx::tmem_wait_ld();
+          uint32_t dh[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) dh[i] = v[i];
+          if (ci + 1 < nchunk) ptx::tmem_ld32(tb + (ci + 1) * 32, v);  // overlap the next TMEM read
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint4 ua = *reinterpret_cast<const uint4*>(TA + stg16_off(lane, q));
+            const uint4 ub = *reinterpret_cast<const uint4*>(TB + stg16_off(lane, q));
+            const uint32_t* pa = reinterpret_cast<const uint32_t*>(&ua);
+            const uint32_t* pb = reinterpret_cast<const uint32_t*>(&ub);
+            uint32_t oa[4], ob[4], ou[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 a2 = ptx::unpack_bf16(pa[e]);
+              const float2 b2 = ptx::unpack_bf16(pb[e]);
+              float ra[2], rb[2], ru[2];
+              const float av[2] = {a2.x, a2.y}, bvv[2] = {b2.x, b2.y};
+#pragma unroll
+              for (int z = 0; z < 2; ++z) {
+                const float dH = __uint_as_float(dh[q * 8 + e * 2 + z]);
+                const float a = av[z], b = bvv[z];
+                const float sg = sigmoid_fast(a);
+                const float dU = w * dH;
+                if (P.act == 0) {
+                  const float S = a * sg;
+                  const float U = S * b;
+                  rowsum = fmaf(dH, U, rowsum);
+                  ra[z] = dU * b * sg * (1.f + a * (1.f - sg));
+                  rb[z] = dU * S;
+                  ru[z] = w * U;
+                } else {  // non-gated: U = sigma(A), dA = dU sigma'(A)
+                  const float U = act_fwd(P.act, a, sg);
+                  rowsum = fmaf(dH, U, rowsum);
+                  ra[z] = dU * act_grad(P.act, a, sg);
+                  rb[z] = 0.f;
+                  ru[z] = w * U;
+                }
+              }
+              oa[e] = ptx::pack_bf16(ra[0], ra[1]);
+              ob[e] = ptx::pack_bf16(rb[0], rb[1]);
+              ou[e] = ptx::pack_bf16(ru[0], ru[1]);
+            }
+            *reinterpret_cast<uint4*>(TA + stg16_off(lane, q)) = make_uint4(oa[0], oa[1], oa[2], oa[3]);
+            *reinterpret_cast<uint4*>(TB + stg16_off(lane, q)) = make_uint4(ob[0], ob[1], ob[2], ob[3]);
+            *reinterpret_cast<uint4*>(TU + stg16_off(lane, q)) = make_uint4(ou[0], ou[1], ou[2], ou[3]);
+          }
+          ptx::fence_proxy_async();  // generic smem writes -> visible to the TMA stores
+          __syncwarp();
+          if (nvalid == 32) {
+            if (lane == 0) {
+              const int col = t.n0 + 32 * ci;
+              ptx::tma_store_2d(&mA0, TA, col, r0w);
+              if (P.act == 0) ptx::tma_store_2d(&mA1, TB, col, r0w);
+              ptx::tma_store_2d(&mB1, TU, col, r0w);
+            }
+          } else if (nvalid > 0) {
+            const int64_t o = o0 + ci * 32;
+            stg_store_bf16(TA, lane, P.a_save + o, P.h, nvalid);
+            if (P.act == 0) stg_store_bf16(TB, lane, P.b_save + o, P.h, nvalid);
+            stg_store_bf16(TU, lane, P.u + o, P.h, nvalid);
+          }
+          if (lane == 0) ptx::bulk_commit();  // one (possibly empty) group per chunk
+          __syncwarp();
+        }
+        if (valid) P.dg_part[(int64_t)r * P.dg_parts + t.n_tile] = rowsum;
       } else if constexpr (KIND == TC_BWD_DH) {
         // A, B chunks of 32 columns stream through a ring of DH_NBUF cp.async
         // staging buffers (A at +0, B at +2048 of each 4 KB slot; the first
@@ -920,6 +1086,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
       }
       if (++as == 2) { as = 0; aphase ^= 1; }
     }
+    if constexpr (KIND == TC_BWD_DH && CPA && MOEB_DH_TMA)
+      if (lane == 0) ptx::bulk_wait<0>();  // the epilogue's TMA stores are complete
   }
   ptx::tc_fence_before();
   if constexpr (CG == 2) ptx::cluster_sync();
@@ -955,6 +1123,21 @@ static bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t c
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// 2D bf16 row-major [rows, cols] map with a 32 x 32 box, 64-byte swizzle (the
+// epilogue staging layout stg16_off)
+static bool make_map_sw64(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -1085,11 +1268,19 @@ moe_status tc_gemm(const GemmCall& c, cudaStream_t st) {
     }
     case GEMM_BWD_DH: {
       if (R == 0) return MOE_OK;
-      ok &= make_map(&a0, c.dy, T, d, 64, 1);
       ok &= make_map(&b0, c.w3, (uint64_t)E * d, h, 64, 64);
+      if (engine() == ENG_TMA || !MOEB_DH_TMA) {  // dY rows by TMA gather4; cp.async epilogue
+        ok &= make_map(&a0, c.dy, T, d, 64, 1);
+        a1 = a0;
+        b1 = b0;
+      } else {  // epilogue TMA boxes: A (a0), B (a1) in, dA, dB, wU (b1) out
+        ok &= make_map_sw64(&a0, c.a_save, R, h);
+        ok &= make_map_sw64(&a1, gated ? c.b_save : c.a_save, R, h);
+        ok &= make_map_sw64(&b1, c.u, R, h);
+      }
       if (!ok) return MOE_ERR_CUDA;
       P.n_tiles = (int)ceil_div(h, TBN);
-      return launch_tc<TC_BWD_DH>(a0, a0, b0, b0, P, rows_tiles(P.n_tiles), st);
+      return launch_tc<TC_BWD_DH>(a0, a1, b0, b1, P, rows_tiles(P.n_tiles), st);
     }
     case GEMM_BWD_DX: {
       if (R == 0) return MOE_OK;
