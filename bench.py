@@ -77,9 +77,11 @@ class ClockSampler:
         for ln in self.proc.stdout:
             parts = [s.strip() for s in ln.split(",")]
             if len(parts) >= 9:
-                self.rows.append(parts)
+                self.rows.append([time.time()] + parts)
 
-    def stop(self):
+    def stop(self, window=None):
+        """window = (t0, t1) wall times of the timed region: only samples taken
+        inside it count (the sampler also runs in the idle margins around it)."""
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         time.sleep(0.25)
@@ -88,14 +90,17 @@ class ClockSampler:
             self.proc.wait(timeout=2)
         except Exception:
             self.proc.kill()
-        rows = self.rows
+        rows = [r[1:] for r in self.rows if window is None or window[0] <= r[0] <= window[1]]
+        in_window = window is not None and bool(rows)
+        if not rows:
+            rows = [r[1:] for r in self.rows]
         sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
         loaded = [s for s in sm if mx and s > 0.5 * max(mx)] or sm
         return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows),
+                "reasons": reasons, "samples": len(rows), "samples_in_timed_region": in_window,
                 "power_w_max": max((float(r[3]) for r in rows if r[3].replace(".", "").isdigit()), default=None)}
 
 
@@ -149,7 +154,7 @@ def host_f64(inp):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="mixtral")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -251,18 +256,20 @@ def main():
     if use_ep:
         dist.barrier()
     torch.cuda.synchronize()
+    wall0 = time.time()
     ev0.record(st)
     for _ in range(args.steps):
         step()
     ev1.record(st)
     torch.cuda.synchronize()
+    wall1 = time.time()
     if use_ep:
         dist.barrier()
     L.profile_enable(False)
     launches = L.launch_count() - launches0
     ms = ev0.elapsed_time(ev1)
     prof = L.profile_read()
-    clk = clocks.stop()
+    clk = clocks.stop((wall0, wall1))
     if use_ep:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
