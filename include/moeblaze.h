@@ -269,6 +269,19 @@ moe_status moe_profile_enable(int32_t on);
 moe_status moe_profile_reset(void);
 moe_status moe_profile_read(int32_t kind, double* total_ms, int64_t* launches);
 
+/* SM topology used by the expert GEMMs' tile scheduler (not a step of the
+ * method; a B200 placement detail).  A B200 is two dies whose
+ * L2s each cache lines of both dies' HBM, so CTAs on different dies reading
+ * the same operand tile fetch it twice.  The library measures once per device
+ * which die each SM is on (DRAM latency classes of cold lines, topology.cu)
+ * and splits every expert's n-tiles between the dies.  die_of_sm[s] (host
+ * array of max_sm entries) receives 0 or 1 for SM id s, -1 for an SM the
+ * probe did not reach; n_per_die[0..1] the SM counts (n_per_die[1] == 0: no
+ * split, e.g. MOEBLAZE_DIE=0 or an ambiguous measurement).  Results of every
+ * call are independent of this map.  Runs the probe on first use (about a
+ * millisecond, synchronous); MOE_ERR_INVALID_ARG on null pointers. */
+moe_status moe_sm_topology(int32_t* die_of_sm, int32_t max_sm, int32_t* n_per_die);
+
 /* Human-readable status. */
 const char* moe_status_string(moe_status s);
 

@@ -24,7 +24,7 @@ MOE_OP_ROUTE, MOE_OP_DISPATCH, MOE_OP_FFN_FWD, MOE_OP_FFN_BWD, MOE_OP_ROUTER_BWD
 EXPORTS = ("moe_workspace_size", "moe_route", "moe_dispatch_build", "moe_ffn_fwd", "moe_ffn_bwd",
            "moe_gather_rows", "moe_combine_rows", "moe_status_string", "moe_launch_count", "moe_version",
            "moe_profile_enable", "moe_profile_reset", "moe_profile_read", "moe_router_backward", "moe_ep_dest",
-           "moe_ep_send_meta", "moe_ep_slot_grad")
+           "moe_ep_send_meta", "moe_ep_slot_grad", "moe_sm_topology")
 GEMM_KINDS = ("FWD_UP", "FWD_DOWN", "BWD_DH", "BWD_DX", "DW3", "DW12")
 
 
@@ -79,6 +79,8 @@ def load():
     lib.moe_ep_dest.argtypes = [P(MoeProblem), V, I32, I32, V, V]
     lib.moe_ep_send_meta.argtypes = [P(MoeProblem), V, V, I32, I32, V, I64, V, V, V]
     lib.moe_ep_slot_grad.argtypes = [P(MoeProblem), V, I32, I32, V, V, V, V]
+    lib.moe_sm_topology.argtypes = [P(I32), I32, P(I32)]
+    lib.moe_sm_topology.restype = I32
     for fn in ("moe_workspace_size", "moe_route", "moe_dispatch_build", "moe_ffn_fwd", "moe_ffn_bwd",
                "moe_gather_rows", "moe_combine_rows", "moe_router_backward", "moe_ep_dest", "moe_ep_send_meta",
                "moe_ep_slot_grad"):
@@ -94,6 +96,16 @@ def load():
         getattr(lib, fn).restype = I32
     _lib = lib
     return lib
+
+
+def sm_topology(max_sm=256):
+    """(die of each SM id (-1 = not reached), SMs per die) as measured by the
+    library for the expert GEMMs' tile scheduler (moe_sm_topology)."""
+    lib = load()
+    dies = (ctypes.c_int32 * max_sm)()
+    n = (ctypes.c_int32 * 2)()
+    _check(lib.moe_sm_topology(dies, max_sm, n), "moe_sm_topology")
+    return list(dies), [n[0], n[1]]
 
 
 def _check(status, what):

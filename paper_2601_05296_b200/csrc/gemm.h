@@ -39,6 +39,9 @@ __device__ __forceinline__ float act_grad(int act, float a, float sg) {
 }
 
 moe_status run_gemm(const GemmCall& c, cudaStream_t st);
+// die of every SM of the current device, measured once (topology.cu); device
+// array indexed by %smid, n_sm = SMs per die (n_sm[1] == 0: no split)
+const uint8_t* sm_die_map(int n_sm[2]);
 int gemm_dg_parts(const GemmCall& c);  // dg partial columns per row written by BWD_DH
 
 }  // namespace moeb

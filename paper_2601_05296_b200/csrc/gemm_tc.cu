@@ -35,7 +35,9 @@
 // gradient GEMMs on chip only (no padded buffer exists in HBM).
 #include <cudaTypedefs.h>
 
+#include <climits>
 #include <cstdlib>
+#include <mutex>
 
 #include "gemm.h"
 #include "ptx.cuh"
@@ -52,6 +54,9 @@ enum TcKind { TC_FWD_UP = 0, TC_FWD_DOWN = 1, TC_BWD_DH = 2, TC_BWD_DX = 3, TC_D
 #endif
 #ifndef MOEB_DH_NBUF
 #define MOEB_DH_NBUF 4    // BWD_DH epilogue ring depth (A/B chunks of 32 columns per warp)
+#endif
+#ifndef MOEB_DYN
+#define MOEB_DYN 1        // row-kind tiles from the die-aware dynamic scheduler (0: static cluster-strided order)
 #endif
 // timing-only experiments (never in the product build): bit masks over TcKind
 #ifndef MOEB_EXP_NOEPI
@@ -109,7 +114,23 @@ struct TcParams {
   int act;  // MOE_ACT_*: 0 SwiGLU (gated: stacked [W1;W2], A and B); 1 SiLU / 2 ReLU (non-gated)
   int out_mode;                  // FWD_DOWN / BWD_DX target (gemm.h OutMode)
   __nv_bfloat16* out_tok;        // OUT_TOKN destination [T, d]
+  // die-aware dynamic tile scheduler (row kinds, CTA pair): every expert's n-tiles
+  // [0, n_split) form die 0's tile list, [n_split, n_tiles) die 1's; sched[0..1]
+  // are the lists' claim counters (zeroed before the launch), die_map[smid] the
+  // SM's die (topology.cu)
+  int* sched;
+  const uint8_t* die_map;
+  int n_split;
 };
+
+template <int KIND>
+struct KindTraits;
+// row kinds in the CTA-pair engine take their tiles from the dynamic scheduler
+template <int KIND, int CG>
+__host__ __device__ constexpr bool dyn_sched() {
+  return MOEB_DYN && CG == 2 && KIND != TC_ROUTE && KIND != TC_DW3 && KIND != TC_DW12;
+}
+constexpr int SCHED_RING = 4;  // tiles published ahead by the scheduler
 
 template <int KIND>
 struct KindTraits {
@@ -134,10 +155,11 @@ struct TileInfo {
 };
 
 template <int KIND, int CG>
-__device__ __forceinline__ bool decode_tile(int tile, const TcParams& P, const int* s_offs, const int* s_tstart,
+__device__ __forceinline__ bool decode_tile(int tile, const TcParams& P, const int* s_offs, const int* s_mstart,
                                             TileInfo& t) {
   using K = KindTraits<KIND>;
   constexpr int TM = CgCfg<CG>::TM;
+  if (tile < 0) return false;
   if constexpr (KIND == TC_ROUTE) {
     if (tile * TM >= P.T) return false;
     t.e = 0;
@@ -169,21 +191,34 @@ __device__ __forceinline__ bool decode_tile(int tile, const TcParams& P, const i
     t.seg1 = s_offs[t.e + 1];
     t.nk = (t.seg1 - t.seg0 + TBK - 1) / TBK;
   } else {
-    if (tile >= s_tstart[P.E]) return false;
-    t.e = find_segment(s_tstart, P.E, tile);
+    // tile lists: die 0 = every expert's n-tiles [0, ns), die 1 = [ns, n_tiles)
+    // (one list, ns = n_tiles, in the static schedule); s_mstart = prefix sum
+    // of the experts' m-tile counts
+    const int ns = dyn_sched<KIND, CG>() ? P.n_split : P.n_tiles;
+    const int Mt = s_mstart[P.E];
+    int nt, nlo, local = tile;
+    if (tile < Mt * ns) {
+      nt = ns;
+      nlo = 0;
+    } else {
+      nt = P.n_tiles - ns;
+      nlo = ns;
+      local = tile - Mt * ns;
+      if (local >= Mt * nt) return false;
+    }
+    t.e = find_segment(s_mstart, P.E, local / nt);
     t.seg0 = s_offs[t.e];
     t.seg1 = s_offs[t.e + 1];
-    const int mt_e = (t.seg1 - t.seg0 + TM - 1) / TM;
-    const int local = tile - s_tstart[t.e];
-    // grouped rasterisation: blocks of ~RG m-tiles x all n-tiles, m fastest, so
-    // a block's rows stay L2-resident while the weight tiles stream once per
-    // block.  The segment's m-tiles are split into ng = max(1, mt_e / RG) groups
-    // of near-equal size (sizes differ by at most one, the larger first): a
-    // remainder never forms a small group of its own, which would re-stream the
+    const int mt_e = s_mstart[t.e + 1] - s_mstart[t.e];
+    local -= s_mstart[t.e] * nt;
+    // grouped rasterisation: blocks of ~RG m-tiles x the list's n-tiles, m
+    // fastest, so a block's rows stay L2-resident while the weight tiles stream
+    // once per block.  The segment's m-tiles are split into ng = max(1, mt_e / RG)
+    // groups of near-equal size (sizes differ by at most one, the larger first):
+    // a remainder never forms a small group of its own, which would re-stream the
     // expert's whole weight for a handful of rows (9 m-tiles = one group of 9,
     // not 8 + 1)
     constexpr int RG = 8;
-    const int nt = P.n_tiles;
     const int ng = max(1, mt_e / RG);
     const int gsz = mt_e / ng, extra = mt_e - gsz * ng;  // `extra` groups have gsz + 1 m-tiles
     const int big = extra * (gsz + 1) * nt;
@@ -200,8 +235,8 @@ __device__ __forceinline__ bool decode_tile(int tile, const TcParams& P, const i
       within = l2 - g * sz * nt;
       mstart = extra * (gsz + 1) + g * sz;
     }
-    t.n_tile = within / sz;
-    const int mi = mstart + (within - t.n_tile * sz);
+    t.n_tile = nlo + within / sz;
+    const int mi = mstart + (within - (within / sz) * sz);
     t.m0 = t.seg0 + mi * TM;
     t.n0 = t.n_tile * ((KIND == TC_FWD_UP && P.act == 0) ? 128 : 256);
     const int Kdim = (KIND == TC_FWD_UP || KIND == TC_BWD_DH) ? P.d
@@ -321,8 +356,16 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
   uint64_t* ebar = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE + 512);  // BWD_DH: [4 warps][DH_NBUF] TMA loads
+  // dynamic scheduler: tile ring (published by the leader into both CTAs) and its barriers
+  uint64_t* sfull = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE + 768);
+  uint64_t* sempty = sfull + SCHED_RING;
+  int* s_ring = reinterpret_cast<int*>(sempty + SCHED_RING);
   int* s_offs = reinterpret_cast<int*>(smem + STAGES * C::STAGE + 1024);
-  int* s_tstart = s_offs + 260;
+  int* s_mstart = s_offs + 260;
+  constexpr bool DYN = dyn_sched<KIND, CG>();
+  // arrivals that release a ring slot: every tile-iterating warp of both CTAs
+  // (TMA producer, epilogue x4, gathers x4 + relay when gathered) + the MMA warp
+  constexpr int NCONS = 2 * (1 + 4 + (K::gathered ? 5 : 0)) + 1;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int E = P.E;
@@ -356,6 +399,11 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
     }
     if constexpr (KIND == TC_BWD_DH && CPA && MOEB_DH_TMA)
       for (int s = 0; s < 4 * C::DH_NBUF; ++s) ptx::mbar_init(&ebar[s], 1);
+    if constexpr (DYN)
+      for (int s = 0; s < SCHED_RING; ++s) {
+        ptx::mbar_init(&sfull[s], 1);
+        ptx::mbar_init(&sempty[s], NCONS);
+      }
     ptx::fence_mbar_init();
     ptx::fence_proxy_async();
   }
@@ -367,10 +415,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
   if (!K::wgrad && KIND != TC_ROUTE && threadIdx.x == 0) {
     int s = 0;
     for (int e = 0; e < E; ++e) {
-      s_tstart[e] = s;
-      s += ((s_offs[e + 1] - s_offs[e] + C::TM - 1) / C::TM) * P.n_tiles;
+      s_mstart[e] = s;
+      s += (s_offs[e + 1] - s_offs[e] + C::TM - 1) / C::TM;
     }
-    s_tstart[E] = s;
+    s_mstart[E] = s;
   }
   ptx::tc_fence_before();
   if constexpr (CG == 2) ptx::cluster_sync();  // peer barriers initialised + TMEM allocated
@@ -378,13 +426,35 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
+  // i-th tile of this CTA pair: static cluster-strided order, or the dynamic
+  // scheduler's ring (every tile-iterating warp reads every slot once, then
+  // releases it on the leader; the slot value gates the arrive, so the read has
+  // completed before the scheduler may overwrite it)
+  auto fetch = [&](int it) -> int {
+    if constexpr (DYN) {
+      const int slot = it % SCHED_RING;
+      const uint32_t par = (uint32_t)(it / SCHED_RING) & 1u;
+      if (leader) ptx::mbar_wait(&sfull[slot], par);
+      else ptx::mbar_wait_cluster(&sfull[slot], par);
+      const int tile = *reinterpret_cast<volatile int*>(&s_ring[slot]);
+      __syncwarp();
+      if (lane == 0 && tile != INT_MIN) {
+        if (leader) ptx::mbar_arrive(&sempty[slot]);
+        else ptx::mbar_arrive_cluster_relaxed(ptx::mapa(ptx::smem_u32(&sempty[slot]), 0));
+      }
+      return tile;
+    } else {
+      return cluster_id + it * n_clusters;
+    }
+  };
+
   if (warp == 0) {
     // ============================ TMA producer ============================
     const int oob = P.T;  // TMA gather4 row past the end: zero-filled (CG = 1, !CPA only)
     int stage = 0;
     uint32_t phase = 0;
     TileInfo t;
-    for (int tile = cluster_id; decode_tile<KIND, CG>(tile, P, s_offs, s_tstart, t); tile += n_clusters) {
+    for (int it = 0; decode_tile<KIND, CG>(fetch(it), P, s_offs, s_mstart, t); ++it) {
       int gi0 = 0, gi1 = 0, gi2 = 0, gi3 = 0;
       if constexpr (!CPA && (KIND == TC_FWD_UP || KIND == TC_BWD_DH)) {
         const int r = t.m0 + 4 * lane;
@@ -486,7 +556,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
       TileInfo t;
       const __nv_bfloat16* src_base = (KIND == TC_FWD_UP || KIND == TC_DW12) ? P.x : P.dy;
       uint64_t* const done_bar = CG == 2 ? gfull : full;
-      for (int tile = cluster_id; decode_tile<KIND, CG>(tile, P, s_offs, s_tstart, t); tile += n_clusters) {
+      for (int it = 0; decode_tile<KIND, CG>(fetch(it), P, s_offs, s_mstart, t); ++it) {
         if constexpr (KIND == TC_FWD_UP || KIND == TC_BWD_DH) {
           // K-major A, this CTA's 128 rows x 8 chunks: chunk c = gt&7, rows (gt>>3) + 16 i
           const int c = gt & 7, rb = gt >> 3;
@@ -566,7 +636,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
       int stage = 0;
       uint32_t phase = 0;
       TileInfo t;
-      for (int tile = cluster_id; decode_tile<KIND, CG>(tile, P, s_offs, s_tstart, t); tile += n_clusters) {
+      for (int it = 0; decode_tile<KIND, CG>(fetch(it), P, s_offs, s_mstart, t); ++it) {
         for (int kb = 0; kb < t.nk; ++kb) {
           ptx::mbar_wait(&gfull[stage], phase);
           if (lane == 0) {
@@ -590,7 +660,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
       const uint32_t tb = __shfl_sync(0xffffffffu, tmem_base, 0);
       const uint32_t s0 = ptx::smem_u32(smem);
       const uint32_t empty0 = ptx::smem_u32(empty);
-      for (int tile = cluster_id; decode_tile<KIND, CG>(tile, P, s_offs, s_tstart, t); tile += n_clusters) {
+      for (int it = 0; decode_tile<KIND, CG>(fetch(it), P, s_offs, s_mstart, t); ++it) {
         if constexpr (CG == 2) ptx::mbar_wait_cluster(&tempty[as], aphase ^ 1);
         else ptx::mbar_wait(&tempty[as], aphase ^ 1);
         ptx::tc_fence_after();
@@ -631,6 +701,36 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
         if (++as == 2) { as = 0; aphase ^= 1; }
       }
     }
+  } else if (warp == 2) {
+    // ===================== dynamic tile scheduler (leader) =====================
+    // Claims tiles from its die's list first (sched[die]), then from the other
+    // die's list, and publishes each into both CTAs' rings; -1 ends the stream.
+    if constexpr (DYN) {
+      if (leader && lane == 0) {
+        const int Mt = s_mstart[E];
+        const int cnt[2] = {Mt * P.n_split, Mt * (P.n_tiles - P.n_split)};
+        const int my = P.die_map ? (int)P.die_map[ptx::smid() & 255] : 0;
+        int src = my;
+        for (int it = 0;; ++it) {
+          const int slot = it % SCHED_RING;
+          ptx::mbar_wait(&sempty[slot], ((uint32_t)(it / SCHED_RING) & 1u) ^ 1u);
+          int tile = -1;
+          while (src >= 0) {
+            const int x = atomicAdd(&P.sched[src], 1);
+            if (x < cnt[src]) {
+              tile = (src ? cnt[0] : 0) + x;
+              break;
+            }
+            src = (src == my) ? 1 - my : -1;  // own list exhausted: help the other die
+          }
+          s_ring[slot] = tile;
+          ptx::st_cluster_u32(ptx::mapa(ptx::smem_u32(&s_ring[slot]), 1), (uint32_t)tile);
+          ptx::mbar_arrive(&sfull[slot]);
+          ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&sfull[slot]), 1));  // release: orders the ring write
+          if (tile < 0) break;
+        }
+      }
+    }
   } else if (warp >= 4 && warp < 8) {
     // ============================ epilogue ============================
     const int wq = warp & 3;
@@ -651,7 +751,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
       if (P.act == 0) ptx::tma_load_2d(NA + 2048, &mA1, bar, col, row0);
     };
     TileInfo t;
-    for (int tile = cluster_id; decode_tile<KIND, CG>(tile, P, s_offs, s_tstart, t); tile += n_clusters) {
+    for (int it = 0; decode_tile<KIND, CG>(fetch(it), P, s_offs, s_mstart, t); ++it) {
       if constexpr (KIND == TC_BWD_DH && CPA && MOEB_DH_TMA) {
         // the epilogue inputs (A, B rows of this tile) do not depend on the
         // accumulator: start their TMA loads before waiting for it
@@ -1198,6 +1298,23 @@ static moe_status launch_tc_impl(const CUtensorMap& a0, const CUtensorMap& a1, c
   return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
 }
 
+// Claim counters of the dynamic scheduler: a per-device ring of slots, one per
+// launch, zeroed on the launch's stream (concurrent launches on other streams
+// take other slots).
+static int* sched_slot(cudaStream_t st) {
+  constexpr int NSLOT = 256;
+  static std::mutex mu;
+  static int* base[64] = {};
+  static unsigned next[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (!base[dev & 63] && cudaMalloc(&base[dev & 63], NSLOT * 4 * sizeof(int)) != cudaSuccess) return nullptr;
+  int* p = base[dev & 63] + 4 * (next[dev & 63]++ % NSLOT);
+  if (cudaMemsetAsync(p, 0, 4 * sizeof(int), st) != cudaSuccess) return nullptr;
+  return p;
+}
+
 // tiles_for(TM): number of tiles (an upper bound for row kinds) at tile height TM
 template <int KIND, typename F>
 static moe_status launch_tc(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0,
@@ -1205,6 +1322,18 @@ static moe_status launch_tc(const CUtensorMap& a0, const CUtensorMap& a1, const 
   switch (engine()) {
     case ENG_PAIR:
       P.m_tiles = P.m_tiles2;
+      if constexpr (dyn_sched<KIND, 2>()) {
+        // split every expert's n-tiles between the dies in proportion to their SMs
+        int n_sm[2];
+        P.die_map = sm_die_map(n_sm);
+        P.n_split = P.n_tiles;
+        if (P.die_map && n_sm[1] > 0 && P.n_tiles >= 2) {
+          const int ns = (int)((2LL * P.n_tiles * n_sm[0] + (n_sm[0] + n_sm[1])) / (2LL * (n_sm[0] + n_sm[1])));
+          P.n_split = std::min(std::max(ns, 1), P.n_tiles - 1);
+        }
+        P.sched = sched_slot(st);
+        if (!P.sched) return MOE_ERR_CUDA;
+      }
       return launch_tc_impl<KIND, true, 2>(a0, a1, b0, b1, P, tiles_for(256), st);
     case ENG_CTA: return launch_tc_impl<KIND, true, 1>(a0, a1, b0, b1, P, tiles_for(128), st);
     default: return launch_tc_impl<KIND, false, 1>(a0, a1, b0, b1, P, tiles_for(128), st);

@@ -133,3 +133,12 @@ def test_ep_helpers_validation(lib):
     assert lib.moe_ep_send_meta(ctypes.byref(p0), None, None, 4, 2, None, 0, None, None, None) == 0
     ps = L.problem(16, 128, 128, 8, 2, torch.bfloat16, rows=8)
     assert lib.moe_ep_slot_grad(ctypes.byref(ps), None, 4, 2, None, None, None, None) == 1  # sparse source
+
+
+def test_sm_topology_validation(lib):
+    import ctypes
+    n = (ctypes.c_int32 * 2)()
+    assert lib.moe_sm_topology(None, 4, n) != 0
+    dies = (ctypes.c_int32 * 4)()
+    assert lib.moe_sm_topology(dies, 4, None) != 0
+    assert lib.moe_sm_topology(dies, -1, n) != 0
