@@ -42,6 +42,20 @@ def flop_factor(kind, gated=True):
     return f if gated or kind not in ("FWD_UP", "DW12", "BWD_DX") else f // 2
 
 
+def alg_bytes(kind, T, R, d, h, E, gated=True):
+    """Minimum DRAM bytes of one launch of an expert-GEMM kind (bf16 operands,
+    fp32 combine accumulator): every weight, checkpoint and output once, the
+    gathered X / dY rows once."""
+    g = 2 if gated else 1
+    w_up, w_dn = g * E * h * d * 2, E * d * h * 2
+    return {"FWD_UP": T * d * 2 + w_up + (g + 1) * R * h * 2,
+            "FWD_DOWN": R * h * 2 + w_dn + 2 * T * d * 4,
+            "BWD_DH": T * d * 2 + w_dn + g * R * h * 2 + (g + 1) * R * h * 2,
+            "BWD_DX": g * R * h * 2 + w_up + 2 * T * d * 4,
+            "DW3": T * d * 2 + R * h * 2 + w_dn,
+            "DW12": g * R * h * 2 + T * d * 2 + w_up}[kind]
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -296,6 +310,9 @@ def main():
             * R * cfg.d * cfg.h
         roof = {"bound": "tensor", "kernel": f"tc_gemm_kernel<{dom}>", "achieved": round(achieved, 1),
                 "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                "traffic_source": "profiles/ncu_traffic.json: dram__bytes_read.sum + dram__bytes_write.sum per launch "
+                                  "(ncu launch list, same workload)" if traffic else None,
+                "algorithmic_bytes": alg_bytes(dom, cfg.T, R, cfg.d, cfg.h, cfg.E, gated),
                 "peak_source": f"{peaks['source']} bf16 sustained (kernel timed inside the step)",
                 "frac_of_burst": round(achieved / peaks["bf16_tflops"], 4),
                 "flops_per_launch": flops, "avg_launch_ms": round(tot_ms / n_l, 4),
@@ -384,6 +401,7 @@ def main():
                            x.numel() * 2 / 1e6)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "gpu_launches_per_step": launches / args.steps, "clocks": clk,
+            "sm_topology": {"sm_per_die": L.sm_topology()[1], "use": "die split of the expert-GEMM tile lists"},
             "peak_activation_gb": mem["ours"]["peak_gb"] if mem else None, "memory": mem,
         }
         print(json.dumps(out), flush=True)
