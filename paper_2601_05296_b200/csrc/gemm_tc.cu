@@ -55,6 +55,9 @@ enum TcKind { TC_FWD_UP = 0, TC_FWD_DOWN = 1, TC_BWD_DH = 2, TC_BWD_DX = 3, TC_D
 #ifndef MOEB_DH_NBUF
 #define MOEB_DH_NBUF 4    // BWD_DH epilogue ring depth (A/B chunks of 32 columns per warp)
 #endif
+#ifndef MOEB_NTAIL
+#define MOEB_NTAIL 1      // bit 0: DW3, bit 1: BWD_DH (CTA pair): a last n-tile with <= 128 valid columns runs N = 128 MMAs
+#endif
 #ifndef MOEB_DYN
 #define MOEB_DYN 1        // row-kind tiles from the die-aware dynamic scheduler (0: static cluster-strided order)
 #endif
@@ -131,6 +134,14 @@ __host__ __device__ constexpr bool dyn_sched() {
   return MOEB_DYN && CG == 2 && KIND != TC_ROUTE && KIND != TC_DW3 && KIND != TC_DW12;
 }
 constexpr int SCHED_RING = 4;  // tiles published ahead by the scheduler
+// N = 128 tail tiles (N = h, B = MN-major panels of 64 columns, CTA pair) when at most
+// 128 of the tile's 256 output columns exist (h % 256 == 128).  Enabled for DW3; BWD_DH
+// supports it but measured slower (its half-length tail mainloop turns gather-bound
+// under a full-size epilogue; DeepSeek-like BWD_DH 0.79-0.81 -> 0.83-0.84 ms)
+template <int KIND, int CG>
+__host__ __device__ constexpr bool has_ntail() {
+  return CG == 2 && ((MOEB_NTAIL & 1) && KIND == TC_DW3 || (MOEB_NTAIL & 2) && KIND == TC_BWD_DH);
+}
 
 template <int KIND>
 struct KindTraits {
@@ -475,7 +486,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
           } else if constexpr (CG == 1) {
             ptx::mbar_arrive_expect_tx(bar, tma_bytes_per_cta<KIND, CPA, CG>());
           } else {
-            if (leader) ptx::mbar_arrive_expect_tx(bar, 2 * tma_bytes_per_cta<KIND, CPA, CG>());
+            uint32_t bytes = 2 * tma_bytes_per_cta<KIND, CPA, CG>();
+            if constexpr (has_ntail<KIND, CG>())
+              if (P.h - t.n0 <= 128) bytes -= (uint32_t)C::B_BYTES;  // half the B columns per CTA
+            if (leader) ptx::mbar_arrive_expect_tx(bar, bytes);
           }
         }
         __syncwarp();
@@ -504,7 +518,11 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
           if (lane == 1) load(sB, &mB0, k0, t.e * P.d + t.n0 + coloff);
         } else if constexpr (KIND == TC_BWD_DH) {
           if (!CPA) ptx::tma_gather4(sA + 512 * lane, &mA0, bar, k0, gi0, gi1, gi2, gi3);
-          if (lane < NPANEL) load(sB + lane * 8192, &mB0, t.n0 + coloff + 64 * lane, t.e * P.d + k0);
+          if (has_ntail<KIND, CG>() && P.h - t.n0 <= 128) {  // N = 128: one 64-column panel per CTA
+            if (lane == 0) load(sB, &mB0, t.n0 + 64 * (int)crank, t.e * P.d + k0);
+          } else if (lane < NPANEL) {
+            load(sB + lane * 8192, &mB0, t.n0 + coloff + 64 * lane, t.e * P.d + k0);
+          }
         } else if constexpr (KIND == TC_BWD_DX) {
           const bool second = k0 >= P.h;
           const int kk = second ? k0 - P.h : k0;
@@ -521,7 +539,11 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
             const int i3 = r + 3 < t.seg1 ? P.eti[r + 3] : oob;
             ptx::tma_gather4(sA + p * 8192 + g * 512, &mA0, bar, t.m0 + 64 * p, i0, i1, i2, i3);
           }
-          if (lane < NPANEL) load(sB + lane * 8192, &mB0, t.n0 + coloff + 64 * lane, t.seg0 + k0);
+          if (has_ntail<KIND, CG>() && P.h - t.n0 <= 128) {
+            if (lane == 0) load(sB, &mB0, t.n0 + 64 * (int)crank, t.seg0 + k0);
+          } else if (lane < NPANEL) {
+            load(sB + lane * 8192, &mB0, t.n0 + coloff + 64 * lane, t.seg0 + k0);
+          }
         } else {  // TC_DW12
           if (!CPA) {
             const int g = lane & 15, ph = lane >> 4;
@@ -665,6 +687,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
         else ptx::mbar_wait(&tempty[as], aphase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tb + as * TBN;
+        uint32_t tidesc = idesc;
+        if constexpr (has_ntail<KIND, CG>())
+          if (P.h - t.n0 <= 128) tidesc = ptx::umma_idesc_bf16(128 * CG, TBN / 2, K::a_mn ? 1 : 0, K::b_mn ? 1 : 0);
         for (int kb = 0; kb < t.nk; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           if (CPA && K::gathered) ptx::fence_proxy_async();  // cp.async (generic proxy) -> tcgen05 reads
@@ -683,7 +708,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
             }
             __syncwarp();
           } else {
-            ptx::umma_kblock<CG, STEP_A, STEP_B>(d_tmem, (sA >> 4) | LBO_A, ((sA + TA_BYTES) >> 4) | LBO_B, idesc,
+            ptx::umma_kblock<CG, STEP_A, STEP_B>(d_tmem, (sA >> 4) | LBO_A, ((sA + TA_BYTES) >> 4) | LBO_B, tidesc,
                                                  kb != 0, empty0 + 8 * stage, 0x3);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }

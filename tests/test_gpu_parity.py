@@ -98,6 +98,8 @@ LAYER_CASES = [
     ("ragged_bf16", 1000, 128, 256, 16, 6, "bf16", True, "skewed"),
     ("degenerate_bf16", 300, 128, 128, 8, 2, "bf16", False, "degenerate"),
     ("k1_bf16", 333, 256, 256, 4, 1, "bf16", False, "balanced"),
+    # h % 256 == 128: BWD_DH / DW3 run their last n-tile as an N = 128 MMA
+    ("h_tail_bf16", 700, 256, 640, 8, 2, "bf16", False, "balanced"),
 ]
 
 
