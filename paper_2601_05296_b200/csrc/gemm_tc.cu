@@ -44,16 +44,28 @@
 
 namespace moeb {
 
-enum TcKind { TC_FWD_UP = 0, TC_FWD_DOWN = 1, TC_BWD_DH = 2, TC_BWD_DX = 3, TC_DW3 = 4, TC_DW12 = 5, TC_ROUTE = 6 };
+enum TcKind { TC_FWD_UP = 0, TC_FWD_DOWN = 1, TC_BWD_DH = 2, TC_BWD_DX = 3, TC_DW3 = 4, TC_DW12 = 5, TC_ROUTE = 6,
+              TC_BWD_DH_LK = 7 };
+// BWD_DH comes in two smem splits between the mainloop ring and the epilogue's A/B ring:
+// TC_BWD_DH (4 stages, 32-column epilogue chunks) for short K = d, TC_BWD_DH_LK (5 stages,
+// 16-column chunks) for long K (d >= 3072): the extra stage pays off only when the
+// mainloop, not the per-chunk epilogue overhead, is the longer side (profiles/dh16_ab)
+__host__ __device__ constexpr bool is_dh(int k) { return k == TC_BWD_DH || k == TC_BWD_DH_LK; }
 
 #ifndef MOEB_DH_STAGES
-#define MOEB_DH_STAGES 4  // BWD_DH mainloop stages in the CTA-pair engine (smem shared with the epilogue ring)
+#define MOEB_DH_STAGES 5  // BWD_DH mainloop stages in the CTA-pair engine (smem shared with the epilogue ring)
 #endif
 #ifndef MOEB_DH_TMA
 #define MOEB_DH_TMA 1     // BWD_DH epilogue I/O by TMA boxes (1) or per-lane cp.async / stores (0)
 #endif
 #ifndef MOEB_DH_NBUF
-#define MOEB_DH_NBUF 4    // BWD_DH epilogue ring depth (A/B chunks of 32 columns per warp)
+#define MOEB_DH_NBUF 6    // BWD_DH epilogue ring depth (A/B chunks of DH_CW columns per warp)
+#endif
+#ifndef MOEB_DH_STAGES_SK
+#define MOEB_DH_STAGES_SK 4  // the same for the short-K variant (TC_BWD_DH)
+#endif
+#ifndef MOEB_DH_NBUF_SK
+#define MOEB_DH_NBUF_SK 4
 #endif
 #ifndef MOEB_NTAIL
 #define MOEB_NTAIL 1      // bit 0: DW3, bit 1: BWD_DH (CTA pair): a last n-tile with <= 128 valid columns runs N = 128 MMAs
@@ -80,11 +92,16 @@ struct CgCfg {
   static constexpr int STAGE = TA_BYTES + B_BYTES;
   // BWD_DH shares smem between its mainloop ring and the epilogue A/B ring (tools/tune_variants.sh:
   // 4 stages + 4-deep ring beat 3 + 7 by 11 % on the Mixtral layer)
-  static constexpr bool DH = (KIND == 2);
-  static constexpr int STAGES = DH ? (CG == 1 ? 2 : MOEB_DH_STAGES) : (CG == 1 ? 4 : 6);
-  static constexpr int DH_NBUF = MOEB_DH_NBUF;          // BWD_DH: ring of A/B input chunks per warp
+  static constexpr bool DH = is_dh(KIND);
+  static constexpr bool LK = (KIND == TC_BWD_DH_LK) && MOEB_DH_TMA;
+  static constexpr int STAGES = DH ? (CG == 1 ? 2 : (LK ? MOEB_DH_STAGES : MOEB_DH_STAGES_SK)) : (CG == 1 ? 4 : 6);
+  static constexpr int DH_NBUF = LK ? MOEB_DH_NBUF : MOEB_DH_NBUF_SK;  // BWD_DH: ring of A/B input chunks per warp
+  // BWD_DH epilogue chunk: 16 columns (TMA boxes of 32 rows x 32 B, 32-byte swizzle) in the
+  // TMA epilogue, 32 in the cp.async one; a slot holds the A and the B chunk
+  static constexpr int DH_CW = LK ? 16 : 32;
+  static constexpr int DH_SLOT = 2 * 32 * DH_CW * 2;
   // epilogue staging bytes per warp (BWD_DH: the A/B ring + two wU tiles)
-  static constexpr int STG_WARP = DH ? (DH_NBUF * 4096 + 4096) : 6144;
+  static constexpr int STG_WARP = DH ? (DH_NBUF * DH_SLOT + DH_SLOT) : 6144;
   // 1024-aligned: the BWD_DH tiles are TMA boxes in the 64-byte swizzle, whose pattern is
   // taken from the smem address bits
   static constexpr int STG_OFF = (STAGES * STAGE + 1024 /*barriers*/ + 2176 /*offsets, tile starts*/ + 1023) / 1024 * 1024;
@@ -140,16 +157,16 @@ constexpr int SCHED_RING = 4;  // tiles published ahead by the scheduler
 // under a full-size epilogue; DeepSeek-like BWD_DH 0.79-0.81 -> 0.83-0.84 ms)
 template <int KIND, int CG>
 __host__ __device__ constexpr bool has_ntail() {
-  return CG == 2 && ((MOEB_NTAIL & 1) && KIND == TC_DW3 || (MOEB_NTAIL & 2) && KIND == TC_BWD_DH);
+  return CG == 2 && ((MOEB_NTAIL & 1) && KIND == TC_DW3 || (MOEB_NTAIL & 2) && is_dh(KIND));
 }
 
 template <int KIND>
 struct KindTraits {
   static constexpr bool wgrad = (KIND == TC_DW3 || KIND == TC_DW12);
   static constexpr bool a_mn = wgrad;  // A operand MN-major?
-  static constexpr bool b_mn = (KIND == TC_BWD_DH || KIND == TC_BWD_DX || wgrad);
+  static constexpr bool b_mn = (is_dh(KIND) || KIND == TC_BWD_DX || wgrad);
   static constexpr int NT = (KIND == TC_FWD_UP) ? 128 : 256;  // output columns per tile
-  static constexpr bool gather_a = (KIND == TC_FWD_UP || KIND == TC_BWD_DH || KIND == TC_DW3);
+  static constexpr bool gather_a = (KIND == TC_FWD_UP || is_dh(KIND) || KIND == TC_DW3);
   static constexpr bool gather_b = (KIND == TC_DW12);
   static constexpr bool gathered = gather_a || gather_b;
 };
@@ -250,7 +267,7 @@ __device__ __forceinline__ bool decode_tile(int tile, const TcParams& P, const i
     const int mi = mstart + (within - (within / sz) * sz);
     t.m0 = t.seg0 + mi * TM;
     t.n0 = t.n_tile * ((KIND == TC_FWD_UP && P.act == 0) ? 128 : 256);
-    const int Kdim = (KIND == TC_FWD_UP || KIND == TC_BWD_DH) ? P.d
+    const int Kdim = (KIND == TC_FWD_UP || is_dh(KIND)) ? P.d
                      : (KIND == TC_FWD_DOWN ? P.h : (P.act == 0 ? 2 : 1) * P.h);
     t.nk = Kdim / TBK;
   }
@@ -290,6 +307,25 @@ __device__ __forceinline__ void load_bf16x32(const __nv_bfloat16* src, float* v)
 // bf16 tile: 32 rows x 64 B, 16-byte chunk q of row i at i*64 + ((q ^ ((i>>1)&3)) << 4)
 // fp32 tile: 32 rows x 128 B, chunk q (0..7) of row i at i*128 + ((q ^ (i&7)) << 4)
 __device__ __forceinline__ uint32_t stg16_off(int i, int q) { return i * 64 + ((q ^ ((i >> 1) & 3)) << 4); }
+// bf16 tile of 32 rows x 16 columns (32 B), the TMA 32-byte swizzle: chunk q (0..1) of row
+// i at i*32 + ((q ^ ((i>>2)&1)) << 4) (conflict-free for one row per lane)
+__device__ __forceinline__ uint32_t stg8_off(int i, int q) { return i * 32 + ((q ^ ((i >> 2) & 1)) << 4); }
+template <int CW>
+__device__ __forceinline__ uint32_t stgw_off(int i, int q) { return CW == 16 ? stg8_off(i, q) : stg16_off(i, q); }
+template <int CW>
+__device__ __forceinline__ void tmem_ldw(uint32_t taddr, uint32_t (&v)[CW]) {
+  if constexpr (CW == 16) ptx::tmem_ld16(taddr, v);
+  else ptx::tmem_ld32(taddr, v);
+}
+__device__ __forceinline__ void stg8_store_bf16(const uint8_t* stg, int lane, __nv_bfloat16* base, int64_t ld,
+                                                int nvalid) {
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const int row = it * 16 + (lane >> 1), q = lane & 1;
+    if (row < nvalid)
+      *reinterpret_cast<uint4*>(base + row * ld + q * 8) = *reinterpret_cast<const uint4*>(stg + stg8_off(row, q));
+  }
+}
 __device__ __forceinline__ uint32_t stg32_off(int i, int q) { return i * 128 + ((q ^ (i & 7)) << 4); }
 
 __device__ __forceinline__ void stg_put_bf16(uint8_t* stg, int i, const float* v) {
@@ -408,7 +444,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
       ptx::mbar_init(&tfull[s], 1);
       ptx::mbar_init(&tempty[s], 4 * CG);
     }
-    if constexpr (KIND == TC_BWD_DH && CPA && MOEB_DH_TMA)
+    if constexpr (is_dh(KIND) && CPA && MOEB_DH_TMA)
       for (int s = 0; s < 4 * C::DH_NBUF; ++s) ptx::mbar_init(&ebar[s], 1);
     if constexpr (DYN)
       for (int s = 0; s < SCHED_RING; ++s) {
@@ -467,7 +503,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
     TileInfo t;
     for (int it = 0; decode_tile<KIND, CG>(fetch(it), P, s_offs, s_mstart, t); ++it) {
       int gi0 = 0, gi1 = 0, gi2 = 0, gi3 = 0;
-      if constexpr (!CPA && (KIND == TC_FWD_UP || KIND == TC_BWD_DH)) {
+      if constexpr (!CPA && (KIND == TC_FWD_UP || is_dh(KIND))) {
         const int r = t.m0 + 4 * lane;
         gi0 = r + 0 < t.seg1 ? P.eti[r + 0] : oob;
         gi1 = r + 1 < t.seg1 ? P.eti[r + 1] : oob;
@@ -516,7 +552,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
         } else if constexpr (KIND == TC_FWD_DOWN) {
           if (lane == 0) load(sA, &mA0, k0, t.m0 + rowoff);
           if (lane == 1) load(sB, &mB0, k0, t.e * P.d + t.n0 + coloff);
-        } else if constexpr (KIND == TC_BWD_DH) {
+        } else if constexpr (is_dh(KIND)) {
           if (!CPA) ptx::tma_gather4(sA + 512 * lane, &mA0, bar, k0, gi0, gi1, gi2, gi3);
           if (has_ntail<KIND, CG>() && P.h - t.n0 <= 128) {  // N = 128: one 64-column panel per CTA
             if (lane == 0) load(sB, &mB0, t.n0 + 64 * (int)crank, t.e * P.d + k0);
@@ -579,7 +615,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
       const __nv_bfloat16* src_base = (KIND == TC_FWD_UP || KIND == TC_DW12) ? P.x : P.dy;
       uint64_t* const done_bar = CG == 2 ? gfull : full;
       for (int it = 0; decode_tile<KIND, CG>(fetch(it), P, s_offs, s_mstart, t); ++it) {
-        if constexpr (KIND == TC_FWD_UP || KIND == TC_BWD_DH) {
+        if constexpr (KIND == TC_FWD_UP || is_dh(KIND)) {
           // K-major A, this CTA's 128 rows x 8 chunks: chunk c = gt&7, rows (gt>>3) + 16 i
           const int c = gt & 7, rb = gt >> 3;
           const __nv_bfloat16* src[8];
@@ -765,29 +801,30 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
     uint32_t aphase = 0;
     uint32_t gch = 0;  // BWD_DH (TMA epilogue): this warp's running chunk count (ring slot / parity)
     constexpr int DH_PF = C::DH_NBUF - 2;  // chunks loaded ahead (slot reuse distance 2: wait_read<1>)
-    // BWD_DH epilogue TMA: 32 x 32 bf16 boxes (64-byte swizzle = the stg16_off layout) of
-    // A (mA0), B (mA1) loaded and dA, dB, wU (mB1) stored by lane 0
+    // BWD_DH epilogue TMA: 32-row x DH_CW-column bf16 boxes (32-byte swizzle = the stg8_off
+    // layout) of A (mA0), B (mA1) loaded and dA, dB, wU (mB1) stored by lane 0
+    constexpr int CW = C::DH_CW, HALF = C::DH_SLOT / 2;
     auto dh_load = [&](uint32_t g, int col, int row0) {
       const int slot = (int)(g % C::DH_NBUF);
       uint64_t* bar = &ebar[wq * C::DH_NBUF + slot];
-      uint8_t* NA = stg + slot * 4096;
-      ptx::mbar_arrive_expect_tx(bar, P.act == 0 ? 4096u : 2048u);
+      uint8_t* NA = stg + slot * C::DH_SLOT;
+      ptx::mbar_arrive_expect_tx(bar, P.act == 0 ? 2u * HALF : (uint32_t)HALF);
       ptx::tma_load_2d(NA, &mA0, bar, col, row0);
-      if (P.act == 0) ptx::tma_load_2d(NA + 2048, &mA1, bar, col, row0);
+      if (P.act == 0) ptx::tma_load_2d(NA + HALF, &mA1, bar, col, row0);
     };
     TileInfo t;
     for (int it = 0; decode_tile<KIND, CG>(fetch(it), P, s_offs, s_mstart, t); ++it) {
-      if constexpr (KIND == TC_BWD_DH && CPA && MOEB_DH_TMA) {
+      if constexpr (is_dh(KIND) && CPA && MOEB_DH_TMA) {
         // the epilogue inputs (A, B rows of this tile) do not depend on the
         // accumulator: start their TMA loads before waiting for it
         const int r0w = t.m0 + rowoff + wq * 32;
-        const int nchunk = min(TBN, P.h - t.n0) / 32;
+        const int nchunk = min(TBN, P.h - t.n0) / CW;
         if (lane == 0) {
           ptx::bulk_wait_read<1>();
-          for (int ci = 0; ci < DH_PF && ci < nchunk; ++ci) dh_load(gch + ci, t.n0 + 32 * ci, r0w);
+          for (int ci = 0; ci < DH_PF && ci < nchunk; ++ci) dh_load(gch + ci, t.n0 + CW * ci, r0w);
         }
         __syncwarp();
-      } else if constexpr (KIND == TC_BWD_DH) {
+      } else if constexpr (is_dh(KIND)) {
         // the epilogue inputs (A, B rows of this tile) do not depend on the
         // accumulator: start streaming the first chunks before waiting for it
         const int r0w = t.m0 + rowoff + wq * 32;
@@ -809,11 +846,11 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
       const uint32_t tb = tmem_base + ((uint32_t)(wq * 32) << 16) + as * TBN;
       uint32_t v[32];
       if constexpr ((MOEB_EXP_NOEPI >> KIND) & 1) {
-        if constexpr (KIND == TC_BWD_DH && CPA && MOEB_DH_TMA) {
-          const int nchunk = min(TBN, P.h - t.n0) / 32;
+        if constexpr (is_dh(KIND) && CPA && MOEB_DH_TMA) {
+          const int nchunk = min(TBN, P.h - t.n0) / CW;
           for (int ci = 0; ci < DH_PF && ci < nchunk; ++ci, ++gch)
             ptx::mbar_wait(&ebar[wq * C::DH_NBUF + (int)(gch % C::DH_NBUF)], (gch / C::DH_NBUF) & 1);
-        } else if constexpr (KIND == TC_BWD_DH) {
+        } else if constexpr (is_dh(KIND)) {
           asm volatile("cp.async.wait_all;" ::: "memory");
         }
       } else if constexpr (KIND == TC_ROUTE) {
@@ -985,44 +1022,46 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
           }
           __syncwarp();
         }
-      } else if constexpr (KIND == TC_BWD_DH && CPA && MOEB_DH_TMA) {
-        // A, B chunks of 32 columns arrive by TMA in a ring of DH_NBUF slots (A at +0,
-        // B at +2048 of each 4 KB slot; DH_PF chunks ahead, the first ones issued before
+      } else if constexpr (is_dh(KIND) && CPA && MOEB_DH_TMA) {
+        // A, B chunks of CW columns arrive by TMA in a ring of DH_NBUF slots (A at +0,
+        // B at +HALF of each slot; DH_PF chunks ahead, the first ones issued before
         // the accumulator was ready); dA, dB overwrite the consumed slot, wU goes to one
-        // of two tiles, and lane 0 stores the three 32 x 32 boxes by TMA (rows past the
+        // of two tiles, and lane 0 stores the three 32 x CW boxes by TMA (rows past the
         // segment belong to the next expert: a partial row group is stored by hand).
+        // TC_BWD_DH_LK's 16-column chunks keep the ring small enough for a 5-stage mainloop.
         const int r = t.m0 + row;
         const bool valid = r < t.seg1;
         const int r0w = t.m0 + rowoff + wq * 32;
         const int nvalid = max(0, min(32, t.seg1 - r0w));
         const float w = valid ? P.topw[P.row_slot[r]] : 0.f;
         constexpr int NBUF = C::DH_NBUF;
-        const int nchunk = min(TBN, P.h - t.n0) / 32;
+        const int nchunk = min(TBN, P.h - t.n0) / CW;
         const int64_t o0 = (int64_t)r0w * P.h + t.n0;
         float rowsum = 0.f;
-        if (nchunk > 0) ptx::tmem_ld32(tb, v);
+        uint32_t vw[CW];
+        if (nchunk > 0) tmem_ldw<CW>(tb, vw);
 #pragma unroll 1
         for (int ci = 0; ci < nchunk; ++ci, ++gch) {
           const int slot = (int)(gch % NBUF);
-          uint8_t* TA = stg + slot * 4096;
-          uint8_t* TB = TA + 2048;
-          uint8_t* TU = stg + NBUF * 4096 + (gch & 1) * 2048;
+          uint8_t* TA = stg + slot * C::DH_SLOT;
+          uint8_t* TB = TA + HALF;
+          uint8_t* TU = stg + NBUF * C::DH_SLOT + (gch & 1) * HALF;
           if (lane == 0) {
             ptx::bulk_wait_read<1>();  // chunk gch-2's stores have read their slot and wU tile
-            if (ci + DH_PF < nchunk) dh_load(gch + DH_PF, t.n0 + 32 * (ci + DH_PF), r0w);
+            if (ci + DH_PF < nchunk) dh_load(gch + DH_PF, t.n0 + CW * (ci + DH_PF), r0w);
           }
           __syncwarp();
           ptx::mbar_wait(&ebar[wq * NBUF + slot], (gch / NBUF) & 1);
           // accumulator chunk ci was loaded (asynchronously) one iteration ago
           ptx::tmem_wait_ld();
-          uint32_t dh[32];
+          uint32_t dh[CW];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) dh[i] = v[i];
-          if (ci + 1 < nchunk) ptx::tmem_ld32(tb + (ci + 1) * 32, v);  // overlap the next TMEM read
+          for (int i = 0; i < CW; ++i) dh[i] = vw[i];
+          if (ci + 1 < nchunk) tmem_ldw<CW>(tb + (ci + 1) * CW, vw);  // overlap the next TMEM read
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const uint4 ua = *reinterpret_cast<const uint4*>(TA + stg16_off(lane, q));
-            const uint4 ub = *reinterpret_cast<const uint4*>(TB + stg16_off(lane, q));
+          for (int q = 0; q < CW / 8; ++q) {
+            const uint4 ua = *reinterpret_cast<const uint4*>(TA + stgw_off<CW>(lane, q));
+            const uint4 ub = *reinterpret_cast<const uint4*>(TB + stgw_off<CW>(lane, q));
             const uint32_t* pa = reinterpret_cast<const uint32_t*>(&ua);
             const uint32_t* pb = reinterpret_cast<const uint32_t*>(&ub);
             uint32_t oa[4], ob[4], ou[4];
@@ -1057,30 +1096,36 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
               ob[e] = ptx::pack_bf16(rb[0], rb[1]);
               ou[e] = ptx::pack_bf16(ru[0], ru[1]);
             }
-            *reinterpret_cast<uint4*>(TA + stg16_off(lane, q)) = make_uint4(oa[0], oa[1], oa[2], oa[3]);
-            *reinterpret_cast<uint4*>(TB + stg16_off(lane, q)) = make_uint4(ob[0], ob[1], ob[2], ob[3]);
-            *reinterpret_cast<uint4*>(TU + stg16_off(lane, q)) = make_uint4(ou[0], ou[1], ou[2], ou[3]);
+            *reinterpret_cast<uint4*>(TA + stgw_off<CW>(lane, q)) = make_uint4(oa[0], oa[1], oa[2], oa[3]);
+            *reinterpret_cast<uint4*>(TB + stgw_off<CW>(lane, q)) = make_uint4(ob[0], ob[1], ob[2], ob[3]);
+            *reinterpret_cast<uint4*>(TU + stgw_off<CW>(lane, q)) = make_uint4(ou[0], ou[1], ou[2], ou[3]);
           }
           ptx::fence_proxy_async();  // generic smem writes -> visible to the TMA stores
           __syncwarp();
           if (nvalid == 32) {
             if (lane == 0) {
-              const int col = t.n0 + 32 * ci;
+              const int col = t.n0 + CW * ci;
               ptx::tma_store_2d(&mA0, TA, col, r0w);
               if (P.act == 0) ptx::tma_store_2d(&mA1, TB, col, r0w);
               ptx::tma_store_2d(&mB1, TU, col, r0w);
             }
           } else if (nvalid > 0) {
-            const int64_t o = o0 + ci * 32;
-            stg_store_bf16(TA, lane, P.a_save + o, P.h, nvalid);
-            if (P.act == 0) stg_store_bf16(TB, lane, P.b_save + o, P.h, nvalid);
-            stg_store_bf16(TU, lane, P.u + o, P.h, nvalid);
+            const int64_t o = o0 + ci * CW;
+            if constexpr (CW == 16) {
+              stg8_store_bf16(TA, lane, P.a_save + o, P.h, nvalid);
+              if (P.act == 0) stg8_store_bf16(TB, lane, P.b_save + o, P.h, nvalid);
+              stg8_store_bf16(TU, lane, P.u + o, P.h, nvalid);
+            } else {
+              stg_store_bf16(TA, lane, P.a_save + o, P.h, nvalid);
+              if (P.act == 0) stg_store_bf16(TB, lane, P.b_save + o, P.h, nvalid);
+              stg_store_bf16(TU, lane, P.u + o, P.h, nvalid);
+            }
           }
           if (lane == 0) ptx::bulk_commit();  // one (possibly empty) group per chunk
           __syncwarp();
         }
         if (valid) P.dg_part[(int64_t)r * P.dg_parts + t.n_tile] = rowsum;
-      } else if constexpr (KIND == TC_BWD_DH) {
+      } else if constexpr (is_dh(KIND)) {
         // A, B chunks of 32 columns stream through a ring of DH_NBUF cp.async
         // staging buffers (A at +0, B at +2048 of each 4 KB slot; the first
         // slots are filled before the accumulator is ready); dA and dB
@@ -1211,7 +1256,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
       }
       if (++as == 2) { as = 0; aphase ^= 1; }
     }
-    if constexpr (KIND == TC_BWD_DH && CPA && MOEB_DH_TMA)
+    if constexpr (is_dh(KIND) && CPA && MOEB_DH_TMA)
       if (lane == 0) ptx::bulk_wait<0>();  // the epilogue's TMA stores are complete
   }
   ptx::tc_fence_before();
@@ -1252,18 +1297,18 @@ static bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t c
   return r == CUDA_SUCCESS;
 }
 
-// 2D bf16 row-major [rows, cols] map with a 32 x 32 box, 64-byte swizzle (the
-// epilogue staging layout stg16_off)
-static bool make_map_sw64(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols) {
+// 2D bf16 row-major [rows, cols] map with a 32-row x cw-column box (cw = 16: 32-byte
+// swizzle = stg8_off; cw = 32: 64-byte swizzle = stg16_off), the BWD_DH epilogue tiles
+static bool make_map_epi(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t cw) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {cols * 2};
-  cuuint32_t box[2] = {32, 32};
+  cuuint32_t box[2] = {cw, 32};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, cw == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
@@ -1422,18 +1467,22 @@ moe_status tc_gemm(const GemmCall& c, cudaStream_t st) {
     }
     case GEMM_BWD_DH: {
       if (R == 0) return MOE_OK;
+      // long K (d >= 3072): the 5-stage / 16-column-epilogue variant (CTA-pair engine)
+      const bool lk = MOEB_DH_TMA && engine() == ENG_PAIR && d >= 3072;
       ok &= make_map(&b0, c.w3, (uint64_t)E * d, h, 64, 64);
       if (engine() == ENG_TMA || !MOEB_DH_TMA) {  // dY rows by TMA gather4; cp.async epilogue
         ok &= make_map(&a0, c.dy, T, d, 64, 1);
         a1 = a0;
         b1 = b0;
       } else {  // epilogue TMA boxes: A (a0), B (a1) in, dA, dB, wU (b1) out
-        ok &= make_map_sw64(&a0, c.a_save, R, h);
-        ok &= make_map_sw64(&a1, gated ? c.b_save : c.a_save, R, h);
-        ok &= make_map_sw64(&b1, c.u, R, h);
+        const uint32_t cw = lk ? 16 : 32;
+        ok &= make_map_epi(&a0, c.a_save, R, h, cw);
+        ok &= make_map_epi(&a1, gated ? c.b_save : c.a_save, R, h, cw);
+        ok &= make_map_epi(&b1, c.u, R, h, cw);
       }
       if (!ok) return MOE_ERR_CUDA;
       P.n_tiles = (int)ceil_div(h, TBN);
+      if (lk) return launch_tc<TC_BWD_DH_LK>(a0, a1, b0, b1, P, rows_tiles(P.n_tiles), st);
       return launch_tc<TC_BWD_DH>(a0, a1, b0, b1, P, rows_tiles(P.n_tiles), st);
     }
     case GEMM_BWD_DX: {

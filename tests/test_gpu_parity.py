@@ -100,6 +100,8 @@ LAYER_CASES = [
     ("k1_bf16", 333, 256, 256, 4, 1, "bf16", False, "balanced"),
     # h % 256 == 128: BWD_DH / DW3 run their last n-tile as an N = 128 MMA
     ("h_tail_bf16", 700, 256, 640, 8, 2, "bf16", False, "balanced"),
+    # d >= 3072: BWD_DH runs its long-K variant (5 stages, 16-column epilogue chunks)
+    ("long_k_bf16", 300, 3072, 384, 4, 2, "bf16", False, "skewed"),
 ]
 
 
