@@ -152,7 +152,9 @@ def oracle_tokens_per_s(inp_host, cfg, budget_s=15.0, min_tokens=64, fixed_token
     t2 = run(s2)
     per_tok = max((t2 - t1) / (s2 - s1), 1e-6)
     fixed = max(t1 - per_tok * s1, 0.0)
-    S = int(min(cfg.T, max(s2, (budget_s - fixed) / per_tok)))
+    # the fit extrapolates from small, weight-read-bound samples; cap it by linear
+    # scaling of the larger sample (conservative: t2 includes the fixed part)
+    S = int(min(cfg.T, max(s2, (budget_s - fixed) / per_tok), max(s2, s2 * budget_s / t2)))
     if S <= s2:
         return s2 / t2, s2, t2, threads
     t = run(S)

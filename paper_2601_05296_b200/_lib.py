@@ -95,6 +95,12 @@ def load():
            "moe_ep_send_meta", "moe_ep_slot_grad"):
         getattr(lib, fn).restype = I32
     _lib = lib
+    if torch.cuda.is_available():
+        # measure the SM -> die map now (synchronous, ~ms): a first GEMM call inside a
+        # CUDA-graph capture must not have to run the probe
+        d = (ctypes.c_int32 * 256)()
+        n = (ctypes.c_int32 * 2)()
+        lib.moe_sm_topology(d, 256, n)
     return lib
 
 
