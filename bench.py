@@ -179,6 +179,8 @@ def main():
     ap.add_argument("--no-memory", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=10.0)
     ap.add_argument("--ep", action="store_true", help="use the expert-parallel path even at N = 1")
+    ap.add_argument("--retain-recv-x", action="store_true",
+                    help="EP: keep the received X rows from forward for dW1/dW2 (one a2a unit less, more memory)")
     ap.add_argument("--checkpoint", default="ab", choices=["ab", "none"],
                     help="activation checkpoint policy: ab = save A, B (paper); none = recompute A, B in backward")
     ap.add_argument("--activation", default="swiglu", choices=["swiglu", "silu", "relu"],
@@ -234,7 +236,7 @@ def main():
         if not gated or det:
             raise SystemExit("--activation/--deterministic are single-GPU options (the EP receiver runs k = 1)")
         from paper_2601_05296_b200.ep import ExpertParallelMoE
-        ep = ExpertParallelMoE(cfg.E, k, renorm, group=None)
+        ep = ExpertParallelMoE(cfg.E, k, renorm, group=None, retain_recv_x=args.retain_recv_x)
         # each rank keeps only its experts' weights; the router is replicated
         lo, hi = ep.local_experts
         w1, w2, w3 = w1[lo:hi].contiguous(), w2[lo:hi].contiguous(), w3[lo:hi].contiguous()
@@ -398,6 +400,7 @@ def main():
                        "renormalize": renorm, "checkpoint": args.checkpoint, "activation": act,
                        "deterministic": det,
                        "parallelism": f"ep{world}" if ep is not None else "single-GPU",
+                       **({"retain_recv_x": True} if args.retain_recv_x else {}),
                        "l2": "no flush: inputs larger than L2 (weights %.2f GB + X %.0f MB vs 126 MB L2)" % (
                            (3 if gated else 2) * w1.numel() * 2 * (world if world > 1 else 1) / 1e9,
                            x.numel() * 2 / 1e6)},

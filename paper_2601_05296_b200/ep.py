@@ -149,9 +149,13 @@ class ExpertParallelMoE:
 
     overlap: run C4b (X rows) and C5 (dX rows, gate grads) on a side CUDA
     stream against the backward GEMMs (default: on for CUDA tensors over NCCL).
+    retain_recv_x: keep the X rows received in forward for the dW1/dW2 GEMM
+    instead of sending them again in backward: one a2a unit less
+    per step, R_recv x d saved activation bytes more (a permuted copy of X, which
+    the default -- the north star's no-permuted-buffer rule -- does not keep).
     """
 
-    def __init__(self, E, k, renormalize=False, group=None, ops=None, a2a=None, overlap=None):
+    def __init__(self, E, k, renormalize=False, group=None, ops=None, a2a=None, overlap=None, retain_recv_x=False):
         self.P = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         if E % self.P:
@@ -162,6 +166,7 @@ class ExpertParallelMoE:
         self.ops = ops or CudaOps()
         self._a2a = a2a or nccl_a2a
         self.overlap = overlap
+        self.retain_recv_x = retain_recv_x
         self.last_rows_received = 0   # (token, expert) rows computed here
         self.last_rows_sent = 0       # token rows sent (X), after dedup
         self.last_pairs_sent = 0      # (token, expert) pairs they carry
@@ -207,13 +212,14 @@ class ExpertParallelMoE:
             y_rows, a_l, b_l = ops.ffn_fwd(x_recv, w1l, w2l, w3l, w_l, disp_l, n_pairs)
         else:
             y_rows, a_l, b_l = x_recv.new_zeros(U, d), None, None
+        x_keep = x_recv if self.retain_recv_x else None
         del x_recv
         # C3: per-(token, rank) partial outputs back; token-side sum through send_pos
         y_back = self.a2a(y_rows, recv_split, send_split)
         y = ops.combine(y_back, plan.tim, T, d, P)
         ctx = dict(x=x, wg=wg, w1l=w1l, w2l=w2l, w3l=w3l, logits=logits, ids=ids, w=w, plan=plan, send_tok=send_tok,
                    send_split=send_split, recv_split=recv_split, w_l=w_l, disp_l=disp_l, a_l=a_l, b_l=b_l,
-                   n_pairs=n_pairs)
+                   n_pairs=n_pairs, x_recv=x_keep)
         return y, ctx
 
     def backward(self, ctx, dy):
@@ -229,18 +235,25 @@ class ExpertParallelMoE:
         sctx = (lambda: torch.cuda.stream(side)) if streams else contextlib.nullcontext
         # C4a: dY rows to the expert owners (the dH GEMM needs them first)
         dy_recv = self.a2a(ops.gather_rows(dy, ctx["send_tok"]), ss, rs)
-        # C4b: X rows again, on the side stream (only the dW1/dW2 GEMM reads them)
-        x_send = ops.gather_rows(x, ctx["send_tok"])
+        # C4b: X rows again, on the side stream (only the dW1/dW2 GEMM reads them),
+        # unless forward kept them (retain_recv_x)
+        x_recv = ctx.pop("x_recv", None)
         x_ready = dx_ready = None
-        if streams:
-            side.wait_stream(main)
-        with sctx():
-            x_recv = self.a2a(x_send, ss, rs)
-        if streams:
+        if x_recv is None:
+            x_send = ops.gather_rows(x, ctx["send_tok"])
+            if streams:
+                side.wait_stream(main)
+            with sctx():
+                x_recv = self.a2a(x_send, ss, rs)
+            if streams:
+                x_ready = torch.cuda.Event()
+                x_ready.record(side)
+                x_recv.record_stream(main)
+                x_send.record_stream(side)
+        elif streams:
             x_ready = torch.cuda.Event()
-            x_ready.record(side)
-            x_recv.record_stream(main)
-            x_send.record_stream(side)
+            x_ready.record(main)
+        if streams:
             # torch creates the CUDA event lazily at its first record: create it
             # now so the library gets a real handle to re-record after dX is final
             dx_ready = torch.cuda.Event()

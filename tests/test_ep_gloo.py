@@ -99,12 +99,12 @@ def _inputs(rank, P, renorm, routing, c=CFG):
     return {n: f(W[n]) for n in ("w_gate", "w1", "w2", "w3")}, [(f(X[r]["x"]), f(X[r]["dy"])) for r in range(P)]
 
 
-def _worker(rank, P, port, renorm, routing, q, c=CFG):
+def _worker(rank, P, port, renorm, routing, q, c=CFG, retain=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=P)
     from paper_2601_05296_b200.ep import ExpertParallelMoE
     W, XS = _inputs(rank, P, renorm, routing, c)
-    ep = ExpertParallelMoE(c["E"], c["k"], renorm, ops=OracleOps(), a2a=gloo_a2a)
+    ep = ExpertParallelMoE(c["E"], c["k"], renorm, ops=OracleOps(), a2a=gloo_a2a, retain_recv_x=retain)
     lo, hi = ep.local_experts
     x, dy = XS[rank]
     y, g = ep.step(x, W["w_gate"], W["w1"][lo:hi], W["w2"][lo:hi], W["w3"][lo:hi], dy)
@@ -121,16 +121,19 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("P,renorm,routing,c", [(2, False, "balanced", CFG), (2, True, "skewed", CFG),
-                                               (4, False, "balanced", CFG), (4, False, "degenerate", CFG),
-                                               (2, False, "balanced", CFG6), (4, True, "skewed", CFG6)])
-def test_ep_matches_single_process_oracle(P, renorm, routing, c):
+@pytest.mark.parametrize("P,renorm,routing,c,retain", [(2, False, "balanced", CFG, False), (2, True, "skewed", CFG, False),
+                                                      (4, False, "balanced", CFG, False),
+                                                      (4, False, "degenerate", CFG, False),
+                                                      (2, False, "balanced", CFG6, False),
+                                                      (4, True, "skewed", CFG6, False),
+                                                      (4, False, "skewed", CFG6, True)])
+def test_ep_matches_single_process_oracle(P, renorm, routing, c, retain):
     """Every rank's y, dx, dg, dW_g and local expert grads equal the fp64 oracle
     over the concatenated tokens; each token row is sent once per owning rank."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, P, port, renorm, routing, q, c)) for r in range(P)]
+    procs = [ctx.Process(target=_worker, args=(r, P, port, renorm, routing, q, c, retain)) for r in range(P)]
     for p in procs:
         p.start()
     res = [q.get(timeout=120) for _ in range(P)]
