@@ -37,7 +37,7 @@ def _inputs(P, routing="balanced"):
     return W, [(X["x"], X["dy"]) for X in XS]
 
 
-def _worker(rank, P, port, q, routing, backend="gloo"):
+def _worker(rank, P, port, q, routing, backend="gloo", retain=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dev = torch.device("cuda", 0)
@@ -47,7 +47,8 @@ def _worker(rank, P, port, q, routing, backend="gloo"):
         dist.init_process_group("gloo", rank=rank, world_size=P)
     from paper_2601_05296_b200.ep import ExpertParallelMoE
     W, XS = _inputs(P, routing)
-    ep = ExpertParallelMoE(CFG["E"], CFG["k"], False, a2a=staged_a2a if backend == "gloo" else None)
+    ep = ExpertParallelMoE(CFG["E"], CFG["k"], False, a2a=staged_a2a if backend == "gloo" else None,
+                           retain_recv_x=retain)
     assert ep._use_streams(XS[rank][0].to(dev)) == (backend == "nccl")
     lo, hi = ep.local_experts
     x, dy = (t.to(dev) for t in XS[rank])
@@ -69,16 +70,17 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("P,routing,backend", [(1, "balanced", "gloo"), (2, "balanced", "gloo"),
-                                               (2, "degenerate", "gloo"), (1, "balanced", "nccl"),
-                                               (1, "skewed", "nccl")])
-def test_ep_cuda_matches_single_gpu(P, routing, backend):
+@pytest.mark.parametrize("P,routing,backend,retain", [(1, "balanced", "gloo", False), (2, "balanced", "gloo", False),
+                                                      (2, "degenerate", "gloo", False),
+                                                      (1, "balanced", "nccl", False), (1, "skewed", "nccl", False),
+                                                      (2, "skewed", "gloo", True), (1, "balanced", "nccl", True)])
+def test_ep_cuda_matches_single_gpu(P, routing, backend, retain):
     """degenerate routing: every token picks experts 0,1, so rank 1 receives no rows.
     nccl (P = 1): the product path, with C4b / C5 on the side stream."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, P, port, q, routing, backend)) for r in range(P)]
+    procs = [ctx.Process(target=_worker, args=(r, P, port, q, routing, backend, retain)) for r in range(P)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=300) for _ in range(P)], key=lambda t: t[0])
