@@ -70,6 +70,12 @@ __host__ __device__ constexpr bool is_dh(int k) { return k == TC_BWD_DH || k == 
 #ifndef MOEB_NTAIL
 #define MOEB_NTAIL 1      // bit 0: DW3, bit 1: BWD_DH (CTA pair): a last n-tile with <= 128 valid columns runs N = 128 MMAs
 #endif
+#ifndef MOEB_MTAIL
+// FWD_DOWN / BWD_DX (CTA pair): an m-tile with <= 128 rows runs M = 128 MMAs.  Parity-green,
+// but off: interleaved same-box A/B (profiles/mtail_ab_r01.txt) measured the whole Mixtral
+// step 2 % slower with it (every kind, not only the two it changes) and DeepSeek neutral
+#define MOEB_MTAIL 0
+#endif
 #ifndef MOEB_DYN
 #define MOEB_DYN 1        // row-kind tiles from the die-aware dynamic scheduler (0: static cluster-strided order)
 #endif
@@ -155,6 +161,16 @@ constexpr int SCHED_RING = 4;  // tiles published ahead by the scheduler
 // 128 of the tile's 256 output columns exist (h % 256 == 128).  Enabled for DW3; BWD_DH
 // supports it but measured slower (its half-length tail mainloop turns gather-bound
 // under a full-size epilogue; DeepSeek-like BWD_DH 0.79-0.81 -> 0.83-0.84 ms)
+// M = 128 tail tiles: FWD_DOWN and BWD_DX (plain epilogues; A by TMA) in the CTA pair,
+// when a segment's last m-tile has <= 128 rows.  With cta_group::2 and M = 128 each CTA
+// holds 64 rows of A and of the accumulator; the accumulator's first 128 columns sit in
+// TMEM lanes 0-63, the other 128 in lanes 64-127, both at columns 0-127 (the 2-SM
+// M_MMA = 64 layout of CUTLASS's tmem_frg_2sm), so epilogue warp wq handles rows
+// 32 (wq & 1) + lane and output columns 128 (wq >> 1) + [0, 128).
+template <int KIND, int CG>
+__host__ __device__ constexpr bool has_mtail() {
+  return MOEB_MTAIL && CG == 2 && (KIND == TC_FWD_DOWN || KIND == TC_BWD_DX);
+}
 template <int KIND, int CG>
 __host__ __device__ constexpr bool has_ntail() {
   return CG == 2 && ((MOEB_NTAIL & 1) && KIND == TC_DW3 || (MOEB_NTAIL & 2) && is_dh(KIND));
@@ -550,7 +566,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
               load(sB, (gated && crank) ? &mB1 : &mB0, k0, t.e * P.h + t.n0 + (gated ? 0 : 128 * (int)crank));
           }
         } else if constexpr (KIND == TC_FWD_DOWN) {
-          if (lane == 0) load(sA, &mA0, k0, t.m0 + rowoff);
+          // M = 128 tail: this CTA's 64 rows start at m0 + 64 * rank (the box's other 64 rows are unused)
+          const int arow = (has_mtail<KIND, CG>() && t.seg1 - t.m0 <= 128) ? 64 * (int)crank : rowoff;
+          if (lane == 0) load(sA, &mA0, k0, t.m0 + arow);
           if (lane == 1) load(sB, &mB0, k0, t.e * P.d + t.n0 + coloff);
         } else if constexpr (is_dh(KIND)) {
           if (!CPA) ptx::tma_gather4(sA + 512 * lane, &mA0, bar, k0, gi0, gi1, gi2, gi3);
@@ -562,7 +580,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
         } else if constexpr (KIND == TC_BWD_DX) {
           const bool second = k0 >= P.h;
           const int kk = second ? k0 - P.h : k0;
-          if (lane == 0) load(sA, second ? &mA1 : &mA0, kk, t.m0 + rowoff);
+          const int arow = (has_mtail<KIND, CG>() && t.seg1 - t.m0 <= 128) ? 64 * (int)crank : rowoff;
+          if (lane == 0) load(sA, second ? &mA1 : &mA0, kk, t.m0 + arow);
           if (lane >= 4 && lane < 4 + NPANEL)
             load(sB + (lane - 4) * 8192, second ? &mB1 : &mB0, t.n0 + coloff + 64 * (lane - 4), t.e * P.h + kk);
         } else if constexpr (KIND == TC_DW3) {
@@ -724,6 +743,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
         ptx::tc_fence_after();
         const uint32_t d_tmem = tb + as * TBN;
         uint32_t tidesc = idesc;
+        if constexpr (has_mtail<KIND, CG>())
+          if (t.seg1 - t.m0 <= 128) tidesc = ptx::umma_idesc_bf16(128, TBN, K::a_mn ? 1 : 0, K::b_mn ? 1 : 0);
         if constexpr (has_ntail<KIND, CG>())
           if (P.h - t.n0 <= 128) tidesc = ptx::umma_idesc_bf16(128 * CG, TBN / 2, K::a_mn ? 1 : 0, K::b_mn ? 1 : 0);
         for (int kb = 0; kb < t.nk; ++kb) {
@@ -970,8 +991,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
           __syncwarp();
         }
       } else if constexpr (KIND == TC_FWD_DOWN || KIND == TC_BWD_DX) {
-        const int r = t.m0 + row;
-        const int r0w = t.m0 + rowoff + wq * 32;
+        // rows / columns of this warp (M = 128 tail: 32 rows x 128 columns, see has_mtail)
+        const bool half = has_mtail<KIND, CG>() && t.seg1 - t.m0 <= 128;
+        const int r0w = t.m0 + (half ? 64 * (int)crank + 32 * (wq & 1) : rowoff + wq * 32);
+        const int coff = half ? 128 * (wq >> 1) : 0;
+        const int ncol = half ? 128 : TBN;
+        const int r = r0w + lane;
         const int nvalid = max(0, min(32, t.seg1 - r0w));
         const int N = P.d;
         float w = 1.f;
@@ -981,9 +1006,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
           if constexpr (KIND == TC_FWD_DOWN) w = P.topw[P.row_slot[r]];
         }
 #pragma unroll 1
-        for (int c = 0; c < TBN; c += 32) {
+        for (int cc = 0; cc < ncol; cc += 32) {
+          const int c = coff + cc;  // output column within the tile
           if (t.n0 + c >= N) break;
-          ptx::tmem_ld32(tb + c, v);
+          ptx::tmem_ld32(tb + cc, v);
           ptx::tmem_wait_ld();
 #pragma unroll
           for (int q = 0; q < 8; ++q)
