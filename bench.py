@@ -158,6 +158,10 @@ def oracle_tokens_per_s(inp_host, cfg, budget_s=15.0, min_tokens=64, fixed_token
     if S <= s2:
         return s2 / t2, s2, t2, threads
     t = run(S)
+    if t < 0.5 * budget_s and S < cfg.T:
+        # the capped sample came out short: one more, scaled from this (compute-bound) run
+        S = int(min(cfg.T, S * 0.8 * budget_s / t))
+        t = run(S)
     return S / t, S, t, threads
 
 
@@ -177,7 +181,7 @@ def main():
     ap.add_argument("--renormalize", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-memory", action="store_true")
-    ap.add_argument("--cpu-budget-s", type=float, default=10.0)
+    ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--ep", action="store_true", help="use the expert-parallel path even at N = 1")
     ap.add_argument("--retain-recv-x", action="store_true",
                     help="EP: keep the received X rows from forward for dW1/dW2 (one a2a unit less, more memory)")
