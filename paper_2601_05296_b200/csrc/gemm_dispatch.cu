@@ -9,9 +9,9 @@ namespace moeb {
 moe_status simt_gemm(const GemmCall& c, cudaStream_t st);
 int simt_dg_parts(int h);
 moe_status tc_gemm(const GemmCall& c, cudaStream_t st);
-int tc_dg_parts(int h);
+int tc_dg_parts(int h, int d);
 
-int gemm_dg_parts(const GemmCall& c) { return c.bf16 ? tc_dg_parts(c.h) : simt_dg_parts(c.h); }
+int gemm_dg_parts(const GemmCall& c) { return c.bf16 ? tc_dg_parts(c.h, c.d) : simt_dg_parts(c.h); }
 
 namespace {
 struct ProfRec { int kind; cudaEvent_t a, b; };

@@ -46,10 +46,11 @@ namespace moeb {
 
 enum TcKind { TC_FWD_UP = 0, TC_FWD_DOWN = 1, TC_BWD_DH = 2, TC_BWD_DX = 3, TC_DW3 = 4, TC_DW12 = 5, TC_ROUTE = 6,
               TC_BWD_DH_LK = 7 };
-// BWD_DH comes in two smem splits between the mainloop ring and the epilogue's A/B ring:
-// TC_BWD_DH (4 stages, 32-column epilogue chunks) for short K = d, TC_BWD_DH_LK (5 stages,
-// 16-column chunks) for long K (d >= 3072): the extra stage pays off only when the
-// mainloop, not the per-chunk epilogue overhead, is the longer side (profiles/dh16_ab)
+// BWD_DH comes in two forms: TC_BWD_DH (4 epilogue warps, 32-column chunks, 4 stages; the
+// 1-CTA engines and the cp.async epilogue) and TC_BWD_DH_LK (16-column chunks: 128
+// registers, so 8 epilogue warps fit; 4 stages) -- the CTA-pair default for every d >=
+// MOEB_DH_LK_MIN_D.  Its SwiGLU-backward epilogue (10 bytes per output element) was the
+// bottleneck under short mainloops (K = d = 2048)
 __host__ __device__ constexpr bool is_dh(int k) { return k == TC_BWD_DH || k == TC_BWD_DH_LK; }
 
 #ifndef MOEB_DH_STAGES
@@ -60,6 +61,15 @@ __host__ __device__ constexpr bool is_dh(int k) { return k == TC_BWD_DH || k == 
 #endif
 #ifndef MOEB_DH_NBUF
 #define MOEB_DH_NBUF 6    // BWD_DH epilogue ring depth (A/B chunks of DH_CW columns per warp)
+#endif
+#ifndef MOEB_DH_EPI8
+#define MOEB_DH_EPI8 1    // TC_BWD_DH_LK: 8 epilogue warps (two per TMEM lane quarter, 128 columns each)
+#endif
+#ifndef MOEB_DH8_STAGES
+#define MOEB_DH8_STAGES 4
+#endif
+#ifndef MOEB_DH8_NBUF
+#define MOEB_DH8_NBUF 4
 #endif
 #ifndef MOEB_DH_STAGES_SK
 #define MOEB_DH_STAGES_SK 4  // the same for the short-K variant (TC_BWD_DH)
@@ -86,9 +96,14 @@ __host__ __device__ constexpr bool is_dh(int k) { return k == TC_BWD_DH || k == 
 #ifndef MOEB_EXP_NOMMA
 #define MOEB_EXP_NOMMA 0  // kinds whose MMAs are skipped (measures loads + epilogue)
 #endif
+// epilogue warps: 4 (warps 4-7), or 8 for TC_BWD_DH_LK (warps 4-7 and 12-15: two warps per
+// TMEM lane quarter, each with 128 of the tile's 256 columns; its 16-column chunks keep the
+// kernel at 128 registers, so 16 warps fit the register file)
+__host__ __device__ constexpr int n_epi(int k) { return (k == TC_BWD_DH_LK && MOEB_DH_EPI8 && MOEB_DH_TMA) ? 8 : 4; }
+__host__ __device__ constexpr int tc_threads(int k) { return 32 * (8 + n_epi(k)); }
 constexpr int TBN = 256, TBK = 64;         // MMA N per tile, K block
 constexpr int TA_BYTES = 128 * TBK * 2;    // 16 KB: 128 rows of A per CTA
-constexpr int TC_THREADS = 384;            // 12 warps
+constexpr int TC_THREADS = 384;            // 12 warps (16 with the 8-warp BWD_DH epilogue)
 constexpr int GATHER_THREADS = 128;
 
 template <int CG, int KIND = 0>
@@ -100,8 +115,10 @@ struct CgCfg {
   // 4 stages + 4-deep ring beat 3 + 7 by 11 % on the Mixtral layer)
   static constexpr bool DH = is_dh(KIND);
   static constexpr bool LK = (KIND == TC_BWD_DH_LK) && MOEB_DH_TMA;
-  static constexpr int STAGES = DH ? (CG == 1 ? 2 : (LK ? MOEB_DH_STAGES : MOEB_DH_STAGES_SK)) : (CG == 1 ? 4 : 6);
-  static constexpr int DH_NBUF = LK ? MOEB_DH_NBUF : MOEB_DH_NBUF_SK;  // BWD_DH: ring of A/B input chunks per warp
+  static constexpr int NEPI = n_epi(KIND);
+  static constexpr int STAGES = DH ? (CG == 1 ? 2 : (LK ? (NEPI == 8 ? MOEB_DH8_STAGES : MOEB_DH_STAGES) : MOEB_DH_STAGES_SK))
+                                   : (CG == 1 ? 4 : 6);
+  static constexpr int DH_NBUF = LK ? (NEPI == 8 ? MOEB_DH8_NBUF : MOEB_DH_NBUF) : MOEB_DH_NBUF_SK;  // BWD_DH: A/B ring per warp
   // BWD_DH epilogue chunk: 16 columns (TMA boxes of 32 rows x 32 B, 32-byte swizzle) in the
   // TMA epilogue, 32 in the cp.async one; a slot holds the A and the B chunk
   static constexpr int DH_CW = LK ? 16 : 32;
@@ -111,7 +128,7 @@ struct CgCfg {
   // 1024-aligned: the BWD_DH tiles are TMA boxes in the 64-byte swizzle, whose pattern is
   // taken from the smem address bits
   static constexpr int STG_OFF = (STAGES * STAGE + 1024 /*barriers*/ + 2176 /*offsets, tile starts*/ + 1023) / 1024 * 1024;
-  static constexpr int SMEM = STG_OFF + 4 * STG_WARP + 1024 /*align*/;
+  static constexpr int SMEM = STG_OFF + NEPI * STG_WARP + 1024 /*align*/;
 };
 
 struct TcParams {
@@ -399,7 +416,7 @@ __device__ __forceinline__ void stg_load_bf16_async(uint8_t* stg, int lane, cons
 }
 
 template <int KIND, bool CPA, int CG>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+__global__ void __launch_bounds__(tc_threads(KIND), 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
                const __grid_constant__ CUtensorMap mB0, const __grid_constant__ CUtensorMap mB1, const TcParams P) {
   using K = KindTraits<KIND>;
@@ -420,7 +437,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
   uint64_t* ebar = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE + 512);  // BWD_DH: [4 warps][DH_NBUF] TMA loads
   // dynamic scheduler: tile ring (published by the leader into both CTAs) and its barriers
-  uint64_t* sfull = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE + 768);
+  uint64_t* sfull = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE + 256);
   uint64_t* sempty = sfull + SCHED_RING;
   int* s_ring = reinterpret_cast<int*>(sempty + SCHED_RING);
   int* s_offs = reinterpret_cast<int*>(smem + STAGES * C::STAGE + 1024);
@@ -428,7 +445,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
   constexpr bool DYN = dyn_sched<KIND, CG>();
   // arrivals that release a ring slot: every tile-iterating warp of both CTAs
   // (TMA producer, epilogue x4, gathers x4 + relay when gathered) + the MMA warp
-  constexpr int NCONS = 2 * (1 + 4 + (K::gathered ? 5 : 0)) + 1;
+  constexpr int NCONS = 2 * (1 + C::NEPI + (K::gathered ? 5 : 0)) + 1;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int E = P.E;
@@ -440,7 +457,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
   const int n_clusters = (CG == 2) ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
   if constexpr (KIND != TC_ROUTE)
-    for (int i = threadIdx.x; i <= E; i += TC_THREADS) s_offs[i] = P.offs[i];
+    for (int i = threadIdx.x; i <= E; i += tc_threads(KIND)) s_offs[i] = P.offs[i];
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch(&mA0);
     ptx::tma_prefetch(&mA1);
@@ -458,10 +475,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
     }
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&tfull[s], 1);
-      ptx::mbar_init(&tempty[s], 4 * CG);
+      ptx::mbar_init(&tempty[s], C::NEPI * CG);
     }
     if constexpr (is_dh(KIND) && CPA && MOEB_DH_TMA)
-      for (int s = 0; s < 4 * C::DH_NBUF; ++s) ptx::mbar_init(&ebar[s], 1);
+      for (int s = 0; s < C::NEPI * C::DH_NBUF; ++s) ptx::mbar_init(&ebar[s], 1);
     if constexpr (DYN)
       for (int s = 0; s < SCHED_RING; ++s) {
         ptx::mbar_init(&sfull[s], 1);
@@ -621,7 +638,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
-  } else if (warp >= 8) {
+  } else if (warp >= 8 && warp < 12) {
     // ======================= cp.async row gathers =======================
     // Consecutive lanes copy consecutive 16-byte chunks of the same gathered
     // row (one warp instruction = whole 128-byte lines) into the swizzled
@@ -813,11 +830,15 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
         }
       }
     }
-  } else if (warp >= 4 && warp < 8) {
+  } else if ((warp >= 4 && warp < 8) || warp >= 12) {
     // ============================ epilogue ============================
-    const int wq = warp & 3;
+    const int wq = warp & 3;                       // TMEM lane quarter
+    const int hc = warp >= 12 ? 1 : 0;             // 8-warp BWD_DH: column half of the tile
+    const int ew = wq + 4 * hc;                    // epilogue warp index (staging, barriers)
+    constexpr int NCW = C::NEPI == 8 ? TBN / 2 : TBN;  // columns of the tile per warp
+    const int cb = hc * NCW;                       // this warp's first column within the tile
     const int row = rowoff + wq * 32 + lane;  // row of the tile owned by this thread
-    uint8_t* stg = smem + C::STG_OFF + wq * C::STG_WARP;  // this warp's staging tiles
+    uint8_t* stg = smem + C::STG_OFF + ew * C::STG_WARP;  // this warp's staging tiles
     int as = 0;
     uint32_t aphase = 0;
     uint32_t gch = 0;  // BWD_DH (TMA epilogue): this warp's running chunk count (ring slot / parity)
@@ -827,7 +848,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
     constexpr int CW = C::DH_CW, HALF = C::DH_SLOT / 2;
     auto dh_load = [&](uint32_t g, int col, int row0) {
       const int slot = (int)(g % C::DH_NBUF);
-      uint64_t* bar = &ebar[wq * C::DH_NBUF + slot];
+      uint64_t* bar = &ebar[ew * C::DH_NBUF + slot];
       uint8_t* NA = stg + slot * C::DH_SLOT;
       ptx::mbar_arrive_expect_tx(bar, P.act == 0 ? 2u * HALF : (uint32_t)HALF);
       ptx::tma_load_2d(NA, &mA0, bar, col, row0);
@@ -839,10 +860,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
         // the epilogue inputs (A, B rows of this tile) do not depend on the
         // accumulator: start their TMA loads before waiting for it
         const int r0w = t.m0 + rowoff + wq * 32;
-        const int nchunk = min(TBN, P.h - t.n0) / CW;
+        const int nchunk = max(0, min(NCW, P.h - t.n0 - cb)) / CW;
         if (lane == 0) {
           ptx::bulk_wait_read<1>();
-          for (int ci = 0; ci < DH_PF && ci < nchunk; ++ci) dh_load(gch + ci, t.n0 + CW * ci, r0w);
+          for (int ci = 0; ci < DH_PF && ci < nchunk; ++ci) dh_load(gch + ci, t.n0 + cb + CW * ci, r0w);
         }
         __syncwarp();
       } else if constexpr (is_dh(KIND)) {
@@ -868,9 +889,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
       uint32_t v[32];
       if constexpr ((MOEB_EXP_NOEPI >> KIND) & 1) {
         if constexpr (is_dh(KIND) && CPA && MOEB_DH_TMA) {
-          const int nchunk = min(TBN, P.h - t.n0) / CW;
+          const int nchunk = max(0, min(NCW, P.h - t.n0 - cb)) / CW;
           for (int ci = 0; ci < DH_PF && ci < nchunk; ++ci, ++gch)
-            ptx::mbar_wait(&ebar[wq * C::DH_NBUF + (int)(gch % C::DH_NBUF)], (gch / C::DH_NBUF) & 1);
+            ptx::mbar_wait(&ebar[ew * C::DH_NBUF + (int)(gch % C::DH_NBUF)], (gch / C::DH_NBUF) & 1);
         } else if constexpr (is_dh(KIND)) {
           asm volatile("cp.async.wait_all;" ::: "memory");
         }
@@ -1061,11 +1082,11 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
         const int nvalid = max(0, min(32, t.seg1 - r0w));
         const float w = valid ? P.topw[P.row_slot[r]] : 0.f;
         constexpr int NBUF = C::DH_NBUF;
-        const int nchunk = min(TBN, P.h - t.n0) / CW;
-        const int64_t o0 = (int64_t)r0w * P.h + t.n0;
+        const int nchunk = max(0, min(NCW, P.h - t.n0 - cb)) / CW;
+        const int64_t o0 = (int64_t)r0w * P.h + t.n0 + cb;
         float rowsum = 0.f;
         uint32_t vw[CW];
-        if (nchunk > 0) tmem_ldw<CW>(tb, vw);
+        if (nchunk > 0) tmem_ldw<CW>(tb + cb, vw);
 #pragma unroll 1
         for (int ci = 0; ci < nchunk; ++ci, ++gch) {
           const int slot = (int)(gch % NBUF);
@@ -1074,16 +1095,16 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
           uint8_t* TU = stg + NBUF * C::DH_SLOT + (gch & 1) * HALF;
           if (lane == 0) {
             ptx::bulk_wait_read<1>();  // chunk gch-2's stores have read their slot and wU tile
-            if (ci + DH_PF < nchunk) dh_load(gch + DH_PF, t.n0 + CW * (ci + DH_PF), r0w);
+            if (ci + DH_PF < nchunk) dh_load(gch + DH_PF, t.n0 + cb + CW * (ci + DH_PF), r0w);
           }
           __syncwarp();
-          ptx::mbar_wait(&ebar[wq * NBUF + slot], (gch / NBUF) & 1);
+          ptx::mbar_wait(&ebar[ew * NBUF + slot], (gch / NBUF) & 1);
           // accumulator chunk ci was loaded (asynchronously) one iteration ago
           ptx::tmem_wait_ld();
           uint32_t dh[CW];
 #pragma unroll
           for (int i = 0; i < CW; ++i) dh[i] = vw[i];
-          if (ci + 1 < nchunk) tmem_ldw<CW>(tb + (ci + 1) * CW, vw);  // overlap the next TMEM read
+          if (ci + 1 < nchunk) tmem_ldw<CW>(tb + cb + (ci + 1) * CW, vw);  // overlap the next TMEM read
 #pragma unroll
           for (int q = 0; q < CW / 8; ++q) {
             const uint4 ua = *reinterpret_cast<const uint4*>(TA + stgw_off<CW>(lane, q));
@@ -1130,7 +1151,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
           __syncwarp();
           if (nvalid == 32) {
             if (lane == 0) {
-              const int col = t.n0 + CW * ci;
+              const int col = t.n0 + cb + CW * ci;
               ptx::tma_store_2d(&mA0, TA, col, r0w);
               if (P.act == 0) ptx::tma_store_2d(&mA1, TB, col, r0w);
               ptx::tma_store_2d(&mB1, TU, col, r0w);
@@ -1150,7 +1171,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
           if (lane == 0) ptx::bulk_commit();  // one (possibly empty) group per chunk
           __syncwarp();
         }
-        if (valid) P.dg_part[(int64_t)r * P.dg_parts + t.n_tile] = rowsum;
+        if (valid) P.dg_part[(int64_t)r * P.dg_parts + t.n_tile * (C::NEPI == 8 ? 2 : 1) + hc] = rowsum;
       } else if constexpr (is_dh(KIND)) {
         // A, B chunks of 32 columns stream through a ring of DH_NBUF cp.async
         // staging buffers (A at +0, B at +2048 of each 4 KB slot; the first
@@ -1379,7 +1400,7 @@ static moe_status launch_tc_impl(const CUtensorMap& a0, const CUtensorMap& a1, c
   const int groups = (int)std::min<int64_t>(tiles, num_sms() / CG);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(groups * CG);
-  cfg.blockDim = dim3(TC_THREADS);
+  cfg.blockDim = dim3(tc_threads(KIND));
   cfg.dynamicSmemBytes = CgCfg<CG, KIND>::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attrs[1];
@@ -1436,7 +1457,19 @@ static moe_status launch_tc(const CUtensorMap& a0, const CUtensorMap& a1, const 
   }
 }
 
-int tc_dg_parts(int h) { return (int)ceil_div(h, TBN); }
+// BWD_DH variant: the long-K one for d >= 3072 in the CTA-pair engine
+#ifndef MOEB_DH_LK_MIN_D
+// smallest d that runs TC_BWD_DH_LK; 0 = every shape: with 8 epilogue warps it measured
+// DeepSeek-like BWD_DH 0.74-0.80 -> 0.67-0.70 ms (step +2.5 %) and the Mixtral step neutral
+// against the 4-warp / 5-stage long-K variant (profiles/epi8_ab_r01.txt)
+#define MOEB_DH_LK_MIN_D 0
+#endif
+static bool dh_long_k(int d) { return MOEB_DH_TMA && engine() == ENG_PAIR && d >= MOEB_DH_LK_MIN_D; }
+// gate-grad partial columns per routed row written by BWD_DH (one per n-tile, two with the
+// 8-warp epilogue, whose column halves each write their own)
+int tc_dg_parts(int h, int d) {
+  return (int)ceil_div(h, TBN) * ((dh_long_k(d) && n_epi(TC_BWD_DH_LK) == 8) ? 2 : 1);
+}
 
 // K1 on tensor cores (bf16): logits = X Wg^T with M = 128 tokens, N = E padded
 // to a multiple of 16 (rows past E are TMA zero-fill), K = d.
@@ -1468,7 +1501,7 @@ moe_status tc_gemm(const GemmCall& c, cudaStream_t st) {
   P.out_mode = c.out_mode; P.out_tok = (bf*)c.out_tok;
   P.out0 = (bf*)c.dw_a; P.out1 = (bf*)c.dw_b;
   P.T = (int)T; P.d = d; P.h = h; P.E = E;
-  P.dg_parts = tc_dg_parts(h);
+  P.dg_parts = tc_dg_parts(h, d);
   CUtensorMap a0, a1, b0, b1;
   bool ok = true;
   // upper bound on row tiles of height TM over all expert segments
@@ -1494,7 +1527,7 @@ moe_status tc_gemm(const GemmCall& c, cudaStream_t st) {
     case GEMM_BWD_DH: {
       if (R == 0) return MOE_OK;
       // long K (d >= 3072): the 5-stage / 16-column-epilogue variant (CTA-pair engine)
-      const bool lk = MOEB_DH_TMA && engine() == ENG_PAIR && d >= 3072;
+      const bool lk = dh_long_k(d);
       ok &= make_map(&b0, c.w3, (uint64_t)E * d, h, 64, 64);
       if (engine() == ENG_TMA || !MOEB_DH_TMA) {  // dY rows by TMA gather4; cp.async epilogue
         ok &= make_map(&a0, c.dy, T, d, 64, 1);
