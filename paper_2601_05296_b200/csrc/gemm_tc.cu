@@ -65,6 +65,11 @@ __host__ __device__ constexpr bool is_dh(int k) { return k == TC_BWD_DH || k == 
 #ifndef MOEB_DH_EPI8
 #define MOEB_DH_EPI8 1    // TC_BWD_DH_LK: 8 epilogue warps (two per TMEM lane quarter, 128 columns each)
 #endif
+#ifndef MOEB_RED_EPI8
+// FWD_DOWN / BWD_DX: 8 epilogue warps (128 columns each), 5 mainloop stages.  Parity-green but
+// off: interleaved A/B measured both kinds 1-5 % slower (profiles/red8_ab_r01.txt)
+#define MOEB_RED_EPI8 0
+#endif
 #ifndef MOEB_DH8_STAGES
 #define MOEB_DH8_STAGES 4
 #endif
@@ -99,7 +104,10 @@ __host__ __device__ constexpr bool is_dh(int k) { return k == TC_BWD_DH || k == 
 // epilogue warps: 4 (warps 4-7), or 8 for TC_BWD_DH_LK (warps 4-7 and 12-15: two warps per
 // TMEM lane quarter, each with 128 of the tile's 256 columns; its 16-column chunks keep the
 // kernel at 128 registers, so 16 warps fit the register file)
-__host__ __device__ constexpr int n_epi(int k) { return (k == TC_BWD_DH_LK && MOEB_DH_EPI8 && MOEB_DH_TMA) ? 8 : 4; }
+__host__ __device__ constexpr int n_epi(int k) {
+  return ((k == TC_BWD_DH_LK && MOEB_DH_EPI8 && MOEB_DH_TMA) || ((k == TC_FWD_DOWN || k == TC_BWD_DX) && MOEB_RED_EPI8))
+             ? 8 : 4;
+}
 __host__ __device__ constexpr int tc_threads(int k) { return 32 * (8 + n_epi(k)); }
 constexpr int TBN = 256, TBK = 64;         // MMA N per tile, K block
 constexpr int TA_BYTES = 128 * TBK * 2;    // 16 KB: 128 rows of A per CTA
@@ -117,7 +125,7 @@ struct CgCfg {
   static constexpr bool LK = (KIND == TC_BWD_DH_LK) && MOEB_DH_TMA;
   static constexpr int NEPI = n_epi(KIND);
   static constexpr int STAGES = DH ? (CG == 1 ? 2 : (LK ? (NEPI == 8 ? MOEB_DH8_STAGES : MOEB_DH_STAGES) : MOEB_DH_STAGES_SK))
-                                   : (CG == 1 ? 4 : 6);
+                                   : (CG == 1 ? 4 : (NEPI == 8 ? 5 : 6));
   static constexpr int DH_NBUF = LK ? (NEPI == 8 ? MOEB_DH8_NBUF : MOEB_DH_NBUF) : MOEB_DH_NBUF_SK;  // BWD_DH: A/B ring per warp
   // BWD_DH epilogue chunk: 16 columns (TMA boxes of 32 rows x 32 B, 32-byte swizzle) in the
   // TMA epilogue, 32 in the cp.async one; a slot holds the A and the B chunk
@@ -186,7 +194,7 @@ constexpr int SCHED_RING = 4;  // tiles published ahead by the scheduler
 // 32 (wq & 1) + lane and output columns 128 (wq >> 1) + [0, 128).
 template <int KIND, int CG>
 __host__ __device__ constexpr bool has_mtail() {
-  return MOEB_MTAIL && CG == 2 && (KIND == TC_FWD_DOWN || KIND == TC_BWD_DX);
+  return MOEB_MTAIL && CG == 2 && (KIND == TC_FWD_DOWN || KIND == TC_BWD_DX) && n_epi(KIND) == 4;
 }
 template <int KIND, int CG>
 __host__ __device__ constexpr bool has_ntail() {
@@ -1015,8 +1023,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
         // rows / columns of this warp (M = 128 tail: 32 rows x 128 columns, see has_mtail)
         const bool half = has_mtail<KIND, CG>() && t.seg1 - t.m0 <= 128;
         const int r0w = t.m0 + (half ? 64 * (int)crank + 32 * (wq & 1) : rowoff + wq * 32);
-        const int coff = half ? 128 * (wq >> 1) : 0;
-        const int ncol = half ? 128 : TBN;
+        const int coff = half ? 128 * (wq >> 1) : cb;  // first output column of this warp
+        const int tcol = half ? 0 : cb;                // its first TMEM column
+        const int ncol = half ? 128 : NCW;
         const int r = r0w + lane;
         const int nvalid = max(0, min(32, t.seg1 - r0w));
         const int N = P.d;
@@ -1030,7 +1039,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
         for (int cc = 0; cc < ncol; cc += 32) {
           const int c = coff + cc;  // output column within the tile
           if (t.n0 + c >= N) break;
-          ptx::tmem_ld32(tb + cc, v);
+          ptx::tmem_ld32(tb + tcol + cc, v);
           ptx::tmem_wait_ld();
 #pragma unroll
           for (int q = 0; q < 8; ++q)
