@@ -480,6 +480,22 @@ moe_status launch_router_bwd(const moe_problem* p, const float* logits, const in
 // tensor of the run dtype (EP path) instead of fp32; tim != NULL: acc is the
 // [R,d] fp32 row-result buffer, summed per token in slot order (NEXT-4).
 // bf16 with the router term: tensor cores (router_tc.cu) from the hi/lo split dlhl.
+// out[i] = bf16(acc[i]) over n8 groups of 8 (two 16-byte loads, one 16-byte store per thread
+// per step, grid-stride: the HBM-bound Y finalize)
+__global__ void __launch_bounds__(256) convert_f32_bf16_kernel(const float4* __restrict__ acc, int64_t n8,
+                                                                uint4* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 a = __ldcs(acc + 2 * i), b = __ldcs(acc + 2 * i + 1);
+    uint4 o;
+    __nv_bfloat162 h;
+    h = __floats2bfloat162_rn(a.x, a.y); o.x = *reinterpret_cast<uint32_t*>(&h);
+    h = __floats2bfloat162_rn(a.z, a.w); o.y = *reinterpret_cast<uint32_t*>(&h);
+    h = __floats2bfloat162_rn(b.x, b.y); o.z = *reinterpret_cast<uint32_t*>(&h);
+    h = __floats2bfloat162_rn(b.z, b.w); o.w = *reinterpret_cast<uint32_t*>(&h);
+    out[i] = o;
+  }
+}
+
 moe_status launch_finalize(const moe_problem* p, const void* acc, const float* dl, const __nv_bfloat16* dlhl,
                            const void* wg, void* out, cudaStream_t st, bool acc_is_dtype, const int32_t* tim) {
   if (p->T == 0) return MOE_OK;
@@ -490,6 +506,16 @@ moe_status launch_finalize(const moe_problem* p, const void* acc, const float* d
     dim3 g2((unsigned)ceil_div(p->d, 256), (unsigned)ceil_div(p->T, 64));
     MOE_LAUNCH((router_dx_kernel<float, float>), g2, 256, 0, st, (const float*)acc, tim, p->k, dl, (const float*)wg,
                p->T, p->d, p->E, (float*)out);
+    return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
+  }
+  if (p->dtype == MOE_BF16 && !acc_is_dtype && !tim && p->d % 8 == 0) {
+    // the plain Y conversion (fp32 accumulator -> bf16): 8 columns per thread per step
+    const int64_t n8 = p->T * (int64_t)p->d / 8;
+    int nsm = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(n8, 256), (int64_t)nsm * 8);
+    MOE_LAUNCH(convert_f32_bf16_kernel, blocks, 256, 0, st, (const float4*)acc, n8, (uint4*)out);
     return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
   }
   dim3 grid((unsigned)ceil_div(p->d, 256), (unsigned)ceil_div(p->T, 16));
