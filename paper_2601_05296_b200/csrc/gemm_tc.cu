@@ -7,12 +7,18 @@
 //   warp 1      MMA issuer (one thread): 4 x tcgen05.mma (K16) per 64-wide K
 //               block; tcgen05.commit frees the smem stage / publishes the
 //               accumulator
-//   warp 2      TMEM allocator (512 columns = 2 accumulator stages x 256)
+//   warp 2      TMEM allocator (512 columns = 2 accumulator stages x 256); in
+//               the leader CTA of a pair, lane 0 then runs the die-aware dynamic
+//               tile scheduler of the row kinds (tiles published through a ring
+//               in both CTAs' shared memory; topology.cu measures the SM -> die map)
 //   warp 3      (CTA pair) relays cp.async-gather completion to the leader
 //   warps 4-7   epilogue: tcgen05.ld, one accumulator row per thread
 //   warps 8-11  row gathers: 16-byte cp.async straight from the unpermuted X /
 //               dY through expert_token_indices into the 128B-swizzled UMMA
 //               layout — no routed-token buffer exists
+//   warps 12-15 (BWD_DH, TC_BWD_DH_LK) a second epilogue warp per TMEM lane
+//               quarter: warps 4-7 take columns 0-127 of the tile, 12-15 columns
+//               128-255
 //
 // CG = 2 (default for the expert GEMMs): a CTA pair (cluster of 2) computes a
 // 256 x 256 tile with tcgen05.mma.cta_group::2 — each CTA stages 128 rows of A
