@@ -59,6 +59,33 @@ router_dx_tc_kernel(const __grid_constant__ CUtensorMap mDh, const __grid_consta
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t t0 = (int64_t)blockIdx.x * 128;
   const int n0 = blockIdx.y * 256;
+  const int quad = warp & 3, half = warp >> 2;
+  // the epilogue's accumulator rows (the kernel's bulk traffic) do not depend on the MMA:
+  // chunk c of this warp (32 tokens x 32 columns, row-coalesced) is loaded into registers
+  // one chunk ahead, the first before the MMA is even issued
+  auto load_chunk = [&](int c, float4 (&a)[8]) {
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      const int rr = it * 4 + (lane >> 3), q = lane & 7;
+      const int64_t t = t0 + quad * 32 + rr;
+      const int64_t col = n0 + c + 4 * q;
+      a[it] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (LOAD && t < Tn && n0 + c < d) {
+        if (!tim) {
+          a[it] = ld_acc4<A>(acc + t * d + col);
+        } else {  // ordered combine (NEXT-4): the token's routed rows in slot order, -1 skipped
+          for (int j = 0; j < k; ++j) {
+            const int r = tim[t * k + j];
+            if (r < 0) continue;
+            const float4 b = ld_acc4<A>(acc + (int64_t)r * d + col);
+            a[it].x += b.x; a[it].y += b.y; a[it].z += b.z; a[it].w += b.w;
+          }
+        }
+      }
+    }
+  };
+  float4 a_cur[8];
+  load_chunk(half * 128, a_cur);
   if (tid == 0) {
     ptx::tma_prefetch(&mDh);
     ptx::tma_prefetch(&mDl);
@@ -103,7 +130,6 @@ router_dx_tc_kernel(const __grid_constant__ CUtensorMap mDh, const __grid_consta
   ptx::tc_fence_after();
   // epilogue: 32 tokens x 128 columns per warp in 32-column chunks, staged through a
   // swizzled fp32 tile so the global accesses are row-coalesced
-  const int quad = warp & 3, half = warp >> 2;
   uint8_t* stg = stg_all + warp * 4096;
   const uint32_t tb = tmem + ((uint32_t)(quad * 32) << 16);
 #pragma unroll 1
@@ -119,27 +145,9 @@ router_dx_tc_kernel(const __grid_constant__ CUtensorMap mDh, const __grid_consta
                       __uint_as_float(v[4 * q + 3]));
     __syncwarp();
     float4 a[8];
-    if constexpr (LOAD) {
 #pragma unroll
-      for (int it = 0; it < 8; ++it) {  // all loads of the chunk first (memory-level parallelism)
-        const int rr = it * 4 + (lane >> 3), q = lane & 7;
-        const int64_t t = t0 + quad * 32 + rr;
-        const int64_t col = n0 + c + 4 * q;
-        a[it] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (t < Tn) {
-          if (!tim) {
-            a[it] = ld_acc4<A>(acc + t * d + col);
-          } else {  // ordered combine (NEXT-4): the token's routed rows in slot order, -1 skipped
-            for (int j = 0; j < k; ++j) {
-              const int r = tim[t * k + j];
-              if (r < 0) continue;
-              const float4 b = ld_acc4<A>(acc + (int64_t)r * d + col);
-              a[it].x += b.x; a[it].y += b.y; a[it].z += b.z; a[it].w += b.w;
-            }
-          }
-        }
-      }
-    }
+    for (int it = 0; it < 8; ++it) a[it] = a_cur[it];
+    if (c + 32 < half * 128 + 128) load_chunk(c + 32, a_cur);  // next chunk in flight
 #pragma unroll
     for (int it = 0; it < 8; ++it) {
       const int rr = it * 4 + (lane >> 3), q = lane & 7;
