@@ -27,8 +27,10 @@ constexpr int DT_THREADS = 256;
 constexpr int DT_WARPS = DT_THREADS / 32;
 
 int dispatch_tile_entries(int64_t R) {
+  // small tiles: many CTAs walk their tiles in a few 256-entry rounds (the walk is
+  // latency-bound: 4096-entry tiles gave Mixtral-like R = 16384 only 4 CTAs of 16 rounds);
   // keep the number of tiles <= 256 so the per-CTA scan over tiles stays short
-  int64_t t = 4096;
+  int64_t t = 512;
   while (ceil_div(R, t) > 256) t *= 2;
   return (int)t;
 }
@@ -80,15 +82,31 @@ dispatch_scatter_kernel(const int32_t* __restrict__ ids, int64_t R, int k, int E
   int32_t* base = ss;                 // [E]   running global base of each expert for this tile
   int32_t* wc = base + E;             // [DT_WARPS][E] warp counts of the current round
   int32_t* tot = wc + DT_WARPS * E;   // [E]   totals (for the scan)
+  int32_t* ptot = tot + E;            // [parts][E] partial totals / prefixes over slices of tiles
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int my = blockIdx.x;
-  // per expert: total over all tiles and prefix over tiles < my
-  for (int e = tid; e < E; e += DT_THREADS) {
+  // per expert: total over all tiles and prefix over tiles < my; the tiles are split into
+  // `parts` slices so all threads share the walk (E <= 256: parts * E <= DT_THREADS)
+  const int parts = max(1, DT_THREADS / E);
+  int32_t* ppre = ptot + parts * E;
+  for (int i = tid; i < parts * E; i += DT_THREADS) {
+    const int e = i % E, part = i / E;
+    const int q0 = (int)((int64_t)ntiles * part / parts), q1 = (int)((int64_t)ntiles * (part + 1) / parts);
     int total = 0, pre = 0;
-    for (int q = 0; q < ntiles; ++q) {
+    for (int q = q0; q < q1; ++q) {
       int c = tile_counts[(int64_t)q * E + e];
       if (q < my) pre += c;
       total += c;
+    }
+    ptot[i] = total;
+    ppre[i] = pre;
+  }
+  __syncthreads();
+  for (int e = tid; e < E; e += DT_THREADS) {
+    int total = 0, pre = 0;
+    for (int part = 0; part < parts; ++part) {  // fixed order: integer sums, any order is exact
+      total += ptot[part * E + e];
+      pre += ppre[part * E + e];
     }
     tot[e] = total;
     base[e] = pre;
@@ -171,7 +189,8 @@ moe_status launch_dispatch(const moe_problem* p, const int32_t* ids, const moe_d
   size_t sm1 = sizeof(int32_t) * DT_WARPS * E;
   MOE_LAUNCH(dispatch_hist_kernel, ntiles, DT_THREADS, sm1, st, ids, R, p->k, E, tile, p->check_routing,
              p->rows > 0 ? 1 : 0, ws_tile_counts, status);
-  size_t sm2 = sizeof(int32_t) * (E + DT_WARPS * E + E);
+  const int parts = std::max(1, DT_THREADS / E);
+  size_t sm2 = sizeof(int32_t) * (E + DT_WARPS * E + E + 2 * parts * E);
   MOE_LAUNCH(dispatch_scatter_kernel, ntiles, DT_THREADS, sm2, st, ids, R, p->k, E, tile, ntiles, ws_tile_counts,
              out->expert_counts, out->expert_offsets, out->expert_token_indices, out->token_index_map, out->row_slot,
              p->rows, p->check_routing ? status : nullptr);
