@@ -51,7 +51,12 @@
 namespace moeb {
 
 enum TcKind { TC_FWD_UP = 0, TC_FWD_DOWN = 1, TC_BWD_DH = 2, TC_BWD_DX = 3, TC_DW3 = 4, TC_DW12 = 5, TC_ROUTE = 6,
-              TC_BWD_DH_LK = 7 };
+              TC_BWD_DH_LK = 7, TC_ROUTE_S = 8 };
+// K1 in two smem layouts: TC_ROUTE (any E <= 256: 32 KB of W_g rows per stage, 4 stages) and
+// TC_ROUTE_S (E <= 64: 8 KB per stage, 8 stages).  With T / 128 CTAs (fewer than the SMs at
+// the benchmark shapes) each CTA streams its tokens' X rows, so the bytes in flight per SM
+// set the pace
+__host__ __device__ constexpr bool is_route(int k) { return k == TC_ROUTE || k == TC_ROUTE_S; }
 // BWD_DH comes in two forms: TC_BWD_DH (4 epilogue warps, 32-column chunks, 4 stages; the
 // 1-CTA engines and the cp.async epilogue) and TC_BWD_DH_LK (16-column chunks: 128
 // registers, so 8 epilogue warps fit; 4 stages) -- the CTA-pair default for every d >=
@@ -123,7 +128,7 @@ constexpr int GATHER_THREADS = 128;
 template <int CG, int KIND = 0>
 struct CgCfg {
   static constexpr int TM = 128 * CG;                   // tile rows per CTA group
-  static constexpr int B_BYTES = (TBN / CG) * TBK * 2;  // B per CTA per stage
+  static constexpr int B_BYTES = (KIND == TC_ROUTE_S ? 64 : TBN / CG) * TBK * 2;  // B per CTA per stage
   static constexpr int STAGE = TA_BYTES + B_BYTES;
   // BWD_DH shares smem between its mainloop ring and the epilogue A/B ring (tools/tune_variants.sh:
   // 4 stages + 4-deep ring beat 3 + 7 by 11 % on the Mixtral layer)
@@ -131,7 +136,7 @@ struct CgCfg {
   static constexpr bool LK = (KIND == TC_BWD_DH_LK) && MOEB_DH_TMA;
   static constexpr int NEPI = n_epi(KIND);
   static constexpr int STAGES = DH ? (CG == 1 ? 2 : (LK ? (NEPI == 8 ? MOEB_DH8_STAGES : MOEB_DH_STAGES) : MOEB_DH_STAGES_SK))
-                                   : (CG == 1 ? 4 : (NEPI == 8 ? 5 : 6));
+                                   : (KIND == TC_ROUTE_S ? 8 : CG == 1 ? 4 : (NEPI == 8 ? 5 : 6));
   static constexpr int DH_NBUF = LK ? (NEPI == 8 ? MOEB_DH8_NBUF : MOEB_DH_NBUF) : MOEB_DH_NBUF_SK;  // BWD_DH: A/B ring per warp
   // BWD_DH epilogue chunk: 16 columns (TMA boxes of 32 rows x 32 B, 32-byte swizzle) in the
   // TMA epilogue, 32 in the cp.async one; a slot holds the A and the B chunk
@@ -185,7 +190,7 @@ struct KindTraits;
 // row kinds in the CTA-pair engine take their tiles from the dynamic scheduler
 template <int KIND, int CG>
 __host__ __device__ constexpr bool dyn_sched() {
-  return MOEB_DYN && CG == 2 && KIND != TC_ROUTE && KIND != TC_DW3 && KIND != TC_DW12;
+  return MOEB_DYN && CG == 2 && !is_route(KIND) && KIND != TC_DW3 && KIND != TC_DW12;
 }
 constexpr int SCHED_RING = 4;  // tiles published ahead by the scheduler
 // N = 128 tail tiles (N = h, B = MN-major panels of 64 columns, CTA pair) when at most
@@ -235,7 +240,7 @@ __device__ __forceinline__ bool decode_tile(int tile, const TcParams& P, const i
   using K = KindTraits<KIND>;
   constexpr int TM = CgCfg<CG>::TM;
   if (tile < 0) return false;
-  if constexpr (KIND == TC_ROUTE) {
+  if constexpr (is_route(KIND)) {
     if (tile * TM >= P.T) return false;
     t.e = 0;
     t.seg0 = 0;
@@ -470,7 +475,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
   const int cluster_id = (CG == 2) ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
   const int n_clusters = (CG == 2) ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
-  if constexpr (KIND != TC_ROUTE)
+  if constexpr (!is_route(KIND))
     for (int i = threadIdx.x; i <= E; i += tc_threads(KIND)) s_offs[i] = P.offs[i];
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch(&mA0);
@@ -506,7 +511,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
     else ptx::tmem_alloc(tmem_holder, 512);
   }
   __syncthreads();
-  if (!K::wgrad && KIND != TC_ROUTE && threadIdx.x == 0) {
+  if (!K::wgrad && !is_route(KIND) && threadIdx.x == 0) {
     int s = 0;
     for (int e = 0; e < E; ++e) {
       s_mstart[e] = s;
@@ -564,7 +569,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
         uint64_t* bar = &full[stage];
         const uint32_t bar_c = (CG == 2) ? ptx::mapa(ptx::smem_u32(bar), 0) : 0u;
         if (lane == 0) {
-          if constexpr (KIND == TC_ROUTE) {
+          if constexpr (is_route(KIND)) {
             ptx::mbar_arrive_expect_tx(bar, (uint32_t)(TA_BYTES + P.route_n * 128));
           } else if constexpr (CG == 1) {
             ptx::mbar_arrive_expect_tx(bar, tma_bytes_per_cta<KIND, CPA, CG>());
@@ -581,7 +586,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
           else ptx::tma_load_2d(dst, m, bar, c0, c1);
         };
         const int k0 = kb * TBK;
-        if constexpr (KIND == TC_ROUTE) {
+        if constexpr (is_route(KIND)) {
           if (lane == 0) load(sA, &mA0, k0, t.m0);
           if (lane == 1) load(sB, &mB0, k0, 0);
         } else if constexpr (KIND == TC_FWD_UP) {
@@ -764,7 +769,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
       int as = 0;
       uint32_t aphase = 0;
       TileInfo t;
-      const uint32_t idesc = (KIND == TC_ROUTE) ? P.route_idesc : IDESC;
+      const uint32_t idesc = is_route(KIND) ? P.route_idesc : IDESC;
       const uint32_t tb = __shfl_sync(0xffffffffu, tmem_base, 0);
       const uint32_t s0 = ptx::smem_u32(smem);
       const uint32_t empty0 = ptx::smem_u32(empty);
@@ -909,7 +914,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
         } else if constexpr (is_dh(KIND)) {
           asm volatile("cp.async.wait_all;" ::: "memory");
         }
-      } else if constexpr (KIND == TC_ROUTE) {
+      } else if constexpr (is_route(KIND)) {
         // one token row per thread: logits out, softmax, top-k (desc, ties -> lower id)
         const int r = t.m0 + row;
         const bool valid = r < P.T;
@@ -1498,6 +1503,7 @@ moe_status tc_route(const moe_problem* p, const void* x, const void* wg, float* 
   P.route_idesc = ptx::umma_idesc_bf16(128, P.route_n, 0, 0);
   CUtensorMap a0, b0;
   if (!make_map(&a0, x, p->T, p->d, 64, 128) || !make_map(&b0, wg, p->E, p->d, 64, P.route_n)) return MOE_ERR_CUDA;
+  if (P.route_n <= 64) return launch_tc_impl<TC_ROUTE_S, false, 1>(a0, a0, b0, b0, P, ceil_div(p->T, 128), st);
   return launch_tc_impl<TC_ROUTE, false, 1>(a0, a0, b0, b0, P, ceil_div(p->T, 128), st);
 }
 
