@@ -76,6 +76,12 @@ __host__ __device__ constexpr bool is_dh(int k) { return k == TC_BWD_DH || k == 
 #ifndef MOEB_DH_EPI8
 #define MOEB_DH_EPI8 1    // TC_BWD_DH_LK: 8 epilogue warps (two per TMEM lane quarter, 128 columns each)
 #endif
+#ifndef MOEB_UP_EPI8
+// FWD_UP: 8 epilogue warps (16-column chunks; 64 of the 128 A/B columns each).  Parity-green,
+// off: interleaved A/B measured FWD_UP 3-7 % slower (profiles/up8_ab_r01.txt) -- its epilogue
+// already hides under the mainloop, and 32-byte row segments store less efficiently
+#define MOEB_UP_EPI8 0
+#endif
 #ifndef MOEB_RED_EPI8
 // FWD_DOWN / BWD_DX: 8 epilogue warps (128 columns each), 5 mainloop stages.  Parity-green but
 // off: interleaved A/B measured both kinds 1-5 % slower (profiles/red8_ab_r01.txt)
@@ -116,7 +122,8 @@ __host__ __device__ constexpr bool is_dh(int k) { return k == TC_BWD_DH || k == 
 // TMEM lane quarter, each with 128 of the tile's 256 columns; its 16-column chunks keep the
 // kernel at 128 registers, so 16 warps fit the register file)
 __host__ __device__ constexpr int n_epi(int k) {
-  return ((k == TC_BWD_DH_LK && MOEB_DH_EPI8 && MOEB_DH_TMA) || ((k == TC_FWD_DOWN || k == TC_BWD_DX) && MOEB_RED_EPI8))
+  return ((k == TC_BWD_DH_LK && MOEB_DH_EPI8 && MOEB_DH_TMA) || ((k == TC_FWD_DOWN || k == TC_BWD_DX) && MOEB_RED_EPI8) ||
+          (k == TC_FWD_UP && MOEB_UP_EPI8))
              ? 8 : 4;
 }
 __host__ __device__ constexpr int tc_threads(int k) { return 32 * (8 + n_epi(k)); }
@@ -143,7 +150,7 @@ struct CgCfg {
   static constexpr int DH_CW = LK ? 16 : 32;
   static constexpr int DH_SLOT = 2 * 32 * DH_CW * 2;
   // epilogue staging bytes per warp (BWD_DH: the A/B ring + two wU tiles)
-  static constexpr int STG_WARP = DH ? (DH_NBUF * DH_SLOT + DH_SLOT) : 6144;
+  static constexpr int STG_WARP = DH ? (DH_NBUF * DH_SLOT + DH_SLOT) : ((KIND == TC_FWD_UP && NEPI == 8) ? 3072 : 6144);
   // 1024-aligned: the BWD_DH tiles are TMA boxes in the 64-byte swizzle, whose pattern is
   // taken from the smem address bits
   static constexpr int STG_OFF = (STAGES * STAGE + 1024 /*barriers*/ + 2176 /*offsets, tile starts*/ + 1023) / 1024 * 1024;
@@ -975,6 +982,54 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
             P.ids[(int64_t)r * P.k + j] = sel_e[j];
             P.route_w[(int64_t)r * P.k + j] = P.renorm ? sel_p[j] / wsum : sel_p[j];
           }
+        }
+      } else if constexpr (KIND == TC_FWD_UP && C::NEPI == 8) {
+        // 8 warps: this warp's 32 rows x (gated) columns hc*64 .. +63 of A (TMEM 0-127) and of
+        // B (TMEM 128-255), or (non-gated) columns cb .. cb+127 of A; 16-column chunks through
+        // three 32 x 16 swizzled tiles (A, B, U)
+        const int r0w = t.m0 + rowoff + wq * 32;
+        const int nvalid = max(0, min(32, t.seg1 - r0w));
+        uint8_t* T0 = stg;
+        uint8_t* T1 = stg + 1024;
+        uint8_t* T2 = stg + 2048;
+        const bool gated = P.act == 0;
+        const int cbeg = gated ? hc * 64 : cb, cend = gated ? cbeg + 64 : cb + NCW;
+#pragma unroll 1
+        for (int c = cbeg; c < cend; c += 16) {
+          if (!gated && t.n0 + c >= P.h) break;
+          uint32_t va[16], vb[16];
+          ptx::tmem_ld16(tb + c, va);
+          if (gated) ptx::tmem_ld16(tb + 128 + c, vb);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            uint32_t oa[4], ob[4], ou[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float a0 = __uint_as_float(va[8 * q + 2 * e]), a1 = __uint_as_float(va[8 * q + 2 * e + 1]);
+              oa[e] = ptx::pack_bf16(a0, a1);
+              if (gated) {
+                const float b0 = __uint_as_float(vb[8 * q + 2 * e]), b1 = __uint_as_float(vb[8 * q + 2 * e + 1]);
+                ob[e] = ptx::pack_bf16(b0, b1);
+                ou[e] = ptx::pack_bf16(a0 * sigmoid_fast(a0) * b0, a1 * sigmoid_fast(a1) * b1);
+              } else {
+                ob[e] = 0u;
+                ou[e] = ptx::pack_bf16(act_fwd(P.act, a0, sigmoid_fast(a0)), act_fwd(P.act, a1, sigmoid_fast(a1)));
+              }
+            }
+            *reinterpret_cast<uint4*>(T0 + stg8_off(lane, q)) = make_uint4(oa[0], oa[1], oa[2], oa[3]);
+            if (gated) *reinterpret_cast<uint4*>(T1 + stg8_off(lane, q)) = make_uint4(ob[0], ob[1], ob[2], ob[3]);
+            *reinterpret_cast<uint4*>(T2 + stg8_off(lane, q)) = make_uint4(ou[0], ou[1], ou[2], ou[3]);
+          }
+          __syncwarp();
+          if (nvalid > 0) {
+            // output column of A/B/U: n0 counts A columns (stacked tiles: n0 = n_tile * 128)
+            const int64_t o = (int64_t)r0w * P.h + t.n0 + c;
+            stg8_store_bf16(T0, lane, P.a_save + o, P.h, nvalid);
+            if (gated) stg8_store_bf16(T1, lane, P.b_save + o, P.h, nvalid);
+            stg8_store_bf16(T2, lane, P.u + o, P.h, nvalid);
+          }
+          __syncwarp();
         }
       } else if constexpr (KIND == TC_FWD_UP) {
         const int r0w = t.m0 + rowoff + wq * 32;  // first row of this warp
