@@ -280,11 +280,17 @@ def main():
     torch.cuda.synchronize()
     wall0 = time.time()
     ev0.record(st)
+    step_ev = []
     for _ in range(args.steps):
         step()
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(st)
+        step_ev.append(e)
     ev1.record(st)
     torch.cuda.synchronize()
     wall1 = time.time()
+    bounds = [ev0] + step_ev
+    per_step = [bounds[i].elapsed_time(bounds[i + 1]) for i in range(len(step_ev))]
     if use_ep:
         dist.barrier()
     L.profile_enable(False)
@@ -410,6 +416,8 @@ def main():
                            x.numel() * 2 / 1e6)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "gpu_launches_per_step": launches / args.steps, "clocks": clk,
+            "step_ms": {"median": round(statistics.median(per_step), 4), "min": round(min(per_step), 4),
+                        "max": round(max(per_step), 4), "note": "per-step CUDA events inside the timed region, rank 0"},
             "sm_topology": {"sm_per_die": L.sm_topology()[1], "use": "die split of the expert-GEMM tile lists"},
             "peak_activation_gb": mem["ours"]["peak_gb"] if mem else None, "memory": mem,
         }
