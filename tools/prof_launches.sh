@@ -5,7 +5,7 @@
 TAG=${1:-r01}; FULL=${2:-}
 mkdir -p gpurun_out
 for W in mixtral deepseek; do
-  timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+  timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors_srcunit_ltcfabric.sum,sm__cycles_elapsed.avg.per_second --clock-control none \
     --csv --log-file gpurun_out/launches_${TAG}_${W}.csv \
     python bench.py --workload $W --steps 1 --warmup 1 --no-cpu-baseline --no-memory > gpurun_out/launches_${TAG}_${W}.log 2>&1
 done
