@@ -921,6 +921,61 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
         } else if constexpr (is_dh(KIND)) {
           asm volatile("cp.async.wait_all;" ::: "memory");
         }
+      } else if constexpr (KIND == TC_ROUTE_S) {
+        // E <= 64: the token's logits are read from TMEM once into registers; max,
+        // softmax denominator and the top-k scans (desc, ties -> lower id) run on them
+        const int r = t.m0 + row;
+        const bool valid = r < P.T;
+        uint32_t v1[32];
+        ptx::tmem_ld32(tb, v);
+        if (P.route_n > 32) ptx::tmem_ld32(tb + 32, v1);
+        ptx::tmem_wait_ld();
+        float lg[64];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          lg[i] = i < E ? __uint_as_float(v[i]) : -INFINITY;
+          lg[32 + i] = (32 + i < E && P.route_n > 32) ? __uint_as_float(v1[i]) : -INFINITY;
+        }
+        float mx = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < 64; ++i) mx = fmaxf(mx, lg[i]);
+        if (valid) {
+#pragma unroll
+          for (int i = 0; i < 64; ++i)
+            if (i < E) P.logits[(int64_t)r * E + i] = lg[i];
+        }
+        float sum = 0.f;
+#pragma unroll
+        for (int i = 0; i < 64; ++i)
+          if (i < E) sum += expf(lg[i] - mx);
+        uint64_t taken = 0;
+        float wsum = 0.f;
+        int sel_e[16];
+        float sel_p[16];
+#pragma unroll 1
+        for (int j = 0; j < P.k; ++j) {
+          float bv = -INFINITY;
+          int be = 0x7fffffff;
+#pragma unroll
+          for (int i = 0; i < 64; ++i) {
+            if (i < E && !((taken >> i) & 1ull) && (lg[i] > bv || (lg[i] == bv && i < be))) {
+              bv = lg[i];
+              be = i;
+            }
+          }
+          taken |= 1ull << be;
+          const float pr = expf(bv - mx) / sum;
+          sel_e[j] = be;
+          sel_p[j] = pr;
+          wsum += pr;
+        }
+        if (valid) {
+#pragma unroll 1
+          for (int j = 0; j < P.k; ++j) {
+            P.ids[(int64_t)r * P.k + j] = sel_e[j];
+            P.route_w[(int64_t)r * P.k + j] = P.renorm ? sel_p[j] / wsum : sel_p[j];
+          }
+        }
       } else if constexpr (is_route(KIND)) {
         // one token row per thread: logits out, softmax, top-k (desc, ties -> lower id)
         const int r = t.m0 + row;
