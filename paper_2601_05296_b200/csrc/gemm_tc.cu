@@ -108,6 +108,9 @@ __host__ __device__ constexpr bool is_dh(int k) { return k == TC_BWD_DH || k == 
 // step 2 % slower with it (every kind, not only the two it changes) and DeepSeek neutral
 #define MOEB_MTAIL 0
 #endif
+#ifndef MOEB_DYN_WG
+#define MOEB_DYN_WG 1     // the weight-gradient kinds (DW3, DW12) on the dynamic scheduler too
+#endif
 #ifndef MOEB_DYN
 #define MOEB_DYN 1        // row-kind tiles from the die-aware dynamic scheduler (0: static cluster-strided order)
 #endif
@@ -197,7 +200,7 @@ struct KindTraits;
 // row kinds in the CTA-pair engine take their tiles from the dynamic scheduler
 template <int KIND, int CG>
 __host__ __device__ constexpr bool dyn_sched() {
-  return MOEB_DYN && CG == 2 && !is_route(KIND) && KIND != TC_DW3 && KIND != TC_DW12;
+  return MOEB_DYN && CG == 2 && !is_route(KIND) && (MOEB_DYN_WG || (KIND != TC_DW3 && KIND != TC_DW12));
 }
 constexpr int SCHED_RING = 4;  // tiles published ahead by the scheduler
 // N = 128 tail tiles (N = h, B = MN-major panels of 64 columns, CTA pair) when at most
@@ -257,20 +260,28 @@ __device__ __forceinline__ bool decode_tile(int tile, const TcParams& P, const i
     t.n_tile = 0;
     t.nk = P.d / TBK;
   } else if constexpr (K::wgrad) {
-    const int per_e = P.m_tiles * P.n_tiles;
-    if (tile >= P.E * per_e) return false;
-    t.e = tile / per_e;
-    const int rem = tile - t.e * per_e;
+    // tile lists as for the row kinds: die 0 = every expert's n-tiles [0, ns), die 1 the rest
+    const int ns = dyn_sched<KIND, CG>() ? P.n_split : P.n_tiles;
+    int nt = ns, nlo = 0, local = tile;
+    if (tile >= P.E * P.m_tiles * ns) {
+      nt = P.n_tiles - ns;
+      nlo = ns;
+      local = tile - P.E * P.m_tiles * ns;
+      if (local >= P.E * P.m_tiles * nt) return false;
+    }
+    const int per_e = P.m_tiles * nt;
+    t.e = local / per_e;
+    const int rem = local - t.e * per_e;
     int mt;
     if constexpr (KIND == TC_DW3) {
       // m fastest: the concurrent tiles share the B n-tile (wU rows, h wide: the
       // larger operand) and re-read the small gathered dY from L2
-      t.n_tile = rem / P.m_tiles;
-      mt = rem - t.n_tile * P.m_tiles;
+      t.n_tile = nlo + rem / P.m_tiles;
+      mt = rem - (rem / P.m_tiles) * P.m_tiles;
     } else {
       // n fastest: DW12's A ([dA|dB], 2h wide) is the larger operand
-      mt = rem / P.n_tiles;
-      t.n_tile = rem - mt * P.n_tiles;
+      mt = rem / nt;
+      t.n_tile = nlo + (rem - mt * nt);
     }
     t.m0 = mt * TM;
     t.n0 = t.n_tile * TBN;
@@ -832,7 +843,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
     // die's list, and publishes each into both CTAs' rings; -1 ends the stream.
     if constexpr (DYN) {
       if (leader && lane == 0) {
-        const int Mt = s_mstart[E];
+        const int Mt = K::wgrad ? E * P.m_tiles : s_mstart[E];  // m-tiles over all experts
         const int cnt[2] = {Mt * P.n_split, Mt * (P.n_tiles - P.n_split)};
         const int my = P.die_map ? (int)P.die_map[ptx::smid() & 255] : 0;
         int src = my;
