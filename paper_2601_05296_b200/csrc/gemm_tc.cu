@@ -9,7 +9,7 @@
 //               accumulator
 //   warp 2      TMEM allocator (512 columns = 2 accumulator stages x 256); in
 //               the leader CTA of a pair, lane 0 then runs the die-aware dynamic
-//               tile scheduler of the row kinds (tiles published through a ring
+//               tile scheduler of the expert GEMMs (tiles published through a ring
 //               in both CTAs' shared memory; topology.cu measures the SM -> die map)
 //   warp 3      (CTA pair) relays cp.async-gather completion to the leader
 //   warps 4-7   epilogue: tcgen05.ld, one accumulator row per thread
