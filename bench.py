@@ -318,13 +318,16 @@ def main():
         peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
         traffic = None
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        tsrc = "profiles/ncu_traffic.json"
         if os.path.exists(tp):
-            traffic = json.load(open(tp)).get(args.workload, {}).get(dom)
+            tj = json.load(open(tp))
+            traffic = tj.get(args.workload, {}).get(dom)
+            tsrc = tj.get("source", tsrc)
         all_flops = ((18 if gated else 12) + (flop_factor("FWD_UP", gated) if args.checkpoint == "none" else 0)) \
             * R * cfg.d * cfg.h
         roof = {"bound": "tensor", "kernel": f"tc_gemm_kernel<{dom}>", "achieved": round(achieved, 1),
                 "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                "traffic_source": "profiles/ncu_traffic.json: dram__bytes_read.sum + dram__bytes_write.sum per launch "
+                "traffic_source": f"{tsrc}: dram__bytes_read.sum + dram__bytes_write.sum per launch "
                                   "(ncu launch list, same workload)" if traffic else None,
                 "algorithmic_bytes": alg_bytes(dom, cfg.T, R, cfg.d, cfg.h, cfg.E, gated),
                 "peak_source": f"{peaks['source']} bf16 sustained (kernel timed inside the step)",
