@@ -38,13 +38,14 @@ __device__ __forceinline__ float4 ld_acc4<__nv_bfloat16>(const __nv_bfloat16* p)
 }
 
 // ---------------------------------------------------------------- RDX
-// 256 threads: warp w reads TMEM lane quadrant w & 3, column half w >> 2.
+// 256 threads: warp w reads TMEM lane quadrant w & 3, column half w >> 2.  Two CTAs per SM
+// (<= 128 registers, 2 x 99 KB smem, 2 x 256 TMEM columns) keep twice the accumulator rows in flight.
 // smem: [A_hi 16 KB][A_lo 16 KB][B 32 KB: 4 MN-major panels of 64 cols x 64 e][staging 8 x 4 KB][barriers]
 constexpr int RDX_THREADS = 256;
 constexpr int RDX_SMEM = 16384 * 2 + 32768 + 8 * 4096 + 64 + 1024;
 
 template <bool LOAD, typename A>
-__global__ void __launch_bounds__(RDX_THREADS, 1)
+__global__ void __launch_bounds__(RDX_THREADS, 2)
 router_dx_tc_kernel(const __grid_constant__ CUtensorMap mDh, const __grid_constant__ CUtensorMap mDl,
                     const __grid_constant__ CUtensorMap mWg, const A* __restrict__ acc, const int32_t* __restrict__ tim,
                     int k, int64_t Tn, int d, int E, void* __restrict__ out_) {
