@@ -44,21 +44,34 @@ __global__ void router_bwd_kernel(const float* __restrict__ logits, const int32_
 #pragma unroll
   for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   const float inv = 1.f / s;
-  // selected probabilities and dsel (all lanes compute the same k values)
-  float psum = 0.f, dgw = 0.f;
-  for (int j = 0; j < k; ++j) psum += expf(l[ids[t * k + j]] - m) * inv;
-  if (renorm)
-    for (int j = 0; j < k; ++j) dgw += dg[t * k + j] * (expf(l[ids[t * k + j]] - m) * inv / psum);
-  // <p, dp> = sum_j p_sel_j dsel_j
-  float pdp = 0.f;
-  for (int j = 0; j < k; ++j) {
-    float ds = renorm ? (dg[t * k + j] - dgw) / psum : dg[t * k + j];
-    pdp += expf(l[ids[t * k + j]] - m) * inv * ds;
+  // the k routed slots side by side: lane j < k holds slot j (ids, dg, p_sel), so the
+  // sums over slots are warp reductions instead of k dependent load chains
+  int id_j = -1;
+  float p_j = 0.f, dg_j = 0.f;
+  if (lane < k) {
+    id_j = ids[t * k + lane];
+    dg_j = dg[t * k + lane];
+    p_j = id_j >= 0 ? expf(l[id_j] - m) * inv : 0.f;
   }
-  for (int e = lane; e < E; e += 32) {
+  auto wsum = [](float v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+  };
+  const float psum = wsum(p_j);
+  const float dgw = renorm ? wsum(dg_j * (p_j / psum)) : 0.f;
+  const float ds_j = lane < k ? (renorm ? (dg_j - dgw) / psum : dg_j) : 0.f;
+  // <p, dp> = sum_j p_sel_j dsel_j
+  const float pdp = wsum(p_j * ds_j);
+  for (int e0 = 0; e0 < E; e0 += 32) {  // warp-uniform trip count: the shuffles see all lanes
+    const int e = e0 + lane;
     float dp = 0.f;
-    for (int j = 0; j < k; ++j)
-      if (ids[t * k + j] == e) dp = renorm ? (dg[t * k + j] - dgw) / psum : dg[t * k + j];
+    for (int j = 0; j < k; ++j) {
+      const int idj = __shfl_sync(0xffffffffu, id_j, j);
+      const float dsj = __shfl_sync(0xffffffffu, ds_j, j);
+      if (idj == e) dp = dsj;
+    }
+    if (e >= E) continue;
     float p = expf(l[e] - m) * inv;
     const float v = p * (dp - pdp);
     dlogits[t * E + e] = v;
