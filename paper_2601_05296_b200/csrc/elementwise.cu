@@ -12,17 +12,23 @@
 
 namespace moeb {
 
+// g lanes (1 or 32, chosen by the launcher) per routed slot f: the
+// slot's partials row is read contiguously by the group and tree-summed (fixed order)
 __global__ void dg_reduce_kernel(const float* __restrict__ part, int nparts, const int32_t* __restrict__ tim,
-                                 int64_t R, float* __restrict__ dg) {
-  int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= R) return;
-  const int r = tim[f];
+                                 int64_t R, float* __restrict__ dg, int g) {
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t f = gt / g;
+  const int sub = (int)(gt % g);
   float s = 0.f;
-  if (r >= 0) {  // r < 0: empty slot (sparse slots) -> no routed row, zero gradient
-    const float* p = part + (int64_t)r * nparts;
-    for (int i = 0; i < nparts; ++i) s += p[i];
+  if (f < R) {
+    const int r = tim[f];
+    if (r >= 0) {  // r < 0: empty slot (sparse slots) -> no routed row, zero gradient
+      const float* p = part + (int64_t)r * nparts;
+      for (int i = sub; i < nparts; i += g) s += p[i];
+    }
   }
-  dg[f] = s;
+  for (int o = g >> 1; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);  // stays inside the group
+  if (f < R && sub == 0) dg[f] = s;
 }
 
 // one warp per token
@@ -422,7 +428,10 @@ __global__ void combine_rows_kernel(const T* __restrict__ rows, const int32_t* _
 // ----------------------------------------------------------------- launchers
 moe_status launch_dg_reduce(const float* part, int nparts, const int32_t* tim, int64_t R, float* dg, cudaStream_t st) {
   if (R == 0) return MOE_OK;
-  MOE_LAUNCH(dg_reduce_kernel, (unsigned)ceil_div(R, 256), 256, 0, st, part, nparts, tim, R, dg);
+  // a warp per slot only for long rows (Mixtral-like h: 112 partials, 16.4 -> 9.4 us);
+  // short rows keep a thread per slot (DeepSeek-like, 11 partials: 7.6 us vs 12.4 at g = 16)
+  const int g = nparts >= 32 ? 32 : 1;
+  MOE_LAUNCH(dg_reduce_kernel, (unsigned)ceil_div(R * g, 256), 256, 0, st, part, nparts, tim, R, dg, g);
   return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
 }
 
