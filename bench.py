@@ -11,6 +11,11 @@ Mixtral-like layer (BASELINE.json configs[1]); N > 1 runs the same per-GPU
 workload expert-parallel over NCCL all-to-all (weak scaling).
 
 Prints ONE JSON line on rank 0.  See DESIGN.md §Measurement for every key.
+
+--gpus N > 1 without a torchrun environment re-launches this script under
+torch.distributed.run (N ranks, one per GPU, NCCL, 127.0.0.1); under torchrun
+the world size must equal --gpus.  `value` is the whole-job aggregate (tokens
+of all ranks / max-over-ranks step time), `value_per_gpu` the same / N.
 """
 from __future__ import annotations
 
@@ -165,6 +170,16 @@ def oracle_tokens_per_s(inp_host, cfg, budget_s=15.0, min_tokens=64, fixed_token
     return S / t, S, t, threads
 
 
+def blas_info():
+    """BLAS vendor / threads of the NumPy the oracle runs on (threadpoolctl)."""
+    try:
+        from threadpoolctl import threadpool_info
+        return [{k: i.get(k) for k in ("internal_api", "num_threads", "version", "architecture")}
+                for i in threadpool_info() if i.get("user_api") == "blas"]
+    except Exception as exc:  # report, never fake
+        return repr(exc)[:200]
+
+
 def host_f64(inp):
     import numpy as np
     return {n: v.detach().to("cpu", torch.float32).numpy().astype(np.float64) for n, v in inp.items()}
@@ -185,14 +200,19 @@ def main():
     ap.add_argument("--ep", action="store_true", help="use the expert-parallel path even at N = 1")
     ap.add_argument("--retain-recv-x", action="store_true",
                     help="EP: keep the received X rows from forward for dW1/dW2 (one a2a unit less, more memory)")
-    ap.add_argument("--checkpoint", default="ab", choices=["ab", "none"],
-                    help="activation checkpoint policy: ab = save A, B (paper); none = recompute A, B in backward")
+    ap.add_argument("--checkpoint", default="ab", choices=["ab", "none", "abu"],
+                    help="activation checkpoint policy: ab = save A, B (paper, P:213); none = recompute A, B in "
+                         "backward; abu = Alg. 1 literally (save A, B and wU, P:231)")
     ap.add_argument("--activation", default="swiglu", choices=["swiglu", "silu", "relu"],
                     help="expert FFN: SwiGLU (P:190) or the non-gated W2 sigma(W1 x) of P:75")
     ap.add_argument("--deterministic", action="store_true",
                     help="ordered token-side combine of the k expert outputs (bitwise reproducible, NEXT-4)")
+    ap.add_argument("--launch-check", action="store_true",
+                    help="test hook: start the ranks (gloo, CPU), check the world, print one JSON line, exit")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args.gpus)
 
     global torch
     import torch
@@ -203,6 +223,10 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     cfg = CONFIGS[args.workload]
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (launch one rank per GPU)")
+    if args.launch_check:
+        return launch_check(rank, world)
 
     if args.impl == "reference":
         return run_reference(args, cfg, rank, world)
@@ -216,6 +240,9 @@ def main():
         os.environ.setdefault("RANK", "0")
         os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=dev)
+        if rank == 0:
+            print(f"bench.py: NCCL process group up, world {dist.get_world_size()}, "
+                  f"nccl {'.'.join(map(str, torch.cuda.nccl.version()))}", file=sys.stderr, flush=True)
     from paper_2601_05296_b200 import build as B
     if rank == 0 or world == 1:
         B.build()
@@ -304,6 +331,7 @@ def main():
         ms = float(t.item())
     ms_step = ms / args.steps
     value = world * cfg.T / (ms_step / 1e3)
+    a2a_probe = probe_a2a(dev, world, ep, cfg) if ep is not None and world > 1 else None
 
     # ----------------------------------------------------------------- roofline of the dominant kernel
     peaks = load_peaks()
@@ -397,7 +425,7 @@ def main():
         try:
             host = host_f64({n: inp[n] for n in ("x", "w_gate", "w1", "w2", "w3", "dy")})
             tps, S, secs, threads = oracle_tokens_per_s(host, cfg, budget_s=args.cpu_budget_s, activation=act)
-            cpu = {"value": round(tps, 3), "unit": UNIT, "cores": threads, "kind": "oracle",
+            cpu = {"value": round(tps, 3), "unit": UNIT, "cores": threads, "kind": "oracle", "blas": blas_info(),
                    "sample": f"{S} of {cfg.T} tokens of the {cfg.name} layer, full weights, fwd+bwd incl. router, "
                              f"fp64 NumPy, {secs:.1f} s", "host_cpus": os.cpu_count()}
             del host
@@ -406,27 +434,91 @@ def main():
 
     if rank == 0:
         out = {
-            "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": METRIC, "value": round(value, 1), "value_per_gpu": round(value / world, 1), "unit": UNIT,
+            "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded, moe_inputs)",
-            "config": {"workload": cfg.name, "T_per_gpu": cfg.T, "d": cfg.d, "h": cfg.h, "E": cfg.E, "k": cfg.k,
-                       "renormalize": renorm, "checkpoint": args.checkpoint, "activation": act,
-                       "deterministic": det,
-                       "parallelism": f"ep{world}" if ep is not None else "single-GPU",
-                       **({"retain_recv_x": True} if args.retain_recv_x else {}),
-                       "l2": "no flush: inputs larger than L2 (weights %.2f GB + X %.0f MB vs 126 MB L2)" % (
-                           (3 if gated else 2) * w1.numel() * 2 * (world if world > 1 else 1) / 1e9,
-                           x.numel() * 2 / 1e6)},
+            "config": config_dict(args, cfg, world, ep is not None),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "gpu_launches_per_step": launches / args.steps, "clocks": clk,
             "step_ms": {"median": round(statistics.median(per_step), 4), "min": round(min(per_step), 4),
                         "max": round(max(per_step), 4), "note": "per-step CUDA events inside the timed region, rank 0"},
             "sm_topology": {"sm_per_die": L.sm_topology()[1], "use": "die split of the expert-GEMM tile lists"},
-            "peak_activation_gb": mem["ours"]["peak_gb"] if mem else None, "memory": mem,
+            "peak_activation_gb": mem["ours"]["activation_peak_gb"] if mem else None, "memory": mem,
+            "a2a_probe": a2a_probe,
+            "nccl": ({"world": world, "version": ".".join(map(str, torch.cuda.nccl.version())),
+                      "backend": dist.get_backend()} if use_ep else None),
         }
         print(json.dumps(out), flush=True)
     if use_ep:
         dist.destroy_process_group()
+
+
+def relaunch(n):
+    """--gpus N without a torchrun environment: run this script as N ranks."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    print("bench.py: launching", " ".join(cmd[1:]), file=sys.stderr, flush=True)
+    raise SystemExit(subprocess.call(cmd))
+
+
+def launch_check(rank, world):
+    """--launch-check: the multi-rank plumbing of this script without a GPU (gloo)."""
+    import torch.distributed as dist
+    dist.init_process_group("gloo")
+    t = torch.tensor([rank + 1])
+    dist.all_reduce(t)
+    if rank == 0:
+        print(json.dumps({"launch_check": True, "n_gpus": world, "rank_sum": int(t.item()),
+                          "local_ranks": int(os.environ.get("LOCAL_WORLD_SIZE", "1"))}), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def config_dict(args, cfg, world, ep_path):
+    """The `config` of the JSON line, identical for both arms (--impl ours / reference)."""
+    gated = args.activation == "swiglu"
+    w_gb = (3 if gated else 2) * cfg.E * cfg.h * cfg.d * 2 / 1e9 / (world if ep_path else 1)  # per rank
+    return {"workload": cfg.name, "T_per_gpu": cfg.T, "d": cfg.d, "h": cfg.h, "E": cfg.E, "k": cfg.k,
+            "renormalize": args.renormalize, "checkpoint": args.checkpoint, "activation": args.activation,
+            "deterministic": args.deterministic,
+            "parallelism": f"ep{world}" if ep_path else "single-GPU",
+            **({"retain_recv_x": True} if args.retain_recv_x else {}),
+            "l2": "no flush: inputs larger than L2 (weights %.2f GB + X %.0f MB vs 126 MB L2)" % (
+                w_gb, cfg.T * cfg.d * 2 / 1e6)}
+
+
+def probe_a2a(dev, world, ep, cfg, iters=10):
+    """SURVEY §8(e) comm roofline: NCCL all_to_all_single of the step's X-row volume
+    (the rows this rank sent in the last step, bf16), timed with CUDA events on the
+    current stream, max over ranks.  algbw = bytes leaving this GPU / time."""
+    import torch.distributed as dist
+    rows = max(int(ep.last_rows_sent), world)
+    rows -= rows % world
+    send = torch.empty(rows, cfg.d, dtype=torch.bfloat16, device=dev)
+    recv = torch.empty_like(send)
+    for _ in range(3):
+        dist.all_to_all_single(recv, send)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        dist.all_to_all_single(recv, send)
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / iters], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    off = send.numel() * 2 * (world - 1) / world
+    return {"bytes_per_rank": send.numel() * 2, "ms": round(ms, 4), "algbw_gbs": round(off / (ms / 1e3) / 1e9, 1),
+            "link_peak_gbs": 900.0, "what": "torch.distributed.all_to_all_single (NCCL), equal splits, "
+                                            "the X-row bytes this rank sent in the last step"}
 
 
 def measure_memory(M, x, wg, w1, w2, w3, dy, k, renorm, act="swiglu", det=False):
@@ -456,15 +548,23 @@ def measure_memory(M, x, wg, w1, w2, w3, dy, k, renorm, act="swiglu", det=False)
         y.backward(dy)
         torch.cuda.synchronize()
         peak = torch.cuda.max_memory_allocated() - base
-        return {"saved_gb": round(sum(seen.values()) / 1e9, 4), "peak_gb": round(peak / 1e9, 4)}
+        grads = sum(p.grad.numel() * p.grad.element_size() for p in params if p is not None and p.grad is not None)
+        del y, xd, params
+        return {"saved_gb": round(sum(seen.values()) / 1e9, 4), "peak_gb": round(peak / 1e9, 4),
+                "param_grad_gb": round(grads / 1e9, 4), "activation_peak_gb": round((peak - grads) / 1e9, 4)}
 
     out = {"method": "torch.autograd.graph.saved_tensors_hooks, unique storages excl. parameters (P:289); "
-                     "peak = max_memory_allocated delta over fwd+bwd"}
+                     "peak = max_memory_allocated delta over fwd+bwd; activation_peak = peak - parameter-gradient "
+                     "bytes (both layers produce the same gradients)"}
     out["ours"] = one(lambda xx, a, b, c, d_: M.moe_layer(xx, a, b, c, d_, k, renorm, "ab", act, det))
     out["ours_checkpoint_none"] = one(lambda xx, a, b, c, d_: M.moe_layer(xx, a, b, c, d_, k, renorm, "none", act, det))
+    out["ours_checkpoint_abu"] = one(lambda xx, a, b, c, d_: M.moe_layer(xx, a, b, c, d_, k, renorm, "abu", act, det))
     try:
         out["materialized_baseline"] = one(lambda xx, a, b, c, d_: materialized_moe(xx, a, b, c, d_, k, renorm, act))
         out["saved_ratio"] = round(out["materialized_baseline"]["saved_gb"] / out["ours"]["saved_gb"], 3)
+        out["peak_ratio"] = round(out["materialized_baseline"]["peak_gb"] / out["ours"]["peak_gb"], 3)
+        out["activation_peak_ratio"] = round(out["materialized_baseline"]["activation_peak_gb"] /
+                                             out["ours"]["activation_peak_gb"], 3)
     except Exception as exc:
         out["materialized_baseline"] = {"error": repr(exc)[:300]}
     return out
@@ -492,10 +592,9 @@ def run_reference(args, cfg, rank, world):
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * tot / args.steps, 2),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic (seeded, moe_inputs)",
-           "config": {"workload": cfg.name, "T_per_gpu": cfg.T, "d": cfg.d, "h": cfg.h, "E": cfg.E, "k": cfg.k,
-                      "renormalize": args.renormalize, "checkpoint": args.checkpoint, "activation": args.activation,
-                      "deterministic": args.deterministic},
+           "config": config_dict(args, cfg, world, world > 1 or args.ep),
            "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": threads, "kind": "oracle",
+                            "blas": blas_info(),
                             "sample": f"{S} of {cfg.T} tokens per step, full weights, fwd+bwd incl. router, "
                                       "fp64 NumPy oracle"},
            "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

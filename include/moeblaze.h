@@ -28,8 +28,10 @@
  *    dtype MOE_FP32: every tensor is fp32 and the arithmetic is true fp32
  *    (CUDA-core FMA, no TF32).
  *  - Argument errors are returned synchronously and nothing is launched:
- *    MOE_ERR_INVALID_ARG (null pointer, bad shape: T < 0, d/h/E/k < 1, k > E,
- *    E > 256, k > 16, T*k >= 2^31), MOE_ERR_UNSUPPORTED (bf16 with d or h not
+ *    MOE_ERR_INVALID_ARG (null pointer, bad shape: T < 0, d/h/E/k < 1, E > 256,
+ *    T*k >= 2^31; with every slot routed (rows = 0) also k > E or k > 16; with
+ *    sparse slots (rows > 0) k <= 256 and k > E is valid, since empty slots are
+ *    -1), MOE_ERR_UNSUPPORTED (bf16 with d or h not
  *    a multiple of 128, fp32 with d not a multiple of 8), MOE_ERR_MISALIGNED,
  *    MOE_ERR_WORKSPACE (ws too small).  Launch failures return MOE_ERR_CUDA.
  *    The library never aborts the process.
@@ -77,8 +79,15 @@ typedef struct {
                              the pre-activations A, B, recompute SiLU in backward;
                              MOE_CKPT_NONE (1) = save nothing but X and the routing: A, B
                              live in ws during moe_ffn_fwd (a_save/b_save may be NULL) and
-                             moe_ffn_bwd recomputes them with the fused up-projection
-                             (+4 T*k*d*h flops; results bit-identical to MOE_CKPT_AB) */
+                             moe_ffn_bwd recomputes them with the fused up-projection into
+                             the caller's a_save/b_save, which are then scratch [R, h]
+                             buffers (+4 T*k*d*h flops; results bit-identical to MOE_CKPT_AB);
+                             MOE_CKPT_ABU (2) = Alg. 1 literally ("Store A, B, Y_swi"):
+                             A, B and the gate-weighted activation wU_r = w_r SiLU(A_r) B_r
+                             are saved (u_save [R, h]); the down projection consumes wU
+                             (y += wU W3, the same sum as w (U W3)), the dW3 GEMM reads the
+                             saved wU and the dH GEMM no longer writes it (+R*h
+                             saved elements, -R*h written in backward) */
   int32_t activation;     /* expert FFN: MOE_ACT_SWIGLU (0, default) =
                              SiLU(x W1) * (x W2) W3; MOE_ACT_SILU (1) / MOE_ACT_RELU (2)
                              = the non-gated expert W2 sigma(W1 x) of P:75 (the paper's SiLU /
@@ -104,7 +113,7 @@ typedef struct {
                              0 <= rows <= T*k. */
 } moe_problem;
 
-enum { MOE_CKPT_AB = 0, MOE_CKPT_NONE = 1 };
+enum { MOE_CKPT_AB = 0, MOE_CKPT_NONE = 1, MOE_CKPT_ABU = 2 };
 enum { MOE_ACT_SWIGLU = 0, MOE_ACT_SILU = 1, MOE_ACT_RELU = 2 };
 
 /* The compact dispatch index structures of §4.1.  R = T*k (or
@@ -138,7 +147,9 @@ typedef struct {
 
 /* Bytes of device scratch `ws` that `op` needs for problem `p` (closed form;
  * with deterministic = 0 it has no T*k*d term: no routed-token buffer exists;
- * deterministic = 1 adds the transient [T*k, d] fp32 row-result buffer). */
+ * deterministic = 1 adds the transient [T*k, d] fp32 row-result buffer).  The
+ * first 256 bytes of the FFN workspaces hold the expert GEMMs' tile-scheduler
+ * claim counters (zeroed on the stream by every call that uses them). */
 moe_status moe_workspace_size(const moe_problem* p, moe_op op, size_t* bytes);
 
 /* Gating.  logits = X W_g^T accumulated in fp32; ids[t,:] = the k
@@ -166,10 +177,12 @@ moe_status moe_dispatch_build(const moe_problem* p, const int32_t* topk_ids, con
  *     y[t] += topk_w[row_slot[r]] * (U_r W3_e)     (combine fused into the down GEMM)
  *   a_save, b_save [T*k, h] dtype: the checkpointed pre-activations A, B in
  *   expert-sorted row order, written (ignored, may be NULL,
- *   under MOE_CKPT_NONE).  y [T,d] dtype, written. */
+ *   under MOE_CKPT_NONE).  u_save [T*k, h] dtype: MOE_CKPT_ABU only (else
+ *   ignored, may be NULL): the saved wU_r = topk_w[row_slot[r]] * U_r, written.
+ *   y [T,d] dtype, written. */
 moe_status moe_ffn_fwd(const moe_problem* p, const void* x, const void* w1, const void* w2,
                        const void* w3, const float* topk_w, const moe_dispatch* disp,
-                       void* a_save, void* b_save, void* y,
+                       void* a_save, void* b_save, void* u_save, void* y,
                        void* ws, size_t ws_bytes, void* stream);
 
 /* Expert backward (§3.2, Alg. 1 FusedBackward P:236-253) with the
@@ -180,28 +193,44 @@ moe_status moe_ffn_fwd(const moe_problem* p, const void* x, const void* w1, cons
  *   dw1[e] = sum_r dA_r^T X[eti[r]],  dw2[e] = sum_r dB_r^T X[eti[r]]
  *   dx[t]  = sum_{r: eti[r]=t} (dA_r W1_e^T + dB_r W2_e^T)  [+ router path]
  * a_save/b_save are read (A, B) and OVERWRITTEN with dA, dB (in place); under
- * MOE_CKPT_NONE they are ignored (may be NULL) and A, B are recomputed in ws.
+ * MOE_CKPT_NONE they are caller-provided scratch [R, h] buffers (contents on
+ * entry ignored) that the recomputed A, B, then dA, dB occupy.  u_save
+ * (MOE_CKPT_ABU only, else ignored) is the saved wU, read by the dW3 GEMM.
  * dw1/dw2/dw3 are written (experts with no rows get zeros), not accumulated.
  * d_topk_w [T,k] fp32 may be NULL only if router is NULL.
  * router != NULL: also computes the router backward (renorm-aware) and adds
  * dlogits W_g into dx; router->dw_gate is written.
- * Launch order on `stream`: dH GEMM (dA, dB, wU, gate-grad partials) -> d_topk_w
- * -> dX GEMM -> router backward / dx finalise -> [sync->dx_ready recorded] ->
- * dW3 GEMM -> [sync->x_ready waited] -> dW1/dW2 GEMM (the only kernel after the
- * optional up-projection recompute that reads x).  `sync` may be NULL. */
+ *
+ * Stages (sync->stages; 0 or NULL sync = all, in the order below).  The three
+ * stages may be issued as separate calls with the SAME ws (its contents carry
+ * wU and the tile counters from one stage to the next), so that a caller can
+ * allocate each weight gradient only when its GEMM runs and release A/B
+ * (then dA/dB) as soon as the last GEMM that reads them is done:
+ *   MOE_BWD_DATA: dH GEMM (dA, dB in place, wU into ws unless ABU, gate-grad
+ *                 partials) -> d_topk_w -> dX GEMM -> router backward / dx
+ *                 finalise [-> sync->dx_ready recorded].  Needs dy, x (router
+ *                 or recompute), w1..w3, dx, d_topk_w; dw1..dw3 may be NULL.
+ *   MOE_BWD_DW3:  dW3 = dy^T wU.  Needs dy and dw3; reads wU (ws or u_save).
+ *   MOE_BWD_DW12: [dW1; dW2] = [dA | dB]^T x (the only kernel after the
+ *                 optional recompute that reads x: [sync->x_ready waited]).
+ * In one call the order is DATA -> DW3 -> DW12 (x_ready lets an expert-parallel
+ * receiver overlap the arrival of x with everything before DW12). */
+enum { MOE_BWD_DATA = 1, MOE_BWD_DW3 = 2, MOE_BWD_DW12 = 4, MOE_BWD_ALL = 7 };
 typedef struct {
   void* x_ready;   /* cudaEvent_t or NULL: the stream waits on it (cudaStreamWaitEvent) before
-                      the first kernel that reads x after the dX GEMM; lets an expert-parallel
+                      the first kernel that reads x after the dX GEMM (the dW1/dW2 GEMM, and
+                      the router's dW_g when router != NULL); lets an expert-parallel
                       receiver overlap the arrival of x with the dH / dX GEMMs.  With
                       MOE_CKPT_NONE x is read at the start (recompute), so x must be ready
                       before the call. */
   void* dx_ready;  /* cudaEvent_t or NULL: recorded once dx and d_topk_w are final, before the
                       weight-gradient GEMMs; lets the caller return dx rows while dW1..3 run. */
+  int32_t stages;  /* MOE_BWD_* mask; 0 = MOE_BWD_ALL */
 } moe_bwd_sync;
 
 moe_status moe_ffn_bwd(const moe_problem* p, const void* dy, const void* x, const void* w1,
                        const void* w2, const void* w3, const float* topk_w,
-                       const moe_dispatch* disp, void* a_save, void* b_save,
+                       const moe_dispatch* disp, void* a_save, void* b_save, void* u_save,
                        void* dx, void* dw1, void* dw2, void* dw3, float* d_topk_w,
                        const moe_router_bwd* router, const moe_bwd_sync* sync,
                        void* ws, size_t ws_bytes, void* stream);
@@ -223,40 +252,56 @@ moe_status moe_router_backward(const moe_problem* p, const float* d_topk_w, cons
  * for the token come back already summed over its experts (one row per
  * (token, rank) pair instead of one per (token, expert) pair).
  *
- * moe_ep_dest: dest[t*P + q] = q if some ids[t, j] is owned by rank q, else -1.
+ * Local pairs never travel: a token's slots owned by its own rank (`self_rank`)
+ * are computed where the token lives.  The receiver's problem has the T local
+ * tokens first (their own-rank slots, moe_ep_local_slots) and the received rows
+ * after them, so the local partial output of token t is row t of its output and
+ * is added by moe_combine_rows as `base`.
+ *
+ * moe_ep_dest: dest[t*P + q] = q if some ids[t, j] is owned by rank q and
+ *   q != self_rank, else -1 (self_rank = -1: no rank excluded).
  *   topk_ids [T,k] (p->T, p->k; p->E = global experts) -> dest [T, P] int32.
  *   moe_dispatch_build over dest (T tokens, "k" = E = P, sparse slots, rows =
  *   number of (token, rank) pairs or any upper bound up to T*P) then yields the
  *   send plan: counts[q] rows to rank q, expert_token_indices = the tokens to
  *   send, grouped by rank, ascending (the send order), token_index_map [T,P] =
  *   send position of (t, q) or -1, row_slot = t*P + q.
+ * moe_ep_local_slots: local_ids[t*k + j] = ids[t,j] - rank*experts_per_rank if
+ *   rank owns ids[t,j] else -1; local_w[t*k + j] = topk_w[t,j] there, else 0:
+ *   the sparse topk_ids / topk_w of the local tokens on their own rank.
  * moe_ep_send_meta: for send row i < n_send (send_row_slot = that row_slot):
  *   send_ids[i*k + j] = ids[t,j] - q*experts_per_rank if rank q owns ids[t,j]
  *   else -1, send_w[i*k + j] = topk_w[t,j] (0 for -1): the receiver's sparse
  *   topk_ids / topk_w.
- * moe_ep_slot_grad: dg[t*k + j] = dg_back[send_pos[t*P + q]*k + j] with q the
- *   owner of ids[t,j]: the gate-weight gradients returned by the owners,
- *   back in (token, slot) order.  dg_back [n_send, k] fp32.
+ * moe_ep_slot_grad: dg[t*k + j] = dg_local[t*k + j] if self_rank owns ids[t,j],
+ *   else dg_back[send_pos[t*P + q]*k + j] with q the owner of ids[t,j]: the
+ *   gate-weight gradients computed locally and returned by the owners, in
+ *   (token, slot) order.  dg_back [n_send, k] fp32 (may be NULL when no slot is
+ *   remote); dg_local [T, k] fp32 (ignored when self_rank = -1).
  * moe_gather_rows: dst[i, :] = src[index[i], :] for i < n (rows of `width`
  *   elements of `elem_bytes` in {2,4}; row bytes a multiple of 4); builds the
  *   all-to-all send buffer in send order.  index entries must be in [0, n_src).
- * moe_combine_rows: out[t, :] = sum_{j<k, tim[t*k+j] >= 0} rows[tim[t*k+j], :]
- *   (fixed j order, fp32 accumulation, dtype output; -1 entries skipped): the
- *   token-side combine of returned rows through token_index_map (P:130-135
- *   "gather its k expert outputs"); with the send plan (k = P) it sums a
- *   token's per-rank partial outputs. */
+ * moe_combine_rows: out[t, :] = base[t, :] + sum_{j<k, tim[t*k+j] >= 0}
+ *   rows[tim[t*k+j], :] (base [T, d] optional, NULL = 0; fixed j order, fp32
+ *   accumulation, dtype output; -1 entries skipped; rows may be NULL only if
+ *   every entry is -1; d % 8 == 0): the token-side combine of returned rows
+ *   through token_index_map ("gather its k expert outputs"); with the
+ *   send plan (k = P) it sums a token's per-rank partial outputs. */
 moe_status moe_ep_dest(const moe_problem* p, const int32_t* topk_ids, int32_t experts_per_rank,
-                       int32_t n_ranks, int32_t* dest, void* stream);
+                       int32_t n_ranks, int32_t self_rank, int32_t* dest, void* stream);
+moe_status moe_ep_local_slots(const moe_problem* p, const int32_t* topk_ids, const float* topk_w,
+                              int32_t experts_per_rank, int32_t rank, int32_t* local_ids, float* local_w,
+                              void* stream);
 moe_status moe_ep_send_meta(const moe_problem* p, const int32_t* topk_ids, const float* topk_w,
                             int32_t experts_per_rank, int32_t n_ranks, const int32_t* send_row_slot,
                             int64_t n_send, int32_t* send_ids, float* send_w, void* stream);
 moe_status moe_ep_slot_grad(const moe_problem* p, const int32_t* topk_ids, int32_t experts_per_rank,
-                            int32_t n_ranks, const int32_t* send_pos, const float* dg_back, float* dg,
-                            void* stream);
+                            int32_t n_ranks, const int32_t* send_pos, const float* dg_back,
+                            const float* dg_local, int32_t self_rank, float* dg, void* stream);
 moe_status moe_gather_rows(const void* src, int64_t n_src, const int32_t* index, int64_t n,
                            int64_t width, int32_t elem_bytes, void* dst, void* stream);
 moe_status moe_combine_rows(const moe_problem* p, const void* rows, const int32_t* token_index_map,
-                            void* out, void* stream);
+                            const void* base, void* out, void* stream);
 
 /* Bench instrumentation.  While enabled, every expert-GEMM launch is
  * bracketed by two CUDA events recorded on the launch stream.

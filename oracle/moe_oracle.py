@@ -186,8 +186,9 @@ def ffn_forward(x, w1, w2, w3, ids, w, disp, activation="swiglu"):
         U_r = SiLU(A_r) * B_r                      (Y_swi)
         O_r = U_r W3_e                             (W3_e = w3[e]^T)
         y_t += w[t,j] * O_r                        (P:91)
-    Returns y [T,d] and the checkpointed pre-activations A, B [T*k, h] in
-    expert-sorted row order.
+    Returns y [T,d], the checkpointed pre-activations A, B [T*k, h] in
+    expert-sorted row order and U (Alg. 1's Y_swi, the
+    third tensor Alg. 1 l.11 stores) in the same order.
     Non-gated (activation = "silu" | "relu"): U_r = sigma(A_r), no B
     (returned as None), w2 unused.
     """
@@ -202,6 +203,7 @@ def ffn_forward(x, w1, w2, w3, ids, w, disp, activation="swiglu"):
     y = np.zeros((T, d))
     A = np.zeros((R, h))
     B = np.zeros((R, h)) if gated else None
+    U = np.zeros((R, h))
     for e in range(E):
         lo, hi = int(offs[e]), int(offs[e + 1])
         if hi == lo:
@@ -220,7 +222,8 @@ def ffn_forward(x, w1, w2, w3, ids, w, disp, activation="swiglu"):
         wr = w.reshape(-1)[slots]
         np.add.at(y, toks, wr[:, None] * o)
         A[lo:hi] = a
-    return dict(y=y, A=A, B=B)
+        U[lo:hi] = u
+    return dict(y=y, A=A, B=B, U=U)
 
 
 def ffn_backward(dy, x, w1, w2, w3, ids, w, disp, A, B, activation="swiglu"):

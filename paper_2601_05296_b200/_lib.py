@@ -24,7 +24,7 @@ MOE_OP_ROUTE, MOE_OP_DISPATCH, MOE_OP_FFN_FWD, MOE_OP_FFN_BWD, MOE_OP_ROUTER_BWD
 EXPORTS = ("moe_workspace_size", "moe_route", "moe_dispatch_build", "moe_ffn_fwd", "moe_ffn_bwd",
            "moe_gather_rows", "moe_combine_rows", "moe_status_string", "moe_launch_count", "moe_version",
            "moe_profile_enable", "moe_profile_reset", "moe_profile_read", "moe_router_backward", "moe_ep_dest",
-           "moe_ep_send_meta", "moe_ep_slot_grad", "moe_sm_topology")
+           "moe_ep_send_meta", "moe_ep_slot_grad", "moe_ep_local_slots", "moe_sm_topology")
 GEMM_KINDS = ("FWD_UP", "FWD_DOWN", "BWD_DH", "BWD_DX", "DW3", "DW12")
 
 
@@ -42,7 +42,10 @@ class MoeDispatch(ctypes.Structure):
 
 
 class MoeBwdSync(ctypes.Structure):
-    _fields_ = [("x_ready", ctypes.c_void_p), ("dx_ready", ctypes.c_void_p)]
+    _fields_ = [("x_ready", ctypes.c_void_p), ("dx_ready", ctypes.c_void_p), ("stages", ctypes.c_int32)]
+
+
+MOE_BWD_DATA, MOE_BWD_DW3, MOE_BWD_DW12, MOE_BWD_ALL = 1, 2, 4, 7
 
 
 class MoeRouterBwd(ctypes.Structure):
@@ -70,20 +73,21 @@ def load():
     lib.moe_workspace_size.argtypes = [P(MoeProblem), I32, P(SZ)]
     lib.moe_route.argtypes = [P(MoeProblem), V, V, V, V, V, V, SZ, V]
     lib.moe_dispatch_build.argtypes = [P(MoeProblem), V, P(MoeDispatch), V, SZ, V]
-    lib.moe_ffn_fwd.argtypes = [P(MoeProblem), V, V, V, V, V, P(MoeDispatch), V, V, V, V, SZ, V]
-    lib.moe_ffn_bwd.argtypes = [P(MoeProblem), V, V, V, V, V, V, P(MoeDispatch), V, V, V, V, V, V, V,
+    lib.moe_ffn_fwd.argtypes = [P(MoeProblem), V, V, V, V, V, P(MoeDispatch), V, V, V, V, V, SZ, V]
+    lib.moe_ffn_bwd.argtypes = [P(MoeProblem), V, V, V, V, V, V, P(MoeDispatch), V, V, V, V, V, V, V, V,
                                 P(MoeRouterBwd), P(MoeBwdSync), V, SZ, V]
     lib.moe_gather_rows.argtypes = [V, I64, V, I64, I64, I32, V, V]
-    lib.moe_combine_rows.argtypes = [P(MoeProblem), V, V, V, V]
+    lib.moe_combine_rows.argtypes = [P(MoeProblem), V, V, V, V, V]
     lib.moe_router_backward.argtypes = [P(MoeProblem), V, V, P(MoeRouterBwd), V, V, V, SZ, V]
-    lib.moe_ep_dest.argtypes = [P(MoeProblem), V, I32, I32, V, V]
+    lib.moe_ep_dest.argtypes = [P(MoeProblem), V, I32, I32, I32, V, V]
+    lib.moe_ep_local_slots.argtypes = [P(MoeProblem), V, V, I32, I32, V, V, V]
     lib.moe_ep_send_meta.argtypes = [P(MoeProblem), V, V, I32, I32, V, I64, V, V, V]
-    lib.moe_ep_slot_grad.argtypes = [P(MoeProblem), V, I32, I32, V, V, V, V]
+    lib.moe_ep_slot_grad.argtypes = [P(MoeProblem), V, I32, I32, V, V, V, I32, V, V]
     lib.moe_sm_topology.argtypes = [P(I32), I32, P(I32)]
     lib.moe_sm_topology.restype = I32
     for fn in ("moe_workspace_size", "moe_route", "moe_dispatch_build", "moe_ffn_fwd", "moe_ffn_bwd",
                "moe_gather_rows", "moe_combine_rows", "moe_router_backward", "moe_ep_dest", "moe_ep_send_meta",
-               "moe_ep_slot_grad"):
+               "moe_ep_slot_grad", "moe_ep_local_slots"):
         getattr(lib, fn).restype = I32
     lib.moe_status_string.argtypes = [I32]
     lib.moe_status_string.restype = ctypes.c_char_p
@@ -137,8 +141,8 @@ def _dtype_code(dt):
     raise MoEError(f"unsupported dtype {dt} (bf16 or fp32)")
 
 
-MOE_CKPT_AB, MOE_CKPT_NONE = 0, 1
-CHECKPOINT = {"ab": MOE_CKPT_AB, "none": MOE_CKPT_NONE}
+MOE_CKPT_AB, MOE_CKPT_NONE, MOE_CKPT_ABU = 0, 1, 2
+CHECKPOINT = {"ab": MOE_CKPT_AB, "none": MOE_CKPT_NONE, "abu": MOE_CKPT_ABU}
 
 
 ACTIVATION = {"swiglu": 0, "silu": 1, "relu": 2}
@@ -183,25 +187,26 @@ def moe_dispatch_build(p, topk_ids, disp, ws, stream=None):
                                      _stream(stream)), "moe_dispatch_build")
 
 
-def moe_ffn_fwd(p, x, w1, w2, w3, topk_w, disp, a_save, b_save, y, ws, stream=None):
+def moe_ffn_fwd(p, x, w1, w2, w3, topk_w, disp, a_save, b_save, u_save, y, ws, stream=None):
     _check(load().moe_ffn_fwd(ctypes.byref(p), _ptr(x), _ptr(w1), _ptr(w2), _ptr(w3), _ptr(topk_w),
-                              ctypes.byref(disp), _ptr(a_save), _ptr(b_save), _ptr(y), _ptr(ws), ws.numel(),
-                              _stream(stream)), "moe_ffn_fwd")
+                              ctypes.byref(disp), _ptr(a_save), _ptr(b_save), _ptr(u_save), _ptr(y), _ptr(ws),
+                              ws.numel(), _stream(stream)), "moe_ffn_fwd")
 
 
-def moe_ffn_bwd(p, dy, x, w1, w2, w3, topk_w, disp, a_save, b_save, dx, dw1, dw2, dw3, d_topk_w, router, ws,
-                stream=None, x_ready=None, dx_ready=None):
-    """x_ready / dx_ready: torch.cuda.Event or None (moe_bwd_sync)."""
+def moe_ffn_bwd(p, dy, x, w1, w2, w3, topk_w, disp, a_save, b_save, u_save, dx, dw1, dw2, dw3, d_topk_w, router, ws,
+                stream=None, x_ready=None, dx_ready=None, stages=0):
+    """x_ready / dx_ready: torch.cuda.Event or None; stages: MOE_BWD_* mask, 0 = all (moe_bwd_sync)."""
     sync = None
     for ev in (x_ready, dx_ready):
         if ev is not None and not ev.cuda_event:
             raise MoEError("moe_ffn_bwd: sync events must be created (recorded once) before the call")
-    if x_ready is not None or dx_ready is not None:
+    if x_ready is not None or dx_ready is not None or stages:
         sync = MoeBwdSync(x_ready.cuda_event if x_ready is not None else None,
-                          dx_ready.cuda_event if dx_ready is not None else None)
+                          dx_ready.cuda_event if dx_ready is not None else None, int(stages))
     _check(load().moe_ffn_bwd(ctypes.byref(p), _ptr(dy), _ptr(x), _ptr(w1), _ptr(w2), _ptr(w3), _ptr(topk_w),
-                              ctypes.byref(disp), _ptr(a_save), _ptr(b_save), _ptr(dx), _ptr(dw1), _ptr(dw2),
-                              _ptr(dw3), _ptr(d_topk_w), ctypes.byref(router) if router is not None else None,
+                              ctypes.byref(disp), _ptr(a_save), _ptr(b_save), _ptr(u_save), _ptr(dx), _ptr(dw1),
+                              _ptr(dw2), _ptr(dw3), _ptr(d_topk_w),
+                              ctypes.byref(router) if router is not None else None,
                               ctypes.byref(sync) if sync is not None else None,
                               _ptr(ws), ws.numel(), _stream(stream)), "moe_ffn_bwd")
 
@@ -212,9 +217,14 @@ def moe_router_backward(p, d_topk_w, x, router, dx_partial, dx, ws, stream=None)
            "moe_router_backward")
 
 
-def moe_ep_dest(p, topk_ids, experts_per_rank, n_ranks, dest, stream=None):
-    _check(load().moe_ep_dest(ctypes.byref(p), _ptr(topk_ids), int(experts_per_rank), int(n_ranks), _ptr(dest),
-                              _stream(stream)), "moe_ep_dest")
+def moe_ep_dest(p, topk_ids, experts_per_rank, n_ranks, dest, stream=None, self_rank=-1):
+    _check(load().moe_ep_dest(ctypes.byref(p), _ptr(topk_ids), int(experts_per_rank), int(n_ranks), int(self_rank),
+                              _ptr(dest), _stream(stream)), "moe_ep_dest")
+
+
+def moe_ep_local_slots(p, topk_ids, topk_w, experts_per_rank, rank, local_ids, local_w, stream=None):
+    _check(load().moe_ep_local_slots(ctypes.byref(p), _ptr(topk_ids), _ptr(topk_w), int(experts_per_rank), int(rank),
+                                     _ptr(local_ids), _ptr(local_w), _stream(stream)), "moe_ep_local_slots")
 
 
 def moe_ep_send_meta(p, topk_ids, topk_w, experts_per_rank, n_ranks, send_row_slot, send_ids, send_w, stream=None):
@@ -223,9 +233,11 @@ def moe_ep_send_meta(p, topk_ids, topk_w, experts_per_rank, n_ranks, send_row_sl
                                    _ptr(send_w), _stream(stream)), "moe_ep_send_meta")
 
 
-def moe_ep_slot_grad(p, topk_ids, experts_per_rank, n_ranks, send_pos, dg_back, dg, stream=None):
+def moe_ep_slot_grad(p, topk_ids, experts_per_rank, n_ranks, send_pos, dg_back, dg, stream=None, dg_local=None,
+                     self_rank=-1):
     _check(load().moe_ep_slot_grad(ctypes.byref(p), _ptr(topk_ids), int(experts_per_rank), int(n_ranks),
-                                   _ptr(send_pos), _ptr(dg_back), _ptr(dg), _stream(stream)), "moe_ep_slot_grad")
+                                   _ptr(send_pos), _ptr(dg_back), _ptr(dg_local), int(self_rank), _ptr(dg),
+                                   _stream(stream)), "moe_ep_slot_grad")
 
 
 def moe_gather_rows(src, index, dst, stream=None):
@@ -237,9 +249,9 @@ def moe_gather_rows(src, index, dst, stream=None):
                                   _stream(stream)), "moe_gather_rows")
 
 
-def moe_combine_rows(p, rows, token_index_map, out, stream=None):
-    _check(load().moe_combine_rows(ctypes.byref(p), _ptr(rows), _ptr(token_index_map), _ptr(out), _stream(stream)),
-           "moe_combine_rows")
+def moe_combine_rows(p, rows, token_index_map, out, stream=None, base=None):
+    _check(load().moe_combine_rows(ctypes.byref(p), _ptr(rows), _ptr(token_index_map), _ptr(base), _ptr(out),
+                                   _stream(stream)), "moe_combine_rows")
 
 
 def profile_enable(on=True):

@@ -22,24 +22,32 @@ moe_status launch_router_bwd(const moe_problem*, const float*, const int32_t*, c
 moe_status launch_finalize(const moe_problem*, const void*, const float*, const __nv_bfloat16*, const void*, void*,
                            cudaStream_t, bool, const int32_t*);
 int router_ep8(int E);
-moe_status launch_ep_dest(const int32_t*, int64_t, int, int, int, int32_t*, cudaStream_t);
+moe_status launch_ep_dest(const int32_t*, int64_t, int, int, int, int, int32_t*, cudaStream_t);
+moe_status launch_ep_local_slots(const int32_t*, const float*, int64_t, int, int, int32_t*, float*, cudaStream_t);
 moe_status launch_ep_send_meta(const int32_t*, const float*, int, int, int, const int32_t*, int64_t, int32_t*, float*,
                                cudaStream_t);
-moe_status launch_ep_slot_grad(const int32_t*, int64_t, int, int, int, const int32_t*, const float*, float*, cudaStream_t);
+moe_status launch_ep_slot_grad(const int32_t*, int64_t, int, int, int, const int32_t*, const float*, const float*, int,
+                               float*, cudaStream_t);
 moe_status launch_gather_rows(const void*, const int32_t*, int64_t, int64_t, void*, cudaStream_t);
-moe_status launch_combine_rows(const moe_problem*, const void*, const int32_t*, void*, cudaStream_t);
+moe_status launch_combine_rows(const moe_problem*, const void*, const int32_t*, const void*, void*, cudaStream_t);
 
 static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
 static moe_status validate(const moe_problem* p) {
   if (!p) return MOE_ERR_INVALID_ARG;
   if (p->T < 0 || p->d < 1 || p->h < 1 || p->E < 1 || p->k < 1) return MOE_ERR_INVALID_ARG;
-  if (p->k > p->E || p->E > 256 || p->k > 16) return MOE_ERR_INVALID_ARG;
+  if (p->E > 256) return MOE_ERR_INVALID_ARG;
+  // every slot routed: k distinct experts per token (k <= E), top-k selection keeps <= 16.
+  // Sparse slots (rows > 0, -1 = empty slot): a receiver may own fewer experts than k
+  // (expert parallel with E/P < k), and the rank-level send plan uses k = P
+  if (p->rows == 0 && (p->k > p->E || p->k > 16)) return MOE_ERR_INVALID_ARG;
+  if (p->rows > 0 && p->k > 256) return MOE_ERR_INVALID_ARG;
   if (p->T * (int64_t)p->k >= (int64_t(1) << 31)) return MOE_ERR_INVALID_ARG;
   if (p->dtype != MOE_BF16 && p->dtype != MOE_FP32) return MOE_ERR_INVALID_ARG;
   if (p->dtype == MOE_BF16 && (p->d % 128 != 0 || p->h % 128 != 0)) return MOE_ERR_UNSUPPORTED;
   if (p->dtype == MOE_FP32 && (p->d % 8 != 0)) return MOE_ERR_UNSUPPORTED;
-  if (p->checkpoint != MOE_CKPT_AB && p->checkpoint != MOE_CKPT_NONE) return MOE_ERR_INVALID_ARG;
+  if (p->checkpoint != MOE_CKPT_AB && p->checkpoint != MOE_CKPT_NONE && p->checkpoint != MOE_CKPT_ABU)
+    return MOE_ERR_INVALID_ARG;
   if (p->activation < MOE_ACT_SWIGLU || p->activation > MOE_ACT_RELU) return MOE_ERR_INVALID_ARG;
   if (p->deterministic != 0 && p->deterministic != 1) return MOE_ERR_INVALID_ARG;
   if (p->rows < 0 || p->rows > p->T * (int64_t)p->k) return MOE_ERR_INVALID_ARG;
@@ -70,13 +78,22 @@ static int64_t acc_rows(const moe_problem* p, int mode) {
   return mode == OUT_TOKN ? 0 : (mode == OUT_ROWS ? routed_rows(p) : p->T);
 }
 
+// The FFN workspaces start with the tile-scheduler claim counters of the expert GEMMs: one
+// 16-byte slot per GEMM launch of the call (zeroed on the stream right before that launch),
+// so concurrent calls on other streams and CUDA-graph replays never share counters.
+constexpr size_t SCHED_BYTES = 256;
+enum { SCHED_UP = 0, SCHED_DOWN = 1, SCHED_DH = 2, SCHED_DX = 3, SCHED_DW3 = 4, SCHED_DW12 = 5 };
+static int* sched_at(void* ws, int slot) { return reinterpret_cast<int*>(ws) + 4 * slot; }
+
+// U (or wU under MOE_CKPT_ABU, then the caller's u_save) between the two forward GEMMs
 struct FwdWs { void* u; float* yacc; void* a; void* b; size_t total; };
 static FwdWs fwd_layout(const moe_problem* p, void* base) {
   const int64_t R = routed_rows(p);
   char* b = (char*)base;
-  size_t o = 0;
+  size_t o = SCHED_BYTES;
   FwdWs w;
-  w.u = b + o; o += align256((size_t)R * p->h * esize(p));
+  w.u = nullptr;
+  if (p->checkpoint != MOE_CKPT_ABU) { w.u = b + o; o += align256((size_t)R * p->h * esize(p)); }
   w.yacc = (float*)(b + o); o += align256((size_t)acc_rows(p, out_mode(p, false)) * p->d * 4);
   w.a = w.b = nullptr;
   if (p->checkpoint == MOE_CKPT_NONE) {  // A, B are transient: not checkpointed
@@ -104,24 +121,22 @@ static RouterWs router_layout(const moe_problem* p, void* base) {
   return w;
 }
 
-struct BwdWs { void* wu; float* dxacc; float* dgpart; float* dlogits; __nv_bfloat16* dlhl; float* dwgpart; float* dg; void* a; void* b; size_t total; };
+// wU (written by the dH GEMM, read by the dW3 GEMM; under MOE_CKPT_ABU the caller's saved
+// u_save instead) and the transients of the data-gradient stage
+struct BwdWs { void* wu; float* dxacc; float* dgpart; float* dlogits; __nv_bfloat16* dlhl; float* dwgpart; float* dg; size_t total; };
 static BwdWs bwd_layout(const moe_problem* p, void* base) {
   const int64_t R = routed_rows(p);
   char* b = (char*)base;
-  size_t o = 0;
+  size_t o = SCHED_BYTES;
   BwdWs w;
-  w.wu = b + o; o += align256((size_t)R * p->h * esize(p));
+  w.wu = nullptr;
+  if (p->checkpoint != MOE_CKPT_ABU) { w.wu = b + o; o += align256((size_t)R * p->h * esize(p)); }
   w.dxacc = (float*)(b + o); o += align256((size_t)acc_rows(p, out_mode(p, true)) * p->d * 4);  // router or not
   w.dgpart = (float*)(b + o); o += align256((size_t)R * dg_parts(p) * 4);
   w.dlogits = (float*)(b + o); o += align256((size_t)p->T * p->E * 4);
   w.dlhl = (__nv_bfloat16*)(b + o); o += dlhl_bytes(p);
   w.dwgpart = (float*)(b + o); o += align256((size_t)dwg_chunks(p) * p->E * p->d * 4);
   w.dg = (float*)(b + o); o += align256((size_t)p->T * p->k * 4);
-  w.a = w.b = nullptr;
-  if (p->checkpoint == MOE_CKPT_NONE) {  // recomputed pre-activations
-    w.a = b + o; o += align256((size_t)R * p->h * esize(p));
-    w.b = b + o; o += align256((size_t)R * p->h * esize(p));
-  }
   w.total = o;
   return w;
 }
@@ -186,19 +201,20 @@ moe_status moe_dispatch_build(const moe_problem* p, const int32_t* topk_ids, con
 }
 
 moe_status moe_ffn_fwd(const moe_problem* p, const void* x, const void* w1, const void* w2, const void* w3,
-                       const float* topk_w, const moe_dispatch* disp, void* a_save, void* b_save, void* y, void* ws,
-                       size_t ws_bytes, void* stream) {
+                       const float* topk_w, const moe_dispatch* disp, void* a_save, void* b_save, void* u_save,
+                       void* y, void* ws, size_t ws_bytes, void* stream) {
   moe_status s = validate(p);
   if (s != MOE_OK) return s;
   const bool gated = p->activation == MOE_ACT_SWIGLU;
   if (!disp || !w1 || (gated && !w2) || !w3) return MOE_ERR_INVALID_ARG;
-  const bool ckpt = p->checkpoint == MOE_CKPT_AB;
-  if (p->T > 0 && (!x || !y || !topk_w || (ckpt && (!a_save || (gated && !b_save))) || !ws ||
+  const bool ckpt = p->checkpoint != MOE_CKPT_NONE;
+  const bool abu = p->checkpoint == MOE_CKPT_ABU;
+  if (p->T > 0 && (!x || !y || !topk_w || (ckpt && (!a_save || (gated && !b_save))) || (abu && !u_save) || !ws ||
                    !disp->expert_offsets || !disp->expert_token_indices || !disp->row_slot ||
                    (out_mode(p, false) == OUT_ROWS && !disp->token_index_map)))
     return MOE_ERR_INVALID_ARG;
   if (!aligned16(x) || !aligned16(w1) || !aligned16(w2) || !aligned16(w3) || !aligned16(a_save) ||
-      !aligned16(b_save) || !aligned16(y))
+      !aligned16(b_save) || !aligned16(u_save) || !aligned16(y))
     return MOE_ERR_MISALIGNED;
   FwdWs w = fwd_layout(p, ws);
   if (ws_bytes < w.total) return MOE_ERR_WORKSPACE;
@@ -214,12 +230,15 @@ moe_status moe_ffn_fwd(const moe_problem* p, const void* x, const void* w1, cons
   c.out_mode = mode; c.out_tok = y;
   c.x = x; c.w1 = w1; c.w2 = w2; c.w3 = w3; c.topw = topk_w;
   c.offs = disp->expert_offsets; c.eti = disp->expert_token_indices; c.row_slot = disp->row_slot;
-  c.a_save = a_save; c.b_save = b_save; c.u = w.u; c.acc_out = w.yacc;
+  c.a_save = a_save; c.b_save = b_save; c.u = abu ? u_save : w.u; c.acc_out = w.yacc;
+  c.u_weighted = abu;  // ABU: U carries the gate weight (Alg. 1's saved Y_swi, scaled by w)
   c.T = p->T; c.R = routed_rows(p); c.d = p->d; c.h = p->h; c.E = p->E; c.bf16 = p->dtype == MOE_BF16;
   c.act = p->activation;
   c.which = GEMM_FWD_UP;
+  c.sched = sched_at(ws, SCHED_UP);
   if ((s = run_gemm(c, st)) != MOE_OK) return s;
   c.which = GEMM_FWD_DOWN;
+  c.sched = sched_at(ws, SCHED_DOWN);
   if ((s = run_gemm(c, st)) != MOE_OK) return s;
   if (mode == OUT_TOKN) return MOE_OK;
   return launch_finalize(p, w.yacc, nullptr, nullptr, nullptr, y, st, false,
@@ -228,21 +247,30 @@ moe_status moe_ffn_fwd(const moe_problem* p, const void* x, const void* w1, cons
 
 moe_status moe_ffn_bwd(const moe_problem* p, const void* dy, const void* x, const void* w1, const void* w2,
                        const void* w3, const float* topk_w, const moe_dispatch* disp, void* a_save, void* b_save,
-                       void* dx, void* dw1, void* dw2, void* dw3, float* d_topk_w, const moe_router_bwd* router,
-                       const moe_bwd_sync* sync, void* ws, size_t ws_bytes, void* stream) {
+                       void* u_save, void* dx, void* dw1, void* dw2, void* dw3, float* d_topk_w,
+                       const moe_router_bwd* router, const moe_bwd_sync* sync, void* ws, size_t ws_bytes,
+                       void* stream) {
   moe_status s = validate(p);
   if (s != MOE_OK) return s;
+  const int stages = (sync && sync->stages) ? sync->stages : MOE_BWD_ALL;
+  if (stages & ~MOE_BWD_ALL) return MOE_ERR_INVALID_ARG;
+  const bool s_data = stages & MOE_BWD_DATA, s_dw3 = stages & MOE_BWD_DW3, s_dw12 = stages & MOE_BWD_DW12;
   const bool gated = p->activation == MOE_ACT_SWIGLU;
-  if (!disp || !dw1 || (gated && (!dw2 || !w2)) || !dw3 || !w1 || !w3) return MOE_ERR_INVALID_ARG;
+  const bool abu = p->checkpoint == MOE_CKPT_ABU;
+  if (!disp || (s_dw12 && (!dw1 || (gated && !dw2))) || (s_dw3 && !dw3)) return MOE_ERR_INVALID_ARG;
+  if (s_data && (!w1 || !w3 || (gated && !w2))) return MOE_ERR_INVALID_ARG;
   if (router && (!router->w_gate || !router->dw_gate)) return MOE_ERR_INVALID_ARG;
   if (router && p->T > 0 && (!router->logits || !router->topk_ids)) return MOE_ERR_INVALID_ARG;
   if (router && sparse_slots(p)) return MOE_ERR_INVALID_ARG;  // the router sees every slot of its own tokens
-  const bool ckpt = p->checkpoint == MOE_CKPT_AB;
-  if (p->T > 0 && (!dy || !x || !dx || !topk_w || (ckpt && (!a_save || (gated && !b_save))) || !ws ||
-                   !disp->expert_offsets || !disp->expert_token_indices || !disp->token_index_map || !disp->row_slot))
+  if (p->T > 0 && (!ws || !disp->expert_offsets || !disp->expert_token_indices || !disp->token_index_map ||
+                   !disp->row_slot || !topk_w))
     return MOE_ERR_INVALID_ARG;
-  if (!aligned16(dy) || !aligned16(x) || !aligned16(a_save) || !aligned16(b_save) || !aligned16(dx) ||
-      !aligned16(dw1) || !aligned16(dw2) || !aligned16(dw3))
+  if (p->T > 0 && (s_data || s_dw12) && (!a_save || (gated && !b_save))) return MOE_ERR_INVALID_ARG;
+  if (p->T > 0 && s_data && (!dy || !x || !dx)) return MOE_ERR_INVALID_ARG;
+  if (p->T > 0 && s_dw3 && (!dy || (abu && !u_save))) return MOE_ERR_INVALID_ARG;
+  if (p->T > 0 && s_dw12 && !x) return MOE_ERR_INVALID_ARG;
+  if (!aligned16(dy) || !aligned16(x) || !aligned16(a_save) || !aligned16(b_save) || !aligned16(u_save) ||
+      !aligned16(dx) || !aligned16(dw1) || !aligned16(dw2) || !aligned16(dw3))
     return MOE_ERR_MISALIGNED;
   BwdWs w = bwd_layout(p, ws);
   if (ws_bytes < w.total) return MOE_ERR_WORKSPACE;
@@ -250,54 +278,64 @@ moe_status moe_ffn_bwd(const moe_problem* p, const void* dy, const void* x, cons
   cudaEvent_t x_ready = sync ? (cudaEvent_t)sync->x_ready : nullptr;
   cudaEvent_t dx_ready = sync ? (cudaEvent_t)sync->dx_ready : nullptr;
   const int64_t R = routed_rows(p);
-  if (!ckpt) {
-    a_save = w.a;
-    b_save = w.b;
-  }
   GemmCall c{};
   c.x = x; c.dy = dy; c.w1 = w1; c.w2 = w2; c.w3 = w3; c.topw = topk_w;
   c.offs = disp->expert_offsets; c.eti = disp->expert_token_indices; c.row_slot = disp->row_slot;
-  c.a_save = a_save; c.b_save = b_save; c.u = w.wu; c.acc_out = w.dxacc; c.dg_part = w.dgpart;
+  c.a_save = a_save; c.b_save = b_save; c.u = abu ? u_save : w.wu; c.acc_out = w.dxacc; c.dg_part = w.dgpart;
+  c.dh_skip_u = abu;  // ABU: wU is saved, the dH GEMM does not write it
   c.T = p->T; c.R = R; c.d = p->d; c.h = p->h; c.E = p->E; c.bf16 = p->dtype == MOE_BF16;
   c.act = p->activation;
   const int mode = out_mode(p, router != nullptr);
   c.out_mode = mode; c.out_tok = dx;
-  if (p->T > 0) {
-    if (mode == OUT_RED) MOE_CUDA_CHECK(cudaMemsetAsync(w.dxacc, 0, (size_t)p->T * p->d * 4, st));
-    if (!ckpt) {  // MOE_CKPT_NONE: recompute A, B (and U into the wU buffer) with the fused up-projection
-      c.which = GEMM_FWD_UP;
-      if ((s = run_gemm(c, st)) != MOE_OK) return s;
-    }
-    c.which = GEMM_BWD_DH;  // dH, SwiGLU bwd: dA/dB in place, wU, dg partials
-    if ((s = run_gemm(c, st)) != MOE_OK) return s;
-    float* dg = d_topk_w ? d_topk_w : w.dg;
-    if ((s = launch_dg_reduce(w.dgpart, gemm_dg_parts(c), disp->token_index_map, p->T * p->k, dg, st)) != MOE_OK)
-      return s;
-    c.which = GEMM_BWD_DX;   // dXacc += [dA|dB][W1;W2]
-    if ((s = run_gemm(c, st)) != MOE_OK) return s;
-    if (mode != OUT_TOKN) {  // (k = 1 without router: dx already written by the dX GEMM)
-      const float* dl = nullptr;
-      if (router) {
-        if ((s = launch_router_bwd(p, router->logits, router->topk_ids, dg, x, w.dlogits, w.dlhl, w.dwgpart,
-                                   router->dw_gate, st)) != MOE_OK)
-          return s;
-        dl = w.dlogits;
+  if (s_data) {
+    if (p->T > 0) {
+      if (mode == OUT_RED) MOE_CUDA_CHECK(cudaMemsetAsync(w.dxacc, 0, (size_t)p->T * p->d * 4, st));
+      if (p->checkpoint == MOE_CKPT_NONE) {  // recompute A, B (and U into the wU buffer) with the fused up-projection
+        c.which = GEMM_FWD_UP;
+        c.sched = sched_at(ws, SCHED_UP);
+        if ((s = run_gemm(c, st)) != MOE_OK) return s;
       }
-      if ((s = launch_finalize(p, w.dxacc, dl, w.dlhl, router ? router->w_gate : nullptr, dx, st, false,
-                               mode == OUT_ROWS ? disp->token_index_map : nullptr)) != MOE_OK)
+      c.which = GEMM_BWD_DH;  // dH, SwiGLU bwd: dA/dB in place, wU, dg partials
+      c.sched = sched_at(ws, SCHED_DH);
+      if ((s = run_gemm(c, st)) != MOE_OK) return s;
+      float* dg = d_topk_w ? d_topk_w : w.dg;
+      if ((s = launch_dg_reduce(w.dgpart, gemm_dg_parts(c), disp->token_index_map, p->T * p->k, dg, st)) != MOE_OK)
         return s;
+      c.which = GEMM_BWD_DX;   // dXacc += [dA|dB][W1;W2]
+      c.sched = sched_at(ws, SCHED_DX);
+      if ((s = run_gemm(c, st)) != MOE_OK) return s;
+      if (mode != OUT_TOKN) {  // (k = 1 without router: dx already written by the dX GEMM)
+        const float* dl = nullptr;
+        if (router) {
+          if (x_ready) MOE_CUDA_CHECK(cudaStreamWaitEvent(st, x_ready, 0));  // dW_g = dlogits^T x reads x
+          if ((s = launch_router_bwd(p, router->logits, router->topk_ids, dg, x, w.dlogits, w.dlhl, w.dwgpart,
+                                     router->dw_gate, st)) != MOE_OK)
+            return s;
+          dl = w.dlogits;
+        }
+        if ((s = launch_finalize(p, w.dxacc, dl, w.dlhl, router ? router->w_gate : nullptr, dx, st, false,
+                                 mode == OUT_ROWS ? disp->token_index_map : nullptr)) != MOE_OK)
+          return s;
+      }
+    } else if (router) {
+      MOE_CUDA_CHECK(cudaMemsetAsync(router->dw_gate, 0, (size_t)p->E * p->d * esize(p), st));
     }
-  } else if (router) {
-    MOE_CUDA_CHECK(cudaMemsetAsync(router->dw_gate, 0, (size_t)p->E * p->d * esize(p), st));
+    if (dx_ready) MOE_CUDA_CHECK(cudaEventRecord(dx_ready, st));
   }
-  if (dx_ready) MOE_CUDA_CHECK(cudaEventRecord(dx_ready, st));
-  c.which = GEMM_DW3;      // dW3 = dY^T (wU)
-  c.dw_a = dw3; c.dw_b = nullptr;
-  if ((s = run_gemm(c, st)) != MOE_OK) return s;
-  if (x_ready) MOE_CUDA_CHECK(cudaStreamWaitEvent(st, x_ready, 0));
-  c.which = GEMM_DW12;     // dW1, dW2 = [dA|dB]^T X
-  c.dw_a = dw1; c.dw_b = dw2;
-  return run_gemm(c, st);
+  if (s_dw3) {
+    c.which = GEMM_DW3;      // dW3 = dY^T (wU)
+    c.dw_a = dw3; c.dw_b = nullptr;
+    c.sched = sched_at(ws, SCHED_DW3);
+    if ((s = run_gemm(c, st)) != MOE_OK) return s;
+  }
+  if (s_dw12) {
+    if (x_ready) MOE_CUDA_CHECK(cudaStreamWaitEvent(st, x_ready, 0));
+    c.which = GEMM_DW12;     // dW1, dW2 = [dA|dB]^T X
+    c.dw_a = dw1; c.dw_b = dw2;
+    c.sched = sched_at(ws, SCHED_DW12);
+    if ((s = run_gemm(c, st)) != MOE_OK) return s;
+  }
+  return MOE_OK;
 }
 
 moe_status moe_router_backward(const moe_problem* p, const float* d_topk_w, const void* x, const moe_router_bwd* router,
@@ -321,13 +359,26 @@ moe_status moe_router_backward(const moe_problem* p, const float* d_topk_w, cons
 }
 
 moe_status moe_ep_dest(const moe_problem* p, const int32_t* topk_ids, int32_t experts_per_rank, int32_t n_ranks,
-                       int32_t* dest, void* stream) {
+                       int32_t self_rank, int32_t* dest, void* stream) {
   moe_status s = validate(p);
   if (s != MOE_OK) return s;
   if (experts_per_rank < 1 || n_ranks < 1 || (int64_t)experts_per_rank * n_ranks != p->E || sparse_slots(p))
     return MOE_ERR_INVALID_ARG;
+  if (self_rank < -1 || self_rank >= n_ranks) return MOE_ERR_INVALID_ARG;
   if (p->T > 0 && (!topk_ids || !dest)) return MOE_ERR_INVALID_ARG;
-  return launch_ep_dest(topk_ids, p->T, p->k, experts_per_rank, n_ranks, dest, (cudaStream_t)stream);
+  return launch_ep_dest(topk_ids, p->T, p->k, experts_per_rank, n_ranks, self_rank, dest, (cudaStream_t)stream);
+}
+
+moe_status moe_ep_local_slots(const moe_problem* p, const int32_t* topk_ids, const float* topk_w,
+                              int32_t experts_per_rank, int32_t rank, int32_t* local_ids, float* local_w,
+                              void* stream) {
+  moe_status s = validate(p);
+  if (s != MOE_OK) return s;
+  if (experts_per_rank < 1 || rank < 0 || (int64_t)experts_per_rank * (rank + 1) > p->E || sparse_slots(p))
+    return MOE_ERR_INVALID_ARG;
+  if (p->T > 0 && (!topk_ids || !topk_w || !local_ids || !local_w)) return MOE_ERR_INVALID_ARG;
+  return launch_ep_local_slots(topk_ids, topk_w, p->T * p->k, experts_per_rank, rank, local_ids, local_w,
+                               (cudaStream_t)stream);
 }
 
 moe_status moe_ep_send_meta(const moe_problem* p, const int32_t* topk_ids, const float* topk_w, int32_t experts_per_rank,
@@ -344,14 +395,17 @@ moe_status moe_ep_send_meta(const moe_problem* p, const int32_t* topk_ids, const
 }
 
 moe_status moe_ep_slot_grad(const moe_problem* p, const int32_t* topk_ids, int32_t experts_per_rank, int32_t n_ranks,
-                            const int32_t* send_pos, const float* dg_back, float* dg, void* stream) {
+                            const int32_t* send_pos, const float* dg_back, const float* dg_local, int32_t self_rank,
+                            float* dg, void* stream) {
   moe_status s = validate(p);
   if (s != MOE_OK) return s;
   if (experts_per_rank < 1 || n_ranks < 1 || (int64_t)experts_per_rank * n_ranks != p->E || sparse_slots(p))
     return MOE_ERR_INVALID_ARG;
-  if (p->T > 0 && (!topk_ids || !send_pos || !dg_back || !dg)) return MOE_ERR_INVALID_ARG;
-  return launch_ep_slot_grad(topk_ids, p->T, p->k, experts_per_rank, n_ranks, send_pos, dg_back, dg,
-                             (cudaStream_t)stream);
+  if (self_rank < -1 || self_rank >= n_ranks || (self_rank >= 0 && p->T > 0 && !dg_local)) return MOE_ERR_INVALID_ARG;
+  if (p->T > 0 && (!topk_ids || !send_pos || !dg || (!dg_back && n_ranks > (self_rank >= 0 ? 1 : 0))))
+    return MOE_ERR_INVALID_ARG;
+  return launch_ep_slot_grad(topk_ids, p->T, p->k, experts_per_rank, n_ranks, send_pos, dg_back, dg_local, self_rank,
+                             dg, (cudaStream_t)stream);
 }
 
 moe_status moe_gather_rows(const void* src, int64_t n_src, const int32_t* index, int64_t n, int64_t width,
@@ -363,12 +417,14 @@ moe_status moe_gather_rows(const void* src, int64_t n_src, const int32_t* index,
   return launch_gather_rows(src, index, n, width * elem_bytes, dst, (cudaStream_t)stream);
 }
 
-moe_status moe_combine_rows(const moe_problem* p, const void* rows, const int32_t* token_index_map, void* out,
-                            void* stream) {
+moe_status moe_combine_rows(const moe_problem* p, const void* rows, const int32_t* token_index_map, const void* base,
+                            void* out, void* stream) {
   moe_status s = validate(p);
   if (s != MOE_OK) return s;
-  if (p->T > 0 && (!rows || !token_index_map || !out)) return MOE_ERR_INVALID_ARG;
-  return launch_combine_rows(p, rows, token_index_map, out, (cudaStream_t)stream);
+  if (p->T > 0 && (!token_index_map || !out)) return MOE_ERR_INVALID_ARG;
+  if (p->d % 8 != 0) return MOE_ERR_UNSUPPORTED;
+  if (!aligned16(rows) || !aligned16(base) || !aligned16(out)) return MOE_ERR_MISALIGNED;
+  return launch_combine_rows(p, rows, token_index_map, base, out, (cudaStream_t)stream);
 }
 
 }  // extern "C"

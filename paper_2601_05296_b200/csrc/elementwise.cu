@@ -343,8 +343,9 @@ __global__ void __launch_bounds__(256) finalize_kernel(const A* __restrict__ acc
 }
 
 // ---- expert-parallel plan (NEXT-1: one row per (token, destination rank))
-// dest[t, q] = q if rank q owns one of the token's experts, else -1
-__global__ void ep_dest_kernel(const int32_t* __restrict__ ids, int64_t T, int k, int epr, int P,
+// dest[t, q] = q if rank q owns one of the token's experts, else -1; the column of rank
+// `self` (>= 0) stays -1: those pairs are computed where the token lives (no exchange)
+__global__ void ep_dest_kernel(const int32_t* __restrict__ ids, int64_t T, int k, int epr, int P, int self,
                                int32_t* __restrict__ dest) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= T) return;
@@ -353,7 +354,18 @@ __global__ void ep_dest_kernel(const int32_t* __restrict__ ids, int64_t T, int k
     const int q = ids[t * k + j] / epr;
     mask[q >> 5] |= 1u << (q & 31);
   }
-  for (int q = 0; q < P; ++q) dest[t * P + q] = ((mask[q >> 5] >> (q & 31)) & 1u) ? q : -1;
+  for (int q = 0; q < P; ++q) dest[t * P + q] = (q != self && ((mask[q >> 5] >> (q & 31)) & 1u)) ? q : -1;
+}
+
+// the local rank's own slots of every local token: ids - rank*epr where owned, else -1
+__global__ void ep_local_slots_kernel(const int32_t* __restrict__ ids, const float* __restrict__ topw, int64_t n,
+                                      int epr, int rank, int32_t* __restrict__ lids, float* __restrict__ lw) {
+  const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= n) return;
+  const int e = ids[f];
+  const bool mine = e / epr == rank;
+  lids[f] = mine ? e - rank * epr : -1;
+  lw[f] = mine ? topw[f] : 0.f;
 }
 
 // send row i (row_slot = t*P + q): the token's slots restricted to rank q, local expert ids
@@ -373,16 +385,17 @@ __global__ void ep_send_meta_kernel(const int32_t* __restrict__ ids, const float
   send_w[f] = mine ? topw[t * k + j] : 0.f;
 }
 
-// dg[t, j] = dg_back[send_pos[t, owner(ids[t,j])], j]
+// dg[t, j] = dg_back[send_pos[t, owner(ids[t,j])], j], or dg_local[t, j] when the owner is
+// `self` (computed here, on the receiver's first T token rows)
 __global__ void ep_slot_grad_kernel(const int32_t* __restrict__ ids, int64_t T, int k, int epr, int P,
                                     const int32_t* __restrict__ send_pos, const float* __restrict__ dg_back,
-                                    float* __restrict__ dg) {
+                                    const float* __restrict__ dg_local, int self, float* __restrict__ dg) {
   const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= T * k) return;
   const int64_t t = f / k;
   const int j = (int)(f - t * k);
   const int q = ids[f] / epr;
-  dg[f] = dg_back[(int64_t)send_pos[t * P + q] * k + j];
+  dg[f] = q == self ? dg_local[f] : dg_back[(int64_t)send_pos[t * P + q] * k + j];
 }
 
 // 4-byte row gather for rows that are not a multiple of 16 bytes
@@ -405,15 +418,17 @@ __global__ void gather_rows_kernel(const uint4* __restrict__ src, const int32_t*
 }
 
 // out[t, 8c .. 8c+7] = sum_j rows[tim[t,j], ...] (fixed j order, -1 skipped); d % 8 == 0
+// base (optional, [T, d]): added first (the locally computed partial of the token)
 template <typename T>
-__global__ void combine_rows_kernel(const T* __restrict__ rows, const int32_t* __restrict__ tim, int64_t Tn, int d,
-                                    int k, T* __restrict__ out) {
+__global__ void combine_rows_kernel(const T* __restrict__ rows, const int32_t* __restrict__ tim, const T* __restrict__ base,
+                                    int64_t Tn, int d, int k, T* __restrict__ out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int cpr = d / 8;
   if (i >= Tn * cpr) return;
   const int64_t t = i / cpr;
   const int col = (int)(i - t * cpr) * 8;
   float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (base) load8(base + t * d + col, a);
   for (int j = 0; j < k; ++j) {
     const int r = tim[t * k + j];
     if (r < 0) continue;
@@ -555,9 +570,17 @@ moe_status launch_finalize(const moe_problem* p, const void* acc, const float* d
   return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
 }
 
-moe_status launch_ep_dest(const int32_t* ids, int64_t T, int k, int epr, int P, int32_t* dest, cudaStream_t st) {
+moe_status launch_ep_dest(const int32_t* ids, int64_t T, int k, int epr, int P, int self, int32_t* dest,
+                          cudaStream_t st) {
   if (T == 0) return MOE_OK;
-  MOE_LAUNCH(ep_dest_kernel, (unsigned)ceil_div(T, 256), 256, 0, st, ids, T, k, epr, P, dest);
+  MOE_LAUNCH(ep_dest_kernel, (unsigned)ceil_div(T, 256), 256, 0, st, ids, T, k, epr, P, self, dest);
+  return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
+}
+
+moe_status launch_ep_local_slots(const int32_t* ids, const float* topw, int64_t n, int epr, int rank, int32_t* lids,
+                                 float* lw, cudaStream_t st) {
+  if (n == 0) return MOE_OK;
+  MOE_LAUNCH(ep_local_slots_kernel, (unsigned)ceil_div(n, 256), 256, 0, st, ids, topw, n, epr, rank, lids, lw);
   return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
 }
 
@@ -570,10 +593,10 @@ moe_status launch_ep_send_meta(const int32_t* ids, const float* topw, int k, int
 }
 
 moe_status launch_ep_slot_grad(const int32_t* ids, int64_t T, int k, int epr, int P, const int32_t* send_pos,
-                               const float* dg_back, float* dg, cudaStream_t st) {
+                               const float* dg_back, const float* dg_local, int self, float* dg, cudaStream_t st) {
   if (T == 0) return MOE_OK;
   MOE_LAUNCH(ep_slot_grad_kernel, (unsigned)ceil_div(T * k, 256), 256, 0, st, ids, T, k, epr, P, send_pos, dg_back,
-             dg);
+             dg_local, self, dg);
   return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
 }
 
@@ -592,15 +615,16 @@ moe_status launch_gather_rows(const void* src, const int32_t* index, int64_t n, 
   return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
 }
 
-moe_status launch_combine_rows(const moe_problem* p, const void* rows, const int32_t* tim, void* out, cudaStream_t st) {
+moe_status launch_combine_rows(const moe_problem* p, const void* rows, const int32_t* tim, const void* base, void* out,
+                               cudaStream_t st) {
   const int64_t n = p->T * (p->d / 8);
   if (n == 0) return MOE_OK;
   if (p->dtype == MOE_BF16)
     MOE_LAUNCH(combine_rows_kernel<__nv_bfloat16>, (unsigned)ceil_div(n, 256), 256, 0, st,
-               (const __nv_bfloat16*)rows, tim, p->T, p->d, p->k, (__nv_bfloat16*)out);
+               (const __nv_bfloat16*)rows, tim, (const __nv_bfloat16*)base, p->T, p->d, p->k, (__nv_bfloat16*)out);
   else
-    MOE_LAUNCH(combine_rows_kernel<float>, (unsigned)ceil_div(n, 256), 256, 0, st, (const float*)rows, tim, p->T,
-               p->d, p->k, (float*)out);
+    MOE_LAUNCH(combine_rows_kernel<float>, (unsigned)ceil_div(n, 256), 256, 0, st, (const float*)rows, tim,
+               (const float*)base, p->T, p->d, p->k, (float*)out);
   return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
 }
 

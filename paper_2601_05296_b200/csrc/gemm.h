@@ -23,6 +23,9 @@ struct GemmCall {
   int act;  // MOE_ACT_*: 0 = SwiGLU (gated), 1 = SiLU, 2 = ReLU (non-gated)
   int out_mode;   // FWD_DOWN / BWD_DX epilogue target, OutMode
   void* out_tok;  // OUT_TOKN: [T, d] output in the run dtype
+  bool u_weighted;  // MOE_CKPT_ABU: FWD_UP writes wU = w * U, FWD_DOWN then adds wU W3 (unit weight)
+  bool dh_skip_u;   // MOE_CKPT_ABU: BWD_DH does not write wU (the saved one is read by DW3)
+  int* sched;       // 4 claim counters of the tile scheduler (in the caller's ws; zeroed per launch)
 };
 
 // Where FWD_DOWN / BWD_DX put a routed row's result v (row r, token t = eti[r]):

@@ -35,6 +35,8 @@ struct SimtArgs {
   int act;                               // 0 SwiGLU (gated); 1 SiLU, 2 ReLU (non-gated)
   int out_mode;                          // FWD_DOWN / BWD_DX target (gemm.h OutMode)
   T* out_tok;                            // OUT_TOKN destination [T, d]
+  int u_weighted;                        // MOE_CKPT_ABU: u holds w * U (FWD_UP writes it, FWD_DOWN adds it unscaled)
+  int dh_skip_u;                         // MOE_CKPT_ABU: BWD_DH leaves u (the saved wU) untouched
 };
 
 template <typename T>
@@ -136,7 +138,8 @@ __global__ void __launch_bounds__(ST) simt_rows_kernel(SimtArgs<T> g) {
     const int r = r0 + ty * 4 + i;
     const bool rv = r < seg1;
     const int slot = rv ? g.row_slot[r] : 0;
-    const float w = rv ? g.topw[slot] : 0.f;
+    const float w = rv ? ((MODE == FWD_DOWN && g.u_weighted) ? 1.f : g.topw[slot]) : 0.f;
+    const float uw = (MODE == FWD_UP && g.u_weighted) ? w : 1.f;  // scale of the stored U
     const int64_t t = rv ? g.eti[r] : 0;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -148,9 +151,9 @@ __global__ void __launch_bounds__(ST) simt_rows_kernel(SimtArgs<T> g) {
         g.a_save[o] = from_f32<T>(a);
         if (gated) {
           g.b_save[o] = from_f32<T>(b);
-          g.u[o] = from_f32<T>(a * sigmoidf_(a) * b);
+          g.u[o] = from_f32<T>(uw * (a * sigmoidf_(a) * b));
         } else {
-          g.u[o] = from_f32<T>(act_fwd(g.act, a, sigmoidf_(a)));
+          g.u[o] = from_f32<T>(uw * act_fwd(g.act, a, sigmoidf_(a)));
         }
       } else if (MODE == FWD_DOWN) {
         simt_out(g, r, t, n, w * acc[0][i][j]);
@@ -162,12 +165,12 @@ __global__ void __launch_bounds__(ST) simt_rows_kernel(SimtArgs<T> g) {
           rowsum[i] += dH * U;
           g.a_save[o] = from_f32<T>(dU * b * s * (1.f + a * (1.f - s)));
           g.b_save[o] = from_f32<T>(dU * S);
-          g.u[o] = from_f32<T>(w * U);
+          if (!g.dh_skip_u) g.u[o] = from_f32<T>(w * U);
         } else {
           const float U = act_fwd(g.act, a, s);
           rowsum[i] += dH * U;
           g.a_save[o] = from_f32<T>(dU * act_grad(g.act, a, s));
-          g.u[o] = from_f32<T>(w * U);
+          if (!g.dh_skip_u) g.u[o] = from_f32<T>(w * U);
         }
       } else {
         simt_out(g, r, t, n, acc[0][i][j]);
@@ -276,13 +279,13 @@ moe_status simt_gemm(const GemmCall& c, cudaStream_t st) {
     using T = __nv_bfloat16;
     SimtArgs<T> g{(const T*)c.x, (const T*)c.dy, (const T*)c.w1, (const T*)c.w2, (const T*)c.w3, c.topw, c.offs, c.eti,
                   c.row_slot, (T*)c.a_save, (T*)c.b_save, (T*)c.u, c.acc_out, c.dg_part, (T*)c.dw_a, (T*)c.dw_b,
-                  c.R, c.d, c.h, c.E, c.act, c.out_mode, (T*)c.out_tok};
+                  c.R, c.d, c.h, c.E, c.act, c.out_mode, (T*)c.out_tok, c.u_weighted, c.dh_skip_u};
     return simt_launch_all<T>(c.which, g, st);
   }
   using T = float;
   SimtArgs<T> g{(const T*)c.x, (const T*)c.dy, (const T*)c.w1, (const T*)c.w2, (const T*)c.w3, c.topw, c.offs, c.eti,
                 c.row_slot, (T*)c.a_save, (T*)c.b_save, (T*)c.u, c.acc_out, c.dg_part, (T*)c.dw_a, (T*)c.dw_b,
-                c.R, c.d, c.h, c.E, c.act, c.out_mode, (T*)c.out_tok};
+                c.R, c.d, c.h, c.E, c.act, c.out_mode, (T*)c.out_tok, c.u_weighted, c.dh_skip_u};
   return simt_launch_all<T>(c.which, g, st);
 }
 

@@ -43,7 +43,6 @@
 
 #include <climits>
 #include <cstdlib>
-#include <mutex>
 
 #include "gemm.h"
 #include "ptx.cuh"
@@ -193,6 +192,8 @@ struct TcParams {
   int* sched;
   const uint8_t* die_map;
   int n_split;
+  int u_weighted;  // MOE_CKPT_ABU: FWD_UP stores w * U; FWD_DOWN then adds U W3 with unit weight
+  int dh_skip_u;   // MOE_CKPT_ABU: BWD_DH writes dA, dB only (wU is saved from the forward)
 };
 
 template <int KIND>
@@ -547,6 +548,19 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
   // scheduler's ring (every tile-iterating warp reads every slot once, then
   // releases it on the leader; the slot value gates the arrive, so the read has
   // completed before the scheduler may overwrite it)
+  // the tile after the current one without consuming it (the ring slot is released by the
+  // regular fetch later): lets the BWD_DH epilogue prefetch its next inputs into L2
+  auto peek = [&](int it) -> int {
+    if constexpr (DYN) {
+      const int slot = it % SCHED_RING;
+      const uint32_t par = (uint32_t)(it / SCHED_RING) & 1u;
+      if (leader) ptx::mbar_wait(&sfull[slot], par);
+      else ptx::mbar_wait_cluster(&sfull[slot], par);
+      return *reinterpret_cast<volatile int*>(&s_ring[slot]);
+    } else {
+      return cluster_id + it * n_clusters;
+    }
+  };
   auto fetch = [&](int it) -> int {
     if constexpr (DYN) {
       const int slot = it % SCHED_RING;
@@ -901,6 +915,18 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
         if (lane == 0) {
           ptx::bulk_wait_read<1>();
           for (int ci = 0; ci < DH_PF && ci < nchunk; ++ci) dh_load(gch + ci, t.n0 + cb + CW * ci, r0w);
+          // the NEXT tile's A, B boxes of this warp go to L2 now, a whole tile ahead: the
+          // ring's loads then hit L2 instead of paying HBM latency DH_PF chunks ahead
+          TileInfo tn;
+          if (decode_tile<KIND, CG>(peek(it + 1), P, s_offs, s_mstart, tn)) {
+            const int r0n = tn.m0 + rowoff + wq * 32;
+            const int ncn = max(0, min(NCW, P.h - tn.n0 - cb)) / CW;
+            if (r0n < tn.seg1)
+              for (int ci = 0; ci < ncn; ++ci) {
+                ptx::tma_prefetch_l2_2d(&mA0, tn.n0 + cb + CW * ci, r0n);
+                if (P.act == 0) ptx::tma_prefetch_l2_2d(&mA1, tn.n0 + cb + CW * ci, r0n);
+              }
+          }
         }
         __syncwarp();
       } else if constexpr (is_dh(KIND)) {
@@ -1060,6 +1086,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
         uint8_t* T2 = stg + 2048;
         const bool gated = P.act == 0;
         const int cbeg = gated ? hc * 64 : cb, cend = gated ? cbeg + 64 : cb + NCW;
+        const int rr = t.m0 + row;
+        const float uw = !P.u_weighted ? 1.f : (rr < t.seg1 ? P.topw[P.row_slot[rr]] : 0.f);
 #pragma unroll 1
         for (int c = cbeg; c < cend; c += 16) {
           if (!gated && t.n0 + c >= P.h) break;
@@ -1077,10 +1105,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
               if (gated) {
                 const float b0 = __uint_as_float(vb[8 * q + 2 * e]), b1 = __uint_as_float(vb[8 * q + 2 * e + 1]);
                 ob[e] = ptx::pack_bf16(b0, b1);
-                ou[e] = ptx::pack_bf16(a0 * sigmoid_fast(a0) * b0, a1 * sigmoid_fast(a1) * b1);
+                ou[e] = ptx::pack_bf16(uw * (a0 * sigmoid_fast(a0) * b0), uw * (a1 * sigmoid_fast(a1) * b1));
               } else {
                 ob[e] = 0u;
-                ou[e] = ptx::pack_bf16(act_fwd(P.act, a0, sigmoid_fast(a0)), act_fwd(P.act, a1, sigmoid_fast(a1)));
+                ou[e] = ptx::pack_bf16(uw * act_fwd(P.act, a0, sigmoid_fast(a0)), uw * act_fwd(P.act, a1, sigmoid_fast(a1)));
               }
             }
             *reinterpret_cast<uint4*>(T0 + stg8_off(lane, q)) = make_uint4(oa[0], oa[1], oa[2], oa[3]);
@@ -1104,6 +1132,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
         uint8_t* T1 = stg + 2048;
         uint8_t* T2 = stg + 4096;
         uint32_t bv[32];
+        // MOE_CKPT_ABU: the stored activation is wU (the gate weight of this row folded in)
+        const int rr = t.m0 + row;
+        const float uw = !P.u_weighted ? 1.f : (rr < t.seg1 ? P.topw[P.row_slot[rr]] : 0.f);
         if (P.act != 0) {  // non-gated: 256 columns of A, U = sigma(A)
 #pragma unroll 1
           for (int c = 0; c < TBN; c += 32) {
@@ -1114,7 +1145,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               a[i] = __uint_as_float(v[i]);
-              u[i] = act_fwd(P.act, a[i], sigmoid_fast(a[i]));
+              u[i] = uw * act_fwd(P.act, a[i], sigmoid_fast(a[i]));
             }
             stg_put_bf16(T0, lane, a);
             stg_put_bf16(T2, lane, u);
@@ -1137,7 +1168,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
           for (int i = 0; i < 32; ++i) {
             a[i] = __uint_as_float(v[i]);
             b[i] = __uint_as_float(bv[i]);
-            u[i] = a[i] * sigmoid_fast(a[i]) * b[i];
+            u[i] = uw * (a[i] * sigmoid_fast(a[i]) * b[i]);
           }
           stg_put_bf16(T0, lane, a);
           stg_put_bf16(T1, lane, b);
@@ -1165,7 +1196,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
         int tok = 0;
         if (r < t.seg1) {
           tok = P.eti[r];
-          if constexpr (KIND == TC_FWD_DOWN) w = P.topw[P.row_slot[r]];
+          if constexpr (KIND == TC_FWD_DOWN) w = P.u_weighted ? 1.f : P.topw[P.row_slot[r]];
         }
 #pragma unroll 1
         for (int cc = 0; cc < ncol; cc += 32) {
@@ -1286,7 +1317,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
             }
             *reinterpret_cast<uint4*>(TA + stgw_off<CW>(lane, q)) = make_uint4(oa[0], oa[1], oa[2], oa[3]);
             *reinterpret_cast<uint4*>(TB + stgw_off<CW>(lane, q)) = make_uint4(ob[0], ob[1], ob[2], ob[3]);
-            *reinterpret_cast<uint4*>(TU + stgw_off<CW>(lane, q)) = make_uint4(ou[0], ou[1], ou[2], ou[3]);
+            if (!P.dh_skip_u)
+              *reinterpret_cast<uint4*>(TU + stgw_off<CW>(lane, q)) = make_uint4(ou[0], ou[1], ou[2], ou[3]);
           }
           ptx::fence_proxy_async();  // generic smem writes -> visible to the TMA stores
           __syncwarp();
@@ -1295,18 +1327,18 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
               const int col = t.n0 + cb + CW * ci;
               ptx::tma_store_2d(&mA0, TA, col, r0w);
               if (P.act == 0) ptx::tma_store_2d(&mA1, TB, col, r0w);
-              ptx::tma_store_2d(&mB1, TU, col, r0w);
+              if (!P.dh_skip_u) ptx::tma_store_2d(&mB1, TU, col, r0w);
             }
           } else if (nvalid > 0) {
             const int64_t o = o0 + ci * CW;
             if constexpr (CW == 16) {
               stg8_store_bf16(TA, lane, P.a_save + o, P.h, nvalid);
               if (P.act == 0) stg8_store_bf16(TB, lane, P.b_save + o, P.h, nvalid);
-              stg8_store_bf16(TU, lane, P.u + o, P.h, nvalid);
+              if (!P.dh_skip_u) stg8_store_bf16(TU, lane, P.u + o, P.h, nvalid);
             } else {
               stg_store_bf16(TA, lane, P.a_save + o, P.h, nvalid);
               if (P.act == 0) stg_store_bf16(TB, lane, P.b_save + o, P.h, nvalid);
-              stg_store_bf16(TU, lane, P.u + o, P.h, nvalid);
+              if (!P.dh_skip_u) stg_store_bf16(TU, lane, P.u + o, P.h, nvalid);
             }
           }
           if (lane == 0) ptx::bulk_commit();  // one (possibly empty) group per chunk
@@ -1398,7 +1430,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
             const int64_t o = o0 + ci * 32;
             stg_store_bf16(TA, lane, P.a_save + o, P.h, nvalid);
             if (P.act == 0) stg_store_bf16(TB, lane, P.b_save + o, P.h, nvalid);
-            stg_store_bf16(TU, lane, P.u + o, P.h, nvalid);
+            if (!P.dh_skip_u) stg_store_bf16(TU, lane, P.u + o, P.h, nvalid);
           }
           __syncwarp();
         }
@@ -1556,22 +1588,7 @@ static moe_status launch_tc_impl(const CUtensorMap& a0, const CUtensorMap& a1, c
   return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
 }
 
-// Claim counters of the dynamic scheduler: a per-device ring of slots, one per
-// launch, zeroed on the launch's stream (concurrent launches on other streams
-// take other slots).
-static int* sched_slot(cudaStream_t st) {
-  constexpr int NSLOT = 256;
-  static std::mutex mu;
-  static int* base[64] = {};
-  static unsigned next[64] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lk(mu);
-  if (!base[dev & 63] && cudaMalloc(&base[dev & 63], NSLOT * 4 * sizeof(int)) != cudaSuccess) return nullptr;
-  int* p = base[dev & 63] + 4 * (next[dev & 63]++ % NSLOT);
-  if (cudaMemsetAsync(p, 0, 4 * sizeof(int), st) != cudaSuccess) return nullptr;
-  return p;
-}
+
 
 // tiles_for(TM): number of tiles (an upper bound for row kinds) at tile height TM
 template <int KIND, typename F>
@@ -1589,8 +1606,9 @@ static moe_status launch_tc(const CUtensorMap& a0, const CUtensorMap& a1, const 
           const int ns = (int)((2LL * P.n_tiles * n_sm[0] + (n_sm[0] + n_sm[1])) / (2LL * (n_sm[0] + n_sm[1])));
           P.n_split = std::min(std::max(ns, 1), P.n_tiles - 1);
         }
-        P.sched = sched_slot(st);
-        if (!P.sched) return MOE_ERR_CUDA;
+        // claim counters: the caller's 16-byte workspace slot for this launch, zeroed on the
+        // launch stream (stream-ordered, so CUDA-graph replays and other streams never share them)
+        if (!P.sched || cudaMemsetAsync(P.sched, 0, 4 * sizeof(int), st) != cudaSuccess) return MOE_ERR_CUDA;
       }
       return launch_tc_impl<KIND, true, 2>(a0, a1, b0, b1, P, tiles_for(256), st);
     case ENG_CTA: return launch_tc_impl<KIND, true, 1>(a0, a1, b0, b1, P, tiles_for(128), st);
@@ -1642,6 +1660,8 @@ moe_status tc_gemm(const GemmCall& c, cudaStream_t st) {
   P.acc_out = c.acc_out; P.dg_part = c.dg_part;
   P.out_mode = c.out_mode; P.out_tok = (bf*)c.out_tok;
   P.out0 = (bf*)c.dw_a; P.out1 = (bf*)c.dw_b;
+  P.sched = c.sched;
+  P.u_weighted = c.u_weighted; P.dh_skip_u = c.dh_skip_u;
   P.T = (int)T; P.d = d; P.h = h; P.E = E;
   P.dg_parts = tc_dg_parts(h, d);
   CUtensorMap a0, a1, b0, b1;

@@ -5,33 +5,44 @@ layer shards naturally by expert: rank r owns experts [r*E/P, (r+1)*E/P);
 tokens stay data-parallel (T per rank); the router W_g is replicated.
 
 Per-destination dedup (NEXT-1).  A token whose k experts live on m <= min(k, P)
-ranks travels m times, not k times: the send plan is the MoEBlaze dispatch
-itself, applied one level up -- moe_ep_dest marks, per token, the ranks owning
-any of its experts (dest [T, P], -1 elsewhere) and moe_dispatch_build over dest
-(sparse slots) yields the send order (tokens grouped by rank, ascending), the
-per-rank row counts and the inverse map send_pos [T, P] (P:123-135 with
-"experts" = ranks).  Each sent row carries the token's k slots restricted to
-the receiving rank (moe_ep_send_meta: local expert id or -1, gate weight), so
-the receiver runs the SAME fused kernels as a sparse-slot problem (p.rows = its
-routed (token, expert) rows): FWD_DOWN's red.add combine then sums the token's
-local experts before anything travels back -- one return row per (token, rank).
+ranks travels to each of those ranks once, not k times: the send plan is the
+MoEBlaze dispatch itself, applied one level up -- moe_ep_dest marks, per token,
+the ranks owning any of its experts (dest [T, P], -1 elsewhere) and
+moe_dispatch_build over dest (sparse slots) yields the send order (tokens
+grouped by rank, ascending), the per-rank row counts and the inverse map
+send_pos [T, P] (P:123-135 with "experts" = ranks).  Each sent row carries the
+token's k slots restricted to the receiving rank (moe_ep_send_meta: local expert
+id or -1, gate weight), so the receiver runs the SAME fused kernels as a
+sparse-slot problem (p.rows = its routed (token, expert) rows): FWD_DOWN's
+red.add combine then sums the token's local experts before anything travels
+back -- one return row per (token, rank).
+
+Local pairs never travel.  moe_ep_dest excludes the own rank, so a token's slots
+on its own rank's experts are computed in place: the receiver's token rows are
+[the T local tokens (moe_ep_local_slots: their own-rank slots) | the received
+rows], its output rows [0, T) are the local partial outputs, which
+moe_combine_rows adds as `base` to the returned rows.  At P = 1 nothing is
+exchanged and the step is the single-GPU layer plus the plan bookkeeping.
 
 Forward, per rank:
   1. moe_route + moe_dispatch_build over the global experts (per-expert counts).
-  2. send plan (moe_ep_dest + moe_dispatch_build); C1: all-to-all of the
-     [rows, pairs per local expert] counts; ONE device->host read of the split
-     sizes (the only host sync of the step).
-  3. C2: X rows in send order (moe_gather_rows) + the packed slot metadata.
-  4. receiver: sparse dispatch over the received slots, moe_ffn_fwd; C3 returns
-     one row per (token, rank); moe_combine_rows sums them through send_pos.
+  2. send plan (moe_ep_dest without self + moe_dispatch_build); C1: all-to-all of
+     the [rows, pairs per local expert] counts; ONE device->host read of the
+     split sizes (the only host sync of the step: buffers are sized by it).
+  3. C2: remote X rows in send order (moe_gather_rows) + the packed slot
+     metadata, received behind the local tokens' rows.
+  4. receiver: sparse dispatch over [local slots | received slots], moe_ffn_fwd;
+     C3 returns one row per (remote token, rank); moe_combine_rows adds them to
+     the local partial through send_pos.
 Backward:
-  C4a: dY rows to the owners (needed first); C4b: X rows again (keeping the
-  received X would be a saved permuted activation) on a side stream, overlapped
-  with the dH / dX GEMMs -- moe_ffn_bwd waits for it only before the dW1/dW2
-  GEMM (moe_bwd_sync.x_ready).  C5: dX rows and gate-weight gradients return on
-  the side stream as soon as moe_ffn_bwd records dx_ready, overlapped with the
-  dW3 / dW1,dW2 GEMMs.  moe_combine_rows + moe_ep_slot_grad + moe_router_backward
-  on the source; C6: all_reduce of dW_g.  Expert weight grads stay local.
+  C4a: remote dY rows to the owners (needed first); C4b: remote X rows again
+  (keeping the received X would be a saved permuted activation) on a side
+  stream, overlapped with the dH / dX GEMMs -- moe_ffn_bwd waits for it only
+  before the dW1/dW2 GEMM (moe_bwd_sync.x_ready).  C5: dX rows and gate-weight
+  gradients return on the side stream as soon as moe_ffn_bwd records dx_ready,
+  overlapped with the dW3 / dW1,dW2 GEMMs.  moe_combine_rows (local dX partial
+  as base) + moe_ep_slot_grad (local dg) + moe_router_backward on the source;
+  C6: all_reduce of dW_g.  Expert weight grads stay local.
 
 `ops` (the compute) and `a2a` (the exchange) are injectable so the host-side
 bookkeeping is testable with gloo on CPU; the product binds CudaOps (the C ABI)
@@ -68,11 +79,16 @@ class CudaOps:
         L.moe_dispatch_build(p, ids, disp.c(), ws)
         return disp
 
-    def ep_dest(self, ids, E, El, P):
+    def ep_dest(self, ids, E, El, P, self_rank=-1):
         T, k = ids.shape
         dest = torch.empty(T, P, dtype=torch.int32, device=ids.device)
-        L.moe_ep_dest(L.problem(T, 128, 128, E, k, torch.bfloat16), ids, El, P, dest)
+        L.moe_ep_dest(L.problem(T, 128, 128, E, k, torch.bfloat16), ids, El, P, dest, self_rank=self_rank)
         return dest
+
+    def local_slots(self, ids, w, E, El, rank, out_ids, out_w):
+        """moe_ep_local_slots into out_ids / out_w ([T, k] views of the receiver's slot arrays)."""
+        T, k = ids.shape
+        L.moe_ep_local_slots(L.problem(T, 128, 128, E, k, torch.bfloat16), ids, w, El, rank, out_ids, out_w)
 
     def send_meta(self, ids, w, E, El, P, send_row_slot):
         T, k = ids.shape
@@ -82,10 +98,12 @@ class CudaOps:
         L.moe_ep_send_meta(L.problem(T, 128, 128, E, k, torch.bfloat16), ids, w, El, P, send_row_slot, sid, sw)
         return sid, sw
 
-    def slot_grad(self, ids, E, El, P, send_pos, dg_back):
+    def slot_grad(self, ids, E, El, P, send_pos, dg_back, dg_local=None, self_rank=-1):
         T, k = ids.shape
         dg = torch.empty(T, k, dtype=torch.float32, device=ids.device)
-        L.moe_ep_slot_grad(L.problem(T, 128, 128, E, k, torch.bfloat16), ids, El, P, send_pos, dg_back, dg)
+        L.moe_ep_slot_grad(L.problem(T, 128, 128, E, k, torch.bfloat16), ids, El, P, send_pos,
+                           dg_back if dg_back is not None and dg_back.numel() else None, dg, dg_local=dg_local,
+                           self_rank=self_rank)
         return dg
 
     def gather_rows(self, src, index):
@@ -103,7 +121,7 @@ class CudaOps:
         b = torch.empty(rows, h, dtype=x.dtype, device=x.device)
         y = torch.empty(T, d, dtype=x.dtype, device=x.device)
         ws = L.workspace(p, L.MOE_OP_FFN_FWD, x.device)
-        L.moe_ffn_fwd(p, x, w1, w2, w3, w, disp.c(), a, b, y, ws)
+        L.moe_ffn_fwd(p, x, w1, w2, w3, w, disp.c(), a, b, None, y, ws)
         return y, a, b
 
     def ffn_bwd(self, dy, x, w1, w2, w3, w, disp, a, b, rows, x_ready=None, dx_ready=None):
@@ -115,14 +133,16 @@ class CudaOps:
         dw1, dw2, dw3 = torch.empty_like(w1), torch.empty_like(w2), torch.empty_like(w3)
         dg = torch.empty(T, k, dtype=torch.float32, device=dy.device)
         ws = L.workspace(p, L.MOE_OP_FFN_BWD, dy.device)
-        L.moe_ffn_bwd(p, dy, x, w1, w2, w3, w, disp.c(), a, b, dx, dw1, dw2, dw3, dg, None, ws,
+        L.moe_ffn_bwd(p, dy, x, w1, w2, w3, w, disp.c(), a, b, None, dx, dw1, dw2, dw3, dg, None, ws,
                       x_ready=x_ready, dx_ready=dx_ready)
         return dict(dx=dx, dw1=dw1, dw2=dw2, dw3=dw3, dg=dg)
 
-    def combine(self, rows, tim, T, d, k):
-        out = torch.empty(T, d, dtype=rows.dtype, device=rows.device)
-        p = L.problem(T, d, 128, max(k, 1), k, rows.dtype)
-        L.moe_combine_rows(p, rows, tim, out)
+    def combine(self, rows, tim, T, d, k, base=None):
+        """out[t] = base[t] + sum of the returned rows of t (moe_combine_rows)."""
+        ref = base if base is not None else rows
+        out = torch.empty(T, d, dtype=ref.dtype, device=ref.device)
+        p = L.problem(T, d, 128, max(k, 1), k, ref.dtype, rows=T * k)  # sparse: -1 entries are expected
+        L.moe_combine_rows(p, rows if rows.numel() else None, tim, out, base=base)
         return out
 
     def router_backward(self, dg, x, wg, logits, ids, dx_partial, renorm):
@@ -138,9 +158,15 @@ class CudaOps:
         return dx, dwg
 
 
-def nccl_a2a(send, send_split, recv_split, group=None):
-    out = torch.empty((sum(recv_split),) + tuple(send.shape[1:]), dtype=send.dtype, device=send.device)
-    dist.all_to_all_single(out, send.contiguous(), recv_split, send_split, group=group)
+def nccl_a2a(send, send_split, recv_split, group=None, out=None):
+    """all_to_all_single; `out` (optional) = a contiguous receive buffer, e.g. the
+    tail of the receiver's row array behind its local tokens."""
+    if out is None:
+        out = torch.empty((sum(recv_split),) + tuple(send.shape[1:]), dtype=send.dtype, device=send.device)
+    if dist.get_world_size(group) > 1:
+        dist.all_to_all_single(out, send.contiguous(), recv_split, send_split, group=group)
+    elif out.numel():
+        out.copy_(send)  # one rank: the exchange is the identity
     return out
 
 
@@ -168,24 +194,34 @@ class ExpertParallelMoE:
         self.overlap = overlap
         self.retain_recv_x = retain_recv_x
         self.last_rows_received = 0   # (token, expert) rows computed here
-        self.last_rows_sent = 0       # token rows sent (X), after dedup
+        self.last_rows_sent = 0       # token rows sent (X) to other ranks, after dedup
         self.last_pairs_sent = 0      # (token, expert) pairs they carry
 
-    def a2a(self, send, send_split, recv_split):
-        return self._a2a(send, send_split, recv_split, self.group)
+    def a2a(self, send, send_split, recv_split, out=None):
+        if out is not None and not sum(recv_split) and not sum(send_split):
+            return out  # nothing to exchange at all (e.g. P = 1)
+        return self._a2a(send, send_split, recv_split, self.group, out=out)
 
     def _use_streams(self, x):
         if self.overlap is not None:
             return bool(self.overlap) and x.is_cuda
         return x.is_cuda and dist.get_backend(self.group) == "nccl"
 
+    def _rows(self, local, send_tok, send_split, recv_split):
+        """[T + U, ...] buffer: the local rows first, the U received rows behind them (C2 / C4)."""
+        T = local.shape[0]
+        buf = torch.empty((T + sum(recv_split),) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+        buf[:T].copy_(local)
+        self.a2a(self.ops.gather_rows(local, send_tok), send_split, recv_split, out=buf[T:])
+        return buf
+
     def forward(self, x, wg, w1l, w2l, w3l):
-        ops, P, El, k, E = self.ops, self.P, self.El, self.k, self.E
+        ops, P, El, k, E, me = self.ops, self.P, self.El, self.k, self.E, self.rank
         T, d = x.shape
         logits, ids, w = ops.route(x, wg, k, self.renorm)
         disp = ops.dispatch(ids, E, x.dtype)
-        # send plan: one row per (token, owning rank)
-        dest = ops.ep_dest(ids, E, El, P)
+        # send plan: one row per (token, owning remote rank); own-rank pairs stay here
+        dest = ops.ep_dest(ids, E, El, P, self_rank=me)
         plan = ops.dispatch(dest, P, x.dtype, rows=T * min(k, P))
         # C1: [rows to q, pairs per local expert of q] -> owners; one host read of all split sizes
         cnt = torch.cat([plan.counts.view(P, 1), disp.counts.view(P, El)], 1).reshape(-1).contiguous()
@@ -194,61 +230,72 @@ class ExpertParallelMoE:
         send_split = host[:P].tolist()
         rc_h = host[P:].view(P, El + 1)
         recv_split = rc_h[:, 0].tolist()
-        n_pairs = int(rc_h[:, 1:].sum())
+        n_pairs = int(rc_h[:, 1:].sum())  # incl. the own rank's pairs (row `me` of rc_h)
         n_send = int(sum(send_split))
+        U = int(sum(recv_split))
         self.last_rows_received = n_pairs
         self.last_rows_sent = n_send
         self.last_pairs_sent = T * k
         send_tok = plan.eti[:n_send]
+        # receiver slots: [local tokens' own-rank slots | received slots] (packed ids | w bits)
+        wcols = k * w.element_size() // 4
+        meta = torch.empty(T + U, k + wcols, dtype=torch.int32, device=x.device)
+        lid = torch.empty(T, k, dtype=torch.int32, device=x.device)
+        lw = torch.empty(T, k, dtype=w.dtype, device=x.device)
+        ops.local_slots(ids, w, E, El, me, lid, lw)
+        meta[:T, :k] = lid
+        meta[:T, k:] = lw.view(torch.int32)
         sid, sw = ops.send_meta(ids, w, E, El, P, plan.row_slot[:n_send])
-        # C2: token rows + their slot metadata (local expert id or -1, gate weight) in one int32 payload
-        x_recv = self.a2a(ops.gather_rows(x, send_tok), send_split, recv_split)
-        meta = self.a2a(torch.cat([sid, sw.view(torch.int32)], 1), send_split, recv_split)
+        # C2: remote token rows + their slot metadata, received behind the local rows
+        x_l = self._rows(x, send_tok, send_split, recv_split)
+        self.a2a(torch.cat([sid, sw.view(torch.int32)], 1), send_split, recv_split, out=meta[T:])
         ids_l = meta[:, :k].contiguous()
-        w_l = meta[:, k:].contiguous().view(sw.dtype)
-        U = x_recv.shape[0]
+        w_l = meta[:, k:].contiguous().view(w.dtype)
         disp_l = ops.dispatch(ids_l, El, x.dtype, rows=n_pairs) if n_pairs else None
         if n_pairs:
-            y_rows, a_l, b_l = ops.ffn_fwd(x_recv, w1l, w2l, w3l, w_l, disp_l, n_pairs)
+            y_rows, a_l, b_l = ops.ffn_fwd(x_l, w1l, w2l, w3l, w_l, disp_l, n_pairs)
         else:
-            y_rows, a_l, b_l = x_recv.new_zeros(U, d), None, None
-        x_keep = x_recv if self.retain_recv_x else None
-        del x_recv
-        # C3: per-(token, rank) partial outputs back; token-side sum through send_pos
-        y_back = self.a2a(y_rows, recv_split, send_split)
-        y = ops.combine(y_back, plan.tim, T, d, P)
+            y_rows, a_l, b_l = x_l.new_zeros(T + U, d), None, None
+        x_keep = x_l if self.retain_recv_x else None
+        del x_l
+        # C3: per-(remote token, rank) partial outputs back; token-side sum through send_pos,
+        # on top of the local partial (rows [0, T) of the receiver's output)
+        y_back = self.a2a(y_rows[T:], recv_split, send_split)
+        y = ops.combine(y_back, plan.tim, T, d, P, base=y_rows[:T])
         ctx = dict(x=x, wg=wg, w1l=w1l, w2l=w2l, w3l=w3l, logits=logits, ids=ids, w=w, plan=plan, send_tok=send_tok,
                    send_split=send_split, recv_split=recv_split, w_l=w_l, disp_l=disp_l, a_l=a_l, b_l=b_l,
-                   n_pairs=n_pairs, x_recv=x_keep)
+                   n_pairs=n_pairs, x_recv=x_keep, U=U)
         return y, ctx
 
     def backward(self, ctx, dy):
-        ops, P, El, E, k = self.ops, self.P, self.El, self.E, self.k
+        ops, P, El, E, k, me = self.ops, self.P, self.El, self.E, self.k, self.rank
         x, plan = ctx["x"], ctx["plan"]
         T, d = x.shape
         ss, rs = ctx["send_split"], ctx["recv_split"]
-        n_pairs = ctx["n_pairs"]
+        n_pairs, U = ctx["n_pairs"], ctx["U"]
         w1l, w2l, w3l = ctx["w1l"], ctx["w2l"], ctx["w3l"]
         streams = self._use_streams(x)
         main = torch.cuda.current_stream() if streams else None
         side = torch.cuda.Stream(device=x.device) if streams else None
         sctx = (lambda: torch.cuda.stream(side)) if streams else contextlib.nullcontext
-        # C4a: dY rows to the expert owners (the dH GEMM needs them first)
-        dy_recv = self.a2a(ops.gather_rows(dy, ctx["send_tok"]), ss, rs)
-        # C4b: X rows again, on the side stream (only the dW1/dW2 GEMM reads them),
-        # unless forward kept them (retain_recv_x)
-        x_recv = ctx.pop("x_recv", None)
+        # C4a: remote dY rows to the expert owners (the dH GEMM needs them first)
+        dy_l = self._rows(dy, ctx["send_tok"], ss, rs)
+        # C4b: remote X rows again, on the side stream (only the dW1/dW2 GEMM reads
+        # them), unless forward kept them (retain_recv_x)
+        x_l = ctx.pop("x_recv", None)
         x_ready = dx_ready = None
-        if x_recv is None:
+        if x_l is None:
+            x_l = torch.empty(T + U, d, dtype=x.dtype, device=x.device)
+            x_l[:T].copy_(x)
             x_send = ops.gather_rows(x, ctx["send_tok"])
             if streams:
                 side.wait_stream(main)
             with sctx():
-                x_recv = self.a2a(x_send, ss, rs)
+                self.a2a(x_send, ss, rs, out=x_l[T:])
             if streams:
                 x_ready = torch.cuda.Event()
                 x_ready.record(side)
-                x_recv.record_stream(main)
+                x_l.record_stream(side)
                 x_send.record_stream(side)
         elif streams:
             x_ready = torch.cuda.Event()
@@ -258,34 +305,34 @@ class ExpertParallelMoE:
             # now so the library gets a real handle to re-record after dX is final
             dx_ready = torch.cuda.Event()
             dx_ready.record(main)
-        U = dy_recv.shape[0]
         if n_pairs:
-            g = ops.ffn_bwd(dy_recv, x_recv, w1l, w2l, w3l, ctx["w_l"], ctx["disp_l"], ctx["a_l"], ctx["b_l"],
+            g = ops.ffn_bwd(dy_l, x_l, w1l, w2l, w3l, ctx["w_l"], ctx["disp_l"], ctx["a_l"], ctx["b_l"],
                             n_pairs, x_ready=x_ready, dx_ready=dx_ready)
         else:  # nothing routed here: zero expert grads
-            g = dict(dx=dy_recv.new_zeros(U, d), dg=torch.zeros(U, k, dtype=ctx["w_l"].dtype, device=dy.device),
+            g = dict(dx=dy_l.new_zeros(T + U, d), dg=torch.zeros(T + U, k, dtype=ctx["w_l"].dtype, device=dy.device),
                      dw1=torch.zeros_like(w1l), dw2=torch.zeros_like(w2l), dw3=torch.zeros_like(w3l))
             if streams:
                 dx_ready.record(main)
                 main.wait_event(x_ready)
-        # C5: per-(token, rank) dX partials and the gate-weight gradients back, on the side stream
+        # C5: per-(remote token, rank) dX partials and the gate-weight gradients back, on the side stream
         with sctx():
             if streams:
                 side.wait_event(dx_ready)
                 g["dx"].record_stream(side)
                 g["dg"].record_stream(side)
-            dx_back = self.a2a(g["dx"], rs, ss)
-            dg_back = self.a2a(g["dg"], rs, ss)
+            dx_back = self.a2a(g["dx"][T:], rs, ss)
+            dg_back = self.a2a(g["dg"][T:], rs, ss)
         if streams:
             main.wait_stream(side)
             dx_back.record_stream(main)
             dg_back.record_stream(main)
-        dx_part = ops.combine(dx_back, plan.tim, T, d, P)
-        dg = ops.slot_grad(ctx["ids"], E, El, P, plan.tim, dg_back)
+        dx_part = ops.combine(dx_back, plan.tim, T, d, P, base=g["dx"][:T])
+        dg = ops.slot_grad(ctx["ids"], E, El, P, plan.tim, dg_back, dg_local=g["dg"][:T], self_rank=me)
         dx, dwg = ops.router_backward(dg, x, ctx["wg"], ctx["logits"], ctx["ids"], dx_part, self.renorm)
         # C6: replicated router
         acc = dwg.float() if dwg.element_size() < 4 else dwg  # reduce 16-bit grads in fp32
-        dist.all_reduce(acc, group=self.group)
+        if P > 1:
+            dist.all_reduce(acc, group=self.group)
         dwg = acc.to(dwg.dtype)
         return dict(dx=dx, dw_gate=dwg, dw1=g["dw1"], dw2=g["dw2"], dw3=g["dw3"], dg=dg)
 

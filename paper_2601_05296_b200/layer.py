@@ -64,7 +64,8 @@ def dispatch_build(ids, E, check_routing=False, stream=None, dtype=torch.bfloat1
 def ffn_fwd(x, w1, w2, w3, topk_w, disp: Dispatch, renormalize=False, stream=None, checkpoint="ab",
             activation="swiglu", deterministic=False):
     """moe_ffn_fwd (§3.1, Alg. 1 FusedForward): returns y, A, B (A, B checkpointed;
-    None, None under checkpoint="none", where backward recomputes them).
+    None, None under checkpoint="none", where backward recomputes them), and under
+    checkpoint="abu" (Alg. 1 literally) a fourth element, the saved wU.
     activation "silu" | "relu": the non-gated expert W2 sigma(W1 x); w2
     may be None and B is None.  deterministic: ordered token-side combine
     (bitwise reproducible for every k; NEXT-4)."""
@@ -74,30 +75,41 @@ def ffn_fwd(x, w1, w2, w3, topk_w, disp: Dispatch, renormalize=False, stream=Non
     p = _problem(T, d, h, E, k, x.dtype, renormalize, checkpoint=checkpoint, activation=activation,
                  deterministic=deterministic)
     R = T * k
-    save = checkpoint == "ab"
+    save = checkpoint in ("ab", "abu")
     gated = activation == "swiglu"
     a = torch.empty(R, h, dtype=x.dtype, device=x.device) if save else None
     b = torch.empty(R, h, dtype=x.dtype, device=x.device) if (save and gated) else None
+    u = torch.empty(R, h, dtype=x.dtype, device=x.device) if checkpoint == "abu" else None
     y = torch.empty(T, d, dtype=x.dtype, device=x.device)
     ws = L.workspace(p, L.MOE_OP_FFN_FWD, x.device)
-    L.moe_ffn_fwd(p, x, w1, w2, w3, topk_w, disp.c(), a, b, y, ws, stream)
-    return y, a, b
+    L.moe_ffn_fwd(p, x, w1, w2, w3, topk_w, disp.c(), a, b, u, y, ws, stream)
+    return (y, a, b, u) if checkpoint == "abu" else (y, a, b)
 
 
 def ffn_bwd(dy, x, w1, w2, w3, topk_w, disp: Dispatch, a_save, b_save, w_gate=None, logits=None,
-            renormalize=False, stream=None, checkpoint="ab", activation="swiglu", deterministic=False):
+            renormalize=False, stream=None, checkpoint="ab", activation="swiglu", deterministic=False, u_save=None,
+            staged=False, release_ab=False):
     """moe_ffn_bwd (§3.2, Alg. 1 FusedBackward).  a_save/b_save are overwritten
-    with dA/dB (checkpoint="none": pass None, A and B are recomputed).  With
-    w_gate/logits: router backward too (dx includes it)."""
+    with dA/dB (checkpoint="none": pass None, A and B are recomputed into
+    scratch buffers); u_save = the saved wU under checkpoint="abu".  With
+    w_gate/logits: router backward too (dx includes it).
+
+    staged=True issues the three MOE_BWD_* stages as separate calls on the same
+    workspace and allocates each weight gradient only when its GEMM runs:
+    data grads -> dW1/dW2 (the last reader of A/B: with release_ab their
+    storage is released here) -> dW3 (reads wU).  Same results, lower peak."""
     T, d = x.shape
     E, h, _ = w1.shape
     k = topk_w.shape[1]
     p = _problem(T, d, h, E, k, x.dtype, renormalize, checkpoint=checkpoint, activation=activation,
                  deterministic=deterministic)
+    gated = activation == "swiglu"
+    R = T * k
+    if checkpoint == "none":  # scratch for the recomputed A, B (then dA, dB)
+        a_save = torch.empty(R, h, dtype=x.dtype, device=x.device)
+        b_save = torch.empty(R, h, dtype=x.dtype, device=x.device) if gated else None
+        release_ab = True
     dx = torch.empty_like(x)
-    dw1 = torch.empty_like(w1)
-    dw2 = torch.empty_like(w2) if activation == "swiglu" else None
-    dw3 = torch.empty_like(w3)
     dg = torch.empty(T, k, dtype=torch.float32, device=x.device)
     router = None
     dwg = None
@@ -105,51 +117,80 @@ def ffn_bwd(dy, x, w1, w2, w3, topk_w, disp: Dispatch, a_save, b_save, w_gate=No
         dwg = torch.empty_like(w_gate)
         router = L.MoeRouterBwd(w_gate.data_ptr(), logits.data_ptr(), disp.ids.data_ptr(), dwg.data_ptr())
     ws = L.workspace(p, L.MOE_OP_FFN_BWD, x.device)
-    L.moe_ffn_bwd(p, dy, x, w1, w2, w3, topk_w, disp.c(), a_save, b_save, dx, dw1, dw2, dw3, dg, router, ws, stream)
+    args = (p, dy, x, w1, w2, w3, topk_w, disp.c(), a_save, b_save, u_save)
+    if not staged:
+        dw1 = torch.empty_like(w1)
+        dw2 = torch.empty_like(w2) if gated else None
+        dw3 = torch.empty_like(w3)
+        L.moe_ffn_bwd(*args, dx, dw1, dw2, dw3, dg, router, ws, stream)
+    else:
+        L.moe_ffn_bwd(*args, dx, None, None, None, dg, router, ws, stream, stages=L.MOE_BWD_DATA)
+        dw1 = torch.empty_like(w1)
+        dw2 = torch.empty_like(w2) if gated else None
+        L.moe_ffn_bwd(*args, dx, dw1, dw2, None, dg, None, ws, stream, stages=L.MOE_BWD_DW12)
+        if release_ab:  # dA/dB are dead: give their memory back (stream-ordered reuse)
+            for t in (a_save, b_save):
+                if t is not None:
+                    t.untyped_storage().resize_(0)
+        dw3 = torch.empty_like(w3)
+        L.moe_ffn_bwd(*args, dx, None, None, dw3, dg, None, ws, stream, stages=L.MOE_BWD_DW3)
     return dict(dx=dx, dw1=dw1, dw2=dw2, dw3=dw3, dg=dg, dw_gate=dwg)
 
 
 class MoEBlazeFunction(torch.autograd.Function):
     """y = MoE(x): route -> dispatch -> fused expert forward; backward recomputes
     SiLU from the checkpointed A, B.  Saved for backward: x, logits,
-    ids, w, the index structures, A, B — no routed-token buffer.  With
-    checkpoint="none" A, B are not saved either (recomputed in backward)."""
+    ids, w, the index structures, A, B (+ wU under checkpoint="abu") -- no
+    routed-token buffer.  With checkpoint="none" A, B are not saved either
+    (recomputed in backward).  Backward runs staged (ffn_bwd(staged=True)) and
+    releases A/B as soon as dW1/dW2 are done, so it can run only once per
+    forward: the saved A, B are overwritten in place by dA, dB."""
 
     @staticmethod
     def forward(ctx, x, w_gate, w1, w2, w3, k, renormalize, checkpoint="ab", activation="swiglu",
                 deterministic=False):
         logits, ids, w = route(x, w_gate, k, renormalize)
         disp = dispatch_build(ids, w_gate.shape[0], dtype=x.dtype)
-        y, a, b = ffn_fwd(x, w1, w2, w3, w, disp, renormalize, checkpoint=checkpoint, activation=activation,
-                          deterministic=deterministic)
+        out = ffn_fwd(x, w1, w2, w3, w, disp, renormalize, checkpoint=checkpoint, activation=activation,
+                      deterministic=deterministic)
+        y, a, b = out[:3]
         gated = activation == "swiglu"
         saved = [x, w_gate, w1, w2 if gated else w1, w3, logits, ids, w, disp.counts, disp.offs, disp.eti, disp.tim,
                  disp.row_slot]
-        if checkpoint == "ab":
+        if checkpoint in ("ab", "abu"):
             saved += [a, b if gated else a]
+        if checkpoint == "abu":
+            saved += [out[3]]
         ctx.save_for_backward(*saved)
         ctx.renormalize = renormalize
         ctx.checkpoint = checkpoint
         ctx.activation = activation
         ctx.deterministic = deterministic
+        ctx.consumed = False
         return y
 
     @staticmethod
     def backward(ctx, dy):
+        if ctx.consumed:
+            raise RuntimeError("MoEBlazeFunction: backward ran twice on one forward; the checkpointed A, B were "
+                               "overwritten in place by dA, dB (and released) by the first backward")
+        ctx.consumed = True
         t = ctx.saved_tensors
         (x, w_gate, w1, w2, w3, logits, ids, w, counts, offs, eti, tim, row_slot) = t[:13]
         gated = ctx.activation == "swiglu"
-        a, b = (t[13], t[14] if gated else None) if ctx.checkpoint == "ab" else (None, None)
+        a, b = (t[13], t[14] if gated else None) if ctx.checkpoint in ("ab", "abu") else (None, None)
+        u = t[15] if ctx.checkpoint == "abu" else None
         disp = Dispatch(counts, offs, eti, tim, row_slot, ids)
         g = ffn_bwd(dy.contiguous(), x, w1, w2 if gated else None, w3, w, disp, a, b, w_gate=w_gate, logits=logits,
                     renormalize=ctx.renormalize, checkpoint=ctx.checkpoint, activation=ctx.activation,
-                    deterministic=ctx.deterministic)
+                    deterministic=ctx.deterministic, u_save=u, staged=True, release_ab=True)
         return g["dx"], g["dw_gate"], g["dw1"], g["dw2"], g["dw3"], None, None, None, None, None
 
 
 def moe_layer(x, w_gate, w1, w2, w3, k, renormalize=False, checkpoint="ab", activation="swiglu",
               deterministic=False):
-    """checkpoint: "ab" (paper: save A (,B), recompute the activation) | "none" (recompute A, B).
+    """checkpoint: "ab" (paper: save A (,B), recompute the activation) | "none" (recompute A, B)
+    | "abu" (Alg. 1 literally: save A, B and wU; no recompute of U for dW3).
     activation: "swiglu" | "silu" | "relu" (non-gated W2 sigma(W1 x); w2 unused).
     deterministic: ordered combine of a token's k expert outputs (bitwise reproducible for k >= 3)."""
     return MoEBlazeFunction.apply(x, w_gate, w1, w2, w3, k, renormalize, checkpoint, activation, deterministic)

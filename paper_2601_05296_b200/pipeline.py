@@ -21,6 +21,10 @@ class HostPipeline:
     separate stream."""
 
     def __init__(self, step_fn, shape, dtype, device, depth=2):
+        if depth < 2:
+            # load(i + 1) reuses buffer (i + 1) % depth, last read by step i + 1 - depth: with
+            # depth 1 that is step i itself, whose completion event is not recorded yet
+            raise ValueError("HostPipeline needs depth >= 2 (step i+1's copy must not overwrite step i's inputs)")
         self.step_fn = step_fn
         self.depth = depth
         self.dev = torch.device(device)

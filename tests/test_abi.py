@@ -125,14 +125,63 @@ def test_ep_helpers_validation(lib):
     source problems, synchronously (nothing launched: no GPU needed)."""
     from paper_2601_05296_b200 import _lib as L
     p = L.problem(16, 128, 128, 8, 2, torch.bfloat16)
-    assert lib.moe_ep_dest(ctypes.byref(p), None, 3, 2, None, None) == 1        # 3*2 != 8
-    assert lib.moe_ep_dest(ctypes.byref(p), None, 4, 2, None, None) == 1        # null pointers, T > 0
+    assert lib.moe_ep_dest(ctypes.byref(p), None, 3, 2, -1, None, None) == 1    # 3*2 != 8
+    assert lib.moe_ep_dest(ctypes.byref(p), None, 4, 2, -1, None, None) == 1    # null pointers, T > 0
+    assert lib.moe_ep_dest(ctypes.byref(p), None, 4, 2, 2, None, None) == 1     # self_rank out of range
     p0 = L.problem(0, 128, 128, 8, 2, torch.bfloat16)
-    assert lib.moe_ep_dest(ctypes.byref(p0), None, 4, 2, None, None) == 0       # T = 0: nothing to do
+    assert lib.moe_ep_dest(ctypes.byref(p0), None, 4, 2, 1, None, None) == 0    # T = 0: nothing to do
     assert lib.moe_ep_send_meta(ctypes.byref(p), None, None, 4, 2, None, 33, None, None, None) == 1  # n > T*P
     assert lib.moe_ep_send_meta(ctypes.byref(p0), None, None, 4, 2, None, 0, None, None, None) == 0
     ps = L.problem(16, 128, 128, 8, 2, torch.bfloat16, rows=8)
-    assert lib.moe_ep_slot_grad(ctypes.byref(ps), None, 4, 2, None, None, None, None) == 1  # sparse source
+    assert lib.moe_ep_slot_grad(ctypes.byref(ps), None, 4, 2, None, None, None, -1, None, None) == 1  # sparse source
+    assert lib.moe_ep_slot_grad(ctypes.byref(p0), None, 4, 2, None, None, None, 0, None, None) == 0
+    assert lib.moe_ep_local_slots(ctypes.byref(p), None, None, 4, 2, None, None, None) == 1  # rank 2 of 8/4
+    assert lib.moe_ep_local_slots(ctypes.byref(p0), None, None, 4, 1, None, None, None) == 0
+
+
+def test_sparse_slots_allow_fewer_experts_than_k(lib):
+    """an EP receiver owns E/P experts, possibly fewer than k
+    (Mixtral-like E = 8, k = 2 on 8 ranks; DeepSeek-like k = 6 on 16 ranks): with
+    sparse slots (rows > 0) k > E is valid; with every slot routed it is not."""
+    from paper_2601_05296_b200 import _lib as L
+    n = ctypes.c_size_t(0)
+    for E, k in ((1, 2), (4, 6), (2, 8), (1, 64)):
+        sp = L.problem(1024, 256, 512, E, k, torch.bfloat16, rows=1024)
+        assert lib.moe_workspace_size(ctypes.byref(sp), L.MOE_OP_FFN_FWD, ctypes.byref(n)) == 0, (E, k)
+        dense = L.problem(1024, 256, 512, E, k, torch.bfloat16)
+        assert lib.moe_workspace_size(ctypes.byref(dense), L.MOE_OP_FFN_FWD, ctypes.byref(n)) == 1, (E, k)
+    assert lib.moe_workspace_size(ctypes.byref(L.problem(64, 256, 512, 8, 300, torch.bfloat16, rows=10)),
+                                  L.MOE_OP_FFN_FWD, ctypes.byref(n)) == 1   # k <= 256 with sparse slots
+
+
+def test_checkpoint_policy_workspaces(lib):
+    """MOE_CKPT_ABU (Alg. 1 literally): U lives in the caller's u_save, not
+    in ws -- both workspaces shrink by exactly one [T*k, h] activation; every
+    FFN workspace starts with the 256-byte tile-scheduler counter block."""
+    from paper_2601_05296_b200 import _lib as L
+    for (T, d, h, E, k) in [(1024, 256, 512, 8, 2), (300, 128, 384, 16, 6)]:
+        for op in (L.MOE_OP_FFN_FWD, L.MOE_OP_FFN_BWD):
+            ab = L.workspace_size(L.problem(T, d, h, E, k, torch.bfloat16), op)
+            abu = L.workspace_size(L.problem(T, d, h, E, k, torch.bfloat16, checkpoint="abu"), op)
+            assert abs((ab - abu) - T * k * h * 2) <= 256, (op, ab, abu)
+        # MOE_CKPT_NONE: backward recomputes A, B into the caller's scratch a_save/b_save
+        none_b = L.workspace_size(L.problem(T, d, h, E, k, torch.bfloat16, checkpoint="none"), L.MOE_OP_FFN_BWD)
+        assert none_b == L.workspace_size(L.problem(T, d, h, E, k, torch.bfloat16), L.MOE_OP_FFN_BWD)
+
+
+def test_staged_backward_validation(lib):
+    """moe_bwd_sync.stages: an unknown bit is rejected; a stage whose output
+    pointer is missing is rejected; nothing is launched (no GPU here)."""
+    from paper_2601_05296_b200 import _lib as L
+    p = L.problem(16, 128, 128, 4, 2, torch.bfloat16)
+    disp = L.MoeDispatch(256, 256, 256, 256, 256, 256)
+    f = ctypes.c_void_p(256)
+    for stages, dws in ((8, (f, f, f)), (L.MOE_BWD_DW3, (f, f, None)), (L.MOE_BWD_DW12, (None, f, f)),
+                        (L.MOE_BWD_DW12, (f, None, f))):
+        sync = L.MoeBwdSync(None, None, stages)
+        code = lib.moe_ffn_bwd(ctypes.byref(p), f, f, f, f, f, f, ctypes.byref(disp), f, f, None, f, *dws, f, None,
+                               ctypes.byref(sync), f, 1 << 40, None)
+        assert code == 1, (stages, code)
 
 
 def test_sm_topology_validation(lib):

@@ -21,35 +21,39 @@ from tests._util import BF16_TOL, f64, normwise
 pytestmark = pytest.mark.gpu
 
 CFG = dict(T=384, d=256, h=256, E=8, k=2)
+CFG_EL1 = dict(T=384, d=256, h=256, E=2, k=2)   # P = 2: one expert per rank, fewer than k
 
 
-def staged_a2a(send, send_split, recv_split, group=None):
-    out = torch.empty((sum(recv_split),) + tuple(send.shape[1:]), dtype=send.dtype)
-    dist.all_to_all_single(out, send.detach().cpu().contiguous(), recv_split, send_split, group=group)
-    return out.to(send.device)
+def staged_a2a(send, send_split, recv_split, group=None, out=None):
+    res = torch.empty((sum(recv_split),) + tuple(send.shape[1:]), dtype=send.dtype)
+    dist.all_to_all_single(res, send.detach().cpu().contiguous(), recv_split, send_split, group=group)
+    if out is None:
+        return res.to(send.device)
+    out.copy_(res)
+    return out
 
 
-def _inputs(P, routing="balanced"):
-    c = CFG
+def _inputs(P, routing="balanced", c=CFG):
     W = make_inputs(c["T"], c["d"], c["h"], c["E"], c["k"], dtype="bf16", seed=100, routing=routing)
     XS = [make_inputs(c["T"], c["d"], c["h"], c["E"], c["k"], dtype="bf16", seed=r, routing=routing)
           for r in range(P)]
     return W, [(X["x"], X["dy"]) for X in XS]
 
 
-def _worker(rank, P, port, q, routing, backend="gloo", retain=False):
+def _worker(rank, P, port, q, routing, backend="gloo", retain=False, c=CFG):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    torch.cuda.set_device(0)
-    dev = torch.device("cuda", 0)
-    if backend == "nccl":  # one rank: real NCCL all-to-all and the side-stream overlap of C4b / C5
+    gpu = rank if backend == "nccl_multi" else 0
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
+    if backend.startswith("nccl"):  # real NCCL all-to-all and the side-stream overlap of C4b / C5
         dist.init_process_group("nccl", rank=rank, world_size=P, device_id=dev)
     else:
         dist.init_process_group("gloo", rank=rank, world_size=P)
     from paper_2601_05296_b200.ep import ExpertParallelMoE
-    W, XS = _inputs(P, routing)
-    ep = ExpertParallelMoE(CFG["E"], CFG["k"], False, a2a=staged_a2a if backend == "gloo" else None,
+    W, XS = _inputs(P, routing, c)
+    ep = ExpertParallelMoE(c["E"], c["k"], False, a2a=staged_a2a if backend == "gloo" else None,
                            retain_recv_x=retain)
-    assert ep._use_streams(XS[rank][0].to(dev)) == (backend == "nccl")
+    assert ep._use_streams(XS[rank][0].to(dev)) == backend.startswith("nccl")
     lo, hi = ep.local_experts
     x, dy = (t.to(dev) for t in XS[rank])
     wl = [W[n][lo:hi].contiguous().to(dev) for n in ("w1", "w2", "w3")]
@@ -70,17 +74,28 @@ def _port():
     return p
 
 
+@pytest.mark.parametrize("P,routing,backend,retain,c", [(2, "balanced", "gloo", False, CFG_EL1),
+                                                        (2, "balanced", "nccl_multi", False, CFG_EL1)])
+def test_ep_fewer_local_experts_than_k(P, routing, backend, retain, c):
+    test_ep_cuda_matches_single_gpu(P, routing, backend, retain, c)
+
+
 @pytest.mark.parametrize("P,routing,backend,retain", [(1, "balanced", "gloo", False), (2, "balanced", "gloo", False),
                                                       (2, "degenerate", "gloo", False),
                                                       (1, "balanced", "nccl", False), (1, "skewed", "nccl", False),
-                                                      (2, "skewed", "gloo", True), (1, "balanced", "nccl", True)])
-def test_ep_cuda_matches_single_gpu(P, routing, backend, retain):
+                                                      (2, "skewed", "gloo", True), (1, "balanced", "nccl", True),
+                                                      (2, "balanced", "nccl_multi", False),
+                                                      (2, "skewed", "nccl_multi", True)])
+def test_ep_cuda_matches_single_gpu(P, routing, backend, retain, c=CFG):
     """degenerate routing: every token picks experts 0,1, so rank 1 receives no rows.
-    nccl (P = 1): the product path, with C4b / C5 on the side stream."""
+    nccl (P = 1): the product path, with C4b / C5 on the side stream.  nccl_multi:
+    one rank per GPU over real NCCL all-to-all (skipped with fewer than P GPUs)."""
+    if backend == "nccl_multi" and torch.cuda.device_count() < P:
+        pytest.skip(f"needs {P} GPUs (this box has {torch.cuda.device_count()})")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, P, port, q, routing, backend, retain)) for r in range(P)]
+    procs = [ctx.Process(target=_worker, args=(r, P, port, q, routing, backend, retain, c)) for r in range(P)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=300) for _ in range(P)], key=lambda t: t[0])
@@ -88,20 +103,20 @@ def test_ep_cuda_matches_single_gpu(P, routing, backend, retain):
         p.join(timeout=60)
         assert p.exitcode == 0
     import paper_2601_05296_b200 as M
-    W, XS = _inputs(P, routing)
+    W, XS = _inputs(P, routing, c)
     dev = torch.device("cuda", 0)
     x = torch.cat([a for a, _ in XS]).to(dev)
     dy = torch.cat([b for _, b in XS]).to(dev)
     wg, w1, w2, w3 = (W[n].to(dev) for n in ("w_gate", "w1", "w2", "w3"))
-    k = CFG["k"]
+    k = c["k"]
     logits, ids, w = M.route(x, wg, k)
-    disp = M.dispatch_build(ids, CFG["E"])
+    disp = M.dispatch_build(ids, c["E"])
     y, a, b = M.ffn_fwd(x, w1, w2, w3, w, disp)
     g1 = M.ffn_bwd(dy, x, w1, w2, w3, w, disp, a, b, w_gate=wg, logits=logits)
     torch.cuda.synchronize()
     fwd = O.layer_forward(f64(x), f64(wg), f64(w1), f64(w2), f64(w3), k, logits=f64(logits))
     bwd = O.layer_backward(fwd, f64(dy), f64(x), f64(wg), f64(w1), f64(w2), f64(w3))
-    T = CFG["T"]
+    T = c["T"]
     for rank, ye, ge, (lo, hi) in res:
         sl = slice(rank * T, (rank + 1) * T)
         assert normwise(ye, f64(y[sl])) < 1e-2

@@ -26,14 +26,24 @@ def M():
 
 
 def _sparse_ids(T, E, k, seed, p_empty):
+    """k slots per token, each -1 (empty) or a distinct expert of this rank; with
+    E < k (an EP receiver owning fewer experts than a token's k) at most E slots
+    of a token are non-empty."""
     g = np.random.default_rng(seed)
-    ids = np.stack([g.permutation(E)[:k] for _ in range(T)]).astype(np.int32)
+    if k <= E:
+        ids = np.stack([g.permutation(E)[:k] for _ in range(T)]).astype(np.int32)
+    else:
+        ids = np.full((T, k), -1, np.int32)
+        for t in range(T):
+            ids[t, g.permutation(k)[:E]] = g.permutation(E)
     ids[g.random((T, k)) < p_empty] = -1
     return ids
 
 
 @pytest.mark.parametrize("T,E,k,p_empty", [(1, 4, 2, 0.5), (300, 8, 2, 0.3), (5000, 64, 6, 0.7), (4097, 16, 8, 0.9),
-                                           (1000, 4, 1, 0.5), (257, 8, 8, 1.0)])
+                                           (1000, 4, 1, 0.5), (257, 8, 8, 1.0),
+                                           # fewer local experts than k (EP with E/P < k, ADVICE r01)
+                                           (600, 1, 2, 0.3), (900, 2, 8, 0.2), (70, 4, 20, 0.5)])
 def test_sparse_dispatch_bit_exact(M, T, E, k, p_empty):
     from paper_2601_05296_b200.ep import CudaOps
     ids_np = _sparse_ids(T, E, k, T + k, p_empty)
@@ -51,6 +61,9 @@ def test_sparse_dispatch_bit_exact(M, T, E, k, p_empty):
 @pytest.mark.parametrize("T,d,h,E,k,dtype,p_empty", [
     (300, 256, 384, 8, 2, "bf16", 0.4), (777, 512, 256, 16, 6, "bf16", 0.6), (200, 128, 128, 4, 1, "bf16", 0.5),
     (96, 64, 96, 4, 3, "fp32", 0.5),
+    # E (local experts) < k: Mixtral-like E = 8, k = 2 over 8 ranks -> 1 expert per rank;
+    # DeepSeek-like k = 6 over 16 ranks -> 4 experts per rank
+    (500, 256, 384, 1, 2, "bf16", 0.3), (640, 128, 256, 4, 6, "bf16", 0.2), (80, 64, 96, 2, 8, "fp32", 0.4),
 ])
 def test_sparse_layer_parity(M, T, d, h, E, k, dtype, p_empty):
     """An EP receiver's problem: token rows with only some slots routed here.

@@ -70,6 +70,12 @@ def test_single_expert_is_plain_swiglu_mlp():
     ref = _mlp_torch(P["x"], P["w1"][0], P["w2"][0], P["w3"][0])
     assert np.allclose(f["y"], ref, rtol=1e-12, atol=1e-12)
     assert np.allclose(f["A"], P["x"] @ P["w1"][0].T, rtol=1e-12, atol=1e-12)
+    # Y_swi (Alg. 1 l.11), the activation MOE_CKPT_ABU saves: the MLP's hidden layer
+    X = torch.from_numpy(P["x"])
+    hid = F.silu(X @ torch.from_numpy(P["w1"][0]).T) * (X @ torch.from_numpy(P["w2"][0]).T)
+    assert np.allclose(f["U"], hid.numpy(), rtol=1e-12, atol=1e-12)
+    # and U W3 is the expert output: y = U W3 with the gate weight 1
+    assert np.allclose(f["U"] @ P["w3"][0].T, ref, rtol=1e-12, atol=1e-12)
 
 
 def test_identical_experts_with_renorm_is_mlp():
