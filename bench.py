@@ -239,6 +239,7 @@ def main():
         os.environ.setdefault("MASTER_PORT", "29533")
         os.environ.setdefault("RANK", "0")
         os.environ.setdefault("WORLD_SIZE", "1")
+        os.environ.setdefault("NCCL_DEBUG", "WARN")  # stdout carries the one JSON line only
         dist.init_process_group("nccl", device_id=dev)
         if rank == 0:
             print(f"bench.py: NCCL process group up, world {dist.get_world_size()}, "

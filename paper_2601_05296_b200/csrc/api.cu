@@ -402,8 +402,7 @@ moe_status moe_ep_slot_grad(const moe_problem* p, const int32_t* topk_ids, int32
   if (experts_per_rank < 1 || n_ranks < 1 || (int64_t)experts_per_rank * n_ranks != p->E || sparse_slots(p))
     return MOE_ERR_INVALID_ARG;
   if (self_rank < -1 || self_rank >= n_ranks || (self_rank >= 0 && p->T > 0 && !dg_local)) return MOE_ERR_INVALID_ARG;
-  if (p->T > 0 && (!topk_ids || !send_pos || !dg || (!dg_back && n_ranks > (self_rank >= 0 ? 1 : 0))))
-    return MOE_ERR_INVALID_ARG;
+  if (p->T > 0 && (!topk_ids || !send_pos || !dg)) return MOE_ERR_INVALID_ARG;  // dg_back: NULL iff no slot is remote
   return launch_ep_slot_grad(topk_ids, p->T, p->k, experts_per_rank, n_ranks, send_pos, dg_back, dg_local, self_rank,
                              dg, (cudaStream_t)stream);
 }

@@ -50,7 +50,7 @@
 namespace moeb {
 
 enum TcKind { TC_FWD_UP = 0, TC_FWD_DOWN = 1, TC_BWD_DH = 2, TC_BWD_DX = 3, TC_DW3 = 4, TC_DW12 = 5, TC_ROUTE = 6,
-              TC_BWD_DH_LK = 7, TC_ROUTE_S = 8 };
+              TC_BWD_DH_LK = 7, TC_ROUTE_S = 8, TC_BWD_DH_L5 = 9 };
 // K1 in two smem layouts: TC_ROUTE (any E <= 256: 32 KB of W_g rows per stage, 4 stages) and
 // TC_ROUTE_S (E <= 64: 8 KB per stage, 8 stages).  With T / 128 CTAs (fewer than the SMs at
 // the benchmark shapes) each CTA streams its tokens' X rows, so the bytes in flight per SM
@@ -61,7 +61,11 @@ __host__ __device__ constexpr bool is_route(int k) { return k == TC_ROUTE || k =
 // registers, so 8 epilogue warps fit; 4 stages) -- the CTA-pair default for every d >=
 // MOEB_DH_LK_MIN_D.  Its SwiGLU-backward epilogue (10 bytes per output element) was the
 // bottleneck under short mainloops (K = d = 2048)
-__host__ __device__ constexpr bool is_dh(int k) { return k == TC_BWD_DH || k == TC_BWD_DH_LK; }
+// TC_BWD_DH_L5: the same 16-column TMA epilogue on 4 warps, which leaves the shared memory for
+// a 5-stage mainloop -- the better trade for long K (d >= MOEB_DH_L5_MIN_D: Mixtral-like
+// BWD_DH 1.80 -> 1.70 ms), while short K (DeepSeek-like, d = 2048) needs the 8 warps to hide
+// the SwiGLU-backward epilogue (0.69 vs 0.86 ms; profiles/r02c_variants.txt)
+__host__ __device__ constexpr bool is_dh(int k) { return k == TC_BWD_DH || k == TC_BWD_DH_LK || k == TC_BWD_DH_L5; }
 
 #ifndef MOEB_DH_STAGES
 #define MOEB_DH_STAGES 5  // BWD_DH mainloop stages in the CTA-pair engine (smem shared with the epilogue ring)
@@ -71,6 +75,11 @@ __host__ __device__ constexpr bool is_dh(int k) { return k == TC_BWD_DH || k == 
 #endif
 #ifndef MOEB_DH_NBUF
 #define MOEB_DH_NBUF 6    // BWD_DH epilogue ring depth (A/B chunks of DH_CW columns per warp)
+#endif
+#ifndef MOEB_DH_L2PF
+// BWD_DH epilogue: prefetch the next tile's A, B rows into L2.  Off: measured slower on both
+// shapes (DeepSeek-like 0.69 -> 0.74 ms, Mixtral-like 1.80 -> 1.88 ms; profiles/r02c_variants.txt)
+#define MOEB_DH_L2PF 0
 #endif
 #ifndef MOEB_DH_EPI8
 #define MOEB_DH_EPI8 1    // TC_BWD_DH_LK: 8 epilogue warps (two per TMEM lane quarter, 128 columns each)
@@ -142,7 +151,7 @@ struct CgCfg {
   // BWD_DH shares smem between its mainloop ring and the epilogue A/B ring (tools/tune_variants.sh:
   // 4 stages + 4-deep ring beat 3 + 7 by 11 % on the Mixtral layer)
   static constexpr bool DH = is_dh(KIND);
-  static constexpr bool LK = (KIND == TC_BWD_DH_LK) && MOEB_DH_TMA;
+  static constexpr bool LK = (KIND == TC_BWD_DH_LK || KIND == TC_BWD_DH_L5) && MOEB_DH_TMA;
   static constexpr int NEPI = n_epi(KIND);
   static constexpr int STAGES = DH ? (CG == 1 ? 2 : (LK ? (NEPI == 8 ? MOEB_DH8_STAGES : MOEB_DH_STAGES) : MOEB_DH_STAGES_SK))
                                    : (KIND == TC_ROUTE_S ? 8 : CG == 1 ? 4 : (NEPI == 8 ? 5 : 6));
@@ -915,20 +924,28 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
         if (lane == 0) {
           ptx::bulk_wait_read<1>();
           for (int ci = 0; ci < DH_PF && ci < nchunk; ++ci) dh_load(gch + ci, t.n0 + cb + CW * ci, r0w);
-          // the NEXT tile's A, B boxes of this warp go to L2 now, a whole tile ahead: the
-          // ring's loads then hit L2 instead of paying HBM latency DH_PF chunks ahead
+        }
+        __syncwarp();
+        if constexpr (MOEB_DH_L2PF) {
+          // the NEXT tile's A, B rows of this warp go to L2 now, a whole tile ahead: the
+          // ring's TMA loads then hit L2 instead of paying HBM latency DH_PF chunks ahead.
+          // One row per lane, plain prefetch.global.L2 (LSU, not the TMA unit, which the
+          // mainloop's W3 loads and the epilogue's boxes keep busy)
+          int nt = 0;
+          if (lane == 0) nt = peek(it + 1);
+          nt = __shfl_sync(0xffffffffu, nt, 0);
           TileInfo tn;
-          if (decode_tile<KIND, CG>(peek(it + 1), P, s_offs, s_mstart, tn)) {
-            const int r0n = tn.m0 + rowoff + wq * 32;
-            const int ncn = max(0, min(NCW, P.h - tn.n0 - cb)) / CW;
-            if (r0n < tn.seg1)
-              for (int ci = 0; ci < ncn; ++ci) {
-                ptx::tma_prefetch_l2_2d(&mA0, tn.n0 + cb + CW * ci, r0n);
-                if (P.act == 0) ptx::tma_prefetch_l2_2d(&mA1, tn.n0 + cb + CW * ci, r0n);
+          if (decode_tile<KIND, CG>(nt, P, s_offs, s_mstart, tn)) {
+            const int rn = tn.m0 + rowoff + wq * 32 + lane;
+            const int ncol = max(0, min(NCW, P.h - tn.n0 - cb));
+            if (rn < tn.seg1)
+              for (int c = 0; c < ncol; c += 64) {  // 128-byte lines
+                const int64_t o = (int64_t)rn * P.h + tn.n0 + cb + c;
+                ptx::prefetch_l2(P.a_save + o);
+                if (P.act == 0) ptx::prefetch_l2(P.b_save + o);
               }
           }
         }
-        __syncwarp();
       } else if constexpr (is_dh(KIND)) {
         // the epilogue inputs (A, B rows of this tile) do not depend on the
         // accumulator: start streaming the first chunks before waiting for it
@@ -1616,18 +1633,21 @@ static moe_status launch_tc(const CUtensorMap& a0, const CUtensorMap& a1, const 
   }
 }
 
-// BWD_DH variant: the long-K one for d >= 3072 in the CTA-pair engine
+// BWD_DH variants in the CTA-pair engine (TMA epilogue, 16-column chunks): 8 epilogue warps /
+// 4 stages (TC_BWD_DH_LK) below MOEB_DH_L5_MIN_D, 4 warps / 5 stages (TC_BWD_DH_L5) from it
 #ifndef MOEB_DH_LK_MIN_D
-// smallest d that runs TC_BWD_DH_LK; 0 = every shape: with 8 epilogue warps it measured
-// DeepSeek-like BWD_DH 0.74-0.80 -> 0.67-0.70 ms (step +2.5 %) and the Mixtral step neutral
-// against the 4-warp / 5-stage long-K variant (profiles/epi8_ab_r01.txt)
 #define MOEB_DH_LK_MIN_D 0
 #endif
+#ifndef MOEB_DH_L5_MIN_D
+#define MOEB_DH_L5_MIN_D 3072
+#endif
 static bool dh_long_k(int d) { return MOEB_DH_TMA && engine() == ENG_PAIR && d >= MOEB_DH_LK_MIN_D; }
+static bool dh_l5(int d) { return dh_long_k(d) && d >= MOEB_DH_L5_MIN_D; }
 // gate-grad partial columns per routed row written by BWD_DH (one per n-tile, two with the
 // 8-warp epilogue, whose column halves each write their own)
 int tc_dg_parts(int h, int d) {
-  return (int)ceil_div(h, TBN) * ((dh_long_k(d) && n_epi(TC_BWD_DH_LK) == 8) ? 2 : 1);
+  const bool two = dh_long_k(d) && !dh_l5(d) && n_epi(TC_BWD_DH_LK) == 8;
+  return (int)ceil_div(h, TBN) * (two ? 2 : 1);
 }
 
 // K1 on tensor cores (bf16): logits = X Wg^T with M = 128 tokens, N = E padded
@@ -1703,6 +1723,7 @@ moe_status tc_gemm(const GemmCall& c, cudaStream_t st) {
       }
       if (!ok) return MOE_ERR_CUDA;
       P.n_tiles = (int)ceil_div(h, TBN);
+      if (lk && dh_l5(d)) return launch_tc<TC_BWD_DH_L5>(a0, a1, b0, b1, P, rows_tiles(P.n_tiles), st);
       if (lk) return launch_tc<TC_BWD_DH_LK>(a0, a1, b0, b1, P, rows_tiles(P.n_tiles), st);
       return launch_tc<TC_BWD_DH>(a0, a1, b0, b1, P, rows_tiles(P.n_tiles), st);
     }

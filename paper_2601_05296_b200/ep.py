@@ -198,8 +198,7 @@ class ExpertParallelMoE:
         self.last_pairs_sent = 0      # (token, expert) pairs they carry
 
     def a2a(self, send, send_split, recv_split, out=None):
-        if out is not None and not sum(recv_split) and not sum(send_split):
-            return out  # nothing to exchange at all (e.g. P = 1)
+        """Collective: every rank calls it, also with nothing to send or receive."""
         return self._a2a(send, send_split, recv_split, self.group, out=out)
 
     def _use_streams(self, x):

@@ -79,7 +79,8 @@ def test_abu_parity(M, T, d, h, E, k, dtype, act, renorm):
 @pytest.mark.parametrize("dtype", ["bf16", "fp32"])
 def test_staged_backward_bit_identical(M, ckpt, dtype):
     """moe_ffn_bwd issued as three stage calls on one workspace == one call."""
-    T, d, h, E, k = (700, 256, 640, 8, 2) if dtype == "bf16" else (200, 64, 96, 6, 3)
+    # k <= 2: the fused red.add combine is then order-independent, so two runs are bitwise equal
+    T, d, h, E, k = (700, 256, 640, 8, 2) if dtype == "bf16" else (200, 64, 96, 6, 2)
     inp = make_inputs(T, d, h, E, k, dtype=dtype, seed=21, device=DEV)
     x, wg, w1, w2, w3, dy = (inp[n] for n in ("x", "w_gate", "w1", "w2", "w3", "dy"))
     logits, ids, w = M.route(x, wg, k)
