@@ -76,6 +76,9 @@ __host__ __device__ constexpr bool is_dh(int k) { return k == TC_BWD_DH || k == 
 #ifndef MOEB_DH_NBUF
 #define MOEB_DH_NBUF 6    // BWD_DH epilogue ring depth (A/B chunks of DH_CW columns per warp)
 #endif
+#ifndef MOEB_TEMPTY_RELAXED
+#define MOEB_TEMPTY_RELAXED 1  // epilogue -> MMA "accumulator free" arrive without a cluster release fence
+#endif
 #ifndef MOEB_DH_L2PF
 // BWD_DH epilogue: prefetch the next tile's A, B rows into L2.  Off: measured slower on both
 // shapes (DeepSeek-like 0.69 -> 0.74 ms, Mixtral-like 1.80 -> 1.88 ms; profiles/r02c_variants.txt)
@@ -1485,11 +1488,19 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
           __syncwarp();
         }
       }
+      // the accumulator stage is free: its tcgen05.ld's have completed (tcgen05.wait::ld) and
+      // the fence orders them before the arrive.  Relaxed: a release.cluster arrive compiles to
+      // MEMBAR.ALL.GPU, which would make every epilogue warp wait for its own red.adds / stores
+      // to drain at the end of each tile (nothing the MMA warp reads depends on them)
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if constexpr (CG == 2) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty[as]), 0));
-        else ptx::mbar_arrive(&tempty[as]);
+        if constexpr (CG == 2) {
+          if constexpr (MOEB_TEMPTY_RELAXED) ptx::mbar_arrive_cluster_relaxed(ptx::mapa(ptx::smem_u32(&tempty[as]), 0));
+          else ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty[as]), 0));
+        } else {
+          ptx::mbar_arrive(&tempty[as]);
+        }
       }
       if (++as == 2) { as = 0; aphase ^= 1; }
     }
