@@ -231,6 +231,7 @@ def main():
     if args.impl == "reference":
         return run_reference(args, cfg, rank, world)
 
+    numa = bind_numa(local)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     use_ep = world > 1 or args.ep
@@ -283,9 +284,10 @@ def main():
         def step():
             logits, ids, w = M.route(x, wg, k, renorm)
             disp = M.dispatch_build(ids, cfg.E, dtype=x.dtype)
-            y, a, b = M.ffn_fwd(x, w1, w2, w3, w, disp, renorm, checkpoint=ck, activation=act, deterministic=det)
+            out = M.ffn_fwd(x, w1, w2, w3, w, disp, renorm, checkpoint=ck, activation=act, deterministic=det)
+            y, a, b = out[:3]
             g = M.ffn_bwd(dy, x, w1, w2, w3, w, disp, a, b, w_gate=wg, logits=logits, renormalize=renorm,
-                          checkpoint=ck, activation=act, deterministic=det)
+                          checkpoint=ck, activation=act, deterministic=det, u_save=out[3] if ck == "abu" else None)
             return y, g
 
     for _ in range(args.warmup):
@@ -394,20 +396,40 @@ def main():
         n_e2e = args.steps
         ys_h = [torch.empty_like(x_h).pin_memory() for _ in range(2)]
         dxs_h = [torch.empty_like(x_h).pin_memory() for _ in range(2)]
-        pipe.run([x_h] * 2, [dy_h] * 2, ys_h, dxs_h)  # warm-up
+        # the timed region above used the functional API: hand its cached blocks back so the
+        # autograd path's allocation pattern settles during its own warm-up
+        torch.cuda.empty_cache()
+        nw = max(args.warmup, 3)
+        pipe.run([x_h] * nw, [dy_h] * nw, [ys_h[i % 2] for i in range(nw)], [dxs_h[i % 2] for i in range(nw)])
         torch.cuda.synchronize()
+        # the pinned buffers' own PCIe rates (one copy each way, nothing else running)
+        c0, c1, c2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        c0.record(st)
+        pipe.x[0].copy_(x_h, non_blocking=True)
+        c1.record(st)
+        ys_h[0].copy_(pipe.x[0], non_blocking=True)
+        c2.record(st)
+        torch.cuda.synchronize()
+        nb = x_h.numel() * x_h.element_size()
+        pcie = {"h2d_gbs": round(nb / (c0.elapsed_time(c1) / 1e3) / 1e9, 1),
+                "d2h_gbs": round(nb / (c1.elapsed_time(c2) / 1e3) / 1e9, 1), "bytes": nb}
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ms0 = torch.cuda.memory_stats()
         e0.record(st)
         pipe.run([x_h] * n_e2e, [dy_h] * n_e2e, [ys_h[i % 2] for i in range(n_e2e)],
                  [dxs_h[i % 2] for i in range(n_e2e)])
         e1.record(st)
         torch.cuda.synchronize()
+        ms1 = torch.cuda.memory_stats()
+        # cudaMalloc / cudaFree inside the timed loop serialise host and device
+        alloc = {k: ms1.get(k, 0) - ms0.get(k, 0) for k in ("num_device_alloc", "num_device_free", "num_alloc_retries")}
         ems = e0.elapsed_time(e1) / n_e2e
         if use_ep:
             t = torch.tensor([ems], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
         e2e = {"value": round(world * cfg.T / (ems / 1e3), 1), "unit": UNIT, "ms_per_step": round(ems, 4),
+               "pcie": pcie, "host_numa": numa, "allocator_in_timed_loop": alloc,
                "h2d_bytes_per_step": 2 * x.numel() * x.element_size(),
                "d2h_bytes_per_step": 2 * x.numel() * x.element_size(),
                "api": ("paper_2601_05296_b200.ep.ExpertParallelMoE.step" if ep is not None else
@@ -453,6 +475,34 @@ def main():
         print(json.dumps(out), flush=True)
     if use_ep:
         dist.destroy_process_group()
+
+
+def bind_numa(gpu_index):
+    """Pin this process to the CPUs of the GPU's NUMA node, before any pinned host
+    buffer exists: page-locked memory is then allocated on the GPU's local node
+    (first touch), so the e2e leg's H2D/D2H copies do not cross the socket
+    interconnect.  Reported, never required."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+        bus = pynvml.nvmlDeviceGetPciInfo(h).busId
+        bus = (bus.decode() if isinstance(bus, bytes) else bus).lower()
+        bus = bus[-12:] if len(bus) > 12 else bus  # "00000000:xx:yy.z" -> "0000:xx:yy.z"
+        node = int(open(f"/sys/bus/pci/devices/{bus}/numa_node").read().strip())
+        if node < 0:
+            return {"node": None, "bound": False, "why": "no NUMA affinity reported for the GPU"}
+        cpus = set()
+        for part in open(f"/sys/devices/system/node/node{node}/cpulist").read().strip().split(","):
+            a, _, b = part.partition("-")
+            cpus.update(range(int(a), int(b or a) + 1))
+        cpus &= os.sched_getaffinity(0)
+        if not cpus:
+            return {"node": node, "bound": False, "why": "no allowed CPU on the GPU's node"}
+        os.sched_setaffinity(0, cpus)
+        return {"node": node, "cpus": len(cpus), "bound": True}
+    except Exception as exc:  # report, never fail the bench
+        return {"node": None, "bound": False, "why": repr(exc)[:160]}
 
 
 def relaunch(n):

@@ -76,6 +76,9 @@ __host__ __device__ constexpr bool is_dh(int k) { return k == TC_BWD_DH || k == 
 #ifndef MOEB_DH_NBUF
 #define MOEB_DH_NBUF 6    // BWD_DH epilogue ring depth (A/B chunks of DH_CW columns per warp)
 #endif
+#ifndef MOEB_SMEM_TIGHT
+#define MOEB_SMEM_TIGHT 0  // 768-byte barrier block and no alignment slack (lets 8-warp BWD_DH run 5 stages)
+#endif
 #ifndef MOEB_TEMPTY_RELAXED
 #define MOEB_TEMPTY_RELAXED 1  // epilogue -> MMA "accumulator free" arrive without a cluster release fence
 #endif
@@ -167,8 +170,14 @@ struct CgCfg {
   static constexpr int STG_WARP = DH ? (DH_NBUF * DH_SLOT + DH_SLOT) : ((KIND == TC_FWD_UP && NEPI == 8) ? 3072 : 6144);
   // 1024-aligned: the BWD_DH tiles are TMA boxes in the 64-byte swizzle, whose pattern is
   // taken from the smem address bits
-  static constexpr int STG_OFF = (STAGES * STAGE + 1024 /*barriers*/ + 2176 /*offsets, tile starts*/ + 1023) / 1024 * 1024;
-  static constexpr int SMEM = STG_OFF + NEPI * STG_WARP + 1024 /*align*/;
+  // after the stages: barriers (768 B: stage/accumulator/scheduler barriers at +0 / +256, the
+  // BWD_DH epilogue ring's at +512) and the per-expert offsets + tile starts (2 x 260 ints)
+  static constexpr int OFFS_OFF = MOEB_SMEM_TIGHT ? 768 : 1024;
+  static constexpr int STG_OFF = (STAGES * STAGE + OFFS_OFF + (MOEB_SMEM_TIGHT ? 2080 : 2176) + 1023) / 1024 * 1024;
+  // the dynamic shared memory starts 1024-aligned (after the 1 KB the driver reserves per CTA;
+  // profiles/smem_probe_r02e.txt), so the tight layout carries no alignment slack (the kernel
+  // traps if that ever changes)
+  static constexpr int SMEM = STG_OFF + NEPI * STG_WARP + (MOEB_SMEM_TIGHT ? 0 : 1024);
 };
 
 struct TcParams {
@@ -490,7 +499,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
   uint64_t* sfull = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE + 256);
   uint64_t* sempty = sfull + SCHED_RING;
   int* s_ring = reinterpret_cast<int*>(sempty + SCHED_RING);
-  int* s_offs = reinterpret_cast<int*>(smem + STAGES * C::STAGE + 1024);
+  int* s_offs = reinterpret_cast<int*>(smem + STAGES * C::STAGE + C::OFFS_OFF);
+  if constexpr (MOEB_SMEM_TIGHT)
+    if (smem != smem_raw) __trap();  // no alignment slack was allocated
   int* s_mstart = s_offs + 260;
   constexpr bool DYN = dyn_sched<KIND, CG>();
   // arrivals that release a ring slot: every tile-iterating warp of both CTAs
