@@ -77,7 +77,7 @@ __host__ __device__ constexpr bool is_dh(int k) { return k == TC_BWD_DH || k == 
 #define MOEB_DH_NBUF 6    // BWD_DH epilogue ring depth (A/B chunks of DH_CW columns per warp)
 #endif
 #ifndef MOEB_SMEM_TIGHT
-#define MOEB_SMEM_TIGHT 0  // 768-byte barrier block and no alignment slack (lets 8-warp BWD_DH run 5 stages)
+#define MOEB_SMEM_TIGHT 1  // 768-byte barrier block and no alignment slack (lets 8-warp BWD_DH run 5 stages)
 #endif
 #ifndef MOEB_TEMPTY_RELAXED
 #define MOEB_TEMPTY_RELAXED 1  // epilogue -> MMA "accumulator free" arrive without a cluster release fence
@@ -101,11 +101,14 @@ __host__ __device__ constexpr bool is_dh(int k) { return k == TC_BWD_DH || k == 
 // off: interleaved A/B measured both kinds 1-5 % slower (profiles/red8_ab_r01.txt)
 #define MOEB_RED_EPI8 0
 #endif
+// 8-warp BWD_DH: 5 mainloop stages + a 3-deep epilogue ring (one chunk of A/B prefetch) in the
+// tight layout; measured DeepSeek-like BWD_DH 0.681 -> 0.670 ms (mean of 4, interleaved,
+// profiles/variants_r02i_dh5.txt) against 4 stages + a 4-deep ring
 #ifndef MOEB_DH8_STAGES
-#define MOEB_DH8_STAGES 4
+#define MOEB_DH8_STAGES 5
 #endif
 #ifndef MOEB_DH8_NBUF
-#define MOEB_DH8_NBUF 4
+#define MOEB_DH8_NBUF 3
 #endif
 #ifndef MOEB_DH_STAGES_SK
 #define MOEB_DH_STAGES_SK 4  // the same for the short-K variant (TC_BWD_DH)
@@ -481,6 +484,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
   using K = KindTraits<KIND>;
   using C = CgCfg<CG, KIND>;
   static_assert(CG == 1 || CPA, "the CTA-pair path uses the cp.async gather engine");
+  static_assert(C::SMEM <= 232448, "dynamic shared memory over the 227 KB opt-in limit");
   constexpr int STAGES = C::STAGES;
   constexpr int NB = TBN / CG;     // B columns (rows of the B tile) held by this CTA
   constexpr int NPANEL = NB / 64;  // 64-column MN-major panels of B in this CTA
@@ -566,6 +570,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
   else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  // shared::cluster addresses of the barriers other CTAs / the leader signal, translated once:
+  // mapa is a variable-latency instruction, and inside the per-k-block loops its result was
+  // what the producer's TMA issue and the gather relay's arrive waited on (long scoreboard)
+  const uint32_t full_c0 = (CG == 2) ? ptx::mapa(ptx::smem_u32(full), 0) : 0u;     // leader's full[]
+  const uint32_t sempty_c0 = (CG == 2) ? ptx::mapa(ptx::smem_u32(sempty), 0) : 0u; // leader's sempty[]
+  const uint32_t tempty_c0 = (CG == 2) ? ptx::mapa(ptx::smem_u32(tempty), 0) : 0u; // leader's tempty[]
 
   // i-th tile of this CTA pair: static cluster-strided order, or the dynamic
   // scheduler's ring (every tile-iterating warp reads every slot once, then
@@ -594,7 +604,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
       __syncwarp();
       if (lane == 0 && tile != INT_MIN) {
         if (leader) ptx::mbar_arrive(&sempty[slot]);
-        else ptx::mbar_arrive_cluster_relaxed(ptx::mapa(ptx::smem_u32(&sempty[slot]), 0));
+        else ptx::mbar_arrive_cluster_relaxed(sempty_c0 + 8u * (uint32_t)slot);
       }
       return tile;
     } else {
@@ -622,7 +632,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
         uint8_t* sA = smem + stage * C::STAGE;
         uint8_t* sB = sA + TA_BYTES;
         uint64_t* bar = &full[stage];
-        const uint32_t bar_c = (CG == 2) ? ptx::mapa(ptx::smem_u32(bar), 0) : 0u;
+        const uint32_t bar_c = full_c0 + 8u * (uint32_t)stage;  // leader's full[stage] (CTA pair)
         if (lane == 0) {
           if constexpr (is_route(KIND)) {
             ptx::mbar_arrive_expect_tx(bar, (uint32_t)(TA_BYTES + P.route_n * 128));
@@ -809,7 +819,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
           ptx::mbar_wait(&gfull[stage], phase);
           if (lane == 0) {
             ptx::fence_proxy_async();
-            ptx::mbar_arrive_cluster_relaxed(ptx::mapa(ptx::smem_u32(&full[stage]), 0));
+            ptx::mbar_arrive_cluster_relaxed(full_c0 + 8u * (uint32_t)stage);
           }
           __syncwarp();
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -1507,8 +1517,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
       __syncwarp();
       if (lane == 0) {
         if constexpr (CG == 2) {
-          if constexpr (MOEB_TEMPTY_RELAXED) ptx::mbar_arrive_cluster_relaxed(ptx::mapa(ptx::smem_u32(&tempty[as]), 0));
-          else ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty[as]), 0));
+          if constexpr (MOEB_TEMPTY_RELAXED) ptx::mbar_arrive_cluster_relaxed(tempty_c0 + 8u * (uint32_t)as);
+          else ptx::mbar_arrive_cluster(tempty_c0 + 8u * (uint32_t)as);
         } else {
           ptx::mbar_arrive(&tempty[as]);
         }

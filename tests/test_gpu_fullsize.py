@@ -17,7 +17,7 @@ import torch
 
 import oracle as O
 from moe_inputs import CONFIGS, make_inputs
-from tests._util import BF16_TOL, f64, i64, normwise
+from tests._util import BF16_TOL, ROW_TOL_BF16, f64, i64, normwise, rowwise
 
 pytestmark = pytest.mark.gpu
 DEV = "cuda"
@@ -27,27 +27,45 @@ def _sample(n, m, seed):
     return np.sort(np.random.default_rng(seed).choice(n, size=min(m, n), replace=False))
 
 
-@pytest.mark.parametrize("name", ["mixtral", "deepseek", "sweep_4k", "ep"])
-def test_fullsize_sampled_parity(name):
+FULL_CASES = [
+    # workload, renormalize, activation, deterministic, checkpoint
+    ("mixtral", False, "swiglu", False, "ab"), ("deepseek", False, "swiglu", False, "ab"),
+    ("sweep_4k", False, "swiglu", False, "ab"), ("ep", False, "swiglu", False, "ab"),
+    # the non-default modes at full size
+    ("mixtral", True, "swiglu", False, "ab"),          # Mixtral-style renormalised gates
+    ("deepseek", False, "silu", False, "ab"),          # non-gated SiLU experts
+    ("deepseek", False, "swiglu", True, "ab"),         # ordered combine, k = 6
+    ("mixtral", False, "swiglu", False, "abu"),        # Alg. 1 literal checkpoint
+]
+
+
+@pytest.mark.parametrize("name,renorm,act,det,ckpt", FULL_CASES,
+                         ids=["-".join(map(str, c)) for c in FULL_CASES])
+def test_fullsize_sampled_parity(name, renorm, act, det, ckpt):
     import paper_2601_05296_b200 as M
     cfg = CONFIGS[name]
     T, d, h, E, k = cfg.T, cfg.d, cfg.h, cfg.E, cfg.k
+    gated = act == "swiglu"
     inp = make_inputs(T, d, h, E, k, dtype="bf16", seed=0, device=DEV)
-    x, wg, w1, w2, w3, dy = (inp[n] for n in ("x", "w_gate", "w1", "w2", "w3", "dy"))
+    x, wg, w1, w3, dy = (inp[n] for n in ("x", "w_gate", "w1", "w3", "dy"))
+    w2 = inp["w2"] if gated else None
     experts = _sample(E, 2, 2)
     hid = {int(e): _sample(h, 64, 3 + int(e)) for e in experts}
-    logits, ids, w = M.route(x, wg, k)
+    logits, ids, w = M.route(x, wg, k, renorm)
     disp = M.dispatch_build(ids, E)
-    y, a, b = M.ffn_fwd(x, w1, w2, w3, w, disp)
+    out = M.ffn_fwd(x, w1, w2, w3, w, disp, renorm, checkpoint=ckpt, activation=act, deterministic=det)
+    y, a, b = out[:3]
     offs = i64(disp.offs)
-    ckpt = {e: (f64(a[offs[e]:offs[e + 1], torch.from_numpy(S).to(DEV)]),
-                f64(b[offs[e]:offs[e + 1], torch.from_numpy(S).to(DEV)])) for e, S in hid.items()}
-    g = M.ffn_bwd(dy, x, w1, w2, w3, w, disp, a, b, w_gate=wg, logits=logits)
+    sel = {e: torch.from_numpy(S).to(DEV) for e, S in hid.items()}
+    ckpt_a = {e: f64(a[offs[e]:offs[e + 1], sel[e]]) for e in hid}
+    ckpt_b = {e: f64(b[offs[e]:offs[e + 1], sel[e]]) for e in hid} if gated else {}
+    g = M.ffn_bwd(dy, x, w1, w2, w3, w, disp, a, b, w_gate=wg, logits=logits, renormalize=renorm,
+                  checkpoint=ckpt, activation=act, deterministic=det, u_save=out[3] if ckpt == "abu" else None)
     torch.cuda.synchronize()
 
     # routing + dispatch: full, bit-exact
     L = f64(logits)
-    _, rids, rw = O.topk_from_logits(L, k)
+    _, rids, rw = O.topk_from_logits(L, k, renorm)
     assert np.array_equal(i64(ids), rids)
     assert np.abs(f64(w) - rw).max() < 1e-5
     rd = O.dispatch_argsort(rids, E)
@@ -57,25 +75,31 @@ def test_fullsize_sampled_parity(name):
     # sampled tokens: y, dx, dg (full weights, forced routing)
     toks = _sample(T, 48, 1)
     X, DY = f64(x), f64(dy)
-    WG, W1, W2, W3 = f64(wg), f64(w1), f64(w2), f64(w3)
-    fs = O.layer_forward(X[toks], WG, W1, W2, W3, k, logits=L[toks])
-    bs = O.layer_backward(fs, DY[toks], X[toks], WG, W1, W2, W3)
+    WG, W1, W3 = f64(wg), f64(w1), f64(w3)
+    W2 = f64(w2) if gated else None
+    fs = O.layer_forward(X[toks], WG, W1, W2, W3, k, renorm, logits=L[toks], activation=act)
+    bs = O.layer_backward(fs, DY[toks], X[toks], WG, W1, W2, W3, renorm)
     errs = {"y": normwise(y[toks], fs["y"]), "dx": normwise(g["dx"][toks], bs["dx"]),
             "dg": normwise(g["dg"][toks], bs["dg"])}
+    rows = {"y": rowwise(y[toks], fs["y"]), "dx": rowwise(g["dx"][toks], bs["dx"])}
 
     # sampled (expert, hidden-unit) slices of the weight gradients, all routed rows
     for e, S in hid.items():
-        sl = O.ffn_forward(X, W1[:, S, :], W2[:, S, :], W3[:, :, S], rids, rw, rd)
-        sb = O.ffn_backward(DY, X, W1[:, S, :], W2[:, S, :], W3[:, :, S], rids, rw, rd, sl["A"], sl["B"])
+        W2s = W2[:, S, :] if gated else None
+        sl = O.ffn_forward(X, W1[:, S, :], W2s, W3[:, :, S], rids, rw, rd, act)
+        sb = O.ffn_backward(DY, X, W1[:, S, :], W2s, W3[:, :, S], rids, rw, rd, sl["A"], sl["B"], act)
         lo, hi = rd["offs"][e], rd["offs"][e + 1]
-        errs[f"A[{e}]"] = normwise(ckpt[e][0], sl["A"][lo:hi])
-        errs[f"B[{e}]"] = normwise(ckpt[e][1], sl["B"][lo:hi])
-        errs[f"dw1[{e}]"] = normwise(g["dw1"][e][torch.from_numpy(S).to(DEV)], sb["dw1"][e])
-        errs[f"dw2[{e}]"] = normwise(g["dw2"][e][torch.from_numpy(S).to(DEV)], sb["dw2"][e])
-        errs[f"dw3[{e}]"] = normwise(g["dw3"][e][:, torch.from_numpy(S).to(DEV)], sb["dw3"][e])
+        errs[f"A[{e}]"] = normwise(ckpt_a[e], sl["A"][lo:hi])
+        errs[f"dw1[{e}]"] = normwise(g["dw1"][e][sel[e]], sb["dw1"][e])
+        errs[f"dw3[{e}]"] = normwise(g["dw3"][e][:, sel[e]], sb["dw3"][e])
+        rows[f"dw1[{e}]"] = rowwise(g["dw1"][e][sel[e]], sb["dw1"][e])
+        if gated:
+            errs[f"B[{e}]"] = normwise(ckpt_b[e], sl["B"][lo:hi])
+            errs[f"dw2[{e}]"] = normwise(g["dw2"][e][sel[e]], sb["dw2"][e])
     # router backward at full size from the GPU's dg
-    rb = O.router_backward(f64(g["dg"]), X, WG, L, rids)
+    rb = O.router_backward(f64(g["dg"]), X, WG, L, rids, renorm)
     errs["dw_gate"] = normwise(g["dw_gate"], rb["dw_gate"])
     bad = {n: v for n, v in errs.items() if not v <= BF16_TOL}
-    assert not bad, (name, errs)
-    print(name, {n: round(v, 5) for n, v in errs.items()})
+    bad.update({"row:" + n: v for n, v in rows.items() if not v <= ROW_TOL_BF16})
+    assert not bad, (name, errs, rows)
+    print(name, renorm, act, det, ckpt, {n: round(v, 5) for n, v in errs.items()})
