@@ -266,8 +266,9 @@ def main():
         w2 = None
     ep = None
     if use_ep:
-        if not gated or det:
-            raise SystemExit("--activation/--deterministic are single-GPU options (the EP receiver runs k = 1)")
+        if not gated or det or args.checkpoint != "ab":
+            raise SystemExit("--activation/--deterministic/--checkpoint are single-GPU options "
+                             "(the expert-parallel path runs the SwiGLU layer with the A, B checkpoint)")
         from paper_2601_05296_b200.ep import ExpertParallelMoE
         ep = ExpertParallelMoE(cfg.E, k, renorm, group=None, retain_recv_x=args.retain_recv_x)
         # each rank keeps only its experts' weights; the router is replicated

@@ -103,3 +103,37 @@ def test_fullsize_sampled_parity(name, renorm, act, det, ckpt):
     bad.update({"row:" + n: v for n, v in rows.items() if not v <= ROW_TOL_BF16})
     assert not bad, (name, errs, rows)
     print(name, renorm, act, det, ckpt, {n: round(v, 5) for n, v in errs.items()})
+
+
+def test_fullsize_deepseek_full_tensors():
+    """The DeepSeek-like layer (BASELINE configs[2]) compared on EVERY element of
+    every output -- not a sample: the fp64 oracle runs the whole layer (forced
+    routing on the GPU's fp32 logits, ~5 TFLOP in fp64 on the host), so dW_g
+    here comes from the oracle's own dg, independent of the GPU's."""
+    import paper_2601_05296_b200 as M
+    cfg = CONFIGS["deepseek"]
+    T, d, h, E, k = cfg.T, cfg.d, cfg.h, cfg.E, cfg.k
+    inp = make_inputs(T, d, h, E, k, dtype="bf16", seed=0, device=DEV)
+    x, wg, w1, w2, w3, dy = (inp[n] for n in ("x", "w_gate", "w1", "w2", "w3", "dy"))
+    logits, ids, w = M.route(x, wg, k)
+    disp = M.dispatch_build(ids, E)
+    y, a, b = M.ffn_fwd(x, w1, w2, w3, w, disp)
+    A0, B0 = f64(a), f64(b)
+    g = M.ffn_bwd(dy, x, w1, w2, w3, w, disp, a, b, w_gate=wg, logits=logits)
+    torch.cuda.synchronize()
+    X, WG, W1, W2, W3, DY = (f64(t) for t in (x, wg, w1, w2, w3, dy))
+    fwd = O.layer_forward(X, WG, W1, W2, W3, k, logits=f64(logits))
+    assert np.array_equal(i64(ids), fwd["ids"])
+    bwd = O.layer_backward(fwd, DY, X, WG, W1, W2, W3)
+    errs = {"A": normwise(A0, fwd["A"]), "B": normwise(B0, fwd["B"]), "y": normwise(y, fwd["y"]),
+            "dA": normwise(a, bwd["dA"]), "dB": normwise(b, bwd["dB"]), "dg": normwise(g["dg"], bwd["dg"]),
+            "dx": normwise(g["dx"], bwd["dx"]), "dw1": normwise(g["dw1"], bwd["dw1"]),
+            "dw2": normwise(g["dw2"], bwd["dw2"]), "dw3": normwise(g["dw3"], bwd["dw3"]),
+            "dw_gate": normwise(g["dw_gate"], bwd["dw_gate"])}
+    rows = {n: rowwise(g[n] if n in g else y, bwd[n] if n in bwd else fwd["y"]) for n in ("dx", "dw1", "dw3")}
+    rows["y"] = rowwise(y, fwd["y"])
+    bad = {n: v for n, v in errs.items() if not v <= BF16_TOL}
+    bad.update({"row:" + n: v for n, v in rows.items() if not v <= ROW_TOL_BF16})
+    print("deepseek full tensors", {n: round(v, 5) for n, v in errs.items()},
+          "rowwise", {n: round(v, 5) for n, v in rows.items()})
+    assert not bad, (errs, rows)

@@ -12,7 +12,7 @@ import sys
 from collections import defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-NAMES = {0: "FWD_UP", 1: "FWD_DOWN", 2: "BWD_DH", 7: "BWD_DH", 3: "BWD_DX", 4: "DW3", 5: "DW12"}
+NAMES = {0: "FWD_UP", 1: "FWD_DOWN", 2: "BWD_DH", 7: "BWD_DH", 9: "BWD_DH", 3: "BWD_DX", 4: "DW3", 5: "DW12"}
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
