@@ -82,13 +82,25 @@ def main():
                     with torch.autograd.graph.saved_tensors_hooks(pack, lambda t: t):
                         y = fn(xl, *params)
                     del y
+                    # peak of one fwd+bwd (max_memory_allocated delta), minus the parameter gradients
+                    for p in params:
+                        p.grad = None
+                    torch.cuda.synchronize()
+                    base_b = torch.cuda.memory_allocated()
+                    torch.cuda.reset_peak_memory_stats()
+                    run(fn)
+                    torch.cuda.synchronize()
+                    peak = torch.cuda.max_memory_allocated() - base_b
+                    grads = sum(p.grad.numel() * p.grad.element_size() for p in params if p.grad is not None)
                     row[tag] = {"ms": round(ms, 3), "tokens_per_s": round(T / (ms / 1e3), 1),
-                                "saved_gb": round(sum(saved.values()) / 1e9, 4)}
+                                "saved_gb": round(sum(saved.values()) / 1e9, 4), "peak_gb": round(peak / 1e9, 4),
+                                "activation_peak_gb": round((peak - grads) / 1e9, 4)}
                 except Exception as exc:  # report, never fake
                     row[tag] = {"error": repr(exc)[:200]}
             if "ms" in row.get("moeblaze", {}) and "ms" in row.get("materialized", {}):
                 row["speedup"] = round(row["materialized"]["ms"] / row["moeblaze"]["ms"], 3)
                 row["memory_ratio"] = round(row["materialized"]["saved_gb"] / row["moeblaze"]["saved_gb"], 3)
+                row["peak_ratio"] = round(row["materialized"]["peak_gb"] / row["moeblaze"]["peak_gb"], 3)
             print(json.dumps(row), flush=True)
             torch.cuda.empty_cache()
 
