@@ -135,6 +135,12 @@ __host__ __device__ constexpr bool is_dh(int k) { return k == TC_BWD_DH || k == 
 #ifndef MOEB_EXP_NOEPI
 #define MOEB_EXP_NOEPI 0  // kinds whose epilogue is skipped (measures the mainloop alone)
 #endif
+#ifndef MOEB_EXP_SAMEB
+#define MOEB_EXP_SAMEB 0  // kinds whose B tiles all come from one L2-resident panel (operand-stream experiment)
+#endif
+#ifndef MOEB_EXP_NOB
+#define MOEB_EXP_NOB 0    // kinds whose B tiles are not loaded at all (the MMAs reuse stale smem; operand-stream experiment)
+#endif
 #ifndef MOEB_EXP_NOMMA
 #define MOEB_EXP_NOMMA 0  // kinds whose MMAs are skipped (measures loads + epilogue)
 #endif
@@ -642,6 +648,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
             uint32_t bytes = 2 * tma_bytes_per_cta<KIND, CPA, CG>();
             if constexpr (has_ntail<KIND, CG>())
               if (P.h - t.n0 <= 128) bytes -= (uint32_t)C::B_BYTES;  // half the B columns per CTA
+            if constexpr ((MOEB_EXP_NOB >> KIND) & 1) bytes -= 2 * (uint32_t)C::B_BYTES;
             if (leader) ptx::mbar_arrive_expect_tx(bar, bytes);
           }
         }
@@ -651,6 +658,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
           else ptx::tma_load_2d(dst, m, bar, c0, c1);
         };
         const int k0 = kb * TBK;
+        // timing-only experiment: every B tile from expert 0's first panel (results garbage)
+        constexpr bool SAMEB = (MOEB_EXP_SAMEB >> KIND) & 1;
+        const int bk0 = SAMEB ? 0 : k0, be = SAMEB ? 0 : t.e, bn0 = SAMEB ? 0 : t.n0;
+        constexpr bool NOB = (MOEB_EXP_NOB >> KIND) & 1;
         if constexpr (is_route(KIND)) {
           if (lane == 0) load(sA, &mA0, k0, t.m0);
           if (lane == 1) load(sB, &mB0, k0, 0);
@@ -663,20 +674,20 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
             if (lane == 1) load(sB + C::B_BYTES / 2, gated ? &mB1 : &mB0, k0, t.e * P.h + t.n0 + (gated ? 0 : 128));
           } else {
             // gated: CTA 0 holds the W1 rows, CTA 1 the W2 rows; non-gated: W1 rows n0 + 128 * rank
-            if (lane == 0)
-              load(sB, (gated && crank) ? &mB1 : &mB0, k0, t.e * P.h + t.n0 + (gated ? 0 : 128 * (int)crank));
+            if (lane == 0 && !NOB)
+              load(sB, (gated && crank) ? &mB1 : &mB0, bk0, be * P.h + bn0 + (gated ? 0 : 128 * (int)crank));
           }
         } else if constexpr (KIND == TC_FWD_DOWN) {
           // M = 128 tail: this CTA's 64 rows start at m0 + 64 * rank (the box's other 64 rows are unused)
           const int arow = (has_mtail<KIND, CG>() && t.seg1 - t.m0 <= 128) ? 64 * (int)crank : rowoff;
           if (lane == 0) load(sA, &mA0, k0, t.m0 + arow);
-          if (lane == 1) load(sB, &mB0, k0, t.e * P.d + t.n0 + coloff);
+          if (lane == 1 && !NOB) load(sB, &mB0, bk0, be * P.d + bn0 + coloff);
         } else if constexpr (is_dh(KIND)) {
           if (!CPA) ptx::tma_gather4(sA + 512 * lane, &mA0, bar, k0, gi0, gi1, gi2, gi3);
           if (has_ntail<KIND, CG>() && P.h - t.n0 <= 128) {  // N = 128: one 64-column panel per CTA
             if (lane == 0) load(sB, &mB0, t.n0 + 64 * (int)crank, t.e * P.d + k0);
-          } else if (lane < NPANEL) {
-            load(sB + lane * 8192, &mB0, t.n0 + coloff + 64 * lane, t.e * P.d + k0);
+          } else if (lane < NPANEL && !NOB) {
+            load(sB + lane * 8192, &mB0, bn0 + coloff + 64 * lane, be * P.d + bk0);
           }
         } else if constexpr (KIND == TC_BWD_DX) {
           const bool second = k0 >= P.h;
