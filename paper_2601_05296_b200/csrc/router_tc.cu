@@ -58,12 +58,17 @@ router_dx_tc_kernel(const __grid_constant__ CUtensorMap mDh, const __grid_consta
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 65536 + 8 * 4096);  // [0] tma, [1] mma
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t t0 = (int64_t)blockIdx.x * 128;
-  const int n0 = blockIdx.y * 256;
   const int quad = warp & 3, half = warp >> 2;
+  // persistent: the CTA walks tiles (128 tokens x 256 columns) ti = blockIdx.x + i * gridDim.x,
+  // columns fastest; barriers, TMEM and the tensor-map prefetch are set up once per CTA (the
+  // per-CTA setup of 1 024 short CTAs was half the kernel's time)
+  const int ntn = (int)ceil_div(d, 256);
+  const int64_t ntiles = ceil_div(Tn, 128) * ntn;
+  int64_t t0 = 0;
+  int n0 = 0;
   // the epilogue's accumulator rows (the kernel's bulk traffic) do not depend on the MMA:
   // chunk c of this warp (32 tokens x 32 columns, row-coalesced) is loaded into registers
-  // one chunk ahead, the first before the MMA is even issued
+  // one chunk ahead, the first before the tile's MMA is even issued
   auto load_chunk = [&](int c, float4 (&a)[8]) {
 #pragma unroll
     for (int it = 0; it < 8; ++it) {
@@ -85,8 +90,6 @@ router_dx_tc_kernel(const __grid_constant__ CUtensorMap mDh, const __grid_consta
       }
     }
   };
-  float4 a_cur[8];
-  load_chunk(half * 128, a_cur);
   if (tid == 0) {
     ptx::tma_prefetch(&mDh);
     ptx::tma_prefetch(&mDl);
@@ -102,76 +105,84 @@ router_dx_tc_kernel(const __grid_constant__ CUtensorMap mDh, const __grid_consta
   const uint32_t tmem = *tmem_holder;
   constexpr uint32_t IDESC = ptx::umma_idesc_bf16(128, 256, 0, 1);
   const int nkc = (int)ceil_div(E, 64);
-  if (warp == 0) {
-    for (int kc = 0; kc < nkc; ++kc) {
-      const int e0 = kc * 64;
-      if (kc > 0) ptx::mbar_wait(&bars[1], (kc - 1) & 1);  // previous chunk's MMAs done: smem free
-      if (lane == 0) {
-        ptx::mbar_arrive_expect_tx(&bars[0], 65536);
-        ptx::tma_load_2d(sAh, &mDh, &bars[0], e0, (int)t0);
-        ptx::tma_load_2d(sAl, &mDl, &bars[0], e0, (int)t0);
-#pragma unroll
-        for (int p = 0; p < 4; ++p) ptx::tma_load_2d(sB + p * 8192, &mWg, &bars[0], n0 + 64 * p, e0);
-      }
-      __syncwarp();
-      ptx::mbar_wait(&bars[0], kc & 1);
-      ptx::tc_fence_after();
-      const uint32_t bl = (ptx::smem_u32(sB) >> 4) | ((8192u >> 4) << 16);
-      ptx::umma_kblock<1, 2, 128>(tmem, (ptx::smem_u32(sAh) >> 4) | (1u << 16), bl, IDESC, kc > 0,
-                                  ptx::smem_u32(&bars[1]), 0);
-      ptx::umma_kblock<1, 2, 128>(tmem, (ptx::smem_u32(sAl) >> 4) | (1u << 16), bl, IDESC, 1u,
-                                  ptx::smem_u32(&bars[1]), 0);
-    }
-    // (only warp 0 tracks the chunk phases: a late waiter on a parity that repeats
-    // every two chunks could pass on an earlier chunk's completion)
-    ptx::mbar_wait(&bars[1], (nkc - 1) & 1);
-  }
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  // epilogue: 32 tokens x 128 columns per warp in 32-column chunks, staged through a
-  // swizzled fp32 tile so the global accesses are row-coalesced
+  uint32_t gk = 0;  // K chunks issued by this CTA so far (barrier phases)
   uint8_t* stg = stg_all + warp * 4096;
   const uint32_t tb = tmem + ((uint32_t)(quad * 32) << 16);
+  float4 a_cur[8];
 #pragma unroll 1
-  for (int c = half * 128; c < half * 128 + 128; c += 32) {
-    if (n0 + c >= d) break;
-    uint32_t v[32];
-    ptx::tmem_ld32(tb + c, v);
-    ptx::tmem_wait_ld();
+  for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x, gk += nkc) {
+    t0 = (ti / ntn) * 128;
+    n0 = (int)(ti - (ti / ntn) * ntn) * 256;
+    load_chunk(half * 128, a_cur);
+    if (warp == 0) {
+      for (int kc = 0; kc < nkc; ++kc) {
+        const uint32_t g = gk + kc;
+        const int e0 = kc * 64;
+        if (kc > 0) ptx::mbar_wait(&bars[1], (g - 1) & 1);  // previous chunk's MMAs done: smem free
+        if (lane == 0) {
+          ptx::mbar_arrive_expect_tx(&bars[0], 65536);
+          ptx::tma_load_2d(sAh, &mDh, &bars[0], e0, (int)t0);
+          ptx::tma_load_2d(sAl, &mDl, &bars[0], e0, (int)t0);
 #pragma unroll
-    for (int q = 0; q < 8; ++q)
-      *reinterpret_cast<float4*>(stg + lane * 128 + ((q ^ (lane & 7)) << 4)) =
-          make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]), __uint_as_float(v[4 * q + 2]),
-                      __uint_as_float(v[4 * q + 3]));
-    __syncwarp();
-    float4 a[8];
+          for (int p = 0; p < 4; ++p) ptx::tma_load_2d(sB + p * 8192, &mWg, &bars[0], n0 + 64 * p, e0);
+        }
+        __syncwarp();
+        ptx::mbar_wait(&bars[0], g & 1);
+        ptx::tc_fence_after();
+        const uint32_t bl = (ptx::smem_u32(sB) >> 4) | ((8192u >> 4) << 16);
+        ptx::umma_kblock<1, 2, 128>(tmem, (ptx::smem_u32(sAh) >> 4) | (1u << 16), bl, IDESC, kc > 0,
+                                    ptx::smem_u32(&bars[1]), 0);
+        ptx::umma_kblock<1, 2, 128>(tmem, (ptx::smem_u32(sAl) >> 4) | (1u << 16), bl, IDESC, 1u,
+                                    ptx::smem_u32(&bars[1]), 0);
+      }
+      // (only warp 0 tracks the chunk phases: a late waiter on a parity that repeats
+      // every two chunks could pass on an earlier chunk's completion)
+      ptx::mbar_wait(&bars[1], (gk + nkc - 1) & 1);
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    // epilogue: 32 tokens x 128 columns per warp in 32-column chunks, staged through a
+    // swizzled fp32 tile so the global accesses are row-coalesced
+#pragma unroll 1
+    for (int c = half * 128; c < half * 128 + 128; c += 32) {
+      if (n0 + c >= d) break;
+      uint32_t v[32];
+      ptx::tmem_ld32(tb + c, v);
+      ptx::tmem_wait_ld();
 #pragma unroll
-    for (int it = 0; it < 8; ++it) a[it] = a_cur[it];
-    if (c + 32 < half * 128 + 128) load_chunk(c + 32, a_cur);  // next chunk in flight
+      for (int q = 0; q < 8; ++q)
+        *reinterpret_cast<float4*>(stg + lane * 128 + ((q ^ (lane & 7)) << 4)) =
+            make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]), __uint_as_float(v[4 * q + 2]),
+                        __uint_as_float(v[4 * q + 3]));
+      __syncwarp();
+      float4 a[8];
 #pragma unroll
-    for (int it = 0; it < 8; ++it) {
-      const int rr = it * 4 + (lane >> 3), q = lane & 7;
-      const int64_t t = t0 + quad * 32 + rr;
-      if (t < Tn) {
-        const float4 f = *reinterpret_cast<const float4*>(stg + rr * 128 + ((q ^ (rr & 7)) << 4));
-        const int64_t o = t * d + n0 + c + 4 * q;
-        if constexpr (LOAD) {
-          *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(out_) + o) = make_uint2(
-              ptx::pack_bf16(a[it].x + f.x, a[it].y + f.y), ptx::pack_bf16(a[it].z + f.z, a[it].w + f.w));
-        } else {
-          *reinterpret_cast<float4*>(reinterpret_cast<float*>(out_) + o) = f;
+      for (int it = 0; it < 8; ++it) a[it] = a_cur[it];
+      if (c + 32 < half * 128 + 128) load_chunk(c + 32, a_cur);  // next chunk in flight
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int rr = it * 4 + (lane >> 3), q = lane & 7;
+        const int64_t t = t0 + quad * 32 + rr;
+        if (t < Tn) {
+          const float4 f = *reinterpret_cast<const float4*>(stg + rr * 128 + ((q ^ (rr & 7)) << 4));
+          const int64_t o = t * d + n0 + c + 4 * q;
+          if constexpr (LOAD) {
+            *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(out_) + o) = make_uint2(
+                ptx::pack_bf16(a[it].x + f.x, a[it].y + f.y), ptx::pack_bf16(a[it].z + f.z, a[it].w + f.w));
+          } else {
+            *reinterpret_cast<float4*>(reinterpret_cast<float*>(out_) + o) = f;
+          }
         }
       }
+      __syncwarp();
     }
-    __syncwarp();
-  }
-  ptx::tc_fence_before();
-  __syncthreads();
-  if (warp == 0) {
+    // every warp's TMEM reads are complete before the next tile's MMAs overwrite the accumulator
+    ptx::tc_fence_before();
+    __syncthreads();
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem, 256);
   }
+  if (warp == 0) ptx::tmem_dealloc(tmem, 256);
 }
 
 // ---------------------------------------------------------------- DWG
@@ -411,7 +422,16 @@ moe_status launch_router_dx_tc(bool load, const void* acc, bool acc_is_dtype, co
       return MOE_ERR_CUDA;
     attr = true;
   }
-  dim3 grid((unsigned)ceil_div(T, 128), (unsigned)ceil_div(d, 256));
+  // persistent: two CTAs per SM (the kernel's occupancy), each walking its share of the tiles
+  static int n_sm = 0;
+  if (!n_sm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    if (n_sm <= 0) n_sm = 148;
+  }
+  const int64_t ntiles = ceil_div(T, 128) * ceil_div(d, 256);
+  const dim3 grid((unsigned)std::min<int64_t>(ntiles, 2LL * n_sm));
   if (!load)
     router_dx_tc_kernel<false, float><<<grid, RDX_THREADS, RDX_SMEM, st>>>(mh, ml, mw, nullptr, nullptr, k, T, d, E,
                                                                           out);
