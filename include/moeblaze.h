@@ -281,6 +281,10 @@ moe_status moe_router_backward(const moe_problem* p, const float* d_topk_w, cons
  * moe_gather_rows: dst[i, :] = src[index[i], :] for i < n (rows of `width`
  *   elements of `elem_bytes` in {2,4}; row bytes a multiple of 4); builds the
  *   all-to-all send buffer in send order.  index entries must be in [0, n_src).
+ *   index = NULL: dst[i, :] = src[i, :] (n <= n_src), a copy done by a kernel:
+ *   dst may be pinned host memory (UVA-mapped), which the kernel writes over
+ *   PCIe without queueing behind the copy engines' bulk transfers (the EP
+ *   split-size read uses it while the host pipeline streams activations).
  * moe_combine_rows: out[t, :] = base[t, :] + sum_{j<k, tim[t*k+j] >= 0}
  *   rows[tim[t*k+j], :] (base [T, d] optional, NULL = 0; fixed j order, fp32
  *   accumulation, dtype output; -1 entries skipped; rows may be NULL only if

@@ -241,11 +241,13 @@ def moe_ep_slot_grad(p, topk_ids, experts_per_rank, n_ranks, send_pos, dg_back, 
 
 
 def moe_gather_rows(src, index, dst, stream=None):
+    """index None: dst[i] = src[i] for the rows of dst (a kernel copy; dst may be pinned host memory)."""
     n_src = src.shape[0]
     width = 1
     for s_ in src.shape[1:]:
         width *= s_
-    _check(load().moe_gather_rows(_ptr(src), n_src, _ptr(index), index.numel(), width, src.element_size(), _ptr(dst),
+    n = index.numel() if index is not None else dst.shape[0]
+    _check(load().moe_gather_rows(_ptr(src), n_src, _ptr(index), n, width, src.element_size(), _ptr(dst),
                                   _stream(stream)), "moe_gather_rows")
 
 

@@ -410,7 +410,8 @@ moe_status moe_ep_slot_grad(const moe_problem* p, const int32_t* topk_ids, int32
 moe_status moe_gather_rows(const void* src, int64_t n_src, const int32_t* index, int64_t n, int64_t width,
                            int32_t elem_bytes, void* dst, void* stream) {
   if (n < 0 || n_src < 0 || width < 1 || (elem_bytes != 2 && elem_bytes != 4)) return MOE_ERR_INVALID_ARG;
-  if (n > 0 && (!src || !index || !dst)) return MOE_ERR_INVALID_ARG;
+  if (n > 0 && (!src || !dst)) return MOE_ERR_INVALID_ARG;
+  if (!index && n > n_src) return MOE_ERR_INVALID_ARG;  // identity copy of the first n rows
   if ((width * elem_bytes) % 4 != 0) return MOE_ERR_MISALIGNED;
   if ((width * elem_bytes) % 16 == 0 && (!aligned16(src) || !aligned16(dst))) return MOE_ERR_MISALIGNED;
   return launch_gather_rows(src, index, n, width * elem_bytes, dst, (cudaStream_t)stream);

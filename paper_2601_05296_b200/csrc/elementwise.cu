@@ -404,7 +404,7 @@ __global__ void gather_rows4_kernel(const uint32_t* __restrict__ src, const int3
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n * w_per_row) return;
   int64_t row = i / w_per_row, c = i % w_per_row;
-  dst[i] = src[(int64_t)index[row] * w_per_row + c];
+  dst[i] = src[(index ? (int64_t)index[row] : row) * w_per_row + c];
 }
 
 // vectorised row gather: 16-byte chunks
@@ -414,7 +414,7 @@ __global__ void gather_rows_kernel(const uint4* __restrict__ src, const int32_t*
   int64_t total = n * vec_per_row;
   if (i >= total) return;
   int64_t row = i / vec_per_row, c = i % vec_per_row;
-  dst[i] = src[(int64_t)index[row] * vec_per_row + c];
+  dst[i] = src[(index ? (int64_t)index[row] : row) * vec_per_row + c];
 }
 
 // out[t, 8c .. 8c+7] = sum_j rows[tim[t,j], ...] (fixed j order, -1 skipped); d % 8 == 0

@@ -106,6 +106,22 @@ class CudaOps:
                            self_rank=self_rank)
         return dg
 
+    def read_host(self, t):
+        """The split sizes to the host: a kernel writes them into pinned host memory
+        and the host waits on an event -- a plain .cpu() would queue its copy behind
+        the copy engine's bulk transfers of a host-fed pipeline (tens of ms at
+        the EP config), stalling the whole step."""
+        if not t.is_cuda:
+            return t.clone()
+        if getattr(self, "_pinned", None) is None or self._pinned.numel() < t.numel():
+            self._pinned = torch.empty(max(t.numel(), 1024), dtype=t.dtype, pin_memory=True)
+        out = self._pinned[:t.numel()]
+        L.moe_gather_rows(t.reshape(-1, 1), None, out.view(-1, 1))
+        ev = torch.cuda.Event()
+        ev.record()
+        ev.synchronize()
+        return out.clone()
+
     def gather_rows(self, src, index):
         n = index.numel()
         dst = torch.empty((n,) + tuple(src.shape[1:]), dtype=src.dtype, device=src.device)
@@ -225,7 +241,7 @@ class ExpertParallelMoE:
         # C1: [rows to q, pairs per local expert of q] -> owners; one host read of all split sizes
         cnt = torch.cat([plan.counts.view(P, 1), disp.counts.view(P, El)], 1).reshape(-1).contiguous()
         rc = self.a2a(cnt, [El + 1] * P, [El + 1] * P)
-        host = torch.cat([plan.counts, rc]).cpu()
+        host = ops.read_host(torch.cat([plan.counts, rc]))
         send_split = host[:P].tolist()
         rc_h = host[P:].view(P, El + 1)
         recv_split = rc_h[:, 0].tolist()

@@ -220,3 +220,22 @@ def test_rowwise_error_gates(M, case):
     print(name, "rowwise", {n: round(v, 5) for n, v in errs.items()},
           "elementwise(floor 1e-3)", {n: round(v, 4) for n, v in elem.items()})
     assert not bad, (name, errs)
+
+
+def test_kernel_copy_into_pinned_host_memory(M):
+    """moe_gather_rows with index = NULL copies rows with a kernel, also into pinned
+    host memory (UVA): the EP split-size read (ep.CudaOps.read_host) uses it so the
+    read never queues behind the host pipeline's bulk copy-engine transfers."""
+    from paper_2601_05296_b200.ep import CudaOps
+    src = torch.arange(3000, dtype=torch.int32, device=DEV) * 7 - 11
+    pinned = torch.zeros(3000, dtype=torch.int32, pin_memory=True)
+    M._lib.moe_gather_rows(src.view(-1, 1), None, pinned.view(-1, 1))
+    torch.cuda.synchronize()
+    assert torch.equal(pinned, src.cpu())
+    assert torch.equal(CudaOps().read_host(src[:17]), src[:17].cpu())
+    # device rows, identity copy of the first n rows (bf16, 16-byte rows path)
+    a = torch.randn(64, 256, device=DEV).to(torch.bfloat16)
+    b = torch.empty(40, 256, dtype=torch.bfloat16, device=DEV)
+    M._lib.moe_gather_rows(a, None, b)
+    torch.cuda.synchronize()
+    assert torch.equal(b, a[:40])
