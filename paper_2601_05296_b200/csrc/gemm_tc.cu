@@ -76,6 +76,12 @@ __host__ __device__ constexpr bool is_dh(int k) { return k == TC_BWD_DH || k == 
 #ifndef MOEB_DH_NBUF
 #define MOEB_DH_NBUF 6    // BWD_DH epilogue ring depth (A/B chunks of DH_CW columns per warp)
 #endif
+#ifndef MOEB_WIDE_WG
+// weight-gradient kinds (DW3, DW12) on 256 x 512 CTA-pair tiles: two N = 256 accumulators fill
+// the 512 TMEM columns (no double buffer: the short bf16-store epilogue is exposed), for 25 %
+// fewer operand bytes per flop
+#define MOEB_WIDE_WG 0
+#endif
 #ifndef MOEB_SMEM_TIGHT
 #define MOEB_SMEM_TIGHT 1  // 768-byte barrier block and no alignment slack (lets 8-warp BWD_DH run 5 stages)
 #endif
@@ -154,6 +160,13 @@ __host__ __device__ constexpr int n_epi(int k) {
 }
 __host__ __device__ constexpr int tc_threads(int k) { return 32 * (8 + n_epi(k)); }
 constexpr int TBN = 256, TBK = 64;         // MMA N per tile, K block
+// 256 x 512 pair tiles for the weight-gradient kinds (MOEB_WIDE_WG)
+template <int KIND, int CG>
+__host__ __device__ constexpr bool wide_tile() {
+  return MOEB_WIDE_WG && CG == 2 && (KIND == TC_DW3 || KIND == TC_DW12);
+}
+template <int KIND, int CG>
+__host__ __device__ constexpr int tile_n() { return wide_tile<KIND, CG>() ? 2 * TBN : TBN; }
 constexpr int TA_BYTES = 128 * TBK * 2;    // 16 KB: 128 rows of A per CTA
 constexpr int TC_THREADS = 384;            // 12 warps (16 with the 8-warp BWD_DH epilogue)
 constexpr int GATHER_THREADS = 128;
@@ -161,7 +174,7 @@ constexpr int GATHER_THREADS = 128;
 template <int CG, int KIND = 0>
 struct CgCfg {
   static constexpr int TM = 128 * CG;                   // tile rows per CTA group
-  static constexpr int B_BYTES = (KIND == TC_ROUTE_S ? 64 : TBN / CG) * TBK * 2;  // B per CTA per stage
+  static constexpr int B_BYTES = (KIND == TC_ROUTE_S ? 64 : tile_n<KIND, CG>() / CG) * TBK * 2;  // B per CTA per stage
   static constexpr int STAGE = TA_BYTES + B_BYTES;
   // BWD_DH shares smem between its mainloop ring and the epilogue A/B ring (tools/tune_variants.sh:
   // 4 stages + 4-deep ring beat 3 + 7 by 11 % on the Mixtral layer)
@@ -169,7 +182,7 @@ struct CgCfg {
   static constexpr bool LK = (KIND == TC_BWD_DH_LK || KIND == TC_BWD_DH_L5) && MOEB_DH_TMA;
   static constexpr int NEPI = n_epi(KIND);
   static constexpr int STAGES = DH ? (CG == 1 ? 2 : (LK ? (NEPI == 8 ? MOEB_DH8_STAGES : MOEB_DH_STAGES) : MOEB_DH_STAGES_SK))
-                                   : (KIND == TC_ROUTE_S ? 8 : CG == 1 ? 4 : (NEPI == 8 ? 5 : 6));
+                                   : (KIND == TC_ROUTE_S ? 8 : CG == 1 ? 4 : (wide_tile<KIND, CG>() ? 4 : (NEPI == 8 ? 5 : 6)));
   static constexpr int DH_NBUF = LK ? (NEPI == 8 ? MOEB_DH8_NBUF : MOEB_DH_NBUF) : MOEB_DH_NBUF_SK;  // BWD_DH: A/B ring per warp
   // BWD_DH epilogue chunk: 16 columns (TMA boxes of 32 rows x 32 B, 32-byte swizzle) in the
   // TMA epilogue, 32 in the cp.async one; a slot holds the A and the B chunk
@@ -250,7 +263,7 @@ __host__ __device__ constexpr bool has_mtail() {
 }
 template <int KIND, int CG>
 __host__ __device__ constexpr bool has_ntail() {
-  return CG == 2 && ((MOEB_NTAIL & 1) && KIND == TC_DW3 || (MOEB_NTAIL & 2) && is_dh(KIND));
+  return CG == 2 && ((MOEB_NTAIL & 1) && KIND == TC_DW3 && !wide_tile<KIND, CG>() || (MOEB_NTAIL & 2) && is_dh(KIND));
 }
 
 template <int KIND>
@@ -268,7 +281,7 @@ struct KindTraits {
 template <int KIND, bool CPA, int CG>
 __host__ __device__ constexpr uint32_t tma_bytes_per_cta() {
   return ((CPA && KindTraits<KIND>::gather_a) ? 0u : (uint32_t)TA_BYTES) +
-         ((CPA && KindTraits<KIND>::gather_b) ? 0u : (uint32_t)CgCfg<CG>::B_BYTES);
+         ((CPA && KindTraits<KIND>::gather_b) ? 0u : (uint32_t)CgCfg<CG, KIND>::B_BYTES);
 }
 
 struct TileInfo {
@@ -315,7 +328,7 @@ __device__ __forceinline__ bool decode_tile(int tile, const TcParams& P, const i
       t.n_tile = nlo + (rem - mt * nt);
     }
     t.m0 = mt * TM;
-    t.n0 = t.n_tile * TBN;
+    t.n0 = t.n_tile * tile_n<KIND, CG>();
     t.seg0 = s_offs[t.e];
     t.seg1 = s_offs[t.e + 1];
     t.nk = (t.seg1 - t.seg0 + TBK - 1) / TBK;
@@ -492,7 +505,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
   static_assert(CG == 1 || CPA, "the CTA-pair path uses the cp.async gather engine");
   static_assert(C::SMEM <= 232448, "dynamic shared memory over the 227 KB opt-in limit");
   constexpr int STAGES = C::STAGES;
-  constexpr int NB = TBN / CG;     // B columns (rows of the B tile) held by this CTA
+  constexpr bool WIDE = wide_tile<KIND, CG>();
+  constexpr int NB = tile_n<KIND, CG>() / CG;  // B columns (rows of the B tile) held by this CTA
   constexpr int NPANEL = NB / 64;  // 64-column MN-major panels of B in this CTA
   constexpr uint32_t IDESC = ptx::umma_idesc_bf16(128 * CG, TBN, K::a_mn ? 1 : 0, K::b_mn ? 1 : 0);
 
@@ -876,6 +890,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
               else ptx::umma_commit(&empty[stage]);
             }
             __syncwarp();
+          } else if constexpr (WIDE) {
+            // two N = 256 MMAs per K16 step into the two accumulators: B columns [0, 128) and
+            // [128, 256) of each CTA's 256 (panels 0-1 and 2-3)
+            ptx::umma_kblock2<STEP_A, STEP_B>(d_tmem, d_tmem + TBN, (sA >> 4) | LBO_A,
+                                              ((sA + TA_BYTES) >> 4) | LBO_B, ((sA + TA_BYTES + 16384) >> 4) | LBO_B,
+                                              tidesc, kb != 0, empty0 + 8 * stage, 0x3);
           } else {
             ptx::umma_kblock<CG, STEP_A, STEP_B>(d_tmem, (sA >> 4) | LBO_A, ((sA + TA_BYTES) >> 4) | LBO_B, tidesc,
                                                  kb != 0, empty0 + 8 * stage, 0x3);
@@ -892,7 +912,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
           }
         }
         __syncwarp();
-        if (++as == 2) { as = 0; aphase ^= 1; }
+        if (WIDE || ++as == 2) { as = 0; aphase ^= 1; }  // the wide tile fills TMEM: one stage
       }
     }
   } else if (warp == 2) {
@@ -1502,8 +1522,14 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
                              : P.out1 + (int64_t)t.e * P.h * P.d + (int64_t)(m0w - P.h) * P.d;
         }
 #pragma unroll 1
-        for (int c = 0; c < TBN; c += 32) {
-          if (t.n0 + c >= N) break;
+        for (int c = 0; c < tile_n<KIND, CG>(); c += 32) {
+          // wide tile: TMEM column c of accumulator c / 256 holds tile column 256 r + 128 (c / 256) + j,
+          // r = (c % 256) / 128 the CTA whose B columns produced it, j = c % 128
+          const int oc = WIDE ? 256 * ((c & 255) >> 7) + 128 * (c >> 8) + (c & 127) : c;
+          if (t.n0 + oc >= N) {
+            if constexpr (WIDE) continue;
+            else break;
+          }
           float f[32];
           if (t.nk > 0) {
             ptx::tmem_ld32(tb + c, v);
@@ -1516,7 +1542,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
           }
           stg_put_bf16(stg, lane, f);
           __syncwarp();
-          if (nvalid > 0) stg_store_bf16(stg, lane, base + t.n0 + c, N, nvalid);
+          if (nvalid > 0) stg_store_bf16(stg, lane, base + t.n0 + oc, N, nvalid);
           __syncwarp();
         }
       }
@@ -1534,7 +1560,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
           ptx::mbar_arrive(&tempty[as]);
         }
       }
-      if (++as == 2) { as = 0; aphase ^= 1; }
+      if (WIDE || ++as == 2) { as = 0; aphase ^= 1; }
     }
     if constexpr (is_dh(KIND) && CPA && MOEB_DH_TMA)
       if (lane == 0) ptx::bulk_wait<0>();  // the epilogue's TMA stores are complete
@@ -1788,7 +1814,7 @@ moe_status tc_gemm(const GemmCall& c, cudaStream_t st) {
       ok &= make_map(&a0, c.dy, T, d, 64, 1);
       ok &= make_map(&b0, c.u, R, h, 64, 64);
       if (!ok) return MOE_ERR_CUDA;
-      P.n_tiles = (int)ceil_div(h, TBN);
+      P.n_tiles = (int)ceil_div(h, engine() == ENG_PAIR ? tile_n<TC_DW3, 2>() : TBN);
       P.m_tiles = (int)ceil_div(d, 128);
       P.m_tiles2 = (int)ceil_div(d, 256);
       const int64_t nt = P.n_tiles;
@@ -1805,7 +1831,7 @@ moe_status tc_gemm(const GemmCall& c, cudaStream_t st) {
       ok &= make_map(&a1, gated ? c.b_save : c.a_save, R, h, 64, 64);
       ok &= make_map(&b0, c.x, T, d, 64, 1);
       if (!ok) return MOE_ERR_CUDA;
-      P.n_tiles = (int)ceil_div(d, TBN);
+      P.n_tiles = (int)ceil_div(d, engine() == ENG_PAIR ? tile_n<TC_DW12, 2>() : TBN);
       P.m_tiles = (int)ceil_div(M, 128);
       P.m_tiles2 = (int)ceil_div(M, 256);
       const int64_t nt = P.n_tiles;

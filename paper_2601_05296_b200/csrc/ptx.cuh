@@ -268,6 +268,39 @@ __device__ __forceinline__ void umma_commit_e(uint32_t bar_addr) {
 // (smem >> 4) | LBO field, advancing by STEP_A / STEP_B per K16 slice (no carry:
 // smem addresses < 256 KB).  CG = 2: cta_group::2 with a multicast commit.
 constexpr uint32_t DESC_HI = (1024u >> 4) | (1u << 14) | (2u << 29);
+// CTA pair, one 64-deep K block into TWO accumulators (d0, d1) that share the A operand:
+// per K16 step an MMA with B at b0 into d0 and one with B at b1 into d1 (the 256 x 512 pair
+// tile of MOEB_WIDE_WG), then one commit to `bar_addr`
+template <uint32_t STEP_A, uint32_t STEP_B>
+__device__ __forceinline__ void umma_kblock2(uint32_t d0, uint32_t d1, uint32_t a_lo, uint32_t b0_lo, uint32_t b1_lo,
+                                             uint32_t idesc, uint32_t accumulate, uint32_t bar_addr, uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred p, q, e;\n\t.reg .b32 a1, a2, a3, b1, b2, b3, c1, c2, c3;\n\t"
+      ".reg .b64 da0, da1, da2, da3, db0, db1, db2, db3, dc0, dc1, dc2, dc3;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %5, 0;\n\t"
+      "setp.eq.b32 q, 0, 0;\n\t"
+      "add.u32 a1, %2, %8;\n\tadd.u32 a2, %2, %9;\n\tadd.u32 a3, %2, %10;\n\t"
+      "add.u32 b1, %3, %11;\n\tadd.u32 b2, %3, %12;\n\tadd.u32 b3, %3, %13;\n\t"
+      "add.u32 c1, %4, %11;\n\tadd.u32 c2, %4, %12;\n\tadd.u32 c3, %4, %13;\n\t"
+      "mov.b64 da0, {%2, %7};\n\tmov.b64 da1, {a1, %7};\n\tmov.b64 da2, {a2, %7};\n\tmov.b64 da3, {a3, %7};\n\t"
+      "mov.b64 db0, {%3, %7};\n\tmov.b64 db1, {b1, %7};\n\tmov.b64 db2, {b2, %7};\n\tmov.b64 db3, {b3, %7};\n\t"
+      "mov.b64 dc0, {%4, %7};\n\tmov.b64 dc1, {c1, %7};\n\tmov.b64 dc2, {c2, %7};\n\tmov.b64 dc3, {c3, %7};\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], da0, db0, %6, p;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%1], da0, dc0, %6, p;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], da1, db1, %6, q;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%1], da1, dc1, %6, q;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], da2, db2, %6, q;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%1], da2, dc2, %6, q;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], da3, db3, %6, q;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%1], da3, dc3, %6, q;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%14], %15;\n\t}"
+      ::"r"(d0), "r"(d1), "r"(a_lo), "r"(b0_lo), "r"(b1_lo), "r"(accumulate), "r"(idesc), "n"(DESC_HI),
+      "n"(STEP_A), "n"(2 * STEP_A), "n"(3 * STEP_A), "n"(STEP_B), "n"(2 * STEP_B), "n"(3 * STEP_B), "r"(bar_addr),
+      "h"(mask)
+      : "memory");
+}
+
 template <int CG, uint32_t STEP_A, uint32_t STEP_B>
 __device__ __forceinline__ void umma_kblock(uint32_t d_tmem, uint32_t a_lo, uint32_t b_lo, uint32_t idesc,
                                             uint32_t accumulate, uint32_t bar_addr, uint16_t mask) {
