@@ -416,11 +416,16 @@ def main():
                 "d2h_gbs": round(nb / (c1.elapsed_time(c2) / 1e3) / 1e9, 1), "bytes": nb}
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ms0 = torch.cuda.memory_stats()
+        eclk = ClockSampler(local)  # the e2e leg runs after the timed region: its own clocks
+        eclk.start()
+        time.sleep(0.3)
+        ew0 = time.time()
         e0.record(st)
         pipe.run([x_h] * n_e2e, [dy_h] * n_e2e, [ys_h[i % 2] for i in range(n_e2e)],
                  [dxs_h[i % 2] for i in range(n_e2e)])
         e1.record(st)
         torch.cuda.synchronize()
+        e2e_clk = eclk.stop((ew0, time.time()))
         ms1 = torch.cuda.memory_stats()
         # cudaMalloc / cudaFree inside the timed loop serialise host and device
         alloc = {k: ms1.get(k, 0) - ms0.get(k, 0) for k in ("num_device_alloc", "num_device_free", "num_alloc_retries")}
@@ -430,7 +435,7 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
         e2e = {"value": round(world * cfg.T / (ems / 1e3), 1), "unit": UNIT, "ms_per_step": round(ems, 4),
-               "pcie": pcie, "host_numa": numa, "allocator_in_timed_loop": alloc,
+               "pcie": pcie, "host_numa": numa, "allocator_in_timed_loop": alloc, "clocks": e2e_clk,
                "h2d_bytes_per_step": 2 * x.numel() * x.element_size(),
                "d2h_bytes_per_step": 2 * x.numel() * x.element_size(),
                "api": ("paper_2601_05296_b200.ep.ExpertParallelMoE.step" if ep is not None else
