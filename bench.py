@@ -367,6 +367,9 @@ def main():
                 "flops_per_launch": flops, "avg_launch_ms": round(tot_ms / n_l, 4),
                 "share_of_step": round(tot_ms / args.steps / ms_step, 4),
                 "per_kernel_ms": {n: round(v[0] / max(v[1], 1), 4) for n, v in prof.items()},
+                # every kind against the same sustained peak: algorithmic flops per launch / mean launch time
+                "per_kernel_frac": {n: round(flop_factor(n, gated) * R * cfg.d * cfg.h / (v[0] / v[1] / 1e3) / 1e12 /
+                                             peak, 4) for n, v in prof.items() if v[1]},
                 "all_gemms": {"achieved": round(all_flops / (gemm_total_ms / 1e3) / 1e12, 1),
                               "ms_per_step": round(gemm_total_ms, 4),
                               "frac": round(all_flops / (gemm_total_ms / 1e3) / 1e12 / peak, 4)}}
