@@ -85,7 +85,10 @@ def test_ep_fewer_local_experts_than_k(P, routing, backend, retain, c):
                                                       (1, "balanced", "nccl", False), (1, "skewed", "nccl", False),
                                                       (2, "skewed", "gloo", True), (1, "balanced", "nccl", True),
                                                       (2, "balanced", "nccl_multi", False),
-                                                      (2, "skewed", "nccl_multi", True)])
+                                                      (2, "skewed", "nccl_multi", True),
+                                                      # P = 4 and 8 processes sharing one GPU over gloo: the
+                                                      # EP config's rank counts (E = 8: 2 experts, then 1 < k)
+                                                      (4, "balanced", "gloo", False), (8, "skewed", "gloo", False)])
 def test_ep_cuda_matches_single_gpu(P, routing, backend, retain, c=CFG):
     """degenerate routing: every token picks experts 0,1, so rank 1 receives no rows.
     nccl (P = 1): the product path, with C4b / C5 on the side stream.  nccl_multi:
