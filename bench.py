@@ -207,6 +207,7 @@ def main():
                     help="expert FFN: SwiGLU (P:190) or the non-gated W2 sigma(W1 x) of P:75")
     ap.add_argument("--deterministic", action="store_true",
                     help="ordered token-side combine of the k expert outputs (bitwise reproducible, NEXT-4)")
+    ap.add_argument("--no-graph", action="store_true", help="skip the CUDA-graph replay timing")
     ap.add_argument("--launch-check", action="store_true",
                     help="test hook: start the ranks (gloo, CPU), check the world, print one JSON line, exit")
     args = ap.parse_args()
@@ -336,6 +337,16 @@ def main():
     ms_step = ms / args.steps
     value = world * cfg.T / (ms_step / 1e3)
     a2a_probe = probe_a2a(dev, world, ep, cfg) if ep is not None and world > 1 else None
+    # the same step captured once into a CUDA graph and replayed (every kernel runs every
+    # replay; the graph only removes the host launch path and inter-launch gaps).  Reported
+    # next to `value`, which stays the eager timing of the public functional API.
+    graph = None
+    if ep is None and not args.no_graph:
+        try:
+            graph = graph_replay(step, args.steps, st)
+            graph["value"] = round(cfg.T / (graph["ms_per_step"] / 1e3), 1)
+        except Exception as exc:  # report, never fake
+            graph = {"error": repr(exc)[:200]}
 
     # ----------------------------------------------------------------- roofline of the dominant kernel
     peaks = load_peaks()
@@ -477,7 +488,7 @@ def main():
                         "max": round(max(per_step), 4), "note": "per-step CUDA events inside the timed region, rank 0"},
             "sm_topology": {"sm_per_die": L.sm_topology()[1], "use": "die split of the expert-GEMM tile lists"},
             "peak_activation_gb": mem["ours"]["activation_peak_gb"] if mem else None, "memory": mem,
-            "a2a_probe": a2a_probe,
+            "a2a_probe": a2a_probe, "cuda_graph": graph,
             "nccl": ({"world": world, "version": ".".join(map(str, torch.cuda.nccl.version())),
                       "backend": dist.get_backend()} if use_ep else None),
         }
@@ -525,6 +536,33 @@ def relaunch(n):
            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
     print("bench.py: launching", " ".join(cmd[1:]), file=sys.stderr, flush=True)
     raise SystemExit(subprocess.call(cmd))
+
+
+def graph_replay(step, steps, st):
+    """Capture one step (warm, on a side stream as torch requires) and time `steps`
+    replays with CUDA events."""
+    side = torch.cuda.Stream()
+    side.wait_stream(st)
+    with torch.cuda.stream(side):
+        step()
+    st.wait_stream(side)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(steps):
+        g.replay()
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    del g
+    torch.cuda.empty_cache()
+    return {"ms_per_step": round(ms, 4), "replays": steps,
+            "what": "one step captured into a CUDA graph (torch.cuda.graph), replayed; all kernels run each replay"}
 
 
 def launch_check(rank, world):
