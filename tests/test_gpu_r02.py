@@ -76,16 +76,21 @@ def test_abu_parity(M, T, d, h, E, k, dtype, act, renorm):
 
 
 @pytest.mark.parametrize("ckpt", ["ab", "abu", "none"])
-@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
-def test_staged_backward_bit_identical(M, ckpt, dtype):
-    """moe_ffn_bwd issued as three stage calls on one workspace == one call."""
-    # k <= 2: the fused red.add combine is then order-independent, so two runs are bitwise equal
-    T, d, h, E, k = (700, 256, 640, 8, 2) if dtype == "bf16" else (200, 64, 96, 6, 2)
+@pytest.mark.parametrize("dtype,act,det", [("bf16", "swiglu", False), ("fp32", "swiglu", False),
+                                           ("bf16", "silu", False), ("bf16", "swiglu", True)])
+def test_staged_backward_bit_identical(M, ckpt, dtype, act, det):
+    """moe_ffn_bwd issued as three stage calls on one workspace == one call (also
+    for non-gated experts and the ordered combine)."""
+    # k <= 2: the fused red.add combine is then order-independent, so two runs are bitwise
+    # equal; the ordered combine (det) is bitwise reproducible at any k
+    T, d, h, E, k = (700, 256, 640, 8, 6 if det else 2) if dtype == "bf16" else (200, 64, 96, 6, 2)
+    gated = act == "swiglu"
     inp = make_inputs(T, d, h, E, k, dtype=dtype, seed=21, device=DEV)
-    x, wg, w1, w2, w3, dy = (inp[n] for n in ("x", "w_gate", "w1", "w2", "w3", "dy"))
+    x, wg, w1, w3, dy = (inp[n] for n in ("x", "w_gate", "w1", "w3", "dy"))
+    w2 = inp["w2"] if gated else None
     logits, ids, w = M.route(x, wg, k)
     disp = M.dispatch_build(ids, E, dtype=x.dtype)
-    out = M.ffn_fwd(x, w1, w2, w3, w, disp, checkpoint=ckpt)
+    out = M.ffn_fwd(x, w1, w2, w3, w, disp, checkpoint=ckpt, activation=act, deterministic=det)
     a, b = out[1], out[2]
     u = out[3] if ckpt == "abu" else None
     res = []
@@ -93,9 +98,12 @@ def test_staged_backward_bit_identical(M, ckpt, dtype):
         aa = a.clone() if a is not None else None
         bb = b.clone() if b is not None else None
         res.append(M.ffn_bwd(dy, x, w1, w2, w3, w, disp, aa, bb, w_gate=wg, logits=logits, checkpoint=ckpt,
-                             u_save=u, staged=staged))
+                             activation=act, deterministic=det, u_save=u, staged=staged))
     torch.cuda.synchronize()
     for n in ("dx", "dw1", "dw2", "dw3", "dg", "dw_gate"):
+        if res[0][n] is None:
+            assert res[1][n] is None
+            continue
         assert torch.equal(res[0][n], res[1][n]), n
 
 
