@@ -198,6 +198,10 @@ def main():
     ap.add_argument("--no-memory", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--ep", action="store_true", help="use the expert-parallel path even at N = 1")
+    ap.add_argument("--ep-exchange", default="nccl", choices=["nccl", "p2p"],
+                    help="EP exchange: nccl = NCCL all-to-all sized by one host read of the split sizes per "
+                         "step; p2p = device-initiated loads/stores into CUDA-IPC-mapped peer memory, no host "
+                         "sync (worst-case receive buffers)")
     ap.add_argument("--retain-recv-x", action="store_true",
                     help="EP: keep the received X rows from forward for dW1/dW2 (one a2a unit less, more memory)")
     ap.add_argument("--checkpoint", default="ab", choices=["ab", "none", "abu"],
@@ -270,8 +274,12 @@ def main():
         if not gated or det or args.checkpoint != "ab":
             raise SystemExit("--activation/--deterministic/--checkpoint are single-GPU options "
                              "(the expert-parallel path runs the SwiGLU layer with the A, B checkpoint)")
-        from paper_2601_05296_b200.ep import ExpertParallelMoE
-        ep = ExpertParallelMoE(cfg.E, k, renorm, group=None, retain_recv_x=args.retain_recv_x)
+        if args.ep_exchange == "p2p":
+            from paper_2601_05296_b200.ep_p2p import P2PExpertParallelMoE, PeerGroup
+            ep = P2PExpertParallelMoE(PeerGroup.from_group(cfg.T, cfg.d, k, cfg.E, x.dtype, dev), cfg.E, k, renorm)
+        else:
+            from paper_2601_05296_b200.ep import ExpertParallelMoE
+            ep = ExpertParallelMoE(cfg.E, k, renorm, group=None, retain_recv_x=args.retain_recv_x)
         # each rank keeps only its experts' weights; the router is replicated
         lo, hi = ep.local_experts
         w1, w2, w3 = w1[lo:hi].contiguous(), w2[lo:hi].contiguous(), w3[lo:hi].contiguous()
@@ -586,6 +594,7 @@ def config_dict(args, cfg, world, ep_path):
             "renormalize": args.renormalize, "checkpoint": args.checkpoint, "activation": args.activation,
             "deterministic": args.deterministic,
             "parallelism": f"ep{world}" if ep_path else "single-GPU",
+            **({"ep_exchange": args.ep_exchange} if ep_path else {}),
             **({"retain_recv_x": True} if args.retain_recv_x else {}),
             "l2": "no flush: inputs larger than L2 (weights %.2f GB + X %.0f MB vs 126 MB L2)" % (
                 w_gb, cfg.T * cfg.d * 2 / 1e6)}

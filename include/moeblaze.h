@@ -106,10 +106,14 @@ typedef struct {
   int64_t rows;           /* routed (token, expert) rows R.  0 (default): R = T*k, every slot of
                              topk_ids holds an expert id.  > 0: "sparse slots" -- topk_ids entries
                              equal to -1 are empty slots (no expert), skipped by the dispatch
-                             (token_index_map = -1 there, d_topk_w = 0), and R = rows is the
-                             number of non-empty slots (a_save/b_save hold R rows).  Used by the
-                             expert-parallel receiver, whose received token rows carry only the
-                             slots of this rank's experts (SURVEY §8(f) NEXT-1 dedup).
+                             (token_index_map = -1 there, d_topk_w = 0), and rows is the
+                             number of non-empty slots or any upper bound on it: buffers and
+                             workspace are sized for `rows` (a_save/b_save hold rows rows), the
+                             kernels take the actual count from expert_offsets[E] on the
+                             device.  Used by the expert-parallel receiver, whose received
+                             token rows carry only the slots of this rank's experts (SURVEY
+                             §8(f) NEXT-1 dedup); the peer-memory exchange, which never reads
+                             counts on the host, passes the worst case.
                              0 <= rows <= T*k. */
 } moe_problem;
 
@@ -306,6 +310,109 @@ moe_status moe_gather_rows(const void* src, int64_t n_src, const int32_t* index,
                            int64_t width, int32_t elem_bytes, void* dst, void* stream);
 moe_status moe_combine_rows(const moe_problem* p, const void* rows, const int32_t* token_index_map,
                             const void* base, void* out, void* stream);
+
+/* Device-initiated expert-parallel exchange over peer memory (SURVEY §8(f)
+ * NEXT-1: "no host sync in the EP step"; the paper names distribution as
+ * future work).  The NCCL path above sizes its all-to-all buffers from
+ * ONE device->host read of the split sizes per step.  This path has none: every
+ * rank owns a "symmetric" set of receive buffers (same layout on every rank,
+ * mapped into every peer's address space by the caller -- CUDA IPC over
+ * NVLink/NVSwitch), sized for the worst case (P*T token rows), and the kernels
+ * below move rows with plain loads/stores into / out of peer memory; ordering
+ * between ranks is carried by epoch flags in peer memory, never by the host.
+ *
+ * Flags: flags[phase * P + s] (uint64, zero-initialised, written only by rank
+ * s) = the last epoch in which rank s completed `phase` towards this rank.  A
+ * signal is a release store at system scope after a system-scope fence (so
+ * every write that precedes it in stream order -- including the remote row
+ * stores of a push -- is visible first); a wait is an acquire-load spin on the
+ * local flags of every rank, bounded by `timeout_ns`: on expiry it records
+ * 1 + phase in *status (first failure wins) and returns, so a lost peer costs
+ * a wrong result the caller detects through `status`, never a hung GPU.
+ * Epochs must increase by one per step and be the same on every rank.
+ * cmat[s * P + q] = rows rank s sends to rank q in the current step (every
+ * rank's row, written by moe_ep_publish_counts into every peer).
+ * The receive-side row layout is the NCCL path's: row r < T is the local token
+ * r; the rows from rank s start at T + sum_{s' < s} cmat[s' * P + me].
+ *
+ * All pointers are device pointers except the moe_ep_peers struct itself
+ * (host).  peer_* arrays are device arrays of P device pointers, entry q =
+ * rank q's buffer as mapped in this process (entry `rank` = the local buffer).
+ * Errors: MOE_ERR_INVALID_ARG for null/inconsistent arguments, MOE_ERR_CUDA on
+ * launch failure.  Not graph-capturable across steps (the epoch is an argument). */
+enum { MOE_EP_PH_ENTER = 0, MOE_EP_PH_COUNTS = 1, MOE_EP_PH_ROWS = 2, MOE_EP_PH_Y = 3, MOE_EP_PH_DY = 4,
+       MOE_EP_PH_DX = 5, MOE_EP_PH_DWG = 6, MOE_EP_NPHASE = 7 };
+
+typedef struct {
+  int32_t n_ranks;             /* P >= 1 */
+  int32_t rank;                /* this rank, 0 <= rank < P */
+  uint64_t* const* peer_flags; /* [P] -> each rank's flags [MOE_EP_NPHASE * P] (entry rank = local) */
+  int32_t* const* peer_cmat;   /* [P] -> each rank's cmat [P * P] */
+  uint32_t* arrive;            /* local [MOE_EP_NPHASE] zero-initialised counters (last-CTA signal) */
+  int32_t* status;             /* local int32, 0 = ok; 1 + phase of the first wait that timed out */
+  int64_t timeout_ns;          /* per wait; <= 0: 30 s */
+} moe_ep_peers;
+
+/* Signal `phase` of `epoch` to every rank (itself included) after all prior
+ * work on the stream. */
+moe_status moe_ep_signal(const moe_ep_peers* g, int32_t phase, uint64_t epoch, void* stream);
+/* Block the stream until every rank has signalled `phase` of `epoch` here. */
+moe_status moe_ep_wait(const moe_ep_peers* g, int32_t phase, uint64_t epoch, void* stream);
+/* counts [P] (rows this rank sends to each rank) -> row `rank` of every rank's
+ * cmat; then signals MOE_EP_PH_COUNTS. */
+moe_status moe_ep_publish_counts(const moe_ep_peers* g, const int32_t* counts, uint64_t epoch, void* stream);
+/* Fused gather + exchange: for every send position i < send_offs[P], with q
+ * the rank whose segment [send_offs[q], send_offs[q+1]) holds i,
+ *   peer_dst[q] row (dst_row0 + sum_{s<rank} cmat[s*P+q] + i - send_offs[q])
+ *     = src row (index ? index[i] : i)
+ * (rows of row_bytes bytes, a multiple of 4; 16-byte rows move as uint4).
+ * send_offs [P+1] (the send plan's expert_offsets), index = the send order
+ * (its expert_token_indices).  n_max >= send_offs[P] bounds the grid.  Reads
+ * the local cmat, so it must follow moe_ep_wait(MOE_EP_PH_COUNTS).  phase >= 0:
+ * the last CTA signals `phase` to every rank once all rows are stored; < 0:
+ * no signal (a later push's signal covers this one). */
+moe_status moe_ep_push_rows(const moe_ep_peers* g, const void* src, const int32_t* index, const int32_t* send_offs,
+                            int64_t n_max, int64_t row_bytes, int64_t dst_row0, void* const* peer_dst,
+                            int32_t phase, uint64_t epoch, void* stream);
+/* Receiver slots after moe_ep_wait(MOE_EP_PH_ROWS): rows [T, T+U) of ids [T_cap, k]
+ * hold the senders' GLOBAL expert ids; rewrite them to local ids
+ * (id - rank*experts_per_rank where owned, else -1, w = 0 there) and set rows
+ * [T+U, T_cap) to -1 (U = sum_s cmat[s*P+rank]), so moe_dispatch_build over the
+ * T_cap rows (sparse slots, rows = any upper bound) sees exactly the received
+ * (token, local expert) pairs. */
+moe_status moe_ep_recv_prepare(const moe_ep_peers* g, int64_t T, int64_t T_cap, int32_t k, int32_t experts_per_rank,
+                               int32_t* ids, float* w, void* stream);
+/* Fused exchange + combine: out[t] = base[t] + sum_{q != rank, send_pos[t*P+q] >= 0}
+ *   peer_rows[q] row (row0 + sum_{s<rank} cmat[s*P+q] + send_pos[t*P+q] - send_offs[q])
+ * (q ascending, fp32 accumulation, p->dtype rows of p->d, d % 8 == 0; p->T = T
+ * tokens).  send_pos = the send plan's token_index_map [T, P].  Must follow
+ * moe_ep_wait on the phase that published peer_rows. */
+moe_status moe_ep_pull_combine(const moe_ep_peers* g, const moe_problem* p, const void* const* peer_rows,
+                               int64_t row0, const int32_t* send_offs, const int32_t* send_pos, const void* base,
+                               void* out, void* stream);
+/* dg[t*k+j] = dg_local[t*k+j] if this rank owns ids[t,j], else
+ *   peer_dg[q][(row0 + sum_{s<rank} cmat[s*P+q] + send_pos[t*P+q] - send_offs[q]) * k + j]
+ * with q the owner (p->T, p->k, p->E = global experts). */
+moe_status moe_ep_pull_slot_grad(const moe_ep_peers* g, const moe_problem* p, int32_t experts_per_rank,
+                                 const int32_t* topk_ids, const float* const* peer_dg, int64_t row0,
+                                 const int32_t* send_offs, const int32_t* send_pos, const float* dg_local, float* dg,
+                                 void* stream);
+/* out[i] = sum_{q = 0..P-1} peer_src[q][i], i < n, fp32 accumulation in rank
+ * order (bitwise identical on every rank), dtype elements: the all-reduce of
+ * the replicated router's gradient. */
+moe_status moe_ep_pull_sum(const moe_ep_peers* g, const void* const* peer_src, int64_t n, int32_t dtype, void* out,
+                           void* stream);
+/* Mapping the symmetric buffers (host calls, synchronous, once per layer).
+ * moe_ep_ipc_handle: the CUDA IPC handle (64 bytes into handle_out) of the
+ * device allocation containing `ptr` and ptr's byte offset inside it (the
+ * buffer may be a sub-allocation of a caching allocator; not for VMM /
+ * expandable-segment memory).  moe_ep_ipc_open: map a peer's handle into the
+ * CURRENT device's address space (peer access enabled lazily over NVLink;
+ * works as well for another process on the same GPU) and return base + offset
+ * in *ptr_out, *base_out the mapping to pass to moe_ep_ipc_close. */
+moe_status moe_ep_ipc_handle(const void* ptr, void* handle_out, int64_t* offset_out);
+moe_status moe_ep_ipc_open(const void* handle, int64_t offset, void** ptr_out, void** base_out);
+moe_status moe_ep_ipc_close(void* base);
 
 /* Bench instrumentation.  While enabled, every expert-GEMM launch is
  * bracketed by two CUDA events recorded on the launch stream.

@@ -24,7 +24,9 @@ MOE_OP_ROUTE, MOE_OP_DISPATCH, MOE_OP_FFN_FWD, MOE_OP_FFN_BWD, MOE_OP_ROUTER_BWD
 EXPORTS = ("moe_workspace_size", "moe_route", "moe_dispatch_build", "moe_ffn_fwd", "moe_ffn_bwd",
            "moe_gather_rows", "moe_combine_rows", "moe_status_string", "moe_launch_count", "moe_version",
            "moe_profile_enable", "moe_profile_reset", "moe_profile_read", "moe_router_backward", "moe_ep_dest",
-           "moe_ep_send_meta", "moe_ep_slot_grad", "moe_ep_local_slots", "moe_sm_topology")
+           "moe_ep_send_meta", "moe_ep_slot_grad", "moe_ep_local_slots", "moe_sm_topology", "moe_ep_signal",
+           "moe_ep_wait", "moe_ep_publish_counts", "moe_ep_push_rows", "moe_ep_recv_prepare", "moe_ep_pull_combine",
+           "moe_ep_pull_slot_grad", "moe_ep_pull_sum", "moe_ep_ipc_handle", "moe_ep_ipc_open", "moe_ep_ipc_close")
 GEMM_KINDS = ("FWD_UP", "FWD_DOWN", "BWD_DH", "BWD_DX", "DW3", "DW12")
 
 
@@ -51,6 +53,17 @@ MOE_BWD_DATA, MOE_BWD_DW3, MOE_BWD_DW12, MOE_BWD_ALL = 1, 2, 4, 7
 class MoeRouterBwd(ctypes.Structure):
     _fields_ = [("w_gate", ctypes.c_void_p), ("logits", ctypes.c_void_p), ("topk_ids", ctypes.c_void_p),
                 ("dw_gate", ctypes.c_void_p)]
+
+
+# peer-memory exchange phases (moeblaze.h "Device-initiated expert-parallel exchange")
+(MOE_EP_PH_ENTER, MOE_EP_PH_COUNTS, MOE_EP_PH_ROWS, MOE_EP_PH_Y, MOE_EP_PH_DY, MOE_EP_PH_DX, MOE_EP_PH_DWG,
+ MOE_EP_NPHASE) = range(8)
+
+
+class MoeEpPeers(ctypes.Structure):
+    _fields_ = [("n_ranks", ctypes.c_int32), ("rank", ctypes.c_int32), ("peer_flags", ctypes.c_void_p),
+                ("peer_cmat", ctypes.c_void_p), ("arrive", ctypes.c_void_p), ("status", ctypes.c_void_p),
+                ("timeout_ns", ctypes.c_int64)]
 
 
 class MoEError(RuntimeError):
@@ -84,6 +97,18 @@ def load():
     lib.moe_ep_send_meta.argtypes = [P(MoeProblem), V, V, I32, I32, V, I64, V, V, V]
     lib.moe_ep_slot_grad.argtypes = [P(MoeProblem), V, I32, I32, V, V, V, I32, V, V]
     lib.moe_sm_topology.argtypes = [P(I32), I32, P(I32)]
+    U64, G = ctypes.c_uint64, P(MoeEpPeers)
+    lib.moe_ep_signal.argtypes = [G, I32, U64, V]
+    lib.moe_ep_wait.argtypes = [G, I32, U64, V]
+    lib.moe_ep_publish_counts.argtypes = [G, V, U64, V]
+    lib.moe_ep_push_rows.argtypes = [G, V, V, V, I64, I64, I64, V, I32, U64, V]
+    lib.moe_ep_recv_prepare.argtypes = [G, I64, I64, I32, I32, V, V, V]
+    lib.moe_ep_pull_combine.argtypes = [G, P(MoeProblem), V, I64, V, V, V, V, V]
+    lib.moe_ep_pull_slot_grad.argtypes = [G, P(MoeProblem), I32, V, V, I64, V, V, V, V, V]
+    lib.moe_ep_pull_sum.argtypes = [G, V, I64, I32, V, V]
+    lib.moe_ep_ipc_handle.argtypes = [V, V, P(I64)]
+    lib.moe_ep_ipc_open.argtypes = [V, I64, P(V), P(V)]
+    lib.moe_ep_ipc_close.argtypes = [V]
     lib.moe_sm_topology.restype = I32
     for fn in ("moe_workspace_size", "moe_route", "moe_dispatch_build", "moe_ffn_fwd", "moe_ffn_bwd",
                "moe_gather_rows", "moe_combine_rows", "moe_router_backward", "moe_ep_dest", "moe_ep_send_meta",
@@ -96,7 +121,7 @@ def load():
     lib.moe_profile_enable.argtypes = [I32]
     lib.moe_profile_read.argtypes = [I32, P(ctypes.c_double), P(I64)]
     for fn in ("moe_profile_enable", "moe_profile_reset", "moe_profile_read", "moe_router_backward", "moe_ep_dest",
-           "moe_ep_send_meta", "moe_ep_slot_grad"):
+               "moe_ep_send_meta", "moe_ep_slot_grad") + EXPORTS[EXPORTS.index("moe_ep_signal"):]:
         getattr(lib, fn).restype = I32
     _lib = lib
     if torch.cuda.is_available():
@@ -254,6 +279,68 @@ def moe_gather_rows(src, index, dst, stream=None):
 def moe_combine_rows(p, rows, token_index_map, out, stream=None, base=None):
     _check(load().moe_combine_rows(ctypes.byref(p), _ptr(rows), _ptr(token_index_map), _ptr(base), _ptr(out),
                                    _stream(stream)), "moe_combine_rows")
+
+
+def moe_ep_signal(g, phase, epoch, stream=None):
+    _check(load().moe_ep_signal(ctypes.byref(g), int(phase), int(epoch), _stream(stream)), "moe_ep_signal")
+
+
+def moe_ep_wait(g, phase, epoch, stream=None):
+    _check(load().moe_ep_wait(ctypes.byref(g), int(phase), int(epoch), _stream(stream)), "moe_ep_wait")
+
+
+def moe_ep_publish_counts(g, counts, epoch, stream=None):
+    _check(load().moe_ep_publish_counts(ctypes.byref(g), _ptr(counts), int(epoch), _stream(stream)),
+           "moe_ep_publish_counts")
+
+
+def moe_ep_push_rows(g, src, index, send_offs, n_max, row_bytes, dst_row0, peer_dst, phase, epoch, stream=None):
+    """peer_dst: device int64 tensor [P] of the peers' destination addresses."""
+    _check(load().moe_ep_push_rows(ctypes.byref(g), _ptr(src), _ptr(index), _ptr(send_offs), int(n_max),
+                                   int(row_bytes), int(dst_row0), _ptr(peer_dst), int(phase), int(epoch),
+                                   _stream(stream)), "moe_ep_push_rows")
+
+
+def moe_ep_recv_prepare(g, T, T_cap, k, experts_per_rank, ids, w, stream=None):
+    _check(load().moe_ep_recv_prepare(ctypes.byref(g), int(T), int(T_cap), int(k), int(experts_per_rank), _ptr(ids),
+                                      _ptr(w), _stream(stream)), "moe_ep_recv_prepare")
+
+
+def moe_ep_pull_combine(g, p, peer_rows, row0, send_offs, send_pos, base, out, stream=None):
+    _check(load().moe_ep_pull_combine(ctypes.byref(g), ctypes.byref(p), _ptr(peer_rows), int(row0), _ptr(send_offs),
+                                      _ptr(send_pos), _ptr(base), _ptr(out), _stream(stream)), "moe_ep_pull_combine")
+
+
+def moe_ep_pull_slot_grad(g, p, experts_per_rank, topk_ids, peer_dg, row0, send_offs, send_pos, dg_local, dg,
+                          stream=None):
+    _check(load().moe_ep_pull_slot_grad(ctypes.byref(g), ctypes.byref(p), int(experts_per_rank), _ptr(topk_ids),
+                                        _ptr(peer_dg), int(row0), _ptr(send_offs), _ptr(send_pos), _ptr(dg_local),
+                                        _ptr(dg), _stream(stream)), "moe_ep_pull_slot_grad")
+
+
+def moe_ep_pull_sum(g, peer_src, n, dtype, out, stream=None):
+    _check(load().moe_ep_pull_sum(ctypes.byref(g), _ptr(peer_src), int(n), int(dtype), _ptr(out), _stream(stream)),
+           "moe_ep_pull_sum")
+
+
+def ipc_handle(t):
+    """(64-byte CUDA IPC handle of the allocation holding t, byte offset of t in it)."""
+    h = (ctypes.c_char * 64)()
+    off = ctypes.c_int64(0)
+    _check(load().moe_ep_ipc_handle(_ptr(t), h, ctypes.byref(off)), "moe_ep_ipc_handle")
+    return bytes(h), off.value
+
+
+def ipc_open(handle, offset):
+    """Map a peer's (handle, offset) on the current device: (address, mapping base)."""
+    h = (ctypes.c_char * 64).from_buffer_copy(handle)
+    ptr, base = ctypes.c_void_p(), ctypes.c_void_p()
+    _check(load().moe_ep_ipc_open(h, int(offset), ctypes.byref(ptr), ctypes.byref(base)), "moe_ep_ipc_open")
+    return ptr.value, base.value
+
+
+def ipc_close(base):
+    _check(load().moe_ep_ipc_close(ctypes.c_void_p(base)), "moe_ep_ipc_close")
 
 
 def profile_enable(on=True):

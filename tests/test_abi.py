@@ -191,3 +191,38 @@ def test_sm_topology_validation(lib):
     dies = (ctypes.c_int32 * 4)()
     assert lib.moe_sm_topology(dies, 4, None) != 0
     assert lib.moe_sm_topology(dies, -1, n) != 0
+
+
+def test_ep_peer_exchange_validation(lib):
+    """The peer-memory exchange entry points reject a missing / inconsistent
+    peer description and bad phases synchronously; calls with nothing to move
+    return OK without launching (no GPU needed)."""
+    from paper_2601_05296_b200 import _lib as L
+    fake = ctypes.c_void_p(0x1000)  # never dereferenced: every call below returns before a launch
+    g = L.MoeEpPeers(2, 0, fake, fake, fake, fake, 0)
+    bad_rank = L.MoeEpPeers(2, 2, fake, fake, fake, fake, 0)
+    no_tables = L.MoeEpPeers(2, 0, None, None, fake, fake, 0)
+    for gg in (bad_rank, no_tables):
+        assert lib.moe_ep_signal(ctypes.byref(gg), 0, 1, None) == 1
+        assert lib.moe_ep_wait(ctypes.byref(gg), 0, 1, None) == 1
+    assert lib.moe_ep_signal(None, 0, 1, None) == 1
+    assert lib.moe_ep_signal(ctypes.byref(g), L.MOE_EP_NPHASE, 1, None) == 1       # phase out of range
+    assert lib.moe_ep_wait(ctypes.byref(g), -1, 1, None) == 1
+    assert lib.moe_ep_publish_counts(ctypes.byref(g), None, 1, None) == 1          # no counts
+    assert lib.moe_ep_push_rows(ctypes.byref(g), None, None, fake, 4, 6, 0, fake, -1, 1, None) == 1  # row_bytes % 4
+    assert lib.moe_ep_push_rows(ctypes.byref(g), None, None, fake, 4, 8, 0, fake, -1, 1, None) == 1  # src null, n > 0
+    assert lib.moe_ep_recv_prepare(ctypes.byref(g), 16, 8, 2, 4, None, None, None) == 1  # T_cap < T
+    assert lib.moe_ep_recv_prepare(ctypes.byref(g), 16, 16, 2, 4, None, None, None) == 0  # nothing received
+    p = L.problem(16, 100, 128, 8, 2, torch.bfloat16)                                    # d % 8 != 0
+    assert lib.moe_ep_pull_combine(ctypes.byref(g), ctypes.byref(p), fake, 16, fake, fake, None, fake, None) == 1
+    p0 = L.problem(0, 128, 128, 8, 2, torch.bfloat16)
+    assert lib.moe_ep_pull_combine(ctypes.byref(g), ctypes.byref(p0), None, 0, None, None, None, None, None) == 0
+    p8 = L.problem(16, 128, 128, 8, 2, torch.bfloat16)
+    assert lib.moe_ep_pull_slot_grad(ctypes.byref(g), ctypes.byref(p8), 3, None, None, 16, None, None, None, None,
+                                      None) == 1                                         # 3 * 2 ranks != 8 experts
+    assert lib.moe_ep_pull_sum(ctypes.byref(g), None, 10, 7, None, None) == 1            # unknown dtype
+    assert lib.moe_ep_pull_sum(ctypes.byref(g), None, 0, 0, None, None) == 0
+    h = (ctypes.c_char * 64)()
+    off = ctypes.c_int64()
+    assert lib.moe_ep_ipc_handle(None, h, ctypes.byref(off)) == 1
+    assert lib.moe_ep_ipc_close(None) == 1

@@ -49,16 +49,24 @@ def _worker(rank, P, port, q, routing, backend="gloo", retain=False, c=CFG):
         dist.init_process_group("nccl", rank=rank, world_size=P, device_id=dev)
     else:
         dist.init_process_group("gloo", rank=rank, world_size=P)
-    from paper_2601_05296_b200.ep import ExpertParallelMoE
     W, XS = _inputs(P, routing, c)
-    ep = ExpertParallelMoE(c["E"], c["k"], False, a2a=staged_a2a if backend == "gloo" else None,
-                           retain_recv_x=retain)
-    assert ep._use_streams(XS[rank][0].to(dev)) == backend.startswith("nccl")
-    lo, hi = ep.local_experts
     x, dy = (t.to(dev) for t in XS[rank])
+    if backend.startswith("p2p"):  # device-initiated exchange over CUDA-IPC-mapped peer memory
+        from paper_2601_05296_b200.ep_p2p import P2PExpertParallelMoE, PeerGroup
+        pg = PeerGroup.from_group(c["T"], c["d"], c["k"], c["E"], torch.bfloat16, dev, timeout_s=60.0)
+        ep = P2PExpertParallelMoE(pg, c["E"], c["k"])
+    else:
+        from paper_2601_05296_b200.ep import ExpertParallelMoE
+        ep = ExpertParallelMoE(c["E"], c["k"], False, a2a=staged_a2a if backend == "gloo" else None,
+                               retain_recv_x=retain)
+        assert ep._use_streams(x) == backend.startswith("nccl")
+    lo, hi = ep.local_experts
     wl = [W[n][lo:hi].contiguous().to(dev) for n in ("w1", "w2", "w3")]
-    y, g = ep.step(x, W["w_gate"].to(dev), *wl, dy)
+    for _ in range(2 if backend.startswith("p2p") else 1):  # p2p: a second step reuses the buffers
+        y, g = ep.step(x, W["w_gate"].to(dev), *wl, dy)
     torch.cuda.synchronize()
+    if backend.startswith("p2p"):
+        pg.check()
     # numpy (pickled by value): torch tensors would be shared by fd and can
     # vanish when this worker exits before the parent reads the queue
     q.put((rank, y.float().cpu().numpy(), {n: v.float().cpu().numpy() for n, v in g.items()}, (lo, hi)))
@@ -93,7 +101,7 @@ def test_ep_cuda_matches_single_gpu(P, routing, backend, retain, c=CFG):
     """degenerate routing: every token picks experts 0,1, so rank 1 receives no rows.
     nccl (P = 1): the product path, with C4b / C5 on the side stream.  nccl_multi:
     one rank per GPU over real NCCL all-to-all (skipped with fewer than P GPUs)."""
-    if backend == "nccl_multi" and torch.cuda.device_count() < P:
+    if backend.endswith("_multi") and torch.cuda.device_count() < P:
         pytest.skip(f"needs {P} GPUs (this box has {torch.cuda.device_count()})")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -105,6 +113,26 @@ def test_ep_cuda_matches_single_gpu(P, routing, backend, retain, c=CFG):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
+    compare_with_single_gpu(P, routing, c, res)
+
+
+@pytest.mark.parametrize("P,routing,backend", [(1, "balanced", "p2p"), (2, "balanced", "p2p"), (2, "skewed", "p2p"),
+                                               (2, "degenerate", "p2p"), (4, "balanced", "p2p"),
+                                               (2, "balanced", "p2p_multi"), (4, "skewed", "p2p_multi")])
+def test_ep_p2p_matches_single_gpu(P, routing, backend):
+    """The device-initiated exchange (ep_p2p: CUDA-IPC peer memory, epoch flags,
+    no host sync, no NCCL): P processes share cuda:0 (time-sliced contexts, the
+    flags spin across them), or one GPU per rank (p2p_multi, skipped with fewer
+    GPUs).  Two steps per process: the second reuses the symmetric buffers."""
+    test_ep_cuda_matches_single_gpu(P, routing, backend, False, CFG)
+
+
+@pytest.mark.parametrize("P", [2])
+def test_ep_p2p_fewer_local_experts_than_k(P):
+    test_ep_cuda_matches_single_gpu(P, "balanced", "p2p", False, CFG_EL1)
+
+
+def compare_with_single_gpu(P, routing, c, res):
     import paper_2601_05296_b200 as M
     W, XS = _inputs(P, routing, c)
     dev = torch.device("cuda", 0)
@@ -131,3 +159,17 @@ def test_ep_cuda_matches_single_gpu(P, routing, backend, retain, c=CFG):
             assert normwise(ge[n], bwd[n][lo:hi]) < BF16_TOL, n
         assert normwise(ye, fwd["y"][sl]) < BF16_TOL
         assert normwise(ge["dx"], bwd["dx"][sl]) < BF16_TOL
+
+
+@pytest.mark.parametrize("P,routing", [(2, "balanced"), (4, "skewed"), (8, "balanced")])
+def test_ep_p2p_virtual_ranks_one_process(P, routing):
+    """P ranks in one process on one GPU, one stream each (tests/_p2p_virtual.py):
+    the host enqueues all forwards, then all backwards, and never waits -- the
+    run can only finish if the EP step has no host sync."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "tests._p2p_virtual", str(P), routing], cwd=root,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "ok" in r.stdout
