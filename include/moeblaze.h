@@ -138,6 +138,12 @@ typedef struct {
   int32_t* token_index_map;
   int32_t* row_slot;
   const int32_t* token_expert_indices;
+  const int32_t* token_rows;   /* optional device int32 scalar n <= T: token rows [n, T) carry no
+                                  routed slot (sparse problems: their topk_ids rows are all -1).
+                                  moe_ffn_fwd/bwd then zero and finalise the fp32 combine
+                                  accumulator for rows < n only, and leave y / dx rows >= n
+                                  unspecified.  NULL: n = T.  Not read by moe_dispatch_build.
+                                  Set by the peer-memory EP receiver (moe_ep_recv_prepare). */
 } moe_dispatch;
 
 /* Router backward inputs/outputs for moe_ffn_bwd (not in the paper: the
@@ -379,9 +385,10 @@ moe_status moe_ep_push_rows(const moe_ep_peers* g, const void* src, const int32_
  * (id - rank*experts_per_rank where owned, else -1, w = 0 there) and set rows
  * [T+U, T_cap) to -1 (U = sum_s cmat[s*P+rank]), so moe_dispatch_build over the
  * T_cap rows (sparse slots, rows = any upper bound) sees exactly the received
- * (token, local expert) pairs. */
+ * (token, local expert) pairs.  token_rows (optional, device int32) receives
+ * T + U, the moe_dispatch.token_rows bound of the receiver's problem. */
 moe_status moe_ep_recv_prepare(const moe_ep_peers* g, int64_t T, int64_t T_cap, int32_t k, int32_t experts_per_rank,
-                               int32_t* ids, float* w, void* stream);
+                               int32_t* ids, float* w, int32_t* token_rows, void* stream);
 /* Fused exchange + combine: out[t] = base[t] + sum_{q != rank, send_pos[t*P+q] >= 0}
  *   peer_rows[q] row (row0 + sum_{s<rank} cmat[s*P+q] + send_pos[t*P+q] - send_offs[q])
  * (q ascending, fp32 accumulation, p->dtype rows of p->d, d % 8 == 0; p->T = T

@@ -40,7 +40,8 @@ class MoeProblem(ctypes.Structure):
 class MoeDispatch(ctypes.Structure):
     _fields_ = [("expert_counts", ctypes.c_void_p), ("expert_offsets", ctypes.c_void_p),
                 ("expert_token_indices", ctypes.c_void_p), ("token_index_map", ctypes.c_void_p),
-                ("row_slot", ctypes.c_void_p), ("token_expert_indices", ctypes.c_void_p)]
+                ("row_slot", ctypes.c_void_p), ("token_expert_indices", ctypes.c_void_p),
+                ("token_rows", ctypes.c_void_p)]
 
 
 class MoeBwdSync(ctypes.Structure):
@@ -102,7 +103,7 @@ def load():
     lib.moe_ep_wait.argtypes = [G, I32, U64, V]
     lib.moe_ep_publish_counts.argtypes = [G, V, U64, V]
     lib.moe_ep_push_rows.argtypes = [G, V, V, V, I64, I64, I64, V, I32, U64, V]
-    lib.moe_ep_recv_prepare.argtypes = [G, I64, I64, I32, I32, V, V, V]
+    lib.moe_ep_recv_prepare.argtypes = [G, I64, I64, I32, I32, V, V, V, V]
     lib.moe_ep_pull_combine.argtypes = [G, P(MoeProblem), V, I64, V, V, V, V, V]
     lib.moe_ep_pull_slot_grad.argtypes = [G, P(MoeProblem), I32, V, V, I64, V, V, V, V, V]
     lib.moe_ep_pull_sum.argtypes = [G, V, I64, I32, V, V]
@@ -202,9 +203,10 @@ def moe_route(p, x, w_gate, logits, topk_ids, topk_w, stream=None):
                             None, 0, _stream(stream)), "moe_route")
 
 
-def make_dispatch(counts, offs, eti, tim, row_slot, ids):
+def make_dispatch(counts, offs, eti, tim, row_slot, ids, token_rows=None):
+    """token_rows: optional device int32 [1], the moe_dispatch.token_rows bound."""
     return MoeDispatch(counts.data_ptr(), offs.data_ptr(), eti.data_ptr(), tim.data_ptr(), row_slot.data_ptr(),
-                       ids.data_ptr())
+                       ids.data_ptr(), token_rows.data_ptr() if token_rows is not None else None)
 
 
 def moe_dispatch_build(p, topk_ids, disp, ws, stream=None):
@@ -301,9 +303,9 @@ def moe_ep_push_rows(g, src, index, send_offs, n_max, row_bytes, dst_row0, peer_
                                    _stream(stream)), "moe_ep_push_rows")
 
 
-def moe_ep_recv_prepare(g, T, T_cap, k, experts_per_rank, ids, w, stream=None):
+def moe_ep_recv_prepare(g, T, T_cap, k, experts_per_rank, ids, w, token_rows=None, stream=None):
     _check(load().moe_ep_recv_prepare(ctypes.byref(g), int(T), int(T_cap), int(k), int(experts_per_rank), _ptr(ids),
-                                      _ptr(w), _stream(stream)), "moe_ep_recv_prepare")
+                                      _ptr(w), _ptr(token_rows), _stream(stream)), "moe_ep_recv_prepare")
 
 
 def moe_ep_pull_combine(g, p, peer_rows, row0, send_offs, send_pos, base, out, stream=None):

@@ -19,8 +19,9 @@ moe_status launch_dg_reduce(const float*, int, const int32_t*, int64_t, float*, 
 int dwg_chunks(const moe_problem* p);
 moe_status launch_router_bwd(const moe_problem*, const float*, const int32_t*, const float*, const void*, float*,
                              __nv_bfloat16*, float*, void*, cudaStream_t);
+moe_status launch_zero_acc(float*, int64_t, int, const int32_t*, cudaStream_t);
 moe_status launch_finalize(const moe_problem*, const void*, const float*, const __nv_bfloat16*, const void*, void*,
-                           cudaStream_t, bool, const int32_t*);
+                           cudaStream_t, bool, const int32_t*, const int32_t*);
 int router_ep8(int E);
 moe_status launch_ep_dest(const int32_t*, int64_t, int, int, int, int, int32_t*, cudaStream_t);
 moe_status launch_ep_local_slots(const int32_t*, const float*, int64_t, int, int, int32_t*, float*, cudaStream_t);
@@ -225,7 +226,7 @@ moe_status moe_ffn_fwd(const moe_problem* p, const void* x, const void* w1, cons
     b_save = w.b;
   }
   const int mode = out_mode(p, false);
-  if (mode == OUT_RED) MOE_CUDA_CHECK(cudaMemsetAsync(w.yacc, 0, (size_t)p->T * p->d * 4, st));
+  if (mode == OUT_RED && (s = launch_zero_acc(w.yacc, p->T, p->d, disp->token_rows, st)) != MOE_OK) return s;
   GemmCall c{};
   c.out_mode = mode; c.out_tok = y;
   c.x = x; c.w1 = w1; c.w2 = w2; c.w3 = w3; c.topw = topk_w;
@@ -242,7 +243,7 @@ moe_status moe_ffn_fwd(const moe_problem* p, const void* x, const void* w1, cons
   if ((s = run_gemm(c, st)) != MOE_OK) return s;
   if (mode == OUT_TOKN) return MOE_OK;
   return launch_finalize(p, w.yacc, nullptr, nullptr, nullptr, y, st, false,
-                         mode == OUT_ROWS ? disp->token_index_map : nullptr);
+                         mode == OUT_ROWS ? disp->token_index_map : nullptr, disp->token_rows);
 }
 
 moe_status moe_ffn_bwd(const moe_problem* p, const void* dy, const void* x, const void* w1, const void* w2,
@@ -289,7 +290,7 @@ moe_status moe_ffn_bwd(const moe_problem* p, const void* dy, const void* x, cons
   c.out_mode = mode; c.out_tok = dx;
   if (s_data) {
     if (p->T > 0) {
-      if (mode == OUT_RED) MOE_CUDA_CHECK(cudaMemsetAsync(w.dxacc, 0, (size_t)p->T * p->d * 4, st));
+      if (mode == OUT_RED && (s = launch_zero_acc(w.dxacc, p->T, p->d, disp->token_rows, st)) != MOE_OK) return s;
       if (p->checkpoint == MOE_CKPT_NONE) {  // recompute A, B (and U into the wU buffer) with the fused up-projection
         c.which = GEMM_FWD_UP;
         c.sched = sched_at(ws, SCHED_UP);
@@ -314,7 +315,7 @@ moe_status moe_ffn_bwd(const moe_problem* p, const void* dy, const void* x, cons
           dl = w.dlogits;
         }
         if ((s = launch_finalize(p, w.dxacc, dl, w.dlhl, router ? router->w_gate : nullptr, dx, st, false,
-                                 mode == OUT_ROWS ? disp->token_index_map : nullptr)) != MOE_OK)
+                                 mode == OUT_ROWS ? disp->token_index_map : nullptr, disp->token_rows)) != MOE_OK)
           return s;
       }
     } else if (router) {
@@ -355,7 +356,7 @@ moe_status moe_router_backward(const moe_problem* p, const float* d_topk_w, cons
   if ((s = launch_router_bwd(p, router->logits, router->topk_ids, d_topk_w, x, w.dlogits, w.dlhl, w.dwgpart,
                              router->dw_gate, st)) != MOE_OK)
     return s;
-  return launch_finalize(p, dx_partial, w.dlogits, w.dlhl, router->w_gate, dx, st, true, nullptr);
+  return launch_finalize(p, dx_partial, w.dlogits, w.dlhl, router->w_gate, dx, st, true, nullptr, nullptr);
 }
 
 moe_status moe_ep_dest(const moe_problem* p, const int32_t* topk_ids, int32_t experts_per_rank, int32_t n_ranks,

@@ -492,7 +492,9 @@ moe_status launch_router_bwd(const moe_problem* p, const float* logits, const in
 // out[i] = bf16(acc[i]) over n8 groups of 8 (two 16-byte loads, one 16-byte store per thread
 // per step, grid-stride: the HBM-bound Y finalize)
 __global__ void __launch_bounds__(256) convert_f32_bf16_kernel(const float4* __restrict__ acc, int64_t n8,
-                                                                uint4* __restrict__ out) {
+                                                                uint4* __restrict__ out,
+                                                                const int32_t* __restrict__ t_rows, int d8) {
+  if (t_rows) n8 = min64(n8, (int64_t)__ldg(t_rows) * d8);  // rows past the device bound are unused
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
     const float4 a = __ldcs(acc + 2 * i), b = __ldcs(acc + 2 * i + 1);
     uint4 o;
@@ -505,8 +507,40 @@ __global__ void __launch_bounds__(256) convert_f32_bf16_kernel(const float4* __r
   }
 }
 
+// acc[t, :] = 0 for t < *t_rows (the fp32 combine accumulator; the rows past the
+// device-side bound are never referenced)
+__global__ void zero_rows_kernel(float4* __restrict__ acc, int64_t n4, const int32_t* __restrict__ t_rows, int d4) {
+  const int64_t n = min64(n4, (int64_t)__ldg(t_rows) * d4);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+static int sm_count_cached() {
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+  }
+  return nsm;
+}
+
+moe_status launch_zero_acc(float* acc, int64_t T, int d, const int32_t* t_rows, cudaStream_t st) {
+  if (T == 0) return MOE_OK;
+  if (!t_rows || d % 4) {
+    MOE_CUDA_CHECK(cudaMemsetAsync(acc, 0, (size_t)T * d * 4, st));
+    return MOE_OK;
+  }
+  const int64_t n4 = T * (int64_t)d / 4;
+  const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(n4, 256), (int64_t)sm_count_cached() * 8);
+  MOE_LAUNCH(zero_rows_kernel, blocks, 256, 0, st, (float4*)acc, n4, t_rows, d / 4);
+  return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
+}
+
 moe_status launch_finalize(const moe_problem* p, const void* acc, const float* dl, const __nv_bfloat16* dlhl,
-                           const void* wg, void* out, cudaStream_t st, bool acc_is_dtype, const int32_t* tim) {
+                           const void* wg, void* out, cudaStream_t st, bool acc_is_dtype, const int32_t* tim,
+                           const int32_t* t_rows) {
   if (p->T == 0) return MOE_OK;
   typedef __nv_bfloat16 bf;
   if (dl && p->dtype == MOE_BF16)
@@ -520,11 +554,8 @@ moe_status launch_finalize(const moe_problem* p, const void* acc, const float* d
   if (p->dtype == MOE_BF16 && !acc_is_dtype && !tim && p->d % 8 == 0) {
     // the plain Y conversion (fp32 accumulator -> bf16): 8 columns per thread per step
     const int64_t n8 = p->T * (int64_t)p->d / 8;
-    int nsm = 148, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(n8, 256), (int64_t)nsm * 8);
-    MOE_LAUNCH(convert_f32_bf16_kernel, blocks, 256, 0, st, (const float4*)acc, n8, (uint4*)out);
+    const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(n8, 256), (int64_t)sm_count_cached() * 8);
+    MOE_LAUNCH(convert_f32_bf16_kernel, blocks, 256, 0, st, (const float4*)acc, n8, (uint4*)out, t_rows, p->d / 8);
     return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
   }
   dim3 grid((unsigned)ceil_div(p->d, 256), (unsigned)ceil_div(p->T, 16));

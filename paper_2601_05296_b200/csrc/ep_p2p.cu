@@ -123,13 +123,15 @@ __global__ void ep_push_rows_kernel(moe_ep_peers g, const V* __restrict__ src, c
 }
 
 __global__ void ep_recv_prepare_kernel(moe_ep_peers g, int64_t T, int64_t T_cap, int k, int epr,
-                                       int32_t* __restrict__ ids, float* __restrict__ w) {
+                                       int32_t* __restrict__ ids, float* __restrict__ w,
+                                       int32_t* __restrict__ token_rows) {
   __shared__ int64_t s_u;
   if (threadIdx.x == 0) {
     const int32_t* cmat = g.peer_cmat[g.rank];
     int64_t u = 0;
     for (int s = 0; s < g.n_ranks; ++s) u += cmat[s * g.n_ranks + g.rank];
     s_u = u;
+    if (token_rows && blockIdx.x == 0) *token_rows = (int32_t)(T + u);
   }
   __syncthreads();
   const int64_t f0 = T * k, f1 = T_cap * k, fu = (T + s_u) * k;
@@ -280,13 +282,14 @@ moe_status moe_ep_push_rows(const moe_ep_peers* g, const void* src, const int32_
 }
 
 moe_status moe_ep_recv_prepare(const moe_ep_peers* g, int64_t T, int64_t T_cap, int32_t k, int32_t experts_per_rank,
-                               int32_t* ids, float* w, void* stream) {
+                               int32_t* ids, float* w, int32_t* token_rows, void* stream) {
   moe_status s = check_peers(g);
   if (s != MOE_OK) return s;
-  if (T < 0 || T_cap < T || k < 1 || experts_per_rank < 1 || (T_cap > T && (!ids || !w))) return MOE_ERR_INVALID_ARG;
-  if (T_cap == T) return MOE_OK;
-  const unsigned grid = (unsigned)std::min<int64_t>(ceil_div((T_cap - T) * k, 256), 4 * sm_count());
-  MOE_LAUNCH(ep_recv_prepare_kernel, grid, 256, 0, stream, *g, T, T_cap, k, experts_per_rank, ids, w);
+  if (T < 0 || T_cap < T || T_cap >= (1ll << 31) || k < 1 || experts_per_rank < 1 || (T_cap > T && (!ids || !w)))
+    return MOE_ERR_INVALID_ARG;
+  if (T_cap == T && !token_rows) return MOE_OK;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div((T_cap - T) * k, 256), 4 * sm_count()));
+  MOE_LAUNCH(ep_recv_prepare_kernel, grid, 256, 0, stream, *g, T, T_cap, k, experts_per_rank, ids, w, token_rows);
   return launched();
 }
 

@@ -49,8 +49,10 @@ eagerly (CUDA_MODULE_LOADING=EAGER) or it deadlocks until the wait times out.
 
 Cost of host-sync freedom: the receive-side problem has P*T token rows and
 P*T*min(k, El) routed-row capacity (A, B and the FFN workspace are sized for
-it; the kernels process only the actual rows, read from expert_offsets on the
-device), the same trade as fixed-capacity low-latency EP dispatch.
+it; the kernels process only the actual rows: the GEMMs read expert_offsets
+on the device, the accumulator zeroing / finalize read the T + U bound that
+moe_ep_recv_prepare writes into moe_dispatch.token_rows), the same trade as
+fixed-capacity low-latency EP dispatch.
 """
 from __future__ import annotations
 
@@ -208,9 +210,11 @@ class P2PExpertParallelMoE:
         L.moe_ep_push_rows(G, ids, plan.eti, plan.offs, n_send_max, k * 4, T, tab["ids"], -1, e)
         L.moe_ep_push_rows(G, w, plan.eti, plan.offs, n_send_max, k * 4, T, tab["w"], L.MOE_EP_PH_ROWS, e)
         L.moe_ep_wait(G, L.MOE_EP_PH_ROWS, e)
-        L.moe_ep_recv_prepare(G, T, T_cap, k, El, buf["ids"], buf["w"])
+        token_rows = torch.empty(1, dtype=torch.int32, device=x.device)  # T + U, known on the device only
+        L.moe_ep_recv_prepare(G, T, T_cap, k, El, buf["ids"], buf["w"], token_rows)
         n_cap = T_cap * min(k, El)
         disp_l = ops.dispatch(buf["ids"], El, x.dtype, rows=n_cap)
+        disp_l.token_rows = token_rows
         p = L.problem(T_cap, d, h, El, k, x.dtype, rows=n_cap)
         a_l = torch.empty(n_cap, h, dtype=x.dtype, device=x.device)
         b_l = torch.empty(n_cap, h, dtype=x.dtype, device=x.device)

@@ -28,8 +28,10 @@ class Dispatch:
     row_slot: torch.Tensor    # [T*k]    inverse of tim
     ids: torch.Tensor         # [T, k]   token_expert_indices
 
+    token_rows = None         # optional device int32 [1]: token rows >= it carry no slot
+
     def c(self):
-        return L.make_dispatch(self.counts, self.offs, self.eti, self.tim, self.row_slot, self.ids)
+        return L.make_dispatch(self.counts, self.offs, self.eti, self.tim, self.row_slot, self.ids, self.token_rows)
 
 
 def route(x, w_gate, k, renormalize=False, stream=None):

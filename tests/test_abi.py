@@ -211,8 +211,8 @@ def test_ep_peer_exchange_validation(lib):
     assert lib.moe_ep_publish_counts(ctypes.byref(g), None, 1, None) == 1          # no counts
     assert lib.moe_ep_push_rows(ctypes.byref(g), None, None, fake, 4, 6, 0, fake, -1, 1, None) == 1  # row_bytes % 4
     assert lib.moe_ep_push_rows(ctypes.byref(g), None, None, fake, 4, 8, 0, fake, -1, 1, None) == 1  # src null, n > 0
-    assert lib.moe_ep_recv_prepare(ctypes.byref(g), 16, 8, 2, 4, None, None, None) == 1  # T_cap < T
-    assert lib.moe_ep_recv_prepare(ctypes.byref(g), 16, 16, 2, 4, None, None, None) == 0  # nothing received
+    assert lib.moe_ep_recv_prepare(ctypes.byref(g), 16, 8, 2, 4, None, None, None, None) == 1  # T_cap < T
+    assert lib.moe_ep_recv_prepare(ctypes.byref(g), 16, 16, 2, 4, None, None, None, None) == 0  # nothing received
     p = L.problem(16, 100, 128, 8, 2, torch.bfloat16)                                    # d % 8 != 0
     assert lib.moe_ep_pull_combine(ctypes.byref(g), ctypes.byref(p), fake, 16, fake, fake, None, fake, None) == 1
     p0 = L.problem(0, 128, 128, 8, 2, torch.bfloat16)

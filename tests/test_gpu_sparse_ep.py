@@ -135,3 +135,39 @@ def test_ep_plan_helpers_bit_exact(M, T, E, k, P):
         ref = (ref.astype(np.float32) + np.where(tim[:, j:j + 1] >= 0, r64[np.maximum(tim[:, j], 0)], 0)
                .astype(np.float32)).astype(np.float64)
     assert np.array_equal(f64(out), f64(torch.from_numpy(ref.astype(np.float32)).to(torch.bfloat16)))
+
+
+@pytest.mark.parametrize("T,n_valid,d,h,E,k,upper", [(900, 300, 256, 384, 4, 2, False), (1024, 1000, 512, 256, 8, 2, True),
+                                                     (500, 0, 256, 256, 2, 2, True)])
+def test_token_rows_bound_and_upper_bound_rows(M, T, n_valid, d, h, E, k, upper):
+    """moe_dispatch.token_rows (the peer-memory EP receiver's T + U bound on the
+    device) with token rows >= n_valid carrying no slot, and moe_problem.rows
+    given as an upper bound (T*k) instead of the exact count: y, dX, dg of the
+    rows < n_valid and every weight gradient are bit-identical to the exact,
+    unbounded call (same kernels, same rows; only the zeroing / finalize range
+    and the buffer sizes differ)."""
+    from paper_2601_05296_b200.ep import CudaOps
+    inp = make_inputs(T, d, h, E, k, dtype="bf16", seed=7, device=DEV)
+    ids_np = _sparse_ids(T, E, k, 13, 0.3)
+    ids_np[n_valid:] = -1
+    n = int((ids_np >= 0).sum())
+    ids = torch.from_numpy(ids_np).to(DEV)
+    w = torch.rand(T, k, generator=torch.Generator().manual_seed(4)).to(DEV)
+    w[ids < 0] = 0
+    ops = CudaOps()
+    res = []
+    for bounded in (False, True):
+        rows = T * k if (bounded and upper) else max(n, 1)
+        disp = ops.dispatch(ids, E, inp["x"].dtype, rows=rows)
+        if bounded:
+            disp.token_rows = torch.tensor([n_valid], dtype=torch.int32, device=DEV)
+        y, a, b = ops.ffn_fwd(inp["x"], inp["w1"], inp["w2"], inp["w3"], w, disp, rows)
+        g = ops.ffn_bwd(inp["dy"], inp["x"], inp["w1"], inp["w2"], inp["w3"], w, disp, a, b, rows)
+        torch.cuda.synchronize()
+        res.append((y[:n_valid].clone(), g))
+    (y0, g0), (y1, g1) = res
+    assert torch.equal(y0, y1)
+    assert torch.equal(g0["dx"][:n_valid], g1["dx"][:n_valid])
+    assert torch.equal(g0["dg"][:n_valid], g1["dg"][:n_valid])
+    for name in ("dw1", "dw2", "dw3"):
+        assert torch.equal(g0[name], g1[name]), name
