@@ -29,10 +29,11 @@ Step e on rank `me` (every phase signals all ranks, itself included):
              owners' rows of t, read from peer memory (fused combine).
 Backward: DY push of dY rows; moe_ffn_bwd data stage (dX rows into `out`, gate
 grads into `dg`, X still in the symmetric `x` buffer -- nothing is sent twice);
-DX signal, then the dW1/dW2 and dW3 stages run while peers may already pull;
-DX wait; pull-combine of dX, moe_ep_pull_slot_grad of dg; router backward
-into the symmetric `dwg`; DWG signal + wait; moe_ep_pull_sum = the all-reduce
-of the replicated router's gradient (rank order, identical on every rank).
+DX signal; then the dW1/dW2 and dW3 stages on this stream while a side stream
+runs the exchange tail: DX wait, pull-combine of dX, moe_ep_pull_slot_grad of
+dg, router backward into the symmetric `dwg`, DWG signal + wait,
+moe_ep_pull_sum = the all-reduce of the replicated router's gradient (rank
+order, identical on every rank); the streams join before returning.
 
 Buffer reuse is safe by these happens-before chains: peers write my x / ids /
 w / dy / cmat only after ENTER of the next step (after my whole backward);
@@ -253,32 +254,45 @@ class P2PExpertParallelMoE:
         # data grads: dX rows into `out`, gate grads into `dg` -- then peers may pull them
         L.moe_ffn_bwd(*args, buf["out"], None, None, None, buf["dg"], None, ws, stages=L.MOE_BWD_DATA)
         L.moe_ep_signal(G, L.MOE_EP_PH_DX, e)
+        # the exchange tail runs on a side stream while this stream computes dW1/dW2
+        # and dW3: wait for every owner's dX rows, pull-combine them and the gate
+        # grads, router backward, and the dW_g all-reduce.  Everything it touches
+        # is allocated here, on this stream, and stays referenced until the join.
+        wg = ctx["wg"]
+        dx_part = torch.empty(T, d, dtype=x.dtype, device=x.device)
+        dx = torch.empty_like(dx_part)
+        dg = torch.empty(T, k, dtype=torch.float32, device=x.device)
+        dwg = torch.empty_like(wg)
+        pr = L.problem(T, d, 128, E, k, x.dtype, self.renorm)
+        ws_r = L.workspace(pr, L.MOE_OP_ROUTER_BWD, x.device)
+        main = torch.cuda.current_stream()
+        side = self._side_stream(x.device)
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            L.moe_ep_wait(G, L.MOE_EP_PH_DX, e)
+            pc = L.problem(T, d, 128, E, k, x.dtype)
+            L.moe_ep_pull_combine(G, pc, tab["out"], T, plan.offs, plan.tim, buf["out"][:T], dx_part)
+            L.moe_ep_pull_slot_grad(G, pc, El, ctx["ids"], tab["dg"], T, plan.offs, plan.tim, buf["dg"][:T], dg)
+            router = L.MoeRouterBwd(wg.data_ptr(), ctx["logits"].data_ptr(), ctx["ids"].data_ptr(),
+                                    buf["dwg"].data_ptr())
+            L.moe_router_backward(pr, dg, x, router, dx_part, dx, ws_r)
+            L.moe_ep_signal(G, L.MOE_EP_PH_DWG, e)
+            L.moe_ep_wait(G, L.MOE_EP_PH_DWG, e)
+            L.moe_ep_pull_sum(G, tab["dwg"], wg.numel(), L._dtype_code(wg.dtype), dwg)
         dw1, dw2 = torch.empty_like(w1l), torch.empty_like(w2l)
         L.moe_ffn_bwd(*args, buf["out"], dw1, dw2, None, buf["dg"], None, ws, stages=L.MOE_BWD_DW12)
         for t in (a_l, b_l):  # dA / dB are dead after the dW1 / dW2 GEMM
             t.untyped_storage().resize_(0)
         dw3 = torch.empty_like(w3l)
         L.moe_ffn_bwd(*args, buf["out"], None, None, dw3, buf["dg"], None, ws, stages=L.MOE_BWD_DW3)
-        del ws
-        L.moe_ep_wait(G, L.MOE_EP_PH_DX, e)
-        dx_part = torch.empty(T, d, dtype=x.dtype, device=x.device)
-        L.moe_ep_pull_combine(G, L.problem(T, d, 128, E, k, x.dtype), tab["out"], T, plan.offs, plan.tim,
-                              buf["out"][:T], dx_part)
-        dg = torch.empty(T, k, dtype=torch.float32, device=x.device)
-        L.moe_ep_pull_slot_grad(G, L.problem(T, d, 128, E, k, x.dtype), El, ctx["ids"], tab["dg"], T, plan.offs,
-                                plan.tim, buf["dg"][:T], dg)
-        # router backward (its dW_g into the symmetric `dwg`), then the all-reduce as a pull-sum
-        wg = ctx["wg"]
-        pr = L.problem(T, d, 128, E, k, x.dtype, self.renorm)
-        router = L.MoeRouterBwd(wg.data_ptr(), ctx["logits"].data_ptr(), ctx["ids"].data_ptr(),
-                                buf["dwg"].data_ptr())
-        dx = torch.empty_like(dx_part)
-        L.moe_router_backward(pr, dg, x, router, dx_part, dx, L.workspace(pr, L.MOE_OP_ROUTER_BWD, x.device))
-        L.moe_ep_signal(G, L.MOE_EP_PH_DWG, e)
-        L.moe_ep_wait(G, L.MOE_EP_PH_DWG, e)
-        dwg = torch.empty_like(wg)
-        L.moe_ep_pull_sum(G, tab["dwg"], wg.numel(), L._dtype_code(wg.dtype), dwg)
+        main.wait_stream(side)
+        del ws, ws_r
         return dict(dx=dx, dw_gate=dwg, dw1=dw1, dw2=dw2, dw3=dw3, dg=dg)
+
+    def _side_stream(self, device):
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(device=device)
+        return self._side
 
     def step(self, x, wg, w1l, w2l, w3l, dy):
         y, ctx = self.forward(x, wg, w1l, w2l, w3l)
