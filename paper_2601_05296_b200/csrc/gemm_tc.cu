@@ -76,6 +76,11 @@ __host__ __device__ constexpr bool is_dh(int k) { return k == TC_BWD_DH || k == 
 #ifndef MOEB_DH_NBUF
 #define MOEB_DH_NBUF 6    // BWD_DH epilogue ring depth (A/B chunks of DH_CW columns per warp)
 #endif
+#ifndef MOEB_WIDE_ROW
+// 256 x 512 CTA-pair tiles for FWD_DOWN (bit 0) / BWD_DX (bit 1): 25 % fewer operand
+// bytes per flop, single-buffered accumulator (experiment; profiles/SUMMARY_r02.md)
+#define MOEB_WIDE_ROW 0
+#endif
 #ifndef MOEB_WIDE_WG
 // weight-gradient kinds (DW3, DW12) on 256 x 512 CTA-pair tiles: two N = 256 accumulators fill
 // the 512 TMEM columns (no double buffer: the short bf16-store epilogue is exposed), for 25 %
@@ -161,9 +166,11 @@ __host__ __device__ constexpr int n_epi(int k) {
 __host__ __device__ constexpr int tc_threads(int k) { return 32 * (8 + n_epi(k)); }
 constexpr int TBN = 256, TBK = 64;         // MMA N per tile, K block
 // 256 x 512 pair tiles for the weight-gradient kinds (MOEB_WIDE_WG)
+// and (MOEB_WIDE_ROW bits 0 / 1) for the long-K red.add kinds FWD_DOWN / BWD_DX
 template <int KIND, int CG>
 __host__ __device__ constexpr bool wide_tile() {
-  return MOEB_WIDE_WG && CG == 2 && (KIND == TC_DW3 || KIND == TC_DW12);
+  return CG == 2 && ((MOEB_WIDE_WG && (KIND == TC_DW3 || KIND == TC_DW12)) ||
+                     ((MOEB_WIDE_ROW & 1) && KIND == TC_FWD_DOWN) || ((MOEB_WIDE_ROW & 2) && KIND == TC_BWD_DX));
 }
 template <int KIND, int CG>
 __host__ __device__ constexpr int tile_n() { return wide_tile<KIND, CG>() ? 2 * TBN : TBN; }
@@ -380,7 +387,7 @@ __device__ __forceinline__ bool decode_tile(int tile, const TcParams& P, const i
     t.n_tile = nlo + within / sz;
     const int mi = mstart + (within - (within / sz) * sz);
     t.m0 = t.seg0 + mi * TM;
-    t.n0 = t.n_tile * ((KIND == TC_FWD_UP && P.act == 0) ? 128 : 256);
+    t.n0 = t.n_tile * ((KIND == TC_FWD_UP && P.act == 0) ? 128 : tile_n<KIND, CG>());
     const int Kdim = (KIND == TC_FWD_UP || is_dh(KIND)) ? P.d
                      : (KIND == TC_FWD_DOWN ? P.h : (P.act == 0 ? 2 : 1) * P.h);
     t.nk = Kdim / TBK;
@@ -1256,11 +1263,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
         }
       } else if constexpr (KIND == TC_FWD_DOWN || KIND == TC_BWD_DX) {
         // rows / columns of this warp (M = 128 tail: 32 rows x 128 columns, see has_mtail)
+        static_assert(!(WIDE && has_mtail<KIND, CG>()), "wide tiles have no M = 128 tail variant");
         const bool half = has_mtail<KIND, CG>() && t.seg1 - t.m0 <= 128;
         const int r0w = t.m0 + (half ? 64 * (int)crank + 32 * (wq & 1) : rowoff + wq * 32);
         const int coff = half ? 128 * (wq >> 1) : cb;  // first output column of this warp
         const int tcol = half ? 0 : cb;                // its first TMEM column
-        const int ncol = half ? 128 : NCW;
+        const int ncol = half ? 128 : (WIDE ? tile_n<KIND, CG>() : NCW);
         const int r = r0w + lane;
         const int nvalid = max(0, min(32, t.seg1 - r0w));
         const int N = P.d;
@@ -1272,8 +1280,13 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
         }
 #pragma unroll 1
         for (int cc = 0; cc < ncol; cc += 32) {
-          const int c = coff + cc;  // output column within the tile
-          if (t.n0 + c >= N) break;
+          // output column within the tile (wide: TMEM column cc of accumulator cc / 256 holds tile
+          // column 256 r + 128 (cc / 256) + j, r = (cc % 256) / 128 the CTA whose B rows made it)
+          const int c = WIDE ? 256 * ((cc & 255) >> 7) + 128 * (cc >> 8) + (cc & 127) : coff + cc;
+          if (t.n0 + c >= N) {
+            if constexpr (WIDE) continue;
+            else break;
+          }
           ptx::tmem_ld32(tb + tcol + cc, v);
           ptx::tmem_wait_ld();
 #pragma unroll
@@ -1739,7 +1752,8 @@ moe_status tc_gemm(const GemmCall& c, cudaStream_t st) {
   typedef __nv_bfloat16 bf;
   const int64_t T = c.T, R = c.R;
   const int d = c.d, h = c.h, E = c.E;
-  const uint32_t bw = engine() == ENG_PAIR ? 128 : 256;  // K-major W3 box rows held per CTA
+  // K-major W3 box rows held per CTA (the wide FWD_DOWN tile: 256 per CTA of the pair)
+  const uint32_t bw = engine() == ENG_PAIR ? (wide_tile<TC_FWD_DOWN, 2>() ? 256 : 128) : 256;
   TcParams P{};
   P.act = c.act;
   const bool gated = c.act == 0;
@@ -1772,7 +1786,7 @@ moe_status tc_gemm(const GemmCall& c, cudaStream_t st) {
       ok &= make_map(&a0, c.u, R, h, 64, 128);
       ok &= make_map(&b0, c.w3, (uint64_t)E * d, h, 64, bw);
       if (!ok) return MOE_ERR_CUDA;
-      P.n_tiles = (int)ceil_div(d, TBN);
+      P.n_tiles = (int)ceil_div(d, engine() == ENG_PAIR ? tile_n<TC_FWD_DOWN, 2>() : TBN);
       return launch_tc<TC_FWD_DOWN>(a0, a0, b0, b0, P, rows_tiles(P.n_tiles), st);
     }
     case GEMM_BWD_DH: {
@@ -1803,7 +1817,7 @@ moe_status tc_gemm(const GemmCall& c, cudaStream_t st) {
       ok &= make_map(&b0, c.w1, (uint64_t)E * h, d, 64, 64);
       ok &= make_map(&b1, gated ? c.w2 : c.w1, (uint64_t)E * h, d, 64, 64);
       if (!ok) return MOE_ERR_CUDA;
-      P.n_tiles = (int)ceil_div(d, TBN);
+      P.n_tiles = (int)ceil_div(d, engine() == ENG_PAIR ? tile_n<TC_BWD_DX, 2>() : TBN);
       return launch_tc<TC_BWD_DX>(a0, a1, b0, b1, P, rows_tiles(P.n_tiles), st);
     }
     case GEMM_DW3: {
