@@ -76,6 +76,12 @@ __host__ __device__ constexpr bool is_dh(int k) { return k == TC_BWD_DH || k == 
 #ifndef MOEB_DH_NBUF
 #define MOEB_DH_NBUF 6    // BWD_DH epilogue ring depth (A/B chunks of DH_CW columns per warp)
 #endif
+#ifndef MOEB_DIE_EXPERT
+// die-aware schedule of the row kinds: 0 = split every expert's n-tiles between the dies
+// (weights die-local, rows read by both dies); 1 = split the experts (each expert's rows and
+// weights read by one die; experiment)
+#define MOEB_DIE_EXPERT 0
+#endif
 #ifndef MOEB_WIDE_ROW
 // 256 x 512 CTA-pair tiles for FWD_DOWN (bit 0) / BWD_DX (bit 1): 25 % fewer operand
 // bytes per flop, single-buffered accumulator (experiment; profiles/SUMMARY_r02.md)
@@ -242,6 +248,9 @@ struct TcParams {
   int* sched;
   const uint8_t* die_map;
   int n_split;
+  int die_expert;  // MOEB_DIE_EXPERT: the dies split the experts (all n-tiles each), n_split = n_tiles;
+                   // die_sm0_permille = die 0's share of the SMs
+  int die_sm0_permille;
   int u_weighted;  // MOE_CKPT_ABU: FWD_UP stores w * U; FWD_DOWN then adds U W3 with unit weight
   int dh_skip_u;   // MOE_CKPT_ABU: BWD_DH writes dA, dB only (wU is saved from the forward)
 };
@@ -929,7 +938,16 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
     if constexpr (DYN) {
       if (leader && lane == 0) {
         const int Mt = K::wgrad ? E * P.m_tiles : s_mstart[E];  // m-tiles over all experts
-        const int cnt[2] = {Mt * P.n_split, Mt * (P.n_tiles - P.n_split)};
+        int cnt[2] = {Mt * P.n_split, Mt * (P.n_tiles - P.n_split)};
+        if (!K::wgrad && P.die_expert) {
+          // die 0 takes the experts whose m-tiles start below its SM share of all m-tiles
+          const int target = (int)(((int64_t)Mt * P.die_sm0_permille + 500) / 1000);
+          int es = 0;
+          while (es < E && s_mstart[es + 1] <= target) ++es;
+          if (es < E && target - s_mstart[es] > s_mstart[es + 1] - target) ++es;  // nearer boundary
+          cnt[0] = s_mstart[es] * P.n_tiles;
+          cnt[1] = Mt * P.n_tiles - cnt[0];
+        }
         const int my = P.die_map ? (int)P.die_map[ptx::smid() & 255] : 0;
         int src = my;
         for (int it = 0;; ++it) {
@@ -1701,7 +1719,11 @@ static moe_status launch_tc(const CUtensorMap& a0, const CUtensorMap& a1, const 
         int n_sm[2];
         P.die_map = sm_die_map(n_sm);
         P.n_split = P.n_tiles;
-        if (P.die_map && n_sm[1] > 0 && P.n_tiles >= 2) {
+        P.die_expert = 0;
+        if (MOEB_DIE_EXPERT && !KindTraits<KIND>::wgrad && P.die_map && n_sm[1] > 0 && P.E >= 2) {
+          P.die_expert = 1;  // one list per die over all n-tiles, split at an expert boundary
+          P.die_sm0_permille = (int)((1000LL * n_sm[0]) / (n_sm[0] + n_sm[1]));
+        } else if (P.die_map && n_sm[1] > 0 && P.n_tiles >= 2) {
           const int ns = (int)((2LL * P.n_tiles * n_sm[0] + (n_sm[0] + n_sm[1])) / (2LL * (n_sm[0] + n_sm[1])));
           P.n_split = std::min(std::max(ns, 1), P.n_tiles - 1);
         }
