@@ -337,6 +337,7 @@ def main():
     launches = L.launch_count() - launches0
     ms = ev0.elapsed_time(ev1)
     prof = L.profile_read()
+    prof_named = L.profile_read_named()
     clk = clocks.stop((wall0, wall1))
     if use_ep:
         t = torch.tensor([ms], device=dev)
@@ -392,6 +393,8 @@ def main():
                 "all_gemms": {"achieved": round(all_flops / (gemm_total_ms / 1e3) / 1e12, 1),
                               "ms_per_step": round(gemm_total_ms, 4),
                               "frac": round(all_flops / (gemm_total_ms / 1e3) / 1e12 / peak, 4)}}
+
+    hbm_steps = hbm_report(prof_named, cfg, R, k, peaks, ms_step, args.steps) if ep is None else None
 
     # ----------------------------------------------------------------- e2e through the public API (autograd layer)
     e2e = None
@@ -490,7 +493,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded, moe_inputs)",
             "config": config_dict(args, cfg, world, ep is not None),
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "roofline": roof, "hbm_steps": hbm_steps, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "gpu_launches_per_step": launches / args.steps, "clocks": clk,
             "step_ms": {"median": round(statistics.median(per_step), 4), "min": round(min(per_step), 4),
                         "max": round(max(per_step), 4), "note": "per-step CUDA events inside the timed region, rank 0"},
@@ -584,6 +587,38 @@ def launch_check(rank, world):
                           "local_ranks": int(os.environ.get("LOCAL_WORLD_SIZE", "1"))}), flush=True)
     dist.barrier()
     dist.destroy_process_group()
+
+
+def hbm_report(named, cfg, R, k, peaks, ms_step, steps):
+    """The memory-bound steps of the path (north star: achieved HBM GB/s for dispatch
+    and combine), measured live: CUDA events around each step's launches inside the
+    timed region (moe_profile_read_named) and its algorithmic bytes per launch
+    (DESIGN.md §6): each input read once, each output written once."""
+    T, d, E = cfg.T, cfg.d, cfg.E
+    es = 2 if cfg.dtype == "bf16" else 4
+    parts = max(1, (cfg.h + 255) // 256)  # gate-grad partials per routed row (one per BWD_DH n-tile)
+    alg = {
+        "route": T * d * es + E * d * es + T * E * 4 + T * k * 8,        # X, W_g in; logits, ids, w out
+        "dispatch": 4 * R + 4 * R + 3 * 4 * R + 8 * (E + 1),            # ids (hist + scatter); tim, eti, row_slot
+        "zero_acc": T * d * 4,                                           # the fp32 combine accumulator
+        "combine": T * d * 4 + T * d * es,                               # Y_acc in, Y out
+        "dg_reduce": R * parts * 4 + T * k * 4 + T * k * 4,              # partials, tim in; d_topk_w out
+        "router_bwd": T * E * 4 + T * k * 8 + T * d * es + E * d * es,  # logits, ids + dg, X in; dW_g out
+        "finalize_dx": T * d * 4 + T * d * es + E * d * es + T * E * 4,  # dX_acc, W_g, dlogits in; dX out
+    }
+    hbm = peaks["hbm_gbs"]
+    out = {}
+    for name, (tot, n) in named.items():
+        if not n:
+            continue
+        us = tot / n * 1e3
+        b = alg[name]
+        out[name] = {"us_per_launch": round(us, 2), "launches_per_step": round(n / steps, 2),
+                     "algorithmic_bytes": int(b), "achieved_gbs": round(b / (us / 1e6) / 1e9, 1),
+                     "frac_of_hbm": round(b / (us / 1e6) / 1e9 / hbm, 4)}
+    total_us = sum(v["us_per_launch"] * v["launches_per_step"] for v in out.values())
+    return {"peak_gbs": hbm, "peak_source": peaks["source"], "steps": out,
+            "share_of_step": round(total_us / 1e3 / ms_step, 4)}
 
 
 def config_dict(args, cfg, world, ep_path):

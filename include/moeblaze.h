@@ -431,6 +431,11 @@ moe_status moe_ep_ipc_close(void* base);
 moe_status moe_profile_enable(int32_t on);
 moe_status moe_profile_reset(void);
 moe_status moe_profile_read(int32_t kind, double* total_ms, int64_t* launches);
+/* The same for the non-GEMM steps, by name: "route", "dispatch", "zero_acc"
+ * (the fp32 combine accumulators' zeroing), "combine" (Y = dtype(Y_acc)),
+ * "dg_reduce", "router_bwd" (dlogits + dW_g), "finalize_dx" (dX = dtype(dX_acc
+ * + dlogits W_g)).  Unknown names read 0 launches. */
+moe_status moe_profile_read_named(const char* name, double* total_ms, int64_t* launches);
 
 /* SM topology used by the expert GEMMs' tile scheduler (not a step of the
  * method; a B200 placement detail).  A B200 is two dies whose

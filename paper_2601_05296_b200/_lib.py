@@ -26,7 +26,8 @@ EXPORTS = ("moe_workspace_size", "moe_route", "moe_dispatch_build", "moe_ffn_fwd
            "moe_profile_enable", "moe_profile_reset", "moe_profile_read", "moe_router_backward", "moe_ep_dest",
            "moe_ep_send_meta", "moe_ep_slot_grad", "moe_ep_local_slots", "moe_sm_topology", "moe_ep_signal",
            "moe_ep_wait", "moe_ep_publish_counts", "moe_ep_push_rows", "moe_ep_recv_prepare", "moe_ep_pull_combine",
-           "moe_ep_pull_slot_grad", "moe_ep_pull_sum", "moe_ep_ipc_handle", "moe_ep_ipc_open", "moe_ep_ipc_close")
+           "moe_ep_pull_slot_grad", "moe_ep_pull_sum", "moe_ep_ipc_handle", "moe_ep_ipc_open", "moe_ep_ipc_close",
+           "moe_profile_read_named")
 GEMM_KINDS = ("FWD_UP", "FWD_DOWN", "BWD_DH", "BWD_DX", "DW3", "DW12")
 
 
@@ -110,6 +111,7 @@ def load():
     lib.moe_ep_ipc_handle.argtypes = [V, V, P(I64)]
     lib.moe_ep_ipc_open.argtypes = [V, I64, P(V), P(V)]
     lib.moe_ep_ipc_close.argtypes = [V]
+    lib.moe_profile_read_named.argtypes = [ctypes.c_char_p, P(ctypes.c_double), P(I64)]
     lib.moe_sm_topology.restype = I32
     for fn in ("moe_workspace_size", "moe_route", "moe_dispatch_build", "moe_ffn_fwd", "moe_ffn_bwd",
                "moe_gather_rows", "moe_combine_rows", "moe_router_backward", "moe_ep_dest", "moe_ep_send_meta",
@@ -351,6 +353,20 @@ def profile_enable(on=True):
 
 def profile_reset():
     _check(load().moe_profile_reset(), "moe_profile_reset")
+
+
+NAMED_STEPS = ("route", "dispatch", "zero_acc", "combine", "dg_reduce", "router_bwd", "finalize_dx")
+
+
+def profile_read_named(names=NAMED_STEPS):
+    """{step name: (total_ms, launches)} for the non-GEMM steps (moe_profile_read_named)."""
+    out = {}
+    for name in names:
+        t, n = ctypes.c_double(0), ctypes.c_int64(0)
+        _check(load().moe_profile_read_named(name.encode(), ctypes.byref(t), ctypes.byref(n)),
+               "moe_profile_read_named")
+        out[name] = (t.value, n.value)
+    return out
 
 
 def profile_read():

@@ -185,6 +185,7 @@ moe_status moe_route(const moe_problem* p, const void* x, const void* w_gate, fl
   moe_status s = validate(p);
   if (s != MOE_OK) return s;
   if (p->T > 0 && (!x || !w_gate || !logits || !topk_ids || !topk_w)) return MOE_ERR_INVALID_ARG;
+  ProfScope prof("route", (cudaStream_t)stream);
   return launch_route(p, x, w_gate, logits, topk_ids, topk_w, (cudaStream_t)stream);
 }
 
@@ -198,6 +199,7 @@ moe_status moe_dispatch_build(const moe_problem* p, const int32_t* topk_ids, con
   cudaStream_t st = (cudaStream_t)stream;
   int32_t* status = (int32_t*)ws;
   if (p->check_routing) MOE_CUDA_CHECK(cudaMemsetAsync(status, 0, sizeof(int32_t), st));
+  ProfScope prof("dispatch", st);
   return launch_dispatch(p, topk_ids, out, (int32_t*)((char*)ws + 256), status, st);  // rows checked if check_routing
 }
 
@@ -226,7 +228,10 @@ moe_status moe_ffn_fwd(const moe_problem* p, const void* x, const void* w1, cons
     b_save = w.b;
   }
   const int mode = out_mode(p, false);
-  if (mode == OUT_RED && (s = launch_zero_acc(w.yacc, p->T, p->d, disp->token_rows, st)) != MOE_OK) return s;
+  if (mode == OUT_RED) {
+    ProfScope prof("zero_acc", st);
+    if ((s = launch_zero_acc(w.yacc, p->T, p->d, disp->token_rows, st)) != MOE_OK) return s;
+  }
   GemmCall c{};
   c.out_mode = mode; c.out_tok = y;
   c.x = x; c.w1 = w1; c.w2 = w2; c.w3 = w3; c.topw = topk_w;
@@ -242,6 +247,7 @@ moe_status moe_ffn_fwd(const moe_problem* p, const void* x, const void* w1, cons
   c.sched = sched_at(ws, SCHED_DOWN);
   if ((s = run_gemm(c, st)) != MOE_OK) return s;
   if (mode == OUT_TOKN) return MOE_OK;
+  ProfScope prof("combine", st);
   return launch_finalize(p, w.yacc, nullptr, nullptr, nullptr, y, st, false,
                          mode == OUT_ROWS ? disp->token_index_map : nullptr, disp->token_rows);
 }
@@ -290,7 +296,10 @@ moe_status moe_ffn_bwd(const moe_problem* p, const void* dy, const void* x, cons
   c.out_mode = mode; c.out_tok = dx;
   if (s_data) {
     if (p->T > 0) {
-      if (mode == OUT_RED && (s = launch_zero_acc(w.dxacc, p->T, p->d, disp->token_rows, st)) != MOE_OK) return s;
+      if (mode == OUT_RED) {
+        ProfScope prof("zero_acc", st);
+        if ((s = launch_zero_acc(w.dxacc, p->T, p->d, disp->token_rows, st)) != MOE_OK) return s;
+      }
       if (p->checkpoint == MOE_CKPT_NONE) {  // recompute A, B (and U into the wU buffer) with the fused up-projection
         c.which = GEMM_FWD_UP;
         c.sched = sched_at(ws, SCHED_UP);
@@ -300,8 +309,11 @@ moe_status moe_ffn_bwd(const moe_problem* p, const void* dy, const void* x, cons
       c.sched = sched_at(ws, SCHED_DH);
       if ((s = run_gemm(c, st)) != MOE_OK) return s;
       float* dg = d_topk_w ? d_topk_w : w.dg;
-      if ((s = launch_dg_reduce(w.dgpart, gemm_dg_parts(c), disp->token_index_map, p->T * p->k, dg, st)) != MOE_OK)
-        return s;
+      {
+        ProfScope prof("dg_reduce", st);
+        if ((s = launch_dg_reduce(w.dgpart, gemm_dg_parts(c), disp->token_index_map, p->T * p->k, dg, st)) != MOE_OK)
+          return s;
+      }
       c.which = GEMM_BWD_DX;   // dXacc += [dA|dB][W1;W2]
       c.sched = sched_at(ws, SCHED_DX);
       if ((s = run_gemm(c, st)) != MOE_OK) return s;
@@ -309,11 +321,13 @@ moe_status moe_ffn_bwd(const moe_problem* p, const void* dy, const void* x, cons
         const float* dl = nullptr;
         if (router) {
           if (x_ready) MOE_CUDA_CHECK(cudaStreamWaitEvent(st, x_ready, 0));  // dW_g = dlogits^T x reads x
+          ProfScope prof("router_bwd", st);
           if ((s = launch_router_bwd(p, router->logits, router->topk_ids, dg, x, w.dlogits, w.dlhl, w.dwgpart,
                                      router->dw_gate, st)) != MOE_OK)
             return s;
           dl = w.dlogits;
         }
+        ProfScope prof("finalize_dx", st);
         if ((s = launch_finalize(p, w.dxacc, dl, w.dlhl, router ? router->w_gate : nullptr, dx, st, false,
                                  mode == OUT_ROWS ? disp->token_index_map : nullptr, disp->token_rows)) != MOE_OK)
           return s;

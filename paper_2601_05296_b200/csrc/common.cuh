@@ -14,6 +14,16 @@ namespace moeb {
 // report how many of OUR kernels ran inside its timed region.
 void note_launch();
 
+// Bench instrumentation of the non-GEMM steps (moe_profile_read_named): while
+// profiling is on, a scope brackets its launches with two CUDA events on the stream.
+struct ProfScope {
+  const char* name;
+  cudaStream_t st;
+  cudaEvent_t a;
+  ProfScope(const char* name, cudaStream_t st);
+  ~ProfScope();
+};
+
 #define MOE_LAUNCH(kernel, grid, block, smem, stream, ...)                 \
   do {                                                                    \
     kernel<<<(grid), (block), (smem), (cudaStream_t)(stream)>>>(__VA_ARGS__); \
