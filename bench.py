@@ -439,6 +439,28 @@ def main():
         nb = x_h.numel() * x_h.element_size()
         pcie = {"h2d_gbs": round(nb / (c0.elapsed_time(c1) / 1e3) / 1e9, 1),
                 "d2h_gbs": round(nb / (c1.elapsed_time(c2) / 1e3) / 1e9, 1), "bytes": nb}
+        # both directions at once, a step's worth each way (X, dY in; Y, dX out), as the
+        # pipelined e2e step moves them: its PCIe floor per step on this host right now
+        bi = []
+        for _ in range(3):
+            s0, h1, d1 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            s0.record(st)
+            for strm in (pipe.h2d, pipe.d2h):
+                strm.wait_event(s0)
+            with torch.cuda.stream(pipe.h2d):
+                pipe.x[0].copy_(x_h, non_blocking=True)
+                pipe.dy[0].copy_(dy_h, non_blocking=True)
+                h1.record(pipe.h2d)
+            with torch.cuda.stream(pipe.d2h):
+                ys_h[0].copy_(pipe.x[1], non_blocking=True)
+                dxs_h[0].copy_(pipe.dy[1], non_blocking=True)
+                d1.record(pipe.d2h)
+            torch.cuda.synchronize()
+            bi.append((s0.elapsed_time(h1), s0.elapsed_time(d1)))
+        hm, dm = statistics.median(b[0] for b in bi), statistics.median(b[1] for b in bi)
+        pcie["concurrent"] = {"h2d_gbs": round(2 * nb / (hm / 1e3) / 1e9, 1),
+                              "d2h_gbs": round(2 * nb / (dm / 1e3) / 1e9, 1),
+                              "floor_ms_per_step": round(max(hm, dm), 4)}
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ms0 = torch.cuda.memory_stats()
         eclk = ClockSampler(local)  # the e2e leg runs after the timed region: its own clocks
@@ -460,6 +482,9 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
         e2e = {"value": round(world * cfg.T / (ems / 1e3), 1), "unit": UNIT, "ms_per_step": round(ems, 4),
+               # what bounds it: the device step or the PCIe transfers of a step (measured just before)
+               "floor_ms_per_step": {"device": round(ms / args.steps, 4),
+                                     "pcie": pcie["concurrent"]["floor_ms_per_step"]},
                "pcie": pcie, "host_numa": numa, "allocator_in_timed_loop": alloc, "clocks": e2e_clk,
                "h2d_bytes_per_step": 2 * x.numel() * x.element_size(),
                "d2h_bytes_per_step": 2 * x.numel() * x.element_size(),

@@ -195,6 +195,35 @@ moe_status moe_ffn_fwd(const moe_problem* p, const void* x, const void* w1, cons
                        void* a_save, void* b_save, void* u_save, void* y,
                        void* ws, size_t ws_bytes, void* stream);
 
+/* moe_ffn_fwd with the arrival of part of x overlapped (expert parallel: the
+ * received token rows come from the all-to-all while the local ones are
+ * already resident).  Token rows [0, t_ready) of x are
+ * ready at the call; the rows from t_ready on only once sync->x_ready (a
+ * cudaEvent_t) has fired.  The up-projection runs in two launches: each
+ * expert's rows [offsets[e], row_split[e]) -- the rows whose token is < t_ready,
+ * ascending inside an expert, so they come first -- then, after the
+ * stream waits x_ready, rows [row_split[e], offsets[e+1]); then the down
+ * projection and combine as in moe_ffn_fwd.  A, B, U and y are the same as one
+ * moe_ffn_fwd call (every row is computed by the same tile arithmetic).
+ * sync NULL, or row_split NULL: exactly moe_ffn_fwd (x_ready, if set, is
+ * waited first).  fp32 runs (CUDA-core path) wait x_ready before the single
+ * up-projection launch. */
+typedef struct {
+  const int32_t* row_split;  /* [E] device, from moe_dispatch_row_split(t_ready) */
+  void* x_ready;             /* cudaEvent_t or NULL */
+} moe_fwd_sync;
+
+moe_status moe_ffn_fwd_ex(const moe_problem* p, const void* x, const void* w1, const void* w2,
+                          const void* w3, const float* topk_w, const moe_dispatch* disp,
+                          void* a_save, void* b_save, void* u_save, void* y, const moe_fwd_sync* sync,
+                          void* ws, size_t ws_bytes, void* stream);
+
+/* row_split[e] = offsets[e] + #{r in [offsets[e], offsets[e+1]) : eti[r] < t_ready}
+ * (a binary search per expert: eti is ascending inside an expert).
+ * row_split [E] int32 device, written; one launch.  0 <= t_ready <= p->T. */
+moe_status moe_dispatch_row_split(const moe_problem* p, const moe_dispatch* disp, int64_t t_ready,
+                                  int32_t* row_split, void* stream);
+
 /* Expert backward (§3.2, Alg. 1 FusedBackward P:236-253) with the
  * SiLU recomputed from the checkpoint:
  *   dH_r = dy[eti[r]] W3_e^T;  d_topk_w[t,j] = <dH_r, U_r>

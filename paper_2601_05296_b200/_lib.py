@@ -27,7 +27,7 @@ EXPORTS = ("moe_workspace_size", "moe_route", "moe_dispatch_build", "moe_ffn_fwd
            "moe_ep_send_meta", "moe_ep_slot_grad", "moe_ep_local_slots", "moe_sm_topology", "moe_ep_signal",
            "moe_ep_wait", "moe_ep_publish_counts", "moe_ep_push_rows", "moe_ep_recv_prepare", "moe_ep_pull_combine",
            "moe_ep_pull_slot_grad", "moe_ep_pull_sum", "moe_ep_ipc_handle", "moe_ep_ipc_open", "moe_ep_ipc_close",
-           "moe_profile_read_named")
+           "moe_profile_read_named", "moe_ffn_fwd_ex", "moe_dispatch_row_split")
 GEMM_KINDS = ("FWD_UP", "FWD_DOWN", "BWD_DH", "BWD_DX", "DW3", "DW12")
 
 
@@ -50,6 +50,10 @@ class MoeBwdSync(ctypes.Structure):
 
 
 MOE_BWD_DATA, MOE_BWD_DW3, MOE_BWD_DW12, MOE_BWD_ALL = 1, 2, 4, 7
+
+
+class MoeFwdSync(ctypes.Structure):
+    _fields_ = [("row_split", ctypes.c_void_p), ("x_ready", ctypes.c_void_p)]
 
 
 class MoeRouterBwd(ctypes.Structure):
@@ -112,6 +116,8 @@ def load():
     lib.moe_ep_ipc_open.argtypes = [V, I64, P(V), P(V)]
     lib.moe_ep_ipc_close.argtypes = [V]
     lib.moe_profile_read_named.argtypes = [ctypes.c_char_p, P(ctypes.c_double), P(I64)]
+    lib.moe_ffn_fwd_ex.argtypes = [P(MoeProblem), V, V, V, V, V, P(MoeDispatch), V, V, V, V, P(MoeFwdSync), V, SZ, V]
+    lib.moe_dispatch_row_split.argtypes = [P(MoeProblem), P(MoeDispatch), I64, V, V]
     lib.moe_sm_topology.restype = I32
     for fn in ("moe_workspace_size", "moe_route", "moe_dispatch_build", "moe_ffn_fwd", "moe_ffn_bwd",
                "moe_gather_rows", "moe_combine_rows", "moe_router_backward", "moe_ep_dest", "moe_ep_send_meta",
@@ -220,6 +226,23 @@ def moe_ffn_fwd(p, x, w1, w2, w3, topk_w, disp, a_save, b_save, u_save, y, ws, s
     _check(load().moe_ffn_fwd(ctypes.byref(p), _ptr(x), _ptr(w1), _ptr(w2), _ptr(w3), _ptr(topk_w),
                               ctypes.byref(disp), _ptr(a_save), _ptr(b_save), _ptr(u_save), _ptr(y), _ptr(ws),
                               ws.numel(), _stream(stream)), "moe_ffn_fwd")
+
+
+def moe_ffn_fwd_ex(p, x, w1, w2, w3, topk_w, disp, a_save, b_save, u_save, y, ws, row_split=None, x_ready=None,
+                   stream=None):
+    """moe_ffn_fwd with x rows [0, t_ready) resident and the rest ready at x_ready
+    (torch.cuda.Event or None); row_split from moe_dispatch_row_split(t_ready)."""
+    if x_ready is not None and not x_ready.cuda_event:
+        raise MoEError("moe_ffn_fwd_ex: x_ready must be created (recorded once) before the call")
+    sync = MoeFwdSync(_ptr(row_split), x_ready.cuda_event if x_ready is not None else None)
+    _check(load().moe_ffn_fwd_ex(ctypes.byref(p), _ptr(x), _ptr(w1), _ptr(w2), _ptr(w3), _ptr(topk_w),
+                                 ctypes.byref(disp), _ptr(a_save), _ptr(b_save), _ptr(u_save), _ptr(y),
+                                 ctypes.byref(sync), _ptr(ws), ws.numel(), _stream(stream)), "moe_ffn_fwd_ex")
+
+
+def moe_dispatch_row_split(p, disp, t_ready, row_split, stream=None):
+    _check(load().moe_dispatch_row_split(ctypes.byref(p), ctypes.byref(disp), int(t_ready), _ptr(row_split),
+                                         _stream(stream)), "moe_dispatch_row_split")
 
 
 def moe_ffn_bwd(p, dy, x, w1, w2, w3, topk_w, disp, a_save, b_save, u_save, dx, dw1, dw2, dw3, d_topk_w, router, ws,

@@ -31,6 +31,7 @@ moe_status launch_ep_slot_grad(const int32_t*, int64_t, int, int, int, const int
                                float*, cudaStream_t);
 moe_status launch_gather_rows(const void*, const int32_t*, int64_t, int64_t, void*, cudaStream_t);
 moe_status launch_combine_rows(const moe_problem*, const void*, const int32_t*, const void*, void*, cudaStream_t);
+moe_status launch_row_split(const int32_t*, const int32_t*, int, int64_t, int32_t*, cudaStream_t);
 
 static size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
@@ -206,6 +207,22 @@ moe_status moe_dispatch_build(const moe_problem* p, const int32_t* topk_ids, con
 moe_status moe_ffn_fwd(const moe_problem* p, const void* x, const void* w1, const void* w2, const void* w3,
                        const float* topk_w, const moe_dispatch* disp, void* a_save, void* b_save, void* u_save,
                        void* y, void* ws, size_t ws_bytes, void* stream) {
+  return moe_ffn_fwd_ex(p, x, w1, w2, w3, topk_w, disp, a_save, b_save, u_save, y, nullptr, ws, ws_bytes, stream);
+}
+
+moe_status moe_dispatch_row_split(const moe_problem* p, const moe_dispatch* disp, int64_t t_ready, int32_t* row_split,
+                                  void* stream) {
+  moe_status s = validate(p);
+  if (s != MOE_OK) return s;
+  if (!disp || !disp->expert_offsets || !row_split || t_ready < 0 || t_ready > p->T) return MOE_ERR_INVALID_ARG;
+  if (p->T > 0 && !disp->expert_token_indices) return MOE_ERR_INVALID_ARG;
+  return launch_row_split(disp->expert_offsets, disp->expert_token_indices, p->E, t_ready, row_split,
+                          (cudaStream_t)stream);
+}
+
+moe_status moe_ffn_fwd_ex(const moe_problem* p, const void* x, const void* w1, const void* w2, const void* w3,
+                          const float* topk_w, const moe_dispatch* disp, void* a_save, void* b_save, void* u_save,
+                          void* y, const moe_fwd_sync* sync, void* ws, size_t ws_bytes, void* stream) {
   moe_status s = validate(p);
   if (s != MOE_OK) return s;
   const bool gated = p->activation == MOE_ACT_SWIGLU;
@@ -242,7 +259,22 @@ moe_status moe_ffn_fwd(const moe_problem* p, const void* x, const void* w1, cons
   c.act = p->activation;
   c.which = GEMM_FWD_UP;
   c.sched = sched_at(ws, SCHED_UP);
-  if ((s = run_gemm(c, st)) != MOE_OK) return s;
+  cudaEvent_t x_ready = sync ? (cudaEvent_t)sync->x_ready : nullptr;
+  if (sync && sync->row_split && c.bf16 && tc_splits_rows()) {
+    // the rows whose X is resident first, then (after x_ready) the rest: A, B, U land in
+    // the same rows as one launch would write
+    c.row_split = sync->row_split;
+    c.split_half = 1;
+    if ((s = run_gemm(c, st)) != MOE_OK) return s;
+    if (x_ready) MOE_CUDA_CHECK(cudaStreamWaitEvent(st, x_ready, 0));
+    c.split_half = 2;
+    if ((s = run_gemm(c, st)) != MOE_OK) return s;
+    c.row_split = nullptr;
+    c.split_half = 0;
+  } else {
+    if (x_ready) MOE_CUDA_CHECK(cudaStreamWaitEvent(st, x_ready, 0));
+    if ((s = run_gemm(c, st)) != MOE_OK) return s;
+  }
   c.which = GEMM_FWD_DOWN;
   c.sched = sched_at(ws, SCHED_DOWN);
   if ((s = run_gemm(c, st)) != MOE_OK) return s;

@@ -198,6 +198,27 @@ moe_status launch_dispatch(const moe_problem* p, const int32_t* ids, const moe_d
   return MOE_OK;
 }
 
+// row_split[e] = offs[e] + #{r in segment e : eti[r] < t_ready}: lower bound of t_ready in the
+// segment (eti ascending inside an expert); one thread per expert
+__global__ void row_split_kernel(const int32_t* __restrict__ offs, const int32_t* __restrict__ eti, int E,
+                                 int64_t t_ready, int32_t* __restrict__ split) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  int lo = offs[e], hi = offs[e + 1];
+  while (lo < hi) {
+    const int mid = lo + ((hi - lo) >> 1);
+    if ((int64_t)eti[mid] < t_ready) lo = mid + 1;
+    else hi = mid;
+  }
+  split[e] = lo;
+}
+
+moe_status launch_row_split(const int32_t* offs, const int32_t* eti, int E, int64_t t_ready, int32_t* split,
+                            cudaStream_t st) {
+  MOE_LAUNCH(row_split_kernel, (unsigned)ceil_div(E, 128), 128, 0, st, offs, eti, E, t_ready, split);
+  return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
+}
+
 size_t dispatch_ws_bytes(const moe_problem* p) {
   const int64_t R = p->T * p->k;
   const int64_t ntiles = R ? ceil_div(R, dispatch_tile_entries(R)) : 0;

@@ -208,7 +208,10 @@ struct CgCfg {
   // after the stages: barriers (768 B: stage/accumulator/scheduler barriers at +0 / +256, the
   // BWD_DH epilogue ring's at +512) and the per-expert offsets + tile starts (2 x 260 ints)
   static constexpr int OFFS_OFF = MOEB_SMEM_TIGHT ? 768 : 1024;
-  static constexpr int STG_OFF = (STAGES * STAGE + OFFS_OFF + (MOEB_SMEM_TIGHT ? 2080 : 2176) + 1023) / 1024 * 1024;
+  // s_offs + s_mstart (2 x 260 ints); FWD_UP also keeps each segment's end (s_offs + 520: the
+  // row-split launches process [offs[e], split[e]) or [split[e], offs[e+1]))
+  static constexpr int OFFS_BYTES = (MOEB_SMEM_TIGHT ? 2080 : 2176) + (KIND == TC_FWD_UP ? 1040 : 0);
+  static constexpr int STG_OFF = (STAGES * STAGE + OFFS_OFF + OFFS_BYTES + 1023) / 1024 * 1024;
   // the dynamic shared memory starts 1024-aligned (after the 1 KB the driver reserves per CTA;
   // profiles/smem_probe_r02e.txt), so the tight layout carries no alignment slack (the kernel
   // traps if that ever changes)
@@ -253,6 +256,10 @@ struct TcParams {
   int die_sm0_permille;
   int u_weighted;  // MOE_CKPT_ABU: FWD_UP stores w * U; FWD_DOWN then adds U W3 with unit weight
   int dh_skip_u;   // MOE_CKPT_ABU: BWD_DH writes dA, dB only (wU is saved from the forward)
+  // FWD_UP row split (moe_fwd_sync): split_half 1 = rows [offs[e], row_split[e]) of every
+  // expert, 2 = rows [row_split[e], offs[e+1]); 0 = all rows
+  const int32_t* row_split;
+  int split_half;
 };
 
 template <int KIND>
@@ -366,7 +373,7 @@ __device__ __forceinline__ bool decode_tile(int tile, const TcParams& P, const i
     }
     t.e = find_segment(s_mstart, P.E, local / nt);
     t.seg0 = s_offs[t.e];
-    t.seg1 = s_offs[t.e + 1];
+    t.seg1 = KIND == TC_FWD_UP ? s_offs[520 + t.e] : s_offs[t.e + 1];  // FWD_UP: segment ends (row split)
     const int mt_e = s_mstart[t.e + 1] - s_mstart[t.e];
     local -= s_mstart[t.e] * nt;
     // grouped rasterisation: blocks of ~RG m-tiles x the list's n-tiles, m
@@ -557,8 +564,22 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
   const int cluster_id = (CG == 2) ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
   const int n_clusters = (CG == 2) ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
-  if constexpr (!is_route(KIND))
+  if constexpr (KIND == TC_FWD_UP) {
+    // segment [s_offs[e], s_offs[520 + e]) of expert e: the whole segment, or one side of
+    // row_split[e] (split_half 1: the rows before it, 2: the rows from it on)
+    for (int i = threadIdx.x; i < E; i += tc_threads(KIND)) {
+      int lo = P.offs[i], hi = P.offs[i + 1];
+      if (P.split_half) {
+        const int sp = P.row_split[i];
+        if (P.split_half == 1) hi = sp;
+        else lo = sp;
+      }
+      s_offs[i] = lo;
+      s_offs[520 + i] = hi;
+    }
+  } else if constexpr (!is_route(KIND)) {
     for (int i = threadIdx.x; i <= E; i += tc_threads(KIND)) s_offs[i] = P.offs[i];
+  }
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch(&mA0);
     ptx::tma_prefetch(&mA1);
@@ -597,7 +618,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
     int s = 0;
     for (int e = 0; e < E; ++e) {
       s_mstart[e] = s;
-      s += (s_offs[e + 1] - s_offs[e] + C::TM - 1) / C::TM;
+      s += ((KIND == TC_FWD_UP ? s_offs[520 + e] : s_offs[e + 1]) - s_offs[e] + C::TM - 1) / C::TM;
     }
     s_mstart[E] = s;
   }
@@ -1770,6 +1791,9 @@ moe_status tc_route(const moe_problem* p, const void* x, const void* wg, float* 
   return launch_tc_impl<TC_ROUTE, false, 1>(a0, a0, b0, b0, P, ceil_div(p->T, 128), st);
 }
 
+// FWD_UP honours GemmCall.row_split in the CTA-pair engine (the others run all rows)
+bool tc_splits_rows() { return engine() == ENG_PAIR; }
+
 moe_status tc_gemm(const GemmCall& c, cudaStream_t st) {
   typedef __nv_bfloat16 bf;
   const int64_t T = c.T, R = c.R;
@@ -1789,6 +1813,8 @@ moe_status tc_gemm(const GemmCall& c, cudaStream_t st) {
   P.u_weighted = c.u_weighted; P.dh_skip_u = c.dh_skip_u;
   P.T = (int)T; P.d = d; P.h = h; P.E = E;
   P.dg_parts = tc_dg_parts(h, d);
+  P.row_split = c.row_split;
+  P.split_half = c.row_split ? c.split_half : 0;
   CUtensorMap a0, a1, b0, b1;
   bool ok = true;
   // upper bound on row tiles of height TM over all expert segments

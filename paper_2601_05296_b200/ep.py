@@ -29,9 +29,13 @@ Forward, per rank:
   2. send plan (moe_ep_dest without self + moe_dispatch_build); C1: all-to-all of
      the [rows, pairs per local expert] counts; ONE device->host read of the
      split sizes (the only host sync of the step: buffers are sized by it).
-  3. C2: remote X rows in send order (moe_gather_rows) + the packed slot
-     metadata, received behind the local tokens' rows.
-  4. receiver: sparse dispatch over [local slots | received slots], moe_ffn_fwd;
+  3. C2a: the packed slot metadata of the remote rows; the receiver builds its
+     sparse dispatch over [local slots | received slots].  C2b: remote X rows in
+     send order (moe_gather_rows), received behind the local tokens' rows, on a
+     side stream: moe_ffn_fwd_ex runs the up-projection of every expert's local
+     rows (they come first in each expert segment) while it is in flight and
+     waits for it only before the received rows' up-projection.
+  4. receiver: moe_ffn_fwd_ex (split at row T), down projection + combine;
      C3 returns one row per (remote token, rank); moe_combine_rows adds them to
      the local partial through send_pos.
 Backward:
@@ -128,7 +132,10 @@ class CudaOps:
         L.moe_gather_rows(src, index.reshape(-1), dst)
         return dst
 
-    def ffn_fwd(self, x, w1, w2, w3, w, disp, rows):
+    def ffn_fwd(self, x, w1, w2, w3, w, disp, rows, t_ready=None, x_ready=None):
+        """t_ready: x rows [0, t_ready) are resident, the rest arrive at x_ready (a CUDA
+        event or None): moe_ffn_fwd_ex runs the up-projection of each expert's resident
+        rows first and waits x_ready only before the rest (moe_dispatch_row_split)."""
         T, d = x.shape
         E, h, _ = w1.shape
         k = w.shape[1]
@@ -137,7 +144,14 @@ class CudaOps:
         b = torch.empty(rows, h, dtype=x.dtype, device=x.device)
         y = torch.empty(T, d, dtype=x.dtype, device=x.device)
         ws = L.workspace(p, L.MOE_OP_FFN_FWD, x.device)
-        L.moe_ffn_fwd(p, x, w1, w2, w3, w, disp.c(), a, b, None, y, ws)
+        if t_ready is None and x_ready is None:
+            L.moe_ffn_fwd(p, x, w1, w2, w3, w, disp.c(), a, b, None, y, ws)
+        else:
+            split = None
+            if t_ready is not None:
+                split = torch.empty(E, dtype=torch.int32, device=x.device)
+                L.moe_dispatch_row_split(p, disp.c(), t_ready, split)
+            L.moe_ffn_fwd_ex(p, x, w1, w2, w3, w, disp.c(), a, b, None, y, ws, row_split=split, x_ready=x_ready)
         return y, a, b
 
     def ffn_bwd(self, dy, x, w1, w2, w3, w, disp, a, b, rows, x_ready=None, dx_ready=None):
@@ -261,15 +275,40 @@ class ExpertParallelMoE:
         meta[:T, :k] = lid
         meta[:T, k:] = lw.view(torch.int32)
         sid, sw = ops.send_meta(ids, w, E, El, P, plan.row_slot[:n_send])
-        # C2: remote token rows + their slot metadata, received behind the local rows
-        x_l = self._rows(x, send_tok, send_split, recv_split)
+        # C2a: the received rows' slot metadata first (small: the receiver's dispatch needs it)
         self.a2a(torch.cat([sid, sw.view(torch.int32)], 1), send_split, recv_split, out=meta[T:])
         ids_l = meta[:, :k].contiguous()
         w_l = meta[:, k:].contiguous().view(w.dtype)
         disp_l = ops.dispatch(ids_l, El, x.dtype, rows=n_pairs) if n_pairs else None
-        if n_pairs:
-            y_rows, a_l, b_l = ops.ffn_fwd(x_l, w1l, w2l, w3l, w_l, disp_l, n_pairs)
+        # C2b: the remote X rows, received behind the local rows.  With CUDA streams the
+        # all-to-all runs on a side stream, issued BEFORE the expert GEMMs so NCCL's kernel
+        # is resident first (the GEMMs' dynamic tile scheduler hands the remaining tiles to
+        # the CTAs that start later); the up-projection of every expert's local rows
+        # (tokens < T, first in each expert segment) overlaps it, and moe_ffn_fwd_ex waits
+        # for the rows only before the received rows' up-projection
+        streams = self._use_streams(x)
+        x_l = torch.empty((T + U, d), dtype=x.dtype, device=x.device)
+        x_l[:T].copy_(x)
+        x_send = ops.gather_rows(x, send_tok)
+        x_ready = None
+        if streams and U:
+            main, side = torch.cuda.current_stream(), torch.cuda.Stream(device=x.device)
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                self.a2a(x_send, send_split, recv_split, out=x_l[T:])
+            x_ready = torch.cuda.Event()
+            x_ready.record(side)
+            x_l.record_stream(side)
+            x_send.record_stream(side)
         else:
+            self.a2a(x_send, send_split, recv_split, out=x_l[T:])
+        del x_send
+        if n_pairs:
+            y_rows, a_l, b_l = ops.ffn_fwd(x_l, w1l, w2l, w3l, w_l, disp_l, n_pairs,
+                                           t_ready=T if U else None, x_ready=x_ready)
+        else:
+            if x_ready is not None:
+                torch.cuda.current_stream().wait_event(x_ready)
             y_rows, a_l, b_l = x_l.new_zeros(T + U, d), None, None
         x_keep = x_l if self.retain_recv_x else None
         del x_l

@@ -171,3 +171,56 @@ def test_token_rows_bound_and_upper_bound_rows(M, T, n_valid, d, h, E, k, upper)
     assert torch.equal(g0["dg"][:n_valid], g1["dg"][:n_valid])
     for name in ("dw1", "dw2", "dw3"):
         assert torch.equal(g0[name], g1[name]), name
+
+
+@pytest.mark.parametrize("T,d,h,E,k,dtype,p_empty,t_ready", [
+    (700, 256, 384, 8, 2, "bf16", 0.0, 311),      # dense slots, split inside most segments
+    (700, 256, 384, 8, 2, "bf16", 0.0, 0),        # nothing resident: all rows in the second launch
+    (700, 256, 384, 8, 2, "bf16", 0.0, 700),      # everything resident: second launch empty
+    (2000, 512, 256, 16, 6, "bf16", 0.5, 1337),   # sparse receiver rows (EP), k = 6
+    (900, 256, 384, 1, 2, "bf16", 0.3, 450),      # one local expert < k
+    (96, 64, 96, 4, 3, "fp32", 0.5, 40),          # fp32: one launch after x_ready
+])
+def test_ffn_fwd_row_split_identical(M, T, d, h, E, k, dtype, p_empty, t_ready):
+    """moe_ffn_fwd_ex (NEXT-1 forward overlap): the up-projection split at the rows
+    whose token is < t_ready, the rest after an event -- A, B and y bit-identical to
+    one moe_ffn_fwd call (k <= 2: the red.add combine onto zero is order-free), and
+    row_split[e] the lower bound of t_ready in expert e's ascending segment."""
+    from paper_2601_05296_b200 import _lib as L
+    from paper_2601_05296_b200.ep import CudaOps
+    inp = make_inputs(T, d, h, E, k, dtype=dtype, seed=9, device=DEV)
+    ids_np = _sparse_ids(T, E, k, 21, p_empty)
+    n = int((ids_np >= 0).sum())
+    ids = torch.from_numpy(ids_np).to(DEV)
+    w = torch.rand(T, k, generator=torch.Generator().manual_seed(4)).to(DEV)
+    w[ids < 0] = 0
+    ops = CudaOps()
+    disp = ops.dispatch(ids, E, inp["x"].dtype, rows=n)
+    x, w1, w2, w3 = inp["x"], inp["w1"], inp["w2"], inp["w3"]
+    y0, a0, b0 = ops.ffn_fwd(x, w1, w2, w3, w, disp, n)
+    p = L.problem(T, d, h, E, k, x.dtype, rows=n)
+    split = torch.empty(E, dtype=torch.int32, device=DEV)
+    L.moe_dispatch_row_split(p, disp.c(), t_ready, split)
+    torch.cuda.synchronize()
+    offs, eti = i64(disp.offs), i64(disp.eti)[:n]
+    ref = [offs[e] + int(np.searchsorted(eti[offs[e]:offs[e + 1]], t_ready, side="left")) for e in range(E)]
+    assert np.array_equal(i64(split), np.array(ref))
+    # X rows from t_ready on are written only after the event the split launch waits on
+    xs = x.clone()
+    xs[t_ready:] = 0
+    side = torch.cuda.Stream()
+    ev = torch.cuda.Event()
+    ev.record()
+    side.wait_event(ev)
+    with torch.cuda.stream(side):
+        torch.cuda._sleep(20_000_000)  # the late rows land well after the first launch has started
+        xs[t_ready:].copy_(x[t_ready:])
+        ready = torch.cuda.Event()
+        ready.record(side)
+    y1, a1, b1 = ops.ffn_fwd(xs, w1, w2, w3, w, disp, n, t_ready=t_ready, x_ready=ready)
+    torch.cuda.synchronize()
+    if k <= 2:
+        assert torch.equal(y1, y0)
+    else:
+        assert normwise(f64(y1), f64(y0)) < 1e-2
+    assert torch.equal(a1, a0) and torch.equal(b1, b0)
