@@ -212,6 +212,9 @@ def main():
     ap.add_argument("--deterministic", action="store_true",
                     help="ordered token-side combine of the k expert outputs (bitwise reproducible, NEXT-4)")
     ap.add_argument("--no-graph", action="store_true", help="skip the CUDA-graph replay timing")
+    ap.add_argument("--routing", default="balanced", choices=["balanced", "skewed"],
+                    help="synthetic routing structure (DESIGN.md §4): balanced = iid logits (the headline); "
+                         "skewed = Zipf-like per-expert logit bias (alpha 0.25: max/mean expert load 1.5-3.1)")
     ap.add_argument("--launch-check", action="store_true",
                     help="test hook: start the ranks (gloo, CPU), check the world, print one JSON line, exit")
     args = ap.parse_args()
@@ -259,7 +262,7 @@ def main():
     from paper_2601_05296_b200 import _lib as L
     from moe_inputs import make_inputs
 
-    inp = make_inputs(cfg.T, cfg.d, cfg.h, cfg.E, cfg.k, dtype=cfg.dtype, seed=rank, device=dev)
+    inp = make_inputs(cfg.T, cfg.d, cfg.h, cfg.E, cfg.k, dtype=cfg.dtype, seed=rank, device=dev, routing=args.routing)
     torch.cuda.synchronize()
     k = cfg.k
     x, wg, w1, w2, w3, dy = (inp[n] for n in ("x", "w_gate", "w1", "w2", "w3", "dy"))
@@ -303,6 +306,12 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    # the routing this workload produced (reporting only, outside the timed region): per-expert
+    # routed rows over their mean (1.0 = perfectly balanced)
+    _, ids0, _ = M.route(x, wg, k, renorm)
+    cnt = torch.bincount(ids0.flatten().long(), minlength=cfg.E).float()
+    expert_load = {"max_over_mean": round(float(cnt.max() / cnt.mean()), 3),
+                   "min_over_mean": round(float(cnt.min() / cnt.mean()), 3)}
     if use_ep:
         dist.barrier()
 
@@ -518,7 +527,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded, moe_inputs)",
             "config": config_dict(args, cfg, world, ep is not None),
-            "roofline": roof, "hbm_steps": hbm_steps, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "expert_load": expert_load, "roofline": roof, "hbm_steps": hbm_steps, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "gpu_launches_per_step": launches / args.steps, "clocks": clk,
             "step_ms": {"median": round(statistics.median(per_step), 4), "min": round(min(per_step), 4),
                         "max": round(max(per_step), 4), "note": "per-step CUDA events inside the timed region, rank 0"},
@@ -652,7 +661,7 @@ def config_dict(args, cfg, world, ep_path):
     w_gb = (3 if gated else 2) * cfg.E * cfg.h * cfg.d * 2 / 1e9 / (world if ep_path else 1)  # per rank
     return {"workload": cfg.name, "T_per_gpu": cfg.T, "d": cfg.d, "h": cfg.h, "E": cfg.E, "k": cfg.k,
             "renormalize": args.renormalize, "checkpoint": args.checkpoint, "activation": args.activation,
-            "deterministic": args.deterministic,
+            "deterministic": args.deterministic, "routing": args.routing,
             "parallelism": f"ep{world}" if ep_path else "single-GPU",
             **({"ep_exchange": args.ep_exchange} if ep_path else {}),
             **({"retain_recv_x": True} if args.retain_recv_x else {}),
@@ -743,7 +752,7 @@ def run_reference(args, cfg, rank, world):
         return
     import torch
     from moe_inputs import make_inputs
-    inp = make_inputs(cfg.T, cfg.d, cfg.h, cfg.E, cfg.k, dtype=cfg.dtype, seed=0, device="cpu")
+    inp = make_inputs(cfg.T, cfg.d, cfg.h, cfg.E, cfg.k, dtype=cfg.dtype, seed=0, device="cpu", routing=args.routing)
     host = host_f64(inp)
     # per-step sample sized so the whole W + K run stays within ~3 minutes
     budget = 150.0 / (args.steps + args.warmup)

@@ -195,22 +195,31 @@ moe_status moe_ffn_fwd(const moe_problem* p, const void* x, const void* w1, cons
                        void* a_save, void* b_save, void* u_save, void* y,
                        void* ws, size_t ws_bytes, void* stream);
 
-/* moe_ffn_fwd with the arrival of part of x overlapped (expert parallel: the
- * received token rows come from the all-to-all while the local ones are
- * already resident).  Token rows [0, t_ready) of x are
- * ready at the call; the rows from t_ready on only once sync->x_ready (a
- * cudaEvent_t) has fired.  The up-projection runs in two launches: each
- * expert's rows [offsets[e], row_split[e]) -- the rows whose token is < t_ready,
- * ascending inside an expert, so they come first -- then, after the
- * stream waits x_ready, rows [row_split[e], offsets[e+1]); then the down
- * projection and combine as in moe_ffn_fwd.  A, B, U and y are the same as one
- * moe_ffn_fwd call (every row is computed by the same tile arithmetic).
- * sync NULL, or row_split NULL: exactly moe_ffn_fwd (x_ready, if set, is
- * waited first).  fp32 runs (CUDA-core path) wait x_ready before the single
- * up-projection launch. */
+/* moe_ffn_fwd with the exchanges of an expert-parallel receiver overlapped
+ * (SURVEY §8(f) NEXT-1): its token rows are [t_ready local | received], the
+ * received rows' x arrives from the all-to-all (C2) and their y goes back by
+ * another (C3).  Token rows [0, t_ready) of x are ready at the call; the rows
+ * from t_ready on only once sync->x_ready (a cudaEvent_t) has fired.  Each
+ * expert's rows [offsets[e], row_split[e]) are those whose token is < t_ready
+ * (ascending inside an expert, so they come first).  Launch order:
+ *   up-projection of the rows before row_split; wait x_ready; up-projection
+ *   of the rest; then, with y_ready set (bf16, red.add combine, no
+ *   token_rows bound): down-projection of the rows from row_split on, y rows
+ *   [t_ready, T) finalised, y_ready recorded, down-projection of the rows
+ *   before row_split leaving sm_reserve SMs free (for the C3 exchange kernel),
+ *   y rows [0, t_ready) finalised; without y_ready: one down-projection and
+ *   one finalise (y_ready, if set, recorded at the end).
+ * A, B, U and y are the same as one moe_ffn_fwd call (every row is computed
+ * by the same tile arithmetic; the red.add combine of a token's rows runs in
+ * one launch either way).  sync NULL, or row_split NULL: exactly moe_ffn_fwd
+ * (x_ready, if set, waited first; y_ready recorded at the end).  fp32 runs
+ * (CUDA-core path) do not split. */
 typedef struct {
   const int32_t* row_split;  /* [E] device, from moe_dispatch_row_split(t_ready) */
   void* x_ready;             /* cudaEvent_t or NULL */
+  void* y_ready;             /* cudaEvent_t or NULL, recorded (see above) */
+  int64_t t_ready;           /* the split token row (as given to moe_dispatch_row_split) */
+  int32_t sm_reserve;        /* SMs left free by the launches after y_ready; 0 = none */
 } moe_fwd_sync;
 
 moe_status moe_ffn_fwd_ex(const moe_problem* p, const void* x, const void* w1, const void* w2,

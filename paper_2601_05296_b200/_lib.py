@@ -53,7 +53,8 @@ MOE_BWD_DATA, MOE_BWD_DW3, MOE_BWD_DW12, MOE_BWD_ALL = 1, 2, 4, 7
 
 
 class MoeFwdSync(ctypes.Structure):
-    _fields_ = [("row_split", ctypes.c_void_p), ("x_ready", ctypes.c_void_p)]
+    _fields_ = [("row_split", ctypes.c_void_p), ("x_ready", ctypes.c_void_p), ("y_ready", ctypes.c_void_p),
+                ("t_ready", ctypes.c_int64), ("sm_reserve", ctypes.c_int32)]
 
 
 class MoeRouterBwd(ctypes.Structure):
@@ -229,12 +230,16 @@ def moe_ffn_fwd(p, x, w1, w2, w3, topk_w, disp, a_save, b_save, u_save, y, ws, s
 
 
 def moe_ffn_fwd_ex(p, x, w1, w2, w3, topk_w, disp, a_save, b_save, u_save, y, ws, row_split=None, x_ready=None,
-                   stream=None):
-    """moe_ffn_fwd with x rows [0, t_ready) resident and the rest ready at x_ready
-    (torch.cuda.Event or None); row_split from moe_dispatch_row_split(t_ready)."""
-    if x_ready is not None and not x_ready.cuda_event:
-        raise MoEError("moe_ffn_fwd_ex: x_ready must be created (recorded once) before the call")
-    sync = MoeFwdSync(_ptr(row_split), x_ready.cuda_event if x_ready is not None else None)
+                   y_ready=None, t_ready=0, sm_reserve=0, stream=None):
+    """moe_ffn_fwd with x rows [0, t_ready) resident and the rest ready at x_ready, y rows
+    [t_ready, T) signalled by y_ready (torch.cuda.Event or None) before the down projection of
+    the resident rows, which leaves sm_reserve SMs free; row_split from
+    moe_dispatch_row_split(t_ready) (moe_fwd_sync)."""
+    for ev in (x_ready, y_ready):
+        if ev is not None and not ev.cuda_event:
+            raise MoEError("moe_ffn_fwd_ex: events must be created (recorded once) before the call")
+    sync = MoeFwdSync(_ptr(row_split), x_ready.cuda_event if x_ready is not None else None,
+                      y_ready.cuda_event if y_ready is not None else None, int(t_ready), int(sm_reserve))
     _check(load().moe_ffn_fwd_ex(ctypes.byref(p), _ptr(x), _ptr(w1), _ptr(w2), _ptr(w3), _ptr(topk_w),
                                  ctypes.byref(disp), _ptr(a_save), _ptr(b_save), _ptr(u_save), _ptr(y),
                                  ctypes.byref(sync), _ptr(ws), ws.numel(), _stream(stream)), "moe_ffn_fwd_ex")

@@ -239,7 +239,10 @@ moe_status moe_ffn_fwd_ex(const moe_problem* p, const void* x, const void* w1, c
   FwdWs w = fwd_layout(p, ws);
   if (ws_bytes < w.total) return MOE_ERR_WORKSPACE;
   cudaStream_t st = (cudaStream_t)stream;
-  if (p->T == 0) return MOE_OK;
+  if (p->T == 0) {
+    if (sync && sync->y_ready) MOE_CUDA_CHECK(cudaEventRecord((cudaEvent_t)sync->y_ready, st));
+    return MOE_OK;
+  }
   if (!ckpt) {
     a_save = w.a;
     b_save = w.b;
@@ -260,7 +263,9 @@ moe_status moe_ffn_fwd_ex(const moe_problem* p, const void* x, const void* w1, c
   c.which = GEMM_FWD_UP;
   c.sched = sched_at(ws, SCHED_UP);
   cudaEvent_t x_ready = sync ? (cudaEvent_t)sync->x_ready : nullptr;
-  if (sync && sync->row_split && c.bf16 && tc_splits_rows()) {
+  cudaEvent_t y_ready = sync ? (cudaEvent_t)sync->y_ready : nullptr;
+  const bool split = sync && sync->row_split && c.bf16 && tc_splits_rows();
+  if (split) {
     // the rows whose X is resident first, then (after x_ready) the rest: A, B, U land in
     // the same rows as one launch would write
     c.row_split = sync->row_split;
@@ -269,19 +274,47 @@ moe_status moe_ffn_fwd_ex(const moe_problem* p, const void* x, const void* w1, c
     if (x_ready) MOE_CUDA_CHECK(cudaStreamWaitEvent(st, x_ready, 0));
     c.split_half = 2;
     if ((s = run_gemm(c, st)) != MOE_OK) return s;
-    c.row_split = nullptr;
-    c.split_half = 0;
   } else {
     if (x_ready) MOE_CUDA_CHECK(cudaStreamWaitEvent(st, x_ready, 0));
     if ((s = run_gemm(c, st)) != MOE_OK) return s;
   }
   c.which = GEMM_FWD_DOWN;
   c.sched = sched_at(ws, SCHED_DOWN);
+  const int64_t t_ready = split ? sync->t_ready : 0;
+  if (split && y_ready && mode == OUT_RED && !disp->token_rows && t_ready >= 0 && t_ready <= p->T) {
+    // the received rows' y first (their tokens are >= t_ready: they red.add only into rows
+    // [t_ready, T)), finalised and signalled so their return overlaps the local rows' down
+    // projection, which leaves sm_reserve SMs to the exchange kernel
+    const size_t es = esize(p);
+    moe_problem hi = *p, lo = *p;
+    hi.T = p->T - t_ready;
+    lo.T = t_ready;
+    c.split_half = 2;
+    if ((s = run_gemm(c, st)) != MOE_OK) return s;
+    {
+      ProfScope prof("combine", st);
+      if ((s = launch_finalize(&hi, w.yacc + t_ready * p->d, nullptr, nullptr, nullptr,
+                               (char*)y + (size_t)t_ready * p->d * es, st, false, nullptr, nullptr)) != MOE_OK)
+        return s;
+    }
+    MOE_CUDA_CHECK(cudaEventRecord(y_ready, st));
+    c.split_half = 1;
+    c.sm_reserve = sync->sm_reserve;
+    if ((s = run_gemm(c, st)) != MOE_OK) return s;
+    ProfScope prof("combine", st);
+    return launch_finalize(&lo, w.yacc, nullptr, nullptr, nullptr, y, st, false, nullptr, nullptr);
+  }
+  c.row_split = nullptr;
+  c.split_half = 0;
   if ((s = run_gemm(c, st)) != MOE_OK) return s;
-  if (mode == OUT_TOKN) return MOE_OK;
-  ProfScope prof("combine", st);
-  return launch_finalize(p, w.yacc, nullptr, nullptr, nullptr, y, st, false,
-                         mode == OUT_ROWS ? disp->token_index_map : nullptr, disp->token_rows);
+  if (mode != OUT_TOKN) {
+    ProfScope prof("combine", st);
+    if ((s = launch_finalize(p, w.yacc, nullptr, nullptr, nullptr, y, st, false,
+                             mode == OUT_ROWS ? disp->token_index_map : nullptr, disp->token_rows)) != MOE_OK)
+      return s;
+  }
+  if (y_ready) MOE_CUDA_CHECK(cudaEventRecord(y_ready, st));
+  return MOE_OK;
 }
 
 moe_status moe_ffn_bwd(const moe_problem* p, const void* dy, const void* x, const void* w1, const void* w2,

@@ -26,10 +26,11 @@ struct GemmCall {
   bool u_weighted;  // MOE_CKPT_ABU: FWD_UP writes wU = w * U, FWD_DOWN then adds wU W3 (unit weight)
   bool dh_skip_u;   // MOE_CKPT_ABU: BWD_DH does not write wU (the saved one is read by DW3)
   int* sched;       // 4 claim counters of the tile scheduler (in the caller's ws; zeroed per launch)
-  // FWD_UP only (bf16, CTA-pair engine: tc_splits_rows()): split_half 1 = each expert's rows
-  // [offs[e], row_split[e]), 2 = [row_split[e], offs[e+1]); row_split NULL = all rows
+  // FWD_UP / FWD_DOWN only (bf16, CTA-pair engine: tc_splits_rows()): split_half 1 = each
+  // expert's rows [offs[e], row_split[e]), 2 = [row_split[e], offs[e+1]); NULL = all rows
   const int32_t* row_split;
   int split_half;
+  int sm_reserve;  // SMs the launch leaves free for a concurrent exchange kernel (0 = none)
 };
 
 // Where FWD_DOWN / BWD_DX put a routed row's result v (row r, token t = eti[r]):
@@ -46,7 +47,7 @@ __device__ __forceinline__ float act_grad(int act, float a, float sg) {
 }
 
 moe_status run_gemm(const GemmCall& c, cudaStream_t st);
-bool tc_splits_rows();                   // FWD_UP honours GemmCall.row_split
+bool tc_splits_rows();                   // FWD_UP / FWD_DOWN honour GemmCall.row_split
 // die of every SM of the current device, measured once (topology.cu); device
 // array indexed by %smid, n_sm = SMs per die (n_sm[1] == 0: no split)
 const uint8_t* sm_die_map(int n_sm[2]);

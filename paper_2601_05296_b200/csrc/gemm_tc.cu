@@ -66,6 +66,8 @@ __host__ __device__ constexpr bool is_route(int k) { return k == TC_ROUTE || k =
 // BWD_DH 1.80 -> 1.70 ms), while short K (DeepSeek-like, d = 2048) needs the 8 warps to hide
 // the SwiGLU-backward epilogue (0.69 vs 0.86 ms; profiles/r02c_variants.txt)
 __host__ __device__ constexpr bool is_dh(int k) { return k == TC_BWD_DH || k == TC_BWD_DH_LK || k == TC_BWD_DH_L5; }
+// the forward kinds that can run on one side of a per-expert row split (moe_fwd_sync)
+__host__ __device__ constexpr bool splits_rows(int k) { return k == TC_FWD_UP || k == TC_FWD_DOWN; }
 
 #ifndef MOEB_DH_STAGES
 #define MOEB_DH_STAGES 5  // BWD_DH mainloop stages in the CTA-pair engine (smem shared with the epilogue ring)
@@ -112,6 +114,12 @@ __host__ __device__ constexpr bool is_dh(int k) { return k == TC_BWD_DH || k == 
 // off: interleaved A/B measured FWD_UP 3-7 % slower (profiles/up8_ab_r01.txt) -- its epilogue
 // already hides under the mainloop, and 32-byte row segments store less efficiently
 #define MOEB_UP_EPI8 0
+#endif
+#ifndef MOEB_BULK_RED
+// FWD_DOWN / BWD_DX red.add combine (OUT_RED) by bulk reductions from shared memory (one
+// cp.reduce.async.bulk of a row's 32 columns per row, issued by one lane) instead of per-lane
+// red.global.add.v4
+#define MOEB_BULK_RED 0
 #endif
 #ifndef MOEB_RED_EPI8
 // FWD_DOWN / BWD_DX: 8 epilogue warps (128 columns each), 5 mainloop stages.  Parity-green but
@@ -208,9 +216,9 @@ struct CgCfg {
   // after the stages: barriers (768 B: stage/accumulator/scheduler barriers at +0 / +256, the
   // BWD_DH epilogue ring's at +512) and the per-expert offsets + tile starts (2 x 260 ints)
   static constexpr int OFFS_OFF = MOEB_SMEM_TIGHT ? 768 : 1024;
-  // s_offs + s_mstart (2 x 260 ints); FWD_UP also keeps each segment's end (s_offs + 520: the
-  // row-split launches process [offs[e], split[e]) or [split[e], offs[e+1]))
-  static constexpr int OFFS_BYTES = (MOEB_SMEM_TIGHT ? 2080 : 2176) + (KIND == TC_FWD_UP ? 1040 : 0);
+  // s_offs + s_mstart (2 x 260 ints); FWD_UP / FWD_DOWN also keep each segment's end (s_offs +
+  // 520: the row-split launches process [offs[e], split[e]) or [split[e], offs[e+1]))
+  static constexpr int OFFS_BYTES = (MOEB_SMEM_TIGHT ? 2080 : 2176) + (splits_rows(KIND) ? 1040 : 0);
   static constexpr int STG_OFF = (STAGES * STAGE + OFFS_OFF + OFFS_BYTES + 1023) / 1024 * 1024;
   // the dynamic shared memory starts 1024-aligned (after the 1 KB the driver reserves per CTA;
   // profiles/smem_probe_r02e.txt), so the tight layout carries no alignment slack (the kernel
@@ -256,10 +264,11 @@ struct TcParams {
   int die_sm0_permille;
   int u_weighted;  // MOE_CKPT_ABU: FWD_UP stores w * U; FWD_DOWN then adds U W3 with unit weight
   int dh_skip_u;   // MOE_CKPT_ABU: BWD_DH writes dA, dB only (wU is saved from the forward)
-  // FWD_UP row split (moe_fwd_sync): split_half 1 = rows [offs[e], row_split[e]) of every
-  // expert, 2 = rows [row_split[e], offs[e+1]); 0 = all rows
+  // FWD_UP / FWD_DOWN row split (moe_fwd_sync): split_half 1 = rows [offs[e], row_split[e])
+  // of every expert, 2 = rows [row_split[e], offs[e+1]); 0 = all rows
   const int32_t* row_split;
   int split_half;
+  int sm_reserve;  // host only: SMs the launch leaves free (moe_fwd_sync.sm_reserve)
 };
 
 template <int KIND>
@@ -373,7 +382,7 @@ __device__ __forceinline__ bool decode_tile(int tile, const TcParams& P, const i
     }
     t.e = find_segment(s_mstart, P.E, local / nt);
     t.seg0 = s_offs[t.e];
-    t.seg1 = KIND == TC_FWD_UP ? s_offs[520 + t.e] : s_offs[t.e + 1];  // FWD_UP: segment ends (row split)
+    t.seg1 = splits_rows(KIND) ? s_offs[520 + t.e] : s_offs[t.e + 1];  // segment ends (row split)
     const int mt_e = s_mstart[t.e + 1] - s_mstart[t.e];
     local -= s_mstart[t.e] * nt;
     // grouped rasterisation: blocks of ~RG m-tiles x the list's n-tiles, m
@@ -564,7 +573,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
   const int cluster_id = (CG == 2) ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
   const int n_clusters = (CG == 2) ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
-  if constexpr (KIND == TC_FWD_UP) {
+  if constexpr (splits_rows(KIND)) {
     // segment [s_offs[e], s_offs[520 + e]) of expert e: the whole segment, or one side of
     // row_split[e] (split_half 1: the rows before it, 2: the rows from it on)
     for (int i = threadIdx.x; i < E; i += tc_threads(KIND)) {
@@ -618,7 +627,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
     int s = 0;
     for (int e = 0; e < E; ++e) {
       s_mstart[e] = s;
-      s += ((KIND == TC_FWD_UP ? s_offs[520 + e] : s_offs[e + 1]) - s_offs[e] + C::TM - 1) / C::TM;
+      s += ((splits_rows(KIND) ? s_offs[520 + e] : s_offs[e + 1]) - s_offs[e] + C::TM - 1) / C::TM;
     }
     s_mstart[E] = s;
   }
@@ -1328,6 +1337,32 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
           }
           ptx::tmem_ld32(tb + tcol + cc, v);
           ptx::tmem_wait_ld();
+          if constexpr (MOEB_BULK_RED) {
+            if (P.out_mode == OUT_RED) {
+              // lane = row: its 32 scaled values in row-major staging (pitch 144 B: the 16-byte
+              // stores of 8 lanes per phase hit distinct banks), then one lane issues a 128-byte
+              // bulk reduction per row into the token's accumulator row
+              if (lane == 0) ptx::bulk_wait_read<0>();  // the previous chunk's reductions read it
+              __syncwarp();
+              float4* srow = reinterpret_cast<float4*>(stg + lane * 144);
+#pragma unroll
+              for (int q = 0; q < 8; ++q)
+                srow[q] = make_float4(w * __uint_as_float(v[4 * q]), w * __uint_as_float(v[4 * q + 1]),
+                                      w * __uint_as_float(v[4 * q + 2]), w * __uint_as_float(v[4 * q + 3]));
+              ptx::fence_proxy_async();  // generic smem writes -> the async proxy's reads
+              __syncwarp();
+              const float* dst = P.acc_out + (int64_t)tok * N + t.n0 + c;
+              const uint32_t s0 = ptx::smem_u32(stg);
+              for (int rr = 0; rr < nvalid; ++rr) {
+                const float* d_rr = reinterpret_cast<const float*>(
+                    __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(dst), rr));
+                if (lane == 0) ptx::bulk_red_add_f32(d_rr, s0 + 144u * (uint32_t)rr, 128u);
+              }
+              if (lane == 0) ptx::bulk_commit();
+              __syncwarp();
+              continue;
+            }
+          }
 #pragma unroll
           for (int q = 0; q < 8; ++q)
             *reinterpret_cast<float4*>(stg + stg32_off(lane, q)) =
@@ -1614,8 +1649,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
       }
       if (WIDE || ++as == 2) { as = 0; aphase ^= 1; }
     }
-    if constexpr (is_dh(KIND) && CPA && MOEB_DH_TMA)
-      if (lane == 0) ptx::bulk_wait<0>();  // the epilogue's TMA stores are complete
+    if constexpr ((is_dh(KIND) && CPA && MOEB_DH_TMA) || (MOEB_BULK_RED && (KIND == TC_FWD_DOWN || KIND == TC_BWD_DX)))
+      if (lane == 0) ptx::bulk_wait<0>();  // the epilogue's TMA stores / bulk reductions are complete
   }
   ptx::tc_fence_before();
   if constexpr (CG == 2) ptx::cluster_sync();
@@ -1708,7 +1743,9 @@ static moe_status launch_tc_impl(const CUtensorMap& a0, const CUtensorMap& a1, c
     attr = true;
   }
   if (tiles <= 0) return MOE_OK;
-  const int groups = (int)std::min<int64_t>(tiles, num_sms() / CG);
+  // sm_reserve: SMs left free for a concurrent kernel (an exchange overlapping this GEMM)
+  const int avail = std::max(CG, num_sms() - std::max(0, P.sm_reserve));
+  const int groups = (int)std::min<int64_t>(tiles, avail / CG);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(groups * CG);
   cfg.blockDim = dim3(tc_threads(KIND));
@@ -1791,7 +1828,7 @@ moe_status tc_route(const moe_problem* p, const void* x, const void* wg, float* 
   return launch_tc_impl<TC_ROUTE, false, 1>(a0, a0, b0, b0, P, ceil_div(p->T, 128), st);
 }
 
-// FWD_UP honours GemmCall.row_split in the CTA-pair engine (the others run all rows)
+// FWD_UP / FWD_DOWN honour GemmCall.row_split in the CTA-pair engine (the others run all rows)
 bool tc_splits_rows() { return engine() == ENG_PAIR; }
 
 moe_status tc_gemm(const GemmCall& c, cudaStream_t st) {
@@ -1815,6 +1852,7 @@ moe_status tc_gemm(const GemmCall& c, cudaStream_t st) {
   P.dg_parts = tc_dg_parts(h, d);
   P.row_split = c.row_split;
   P.split_half = c.row_split ? c.split_half : 0;
+  P.sm_reserve = c.sm_reserve;
   CUtensorMap a0, a1, b0, b1;
   bool ok = true;
   // upper bound on row tiles of height TM over all expert segments

@@ -35,7 +35,8 @@ Forward, per rank:
      side stream: moe_ffn_fwd_ex runs the up-projection of every expert's local
      rows (they come first in each expert segment) while it is in flight and
      waits for it only before the received rows' up-projection.
-  4. receiver: moe_ffn_fwd_ex (split at row T), down projection + combine;
+  4. receiver: moe_ffn_fwd_ex (split at row T): the received rows' down projection
+     and y first, then (C3 on a side stream) the local rows' down projection;
      C3 returns one row per (remote token, rank); moe_combine_rows adds them to
      the local partial through send_pos.
 Backward:
@@ -132,10 +133,12 @@ class CudaOps:
         L.moe_gather_rows(src, index.reshape(-1), dst)
         return dst
 
-    def ffn_fwd(self, x, w1, w2, w3, w, disp, rows, t_ready=None, x_ready=None):
+    def ffn_fwd(self, x, w1, w2, w3, w, disp, rows, t_ready=None, x_ready=None, y_ready=None, sm_reserve=0):
         """t_ready: x rows [0, t_ready) are resident, the rest arrive at x_ready (a CUDA
         event or None): moe_ffn_fwd_ex runs the up-projection of each expert's resident
-        rows first and waits x_ready only before the rest (moe_dispatch_row_split)."""
+        rows first and waits x_ready only before the rest (moe_dispatch_row_split); with
+        y_ready it also finishes the y rows from t_ready on first, records y_ready, and
+        runs the resident rows' down projection on all but sm_reserve SMs."""
         T, d = x.shape
         E, h, _ = w1.shape
         k = w.shape[1]
@@ -151,7 +154,8 @@ class CudaOps:
             if t_ready is not None:
                 split = torch.empty(E, dtype=torch.int32, device=x.device)
                 L.moe_dispatch_row_split(p, disp.c(), t_ready, split)
-            L.moe_ffn_fwd_ex(p, x, w1, w2, w3, w, disp.c(), a, b, None, y, ws, row_split=split, x_ready=x_ready)
+            L.moe_ffn_fwd_ex(p, x, w1, w2, w3, w, disp.c(), a, b, None, y, ws, row_split=split, x_ready=x_ready,
+                             y_ready=y_ready, t_ready=t_ready or 0, sm_reserve=sm_reserve)
         return y, a, b
 
     def ffn_bwd(self, dy, x, w1, w2, w3, w, disp, a, b, rows, x_ready=None, dx_ready=None):
@@ -205,13 +209,16 @@ class ExpertParallelMoE:
 
     overlap: run C4b (X rows) and C5 (dX rows, gate grads) on a side CUDA
     stream against the backward GEMMs (default: on for CUDA tensors over NCCL).
+    sm_reserve: SMs the local rows' down projection leaves to the C3 all-to-all's kernel
+    (moe_fwd_sync.sm_reserve).
     retain_recv_x: keep the X rows received in forward for the dW1/dW2 GEMM
     instead of sending them again in backward: one a2a unit less
     per step, R_recv x d saved activation bytes more (a permuted copy of X, which
     the default -- the north star's no-permuted-buffer rule -- does not keep).
     """
 
-    def __init__(self, E, k, renormalize=False, group=None, ops=None, a2a=None, overlap=None, retain_recv_x=False):
+    def __init__(self, E, k, renormalize=False, group=None, ops=None, a2a=None, overlap=None, retain_recv_x=False,
+                 sm_reserve=16):
         self.P = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         if E % self.P:
@@ -223,6 +230,7 @@ class ExpertParallelMoE:
         self._a2a = a2a or nccl_a2a
         self.overlap = overlap
         self.retain_recv_x = retain_recv_x
+        self.sm_reserve = sm_reserve
         self.last_rows_received = 0   # (token, expert) rows computed here
         self.last_rows_sent = 0       # token rows sent (X) to other ranks, after dedup
         self.last_pairs_sent = 0      # (token, expert) pairs they carry
@@ -303,9 +311,14 @@ class ExpertParallelMoE:
         else:
             self.a2a(x_send, send_split, recv_split, out=x_l[T:])
         del x_send
+        y_ready = None
+        if streams and U and n_pairs:
+            y_ready = torch.cuda.Event()
+            y_ready.record(torch.cuda.current_stream())  # created now; re-recorded by the library
         if n_pairs:
             y_rows, a_l, b_l = ops.ffn_fwd(x_l, w1l, w2l, w3l, w_l, disp_l, n_pairs,
-                                           t_ready=T if U else None, x_ready=x_ready)
+                                           t_ready=T if U else None, x_ready=x_ready, y_ready=y_ready,
+                                           sm_reserve=self.sm_reserve if y_ready is not None else 0)
         else:
             if x_ready is not None:
                 torch.cuda.current_stream().wait_event(x_ready)
@@ -313,8 +326,19 @@ class ExpertParallelMoE:
         x_keep = x_l if self.retain_recv_x else None
         del x_l
         # C3: per-(remote token, rank) partial outputs back; token-side sum through send_pos,
-        # on top of the local partial (rows [0, T) of the receiver's output)
-        y_back = self.a2a(y_rows[T:], recv_split, send_split)
+        # on top of the local partial (rows [0, T) of the receiver's output).  With streams the
+        # received rows' y is final at y_ready, before the local rows' down projection, which
+        # leaves sm_reserve SMs to this all-to-all's kernel
+        if y_ready is not None:
+            main, side = torch.cuda.current_stream(), torch.cuda.Stream(device=x.device)
+            side.wait_event(y_ready)
+            with torch.cuda.stream(side):
+                y_back = self.a2a(y_rows[T:], recv_split, send_split)
+            y_rows.record_stream(side)
+            main.wait_stream(side)
+            y_back.record_stream(main)
+        else:
+            y_back = self.a2a(y_rows[T:], recv_split, send_split)
         y = ops.combine(y_back, plan.tim, T, d, P, base=y_rows[:T])
         ctx = dict(x=x, wg=wg, w1l=w1l, w2l=w2l, w3l=w3l, logits=logits, ids=ids, w=w, plan=plan, send_tok=send_tok,
                    send_split=send_split, recv_split=recv_split, w_l=w_l, disp_l=disp_l, a_l=a_l, b_l=b_l,

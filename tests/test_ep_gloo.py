@@ -76,7 +76,7 @@ class OracleOps:
     def read_host(self, t):
         return t.clone()
 
-    def ffn_fwd(self, x, w1, w2, w3, w, disp, rows, t_ready=None, x_ready=None):
+    def ffn_fwd(self, x, w1, w2, w3, w, disp, rows, **overlap):  # t_ready, x_ready, ...: scheduling only
         f = O.ffn_forward(x.numpy(), w1.numpy(), w2.numpy(), w3.numpy(), disp.ids.numpy(), w.numpy(), disp.raw)
         return torch.from_numpy(f["y"]), torch.from_numpy(f["A"][:rows]), torch.from_numpy(f["B"][:rows])
 

@@ -183,9 +183,11 @@ def test_token_rows_bound_and_upper_bound_rows(M, T, n_valid, d, h, E, k, upper)
 ])
 def test_ffn_fwd_row_split_identical(M, T, d, h, E, k, dtype, p_empty, t_ready):
     """moe_ffn_fwd_ex (NEXT-1 forward overlap): the up-projection split at the rows
-    whose token is < t_ready, the rest after an event -- A, B and y bit-identical to
-    one moe_ffn_fwd call (k <= 2: the red.add combine onto zero is order-free), and
-    row_split[e] the lower bound of t_ready in expert e's ascending segment."""
+    whose token is < t_ready, the rest after an event; the down projection of the
+    rows from the split on first, y rows [t_ready, T) final at y_ready, then the
+    rest on fewer SMs -- A, B and y bit-identical to one moe_ffn_fwd call (k <= 2:
+    the red.add combine onto zero is order-free), and row_split[e] the lower bound
+    of t_ready in expert e's ascending segment."""
     from paper_2601_05296_b200 import _lib as L
     from paper_2601_05296_b200.ep import CudaOps
     inp = make_inputs(T, d, h, E, k, dtype=dtype, seed=9, device=DEV)
@@ -217,10 +219,22 @@ def test_ffn_fwd_row_split_identical(M, T, d, h, E, k, dtype, p_empty, t_ready):
         xs[t_ready:].copy_(x[t_ready:])
         ready = torch.cuda.Event()
         ready.record(side)
-    y1, a1, b1 = ops.ffn_fwd(xs, w1, w2, w3, w, disp, n, t_ready=t_ready, x_ready=ready)
+    y_ready = torch.cuda.Event()
+    y_ready.record()
+    y1, a1, b1 = ops.ffn_fwd(xs, w1, w2, w3, w, disp, n, t_ready=t_ready, x_ready=ready, y_ready=y_ready,
+                             sm_reserve=40)
+    # what a C3 exchange would read at y_ready: the y rows from t_ready on, already final
+    # (the local rows' down projection runs after it, on 148 - 40 SMs)
+    grab = torch.cuda.Stream()
+    grab.wait_event(y_ready)
+    with torch.cuda.stream(grab):
+        y_hi = y1[t_ready:].clone()
     torch.cuda.synchronize()
-    if k <= 2:
+    if k <= 2:  # a token's rows are all in one launch: its red.adds onto zero are order-free
         assert torch.equal(y1, y0)
+        assert torch.equal(y_hi, y0[t_ready:])
     else:
         assert normwise(f64(y1), f64(y0)) < 1e-2
+        if t_ready < T:
+            assert normwise(f64(y_hi), f64(y0[t_ready:])) < 1e-2
     assert torch.equal(a1, a0) and torch.equal(b1, b0)
