@@ -121,6 +121,12 @@ __host__ __device__ constexpr bool splits_rows(int k) { return k == TC_FWD_UP ||
 // red.global.add.v4
 #define MOEB_BULK_RED 0
 #endif
+#ifndef MOEB_RED_EVICT_LAST
+// FWD_DOWN / BWD_DX red.add combine with an L2 evict_last hint: a token's accumulator row is
+// hit k times at scattered moments of the launch; kept resident, its read-modify-writes
+// need no DRAM read
+#define MOEB_RED_EVICT_LAST 0
+#endif
 #ifndef MOEB_RED_EPI8
 // FWD_DOWN / BWD_DX: 8 epilogue warps (128 columns each), 5 mainloop stages.  Parity-green but
 // off: interleaved A/B measured both kinds 1-5 % slower (profiles/red8_ab_r01.txt)
@@ -1320,6 +1326,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
         const int r = r0w + lane;
         const int nvalid = max(0, min(32, t.seg1 - r0w));
         const int N = P.d;
+        const uint64_t pol = MOEB_RED_EVICT_LAST ? ptx::policy_evict_last() : 0ull;
         float w = 1.f;
         int tok = 0;
         if (r < t.seg1) {
@@ -1390,8 +1397,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
               const int tr = __shfl_sync(0xffffffffu, tok, rr);
               if (rr < nvalid) {
                 const float4 f = *reinterpret_cast<const float4*>(stg + stg32_off(rr, q));
-                if (P.out_mode == OUT_RED)
-                  ptx::red_add_v4(P.acc_out + (int64_t)tr * N + t.n0 + c + 4 * q, f.x, f.y, f.z, f.w);
+                if (P.out_mode == OUT_RED) {
+                  if constexpr (MOEB_RED_EVICT_LAST)
+                    ptx::red_add_v4_hint(P.acc_out + (int64_t)tr * N + t.n0 + c + 4 * q, f.x, f.y, f.z, f.w, pol);
+                  else
+                    ptx::red_add_v4(P.acc_out + (int64_t)tr * N + t.n0 + c + 4 * q, f.x, f.y, f.z, f.w);
+                }
                 else  // OUT_ROWS: expert-sorted row r0w + rr; OUT_TOK: token tr
                   *reinterpret_cast<float4*>(P.acc_out + (int64_t)(P.out_mode == OUT_ROWS ? r0w + rr : tr) * N +
                                              t.n0 + c + 4 * q) = f;
