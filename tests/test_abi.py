@@ -226,3 +226,29 @@ def test_ep_peer_exchange_validation(lib):
     off = ctypes.c_int64()
     assert lib.moe_ep_ipc_handle(None, h, ctypes.byref(off)) == 1
     assert lib.moe_ep_ipc_close(None) == 1
+
+
+def test_forward_overlap_validation(lib):
+    """moe_dispatch_row_split / moe_ffn_fwd_ex (NEXT-1 forward overlap) reject bad
+    arguments synchronously: t_ready outside [0, T], missing dispatch arrays, null
+    operands -- and T = 0 launches nothing (no GPU needed)."""
+    from paper_2601_05296_b200 import _lib as L
+    p = L.problem(1024, 256, 512, 8, 2, torch.bfloat16)
+    fake = ctypes.c_void_p(256)  # never dereferenced: validation fails first
+    d = L.MoeDispatch(fake, fake, fake, fake, fake, fake, None)
+    for t_ready in (-1, 1025):
+        assert lib.moe_dispatch_row_split(ctypes.byref(p), ctypes.byref(d), t_ready, fake, None) == 1
+    assert lib.moe_dispatch_row_split(ctypes.byref(p), None, 0, fake, None) == 1
+    assert lib.moe_dispatch_row_split(ctypes.byref(p), ctypes.byref(d), 0, None, None) == 1
+    nod = L.MoeDispatch(fake, None, fake, fake, fake, fake, None)
+    assert lib.moe_dispatch_row_split(ctypes.byref(p), ctypes.byref(nod), 0, fake, None) == 1
+    sync = L.MoeFwdSync(None, None, None, 0, 0)
+    ws_n = L.workspace_size(p, L.MOE_OP_FFN_FWD)
+    # null x / y / weights: invalid before anything is launched
+    assert lib.moe_ffn_fwd_ex(ctypes.byref(p), None, None, None, None, None, ctypes.byref(d), None, None, None, None,
+                              ctypes.byref(sync), fake, ws_n, None) == 1
+    # workspace too small
+    assert lib.moe_ffn_fwd_ex(ctypes.byref(p), fake, fake, fake, fake, fake, ctypes.byref(d), fake, fake, None, fake,
+                              ctypes.byref(sync), fake, ws_n - 1, None) == 4
+    # the struct layout the binding passes matches the header's field order
+    assert [f[0] for f in L.MoeFwdSync._fields_] == ["row_split", "x_ready", "y_ready", "t_ready", "sm_reserve"]
