@@ -127,9 +127,6 @@ __host__ __device__ constexpr bool splits_rows(int k) { return k == TC_FWD_UP ||
 // need no DRAM read
 #define MOEB_RED_EVICT_LAST 0
 #endif
-#ifndef MOEB_WG_PF
-#define MOEB_WG_PF 0  // DW3 / DW12 epilogue: next TMEM chunk read in flight during this chunk's stores
-#endif
 #ifndef MOEB_RED_EPI8
 // FWD_DOWN / BWD_DX: 8 epilogue warps (128 columns each), 5 mainloop stages.  Parity-green but
 // off: interleaved A/B measured both kinds 1-5 % slower (profiles/red8_ab_r01.txt)
@@ -1622,12 +1619,6 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
           base = (m0w < P.h) ? P.out0 + (int64_t)t.e * P.h * P.d + (int64_t)m0w * P.d
                              : P.out1 + (int64_t)t.e * P.h * P.d + (int64_t)(m0w - P.h) * P.d;
         }
-        // (MOEB_WG_PF: the next chunk's TMEM read is issued before this chunk's stores, so its
-        // latency overlaps them -- it matters where tiles have one or two k-blocks and the
-        // epilogue, not the mainloop, sets the pace: the near-empty experts of skewed routing)
-        constexpr bool PF = MOEB_WG_PF && !WIDE;
-        if constexpr (PF)
-          if (t.nk > 0) ptx::tmem_ld32(tb, v);
 #pragma unroll 1
         for (int c = 0; c < tile_n<KIND, CG>(); c += 32) {
           // wide tile: TMEM column c of accumulator c / 256 holds tile column 256 r + 128 (c / 256) + j,
@@ -1638,12 +1629,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
             else break;
           }
           float f[32];
-          if (PF && t.nk > 0) {
-            ptx::tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
-            if (c + 32 < tile_n<KIND, CG>() && t.n0 + c + 32 < N) ptx::tmem_ld32(tb + c + 32, v);
-          } else if (t.nk > 0) {
+          if (t.nk > 0) {
             ptx::tmem_ld32(tb + c, v);
             ptx::tmem_wait_ld();
 #pragma unroll

@@ -57,9 +57,12 @@ def _worker(rank, P, port, q, routing, backend="gloo", retain=False, c=CFG):
         ep = P2PExpertParallelMoE(pg, c["E"], c["k"])
     else:
         from paper_2601_05296_b200.ep import ExpertParallelMoE
-        ep = ExpertParallelMoE(c["E"], c["k"], False, a2a=staged_a2a if backend == "gloo" else None,
-                               retain_recv_x=retain)
-        assert ep._use_streams(x) == backend.startswith("nccl")
+        # gloo_overlap: the side-stream orchestration (C2b / C3 overlap with the row-split
+        # GEMMs: x_ready, y_ready, sm_reserve; C4b / C5 in backward) over the host-staged
+        # all-to-all -- the only way to run it with received rows on a one-GPU box
+        ep = ExpertParallelMoE(c["E"], c["k"], False, a2a=staged_a2a if backend.startswith("gloo") else None,
+                               retain_recv_x=retain, overlap=True if backend == "gloo_overlap" else None)
+        assert ep._use_streams(x) == (backend.startswith("nccl") or backend == "gloo_overlap")
     lo, hi = ep.local_experts
     wl = [W[n][lo:hi].contiguous().to(dev) for n in ("w1", "w2", "w3")]
     for _ in range(2 if backend.startswith("p2p") else 1):  # p2p: a second step reuses the buffers
@@ -96,7 +99,11 @@ def test_ep_fewer_local_experts_than_k(P, routing, backend, retain, c):
                                                       (2, "skewed", "nccl_multi", True),
                                                       # P = 4 and 8 processes sharing one GPU over gloo: the
                                                       # EP config's rank counts (E = 8: 2 experts, then 1 < k)
-                                                      (4, "balanced", "gloo", False), (8, "skewed", "gloo", False)])
+                                                      (4, "balanced", "gloo", False), (8, "skewed", "gloo", False),
+                                                      # the stream orchestration with received rows (U > 0)
+                                                      (2, "balanced", "gloo_overlap", False),
+                                                      (4, "skewed", "gloo_overlap", False),
+                                                      (2, "degenerate", "gloo_overlap", True)])
 def test_ep_cuda_matches_single_gpu(P, routing, backend, retain, c=CFG):
     """degenerate routing: every token picks experts 0,1, so rank 1 receives no rows.
     nccl (P = 1): the product path, with C4b / C5 on the side stream.  nccl_multi:
