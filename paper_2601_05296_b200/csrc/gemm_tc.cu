@@ -127,6 +127,13 @@ __host__ __device__ constexpr bool splits_rows(int k) { return k == TC_FWD_UP ||
 // need no DRAM read
 #define MOEB_RED_EVICT_LAST 0
 #endif
+#ifndef MOEB_WG_LPT
+// DW3 / DW12 tiles claimed longest-K (largest expert) first.  Skewed routing put the largest
+// expert's 236-k-block tiles wherever its index fell in the list; claimed late they left a
+// tail with most SMs idle: DeepSeek-like skewed DW3 0.82-0.85 -> 0.56 ms, balanced and
+// Mixtral-like unchanged (profiles/variants_r02al_wgrad_lpt.txt)
+#define MOEB_WG_LPT 1
+#endif
 #ifndef MOEB_RED_EPI8
 // FWD_DOWN / BWD_DX: 8 epilogue warps (128 columns each), 5 mainloop stages.  Parity-green but
 // off: interleaved A/B measured both kinds 1-5 % slower (profiles/red8_ab_r01.txt)
@@ -352,8 +359,10 @@ __device__ __forceinline__ bool decode_tile(int tile, const TcParams& P, const i
       if (local >= P.E * P.m_tiles * nt) return false;
     }
     const int per_e = P.m_tiles * nt;
-    t.e = local / per_e;
-    const int rem = local - t.e * per_e;
+    // experts in the order of s_mstart (longest K first, MOEB_WG_LPT) or by index
+    const int pos = local / per_e;
+    t.e = MOEB_WG_LPT ? s_mstart[pos] : pos;
+    const int rem = local - pos * per_e;
     int mt;
     if constexpr (KIND == TC_DW3) {
       // m fastest: the concurrent tiles share the B n-tile (wU rows, h wide: the
@@ -636,6 +645,21 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
       s += ((splits_rows(KIND) ? s_offs[520 + e] : s_offs[e + 1]) - s_offs[e] + C::TM - 1) / C::TM;
     }
     s_mstart[E] = s;
+  }
+  if constexpr (K::wgrad && MOEB_WG_LPT) {
+    // weight-gradient tiles have K = the expert's rows: hand out the longest ones first (LPT),
+    // so a large expert claimed late cannot leave a tail with most SMs idle (skewed routing).
+    // Every CTA derives the same order: rank by (rows desc, expert id asc); s_mstart is unused
+    // by these kinds and holds it
+    for (int e = threadIdx.x; e < E; e += tc_threads(KIND)) {
+      const int ne = s_offs[e + 1] - s_offs[e];
+      int rank = 0;
+      for (int j = 0; j < E; ++j) {
+        const int nj = s_offs[j + 1] - s_offs[j];
+        rank += (nj > ne) || (nj == ne && j < e);
+      }
+      s_mstart[rank] = e;
+    }
   }
   ptx::tc_fence_before();
   if constexpr (CG == 2) ptx::cluster_sync();  // peer barriers initialised + TMEM allocated
