@@ -127,6 +127,9 @@ __host__ __device__ constexpr bool splits_rows(int k) { return k == TC_FWD_UP ||
 // need no DRAM read
 #define MOEB_RED_EVICT_LAST 0
 #endif
+#ifndef MOEB_RG
+#define MOEB_RG 8  // row kinds: m-tiles per rasterisation group (the group's rows stay L2-resident)
+#endif
 #ifndef MOEB_WG_LPT
 // DW3 / DW12 tiles claimed longest-K (largest expert) first.  Skewed routing put the largest
 // expert's 236-k-block tiles wherever its index fell in the list; claimed late they left a
@@ -407,7 +410,7 @@ __device__ __forceinline__ bool decode_tile(int tile, const TcParams& P, const i
     // a remainder never forms a small group of its own, which would re-stream the
     // expert's whole weight for a handful of rows (9 m-tiles = one group of 9,
     // not 8 + 1)
-    constexpr int RG = 8;
+    constexpr int RG = MOEB_RG;
     const int ng = max(1, mt_e / RG);
     const int gsz = mt_e / ng, extra = mt_e - gsz * ng;  // `extra` groups have gsz + 1 m-tiles
     const int big = extra * (gsz + 1) * nt;
