@@ -483,6 +483,14 @@ def main():
         torch.cuda.synchronize()
         e2e_clk = eclk.stop((ew0, time.time()))
         ms1 = torch.cuda.memory_stats()
+        # a second, traced run (not the reported number): per-step copy / kernel timing, to
+        # tell a copy-bound step from copies serialised behind the kernels
+        from paper_2601_05296_b200.pipeline import trace_summary
+        tr = []
+        pipe.run([x_h] * n_e2e, [dy_h] * n_e2e, [ys_h[i % 2] for i in range(n_e2e)],
+                 [dxs_h[i % 2] for i in range(n_e2e)], trace=tr)
+        torch.cuda.synchronize()
+        e2e_trace = trace_summary(tr)
         # cudaMalloc / cudaFree inside the timed loop serialise host and device
         alloc = {k: ms1.get(k, 0) - ms0.get(k, 0) for k in ("num_device_alloc", "num_device_free", "num_alloc_retries")}
         ems = e0.elapsed_time(e1) / n_e2e
@@ -494,7 +502,7 @@ def main():
                # what bounds it: the device step or the PCIe transfers of a step (measured just before)
                "floor_ms_per_step": {"device": round(ms / args.steps, 4),
                                      "pcie": pcie["concurrent"]["floor_ms_per_step"]},
-               "pcie": pcie, "host_numa": numa, "allocator_in_timed_loop": alloc, "clocks": e2e_clk,
+               "pcie": pcie, "trace": e2e_trace, "host_numa": numa, "allocator_in_timed_loop": alloc, "clocks": e2e_clk,
                "h2d_bytes_per_step": 2 * x.numel() * x.element_size(),
                "d2h_bytes_per_step": 2 * x.numel() * x.element_size(),
                "api": ("paper_2601_05296_b200.ep.ExpertParallelMoE.step" if ep is not None else

@@ -36,3 +36,16 @@ def test_host_pipeline_matches_sequential():
     for (ry, rdx), y, dx in zip(ref, ys, dxs):
         assert torch.equal(ry, y)
         assert torch.equal(rdx, dx)
+    # the traced run (bench.py's e2e diagnostics) gives the same results and sane timings
+    from paper_2601_05296_b200.pipeline import trace_summary
+    for t in ys + dxs:
+        t.zero_()
+    tr = []
+    HostPipeline(layer_step, xs[0].shape, xs[0].dtype, dev).run(xs, dys, ys, dxs, trace=tr)
+    torch.cuda.synchronize()
+    for (ry, rdx), y, dx in zip(ref, ys, dxs):
+        assert torch.equal(ry, y) and torch.equal(rdx, dx)
+    summ = trace_summary(tr)
+    assert len(tr) == 1 + len(xs)
+    for key in ("h2d", "comp", "d2h", "run_ms_per_step"):
+        assert summ[key] > 0, (key, summ)
