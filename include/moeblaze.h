@@ -203,8 +203,8 @@ moe_status moe_ffn_fwd(const moe_problem* p, const void* x, const void* w1, cons
  * expert's rows [offsets[e], row_split[e]) are those whose token is < t_ready
  * (ascending inside an expert, so they come first).  Launch order:
  *   up-projection of the rows before row_split; wait x_ready; up-projection
- *   of the rest; then, with y_ready set (bf16, red.add combine, no
- *   token_rows bound): down-projection of the rows from row_split on, y rows
+ *   of the rest; then, with y_ready set (bf16, red.add combine): down-
+ *   projection of the rows from row_split on, y rows
  *   [t_ready, T) finalised, y_ready recorded, down-projection of the rows
  *   before row_split leaving sm_reserve SMs free (for the C3 exchange kernel),
  *   y rows [0, t_ready) finalised; without y_ready: one down-projection and

@@ -20,8 +20,9 @@ int dwg_chunks(const moe_problem* p);
 moe_status launch_router_bwd(const moe_problem*, const float*, const int32_t*, const float*, const void*, float*,
                              __nv_bfloat16*, float*, void*, cudaStream_t);
 moe_status launch_zero_acc(float*, int64_t, int, const int32_t*, cudaStream_t);
+// row0: acc / out start at token row row0 of the problem (t_rows stays the absolute bound)
 moe_status launch_finalize(const moe_problem*, const void*, const float*, const __nv_bfloat16*, const void*, void*,
-                           cudaStream_t, bool, const int32_t*, const int32_t*);
+                           cudaStream_t, bool, const int32_t*, const int32_t*, int64_t row0 = 0);
 int router_ep8(int E);
 moe_status launch_ep_dest(const int32_t*, int64_t, int, int, int, int, int32_t*, cudaStream_t);
 moe_status launch_ep_local_slots(const int32_t*, const float*, int64_t, int, int, int32_t*, float*, cudaStream_t);
@@ -281,7 +282,7 @@ moe_status moe_ffn_fwd_ex(const moe_problem* p, const void* x, const void* w1, c
   c.which = GEMM_FWD_DOWN;
   c.sched = sched_at(ws, SCHED_DOWN);
   const int64_t t_ready = split ? sync->t_ready : 0;
-  if (split && y_ready && mode == OUT_RED && !disp->token_rows && t_ready >= 0 && t_ready <= p->T) {
+  if (split && y_ready && mode == OUT_RED && t_ready >= 0 && t_ready <= p->T) {
     // the received rows' y first (their tokens are >= t_ready: they red.add only into rows
     // [t_ready, T)), finalised and signalled so their return overlaps the local rows' down
     // projection, which leaves sm_reserve SMs to the exchange kernel
@@ -294,7 +295,8 @@ moe_status moe_ffn_fwd_ex(const moe_problem* p, const void* x, const void* w1, c
     {
       ProfScope prof("combine", st);
       if ((s = launch_finalize(&hi, w.yacc + t_ready * p->d, nullptr, nullptr, nullptr,
-                               (char*)y + (size_t)t_ready * p->d * es, st, false, nullptr, nullptr)) != MOE_OK)
+                               (char*)y + (size_t)t_ready * p->d * es, st, false, nullptr, disp->token_rows,
+                               t_ready)) != MOE_OK)
         return s;
     }
     MOE_CUDA_CHECK(cudaEventRecord(y_ready, st));
@@ -302,7 +304,7 @@ moe_status moe_ffn_fwd_ex(const moe_problem* p, const void* x, const void* w1, c
     c.sm_reserve = sync->sm_reserve;
     if ((s = run_gemm(c, st)) != MOE_OK) return s;
     ProfScope prof("combine", st);
-    return launch_finalize(&lo, w.yacc, nullptr, nullptr, nullptr, y, st, false, nullptr, nullptr);
+    return launch_finalize(&lo, w.yacc, nullptr, nullptr, nullptr, y, st, false, nullptr, disp->token_rows);
   }
   c.row_split = nullptr;
   c.split_half = 0;

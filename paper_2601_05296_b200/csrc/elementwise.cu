@@ -493,8 +493,10 @@ moe_status launch_router_bwd(const moe_problem* p, const float* logits, const in
 // per step, grid-stride: the HBM-bound Y finalize)
 __global__ void __launch_bounds__(256) convert_f32_bf16_kernel(const float4* __restrict__ acc, int64_t n8,
                                                                 uint4* __restrict__ out,
-                                                                const int32_t* __restrict__ t_rows, int d8) {
-  if (t_rows) n8 = min64(n8, (int64_t)__ldg(t_rows) * d8);  // rows past the device bound are unused
+                                                                const int32_t* __restrict__ t_rows, int d8,
+                                                                int64_t row0) {
+  // rows past the device bound are unused (acc / out start at token row row0)
+  if (t_rows) n8 = min64(n8, max((int64_t)0, (int64_t)__ldg(t_rows) - row0) * d8);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
     const float4 a = __ldcs(acc + 2 * i), b = __ldcs(acc + 2 * i + 1);
     uint4 o;
@@ -540,7 +542,7 @@ moe_status launch_zero_acc(float* acc, int64_t T, int d, const int32_t* t_rows, 
 
 moe_status launch_finalize(const moe_problem* p, const void* acc, const float* dl, const __nv_bfloat16* dlhl,
                            const void* wg, void* out, cudaStream_t st, bool acc_is_dtype, const int32_t* tim,
-                           const int32_t* t_rows) {
+                           const int32_t* t_rows, int64_t row0) {
   if (p->T == 0) return MOE_OK;
   typedef __nv_bfloat16 bf;
   if (dl && p->dtype == MOE_BF16)
@@ -555,7 +557,8 @@ moe_status launch_finalize(const moe_problem* p, const void* acc, const float* d
     // the plain Y conversion (fp32 accumulator -> bf16): 8 columns per thread per step
     const int64_t n8 = p->T * (int64_t)p->d / 8;
     const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(n8, 256), (int64_t)sm_count_cached() * 8);
-    MOE_LAUNCH(convert_f32_bf16_kernel, blocks, 256, 0, st, (const float4*)acc, n8, (uint4*)out, t_rows, p->d / 8);
+    MOE_LAUNCH(convert_f32_bf16_kernel, blocks, 256, 0, st, (const float4*)acc, n8, (uint4*)out, t_rows, p->d / 8,
+               row0);
     return cudaGetLastError() == cudaSuccess ? MOE_OK : MOE_ERR_CUDA;
   }
   dim3 grid((unsigned)ceil_div(p->d, 256), (unsigned)ceil_div(p->T, 16));

@@ -23,9 +23,12 @@ Step e on rank `me` (every phase signals all ranks, itself included):
              gate weights, gathered straight from the source arrays into the
              owners' buffers at row T + sum_{s<me} cmat[s][q] (no send buffer).
   receiver   moe_ep_recv_prepare (global -> local ids, -1 tail), dispatch over
-             the P*T rows (sparse slots, rows = the worst case), moe_ffn_fwd
-             into the symmetric `out` buffer.
-  Y          signal + wait; moe_ep_pull_combine: y[t] = local partial + the
+             the P*T rows (sparse slots, rows = the worst case), moe_ffn_fwd_ex
+             into the symmetric `out` buffer: the received rows' down
+             projection and y first (rows >= T), then the local rows'.
+  Y          signalled from a side stream as soon as the received rows' y is
+             final (y_ready), so peers pull while this rank computes its own
+             rows; wait; moe_ep_pull_combine: y[t] = local partial + the
              owners' rows of t, read from peer memory (fused combine).
 Backward: DY push of dY rows; moe_ffn_bwd data stage (dX rows into `out`, gate
 grads into `dg`, X still in the symmetric `x` buffer -- nothing is sent twice);
@@ -161,6 +164,8 @@ class P2PExpertParallelMoE:
     peer memory (no host sync, no NCCL).  Same math and results as
     ep.ExpertParallelMoE (per-destination dedup, local pairs never travel)."""
 
+    SM_RESERVE = 2  # SMs the local rows' down projection leaves free for the Y signal kernel
+
     def __init__(self, peers: PeerGroup, E, k, renormalize=False):
         self.peers = peers
         self.P, self.rank = peers.P, peers.rank
@@ -220,9 +225,24 @@ class P2PExpertParallelMoE:
         a_l = torch.empty(n_cap, h, dtype=x.dtype, device=x.device)
         b_l = torch.empty(n_cap, h, dtype=x.dtype, device=x.device)
         ws = L.workspace(p, L.MOE_OP_FFN_FWD, x.device)
-        L.moe_ffn_fwd(p, buf["x"], w1l, w2l, w3l, buf["w"], disp_l.c(), a_l, b_l, None, buf["out"], ws)
+        # the received rows' down projection and y first (rows [T, T + U) of `out`): y_ready
+        # fires before the local rows' down projection, and the Y signal goes out from a side
+        # stream at that moment, so the owners of those tokens pull them while this rank still
+        # computes its own rows (C3 overlap); the GEMM leaves SM_RESERVE SMs free so the signal
+        # kernel is not queued behind it
+        main = torch.cuda.current_stream()
+        split = torch.empty(El, dtype=torch.int32, device=x.device)
+        L.moe_dispatch_row_split(p, disp_l.c(), T, split)
+        y_ready = torch.cuda.Event()
+        y_ready.record(main)  # created now; re-recorded by the library
+        L.moe_ffn_fwd_ex(p, buf["x"], w1l, w2l, w3l, buf["w"], disp_l.c(), a_l, b_l, None, buf["out"], ws,
+                         row_split=split, y_ready=y_ready, t_ready=T, sm_reserve=self.SM_RESERVE)
+        side = self._side_stream(x.device)
+        side.wait_event(y_ready)
+        with torch.cuda.stream(side):
+            L.moe_ep_signal(G, L.MOE_EP_PH_Y, e)
+        main.wait_stream(side)  # later work on this stream is ordered after the signal
         del ws
-        L.moe_ep_signal(G, L.MOE_EP_PH_Y, e)
         L.moe_ep_wait(G, L.MOE_EP_PH_Y, e)
         y = torch.empty(T, d, dtype=x.dtype, device=x.device)
         L.moe_ep_pull_combine(G, L.problem(T, d, 128, E, k, x.dtype), tab["out"], T, plan.offs, plan.tim,
