@@ -139,7 +139,9 @@ __host__ __device__ constexpr bool splits_rows(int k) { return k == TC_FWD_UP ||
 #endif
 #ifndef MOEB_RED_EPI8
 // FWD_DOWN / BWD_DX: 8 epilogue warps (128 columns each), 5 mainloop stages.  Parity-green but
-// off: interleaved A/B measured both kinds 1-5 % slower (profiles/red8_ab_r01.txt)
+// off: interleaved A/B measured both kinds 1-5 % slower (profiles/red8_ab_r01.txt).  (Since the
+// row-split segment ends joined the FWD_DOWN offsets block, its one-CTA engine variants exceed
+// the 227 KB shared-memory limit with this flag; it is kept as the record of round 1.)
 #define MOEB_RED_EPI8 0
 #endif
 // 8-warp BWD_DH: 5 mainloop stages + a 3-deep epilogue ring (one chunk of A/B prefetch) in the
@@ -1353,7 +1355,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ 
         const int r = r0w + lane;
         const int nvalid = max(0, min(32, t.seg1 - r0w));
         const int N = P.d;
-        const uint64_t pol = MOEB_RED_EVICT_LAST ? ptx::policy_evict_last() : 0ull;
+        [[maybe_unused]] const uint64_t pol = MOEB_RED_EVICT_LAST ? ptx::policy_evict_last() : 0ull;
         float w = 1.f;
         int tok = 0;
         if (r < t.seg1) {
