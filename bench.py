@@ -535,7 +535,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded, moe_inputs)",
             "config": config_dict(args, cfg, world, ep is not None),
-            "expert_load": expert_load, "roofline": roof, "hbm_steps": hbm_steps, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "device": device_info(dev), "expert_load": expert_load, "roofline": roof, "hbm_steps": hbm_steps, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "gpu_launches_per_step": launches / args.steps, "clocks": clk,
             "step_ms": {"median": round(statistics.median(per_step), 4), "min": round(min(per_step), 4),
                         "max": round(max(per_step), 4), "note": "per-step CUDA events inside the timed region, rank 0"},
@@ -661,6 +661,14 @@ def hbm_report(named, cfg, R, k, peaks, ms_step, steps):
     total_us = sum(v["us_per_launch"] * v["launches_per_step"] for v in out.values())
     return {"peak_gbs": hbm, "peak_source": peaks["source"], "steps": out,
             "share_of_step": round(total_us / 1e3 / ms_step, 4)}
+
+
+def device_info(dev):
+    """The GPU the line was measured on (cudaDevAttr* via torch): name, SMs, L2 bytes (the
+    `config.l2` policy states the 126 MB nominal; this is the device's own figure)."""
+    p = torch.cuda.get_device_properties(dev)
+    return {"name": p.name, "sm_count": p.multi_processor_count, "l2_bytes": getattr(p, "L2_cache_size", None),
+            "hbm_bytes": p.total_memory}
 
 
 def config_dict(args, cfg, world, ep_path):
