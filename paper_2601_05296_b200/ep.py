@@ -239,6 +239,13 @@ class ExpertParallelMoE:
         """Collective: every rank calls it, also with nothing to send or receive."""
         return self._a2a(send, send_split, recv_split, self.group, out=out)
 
+    def _side_stream(self, device):
+        """One side stream per layer instance (the exchanges of C2b, C3, C4b and C5 are
+        issued on it in program order; creating a stream per step would cost a driver call)."""
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(device=device)
+        return self._side
+
     def _use_streams(self, x):
         if self.overlap is not None:
             return bool(self.overlap) and x.is_cuda
@@ -300,7 +307,7 @@ class ExpertParallelMoE:
         x_send = ops.gather_rows(x, send_tok)
         x_ready = None
         if streams and U:
-            main, side = torch.cuda.current_stream(), torch.cuda.Stream(device=x.device)
+            main, side = torch.cuda.current_stream(), self._side_stream(x.device)
             side.wait_stream(main)
             with torch.cuda.stream(side):
                 self.a2a(x_send, send_split, recv_split, out=x_l[T:])
@@ -330,7 +337,7 @@ class ExpertParallelMoE:
         # received rows' y is final at y_ready, before the local rows' down projection, which
         # leaves sm_reserve SMs to this all-to-all's kernel
         if y_ready is not None:
-            main, side = torch.cuda.current_stream(), torch.cuda.Stream(device=x.device)
+            main, side = torch.cuda.current_stream(), self._side_stream(x.device)
             side.wait_event(y_ready)
             with torch.cuda.stream(side):
                 y_back = self.a2a(y_rows[T:], recv_split, send_split)
@@ -354,7 +361,7 @@ class ExpertParallelMoE:
         w1l, w2l, w3l = ctx["w1l"], ctx["w2l"], ctx["w3l"]
         streams = self._use_streams(x)
         main = torch.cuda.current_stream() if streams else None
-        side = torch.cuda.Stream(device=x.device) if streams else None
+        side = self._side_stream(x.device) if streams else None
         sctx = (lambda: torch.cuda.stream(side)) if streams else contextlib.nullcontext
         # C4a: remote dY rows to the expert owners (the dH GEMM needs them first)
         dy_l = self._rows(dy, ctx["send_tok"], ss, rs)
