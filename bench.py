@@ -10,7 +10,7 @@ of synthetic, seeded inputs already resident in HBM.  N = 1 runs the
 Mixtral-like layer (BASELINE.json configs[1]); N > 1 runs the same per-GPU
 workload expert-parallel over NCCL all-to-all (weak scaling).
 
-Prints ONE JSON line on rank 0.  See DESIGN.md §Measurement for every key.
+Prints ONE JSON line on rank 0.  See DESIGN.md §8d for every key.
 
 --gpus N > 1 without a torchrun environment re-launches this script under
 torch.distributed.run (N ranks, one per GPU, NCCL, 127.0.0.1); under torchrun
