@@ -44,6 +44,10 @@ __device__ __forceinline__ float4 ld_acc4<__nv_bfloat16>(const __nv_bfloat16* p)
 constexpr int RDX_THREADS = 256;
 constexpr int RDX_SMEM = 16384 * 2 + 32768 + 8 * 4096 + 64 + 1024;
 
+#ifndef RDX_L2PF
+#define RDX_L2PF 1  // router dX / finalise: L2 prefetch of the tile's accumulator rows before its MMA
+                    // (ncu 61.5 -> 57.3 us DeepSeek-like, in-step 80 -> 73 / 87 -> 80 us; profiles/variants_r02aw_rdx_l2pf.txt)
+#endif
 template <bool LOAD, typename A>
 __global__ void __launch_bounds__(RDX_THREADS, 2)
 router_dx_tc_kernel(const __grid_constant__ CUtensorMap mDh, const __grid_constant__ CUtensorMap mDl,
@@ -113,6 +117,19 @@ router_dx_tc_kernel(const __grid_constant__ CUtensorMap mDh, const __grid_consta
   for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x, gk += nkc) {
     t0 = (ti / ntn) * 128;
     n0 = (int)(ti - (ti / ntn) * ntn) * 256;
+    if constexpr (RDX_L2PF && LOAD) {
+      // this warp's whole accumulator region (32 rows x 128 columns: 128 lines) to L2 before
+      // the tile's MMA, so the epilogue's one-chunk-ahead register loads hit L2, not HBM
+      if (!tim) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int L = lane + 32 * i, row = L >> 2, seg = L & 3;
+          const int64_t t = t0 + quad * 32 + row;
+          const int64_t col = n0 + half * 128 + seg * 32;
+          if (t < Tn && col < d) ptx::prefetch_l2(acc + t * d + col);
+        }
+      }
+    }
     load_chunk(half * 128, a_cur);
     if (warp == 0) {
       for (int kc = 0; kc < nkc; ++kc) {
