@@ -117,19 +117,23 @@ router_dx_tc_kernel(const __grid_constant__ CUtensorMap mDh, const __grid_consta
   for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x, gk += nkc) {
     t0 = (ti / ntn) * 128;
     n0 = (int)(ti - (ti / ntn) * ntn) * 256;
-    if constexpr (RDX_L2PF && LOAD) {
-      // this warp's whole accumulator region (32 rows x 128 columns: 128 lines) to L2 before
-      // the tile's MMA, so the epilogue's one-chunk-ahead register loads hit L2, not HBM
-      if (!tim) {
+    // this warp's whole accumulator region (32 rows x 128 columns: 128 lines) of tile tt to L2,
+    // so the epilogue's one-chunk-ahead register loads hit L2, not HBM
+    auto prefetch_tile = [&](int64_t tt) {
+      if constexpr (RDX_L2PF && LOAD) {
+        if (tim || tt >= ntiles) return;
+        const int64_t pt0 = (tt / ntn) * 128;
+        const int pn0 = (int)(tt - (tt / ntn) * ntn) * 256;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int L = lane + 32 * i, row = L >> 2, seg = L & 3;
-          const int64_t t = t0 + quad * 32 + row;
-          const int64_t col = n0 + half * 128 + seg * 32;
+          const int64_t t = pt0 + quad * 32 + row;
+          const int64_t col = pn0 + half * 128 + seg * 32;
           if (t < Tn && col < d) ptx::prefetch_l2(acc + t * d + col);
         }
       }
-    }
+    };
+    prefetch_tile(ti);  // before the tile's MMA (a whole epilogue ahead, for the next tile, measured slower)
     load_chunk(half * 128, a_cur);
     if (warp == 0) {
       for (int kc = 0; kc < nkc; ++kc) {
