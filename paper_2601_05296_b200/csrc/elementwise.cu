@@ -512,7 +512,7 @@ __global__ void __launch_bounds__(256) convert_f32_bf16_kernel(const float4* __r
 // acc[t, :] = 0 for t < *t_rows (the fp32 combine accumulator; the rows past the
 // device-side bound are never referenced)
 __global__ void zero_rows_kernel(float4* __restrict__ acc, int64_t n4, const int32_t* __restrict__ t_rows, int d4) {
-  const int64_t n = min64(n4, (int64_t)__ldg(t_rows) * d4);
+  const int64_t n = t_rows ? min64(n4, (int64_t)__ldg(t_rows) * d4) : n4;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
@@ -528,9 +528,12 @@ static int sm_count_cached() {
   return nsm;
 }
 
+#ifndef ZERO_KERNEL
+#define ZERO_KERNEL 0  // 1: the library's zeroing kernel also without a device row bound (A/B vs cudaMemsetAsync)
+#endif
 moe_status launch_zero_acc(float* acc, int64_t T, int d, const int32_t* t_rows, cudaStream_t st) {
   if (T == 0) return MOE_OK;
-  if (!t_rows || d % 4) {
+  if ((!t_rows && !ZERO_KERNEL) || d % 4) {
     MOE_CUDA_CHECK(cudaMemsetAsync(acc, 0, (size_t)T * d * 4, st));
     return MOE_OK;
   }
